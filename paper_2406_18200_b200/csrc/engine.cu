@@ -1,0 +1,1218 @@
+// engine.cu -- the C ABI of seed.h / seed_ops.h: models, paged KV pool, the round, NCCL.
+//
+// Host orchestration of one round (Alg. 1 in the lock-step batched reading, DESIGN R9):
+//   seed_schedule_round  -> completes round r-1 on the host mirrors, FCFS pop (H1)
+//   seed_draft_round     -> gamma batched draft forwards + K1 sampler
+//   seed_verify          -> batched target forward, K4, K5, all-gather
+// Every arithmetic step runs in the kernels of gemm.cu / epilogue.cu / attention.cu /
+// vocab.cu; this file only plans, allocates, uploads descriptors and launches.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <tuple>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/seed.h"
+#include "../../include/seed_ops.h"
+#include "kernels.h"
+
+using seed::GemmPlan;
+using seed::KVLayout;
+using seed::PartialView;
+typedef __nv_bfloat16 bf16;
+
+namespace {
+
+// ------------------------------------------------------------------ NCCL (dlopen'd, a6 only)
+struct Id128 {
+  char b[128];
+};
+typedef int (*InitRankFn)(void**, int, Id128, int);
+struct Nccl {
+  void* lib = nullptr;
+  int (*get_id)(Id128*) = nullptr;
+  InitRankFn init = nullptr;
+  int (*allgather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+  int (*destroy)(void*) = nullptr;
+  bool load() {
+    if (lib) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      lib = dlopen(n, RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+      if (!lib) lib = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (lib) break;
+    }
+    if (!lib) return false;
+    get_id = (int (*)(Id128*))dlsym(lib, "ncclGetUniqueId");
+    init = (InitRankFn)dlsym(lib, "ncclCommInitRank");
+    allgather = (int (*)(const void*, void*, size_t, int, void*, cudaStream_t))dlsym(lib, "ncclAllGather");
+    destroy = (int (*)(void*))dlsym(lib, "ncclCommDestroy");
+    return get_id && init && allgather && destroy;
+  }
+};
+Nccl g_nccl;
+constexpr int kNcclInt32 = 2;
+
+// ------------------------------------------------------------------ descriptor arena
+// pinned host staging + device mirror; one H2D copy per upload
+struct Arena {
+  int32_t* host = nullptr;
+  int32_t* dev = nullptr;
+  size_t cap = 0, used = 0;
+  cudaEvent_t done = nullptr;
+  bool pending = false;
+  cudaError_t init(size_t ints) {
+    cap = ints;
+    cudaError_t e = cudaMallocHost(&host, cap * 4);
+    if (e != cudaSuccess) return e;
+    e = cudaMalloc(&dev, cap * 4);
+    if (e != cudaSuccess) return e;
+    return cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+  }
+  void begin() {
+    if (pending) cudaEventSynchronize(done);
+    pending = false;
+    used = 0;
+  }
+  size_t alloc(size_t n) {  // returns offset (ints), 16-byte aligned
+    size_t off = (used + 3) & ~size_t(3);
+    if (off + n > cap) return (size_t)-1;
+    used = off + n;
+    return off;
+  }
+  cudaError_t upload(cudaStream_t st) {
+    if (!used) return cudaSuccess;
+    cudaError_t e = cudaMemcpyAsync(dev, host, used * 4, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return e;
+    pending = true;
+    return cudaEventRecord(done, st);
+  }
+  void destroy() {
+    if (host) cudaFreeHost(host);
+    if (dev) cudaFree(dev);
+    if (done) cudaEventDestroy(done);
+  }
+};
+
+struct Segment {  // rows of one sequence in a forward chunk
+  int slot, pos0, q_len;
+  int tok_off;    // offset of host tokens in the arena (-1: tokens from a device source)
+};
+
+struct TokSrc {   // device token source for rows (row m reads dev[m * stride])
+  const int32_t* dev;
+  int stride;
+};
+
+struct Model {
+  seed_model_shape sh{};
+  int d = 0, H = 0, Hk = 0, Dh = 0, ff = 0, V = 0, L = 0, nqkv = 0;
+  bf16 *embed = nullptr, *final_norm = nullptr, *lm_head = nullptr;
+  std::vector<bf16*> wqkv, wo, wgu, wdown, an, mn;
+  std::vector<GemmPlan> pq, po, pgu, pd;
+  GemmPlan plm{};
+  // paged KV
+  KVLayout kv{};
+  int32_t* page_table_dev = nullptr;
+  std::vector<int32_t> page_table;        // host mirror [slots][max_pages]
+  std::vector<int32_t> free_pages;
+  std::vector<int32_t> held;              // pages held per slot
+  size_t n_pages = 0;
+  float2* rope = nullptr;
+  // activations for up to m_cap rows per forward chunk
+  int m_cap = 0;
+  float* x = nullptr;
+  bf16 *h = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr, *hlm = nullptr;
+  seed::AttnWorkspace aws{};
+  std::vector<bf16*> owned;
+};
+
+struct SlotState {  // host mirror of one stream slot
+  uint32_t gid = 0;
+  bool used = false;
+  std::vector<int32_t> T;  // validated tokens
+  int prompt_len = 0, L = 0, r = 0, done = 0, len_t = 0, len_d = 0;
+};
+
+constexpr int kMaxChunkRows = 256;
+
+}  // namespace
+
+struct seed_ctx_s {
+  seed_config cfg{};
+  std::string err;
+  bool poisoned = false;
+  int dev = 0;
+  Model dm, tm;                   // draft, target
+  int P = 16, max_pages = 0, n_slots = 0;
+  float* partial = nullptr;
+  size_t partial_floats = 0;
+  std::map<std::tuple<const void*, int, int>, CUtensorMap> xmaps;
+  Arena arena;
+  // stream registry
+  std::vector<SlotState> slots;
+  std::unordered_map<uint32_t, int> gid2slot;
+  seed_sched sched = nullptr;
+  seed_table table = nullptr;
+  // device state (K5)
+  seed::StreamState ds{};
+  // per-round buffers (capacity C = max_batch)
+  int C = 0, G = 0;
+  float *tgt_logits = nullptr, *drf_logits = nullptr;
+  int32_t *xs = nullptr, *vtok = nullptr, *out_tok = nullptr, *out_cnt = nullptr, *out_acc = nullptr;
+  int32_t *records = nullptr, *records_all = nullptr, *records_host = nullptr, *cnt_host = nullptr,
+          *tok_host = nullptr;
+  uint32_t* sids_dev = nullptr;
+  int32_t* rs_dev = nullptr;
+  int32_t* slots_dev = nullptr;
+  cudaEvent_t round_done = nullptr;
+  std::vector<int32_t> last_batch;  // global ids of the batch in flight
+  std::vector<int32_t> drafted;     // batch drafted and not yet verified
+  bool round_pending = false;
+  // NCCL
+  void* comm = nullptr;
+  // profiling
+  bool profile = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
+  size_t ev_used = 0;
+  double gemm_bytes = 0;
+  int64_t gemm_launches = 0, kernel_launches = 0;
+};
+
+namespace {
+
+#define CK(expr)                                                                  \
+  do {                                                                            \
+    cudaError_t _e = (expr);                                                      \
+    if (_e != cudaSuccess) return fail(ctx, SEED_ECUDA, #expr, cudaGetErrorString(_e)); \
+  } while (0)
+
+seed_status fail(seed_ctx ctx, seed_status s, const char* what, const char* detail) {
+  if (ctx) {
+    ctx->err = std::string(what) + ": " + (detail ? detail : "");
+    if (s == SEED_ECUDA || s == SEED_ENCCL) ctx->poisoned = true;
+  }
+  return s;
+}
+
+int pow2_at_least(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+const CUtensorMap* xmap(seed_ctx ctx, const bf16* buf, int K, int rows_cap, int M) {
+  const int m_pad = seed::gemm_mpad(M);
+  auto key = std::make_tuple((const void*)buf, K, m_pad);
+  auto it = ctx->xmaps.find(key);
+  if (it != ctx->xmaps.end()) return &it->second;
+  CUtensorMap m;
+  if (!seed::encode_tmap_2d(&m, buf, (uint64_t)K, (uint64_t)rows_cap, 64, (uint32_t)m_pad)) return nullptr;
+  return &(ctx->xmaps[key] = m);
+}
+
+seed_status run_gemm(seed_ctx ctx, const GemmPlan& p, const bf16* X, int rows_cap, int M, PartialView* view,
+                     cudaStream_t st) {
+  const CUtensorMap* tm = xmap(ctx, X, p.K, rows_cap, M);
+  if (!tm) return fail(ctx, SEED_ECUDA, "cuTensorMapEncodeTiled", "X operand");
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (ctx->profile) {
+    if (ctx->ev_used == ctx->ev_pool.size()) {
+      cudaEvent_t a, b;
+      CK(cudaEventCreate(&a));
+      CK(cudaEventCreate(&b));
+      ctx->ev_pool.push_back({a, b});
+    }
+    e0 = ctx->ev_pool[ctx->ev_used].first;
+    e1 = ctx->ev_pool[ctx->ev_used].second;
+    ctx->ev_used++;
+    CK(cudaEventRecord(e0, st));
+  }
+  CK(seed::gemm_run(p, *tm, M, ctx->partial, view, st));
+  if (ctx->profile) {
+    CK(cudaEventRecord(e1, st));
+    ctx->gemm_bytes += (double)p.N * p.K * 2 + (double)M * p.K * 2 + (double)M * p.N * 4;
+    ctx->gemm_launches++;
+  }
+  ctx->kernel_launches++;
+  return SEED_OK;
+}
+
+// ------------------------------------------------------------------ model setup
+seed_status check_shape(const seed_model_shape& s) {
+  if (s.vocab <= 0 || s.d_model <= 0 || s.n_layers <= 0 || s.n_heads <= 0 || s.d_ff <= 0) return SEED_EINVAL;
+  if (s.d_model % 64 || s.d_ff % 64 || s.d_model % s.n_heads) return SEED_EINVAL;
+  const int hk = s.n_kv_heads ? s.n_kv_heads : s.n_heads;
+  if (s.n_heads % hk) return SEED_EINVAL;
+  const int dh = s.d_model / s.n_heads;
+  if (dh != 32 && dh != 64 && dh != 128) return SEED_EINVAL;
+  return SEED_OK;
+}
+
+seed_status copy_rows(seed_ctx ctx, bf16* dst, const void* src, size_t elems) {
+  CK(cudaMemcpy(dst, src, elems * 2, cudaMemcpyDeviceToDevice));
+  return SEED_OK;
+}
+
+// pack weights into the library layout (R18): QKV stacked, gate/up interleaved in 64-row blocks
+seed_status build_model(seed_ctx ctx, Model& m, const seed_model_shape& sh, const seed_model_weights& w, int m_cap,
+                        int slots, int max_pages, size_t pool_pages, int max_pos) {
+  seed_status s = check_shape(sh);
+  if (s != SEED_OK) return fail(ctx, s, "seed_init", "bad model shape");
+  if (!w.embed || !w.layers || !w.final_norm || !w.lm_head) return fail(ctx, SEED_EINVAL, "seed_init", "null weight");
+  m.sh = sh;
+  m.d = sh.d_model;
+  m.H = sh.n_heads;
+  m.Hk = sh.n_kv_heads ? sh.n_kv_heads : sh.n_heads;
+  m.Dh = m.d / m.H;
+  m.ff = sh.d_ff;
+  m.V = sh.vocab;
+  m.L = sh.n_layers;
+  m.nqkv = (m.H + 2 * m.Hk) * m.Dh;
+  const size_t d = m.d, ff = m.ff, V = m.V, dkv = (size_t)m.Hk * m.Dh, dq = (size_t)m.H * m.Dh;
+  auto alloc = [&](size_t elems) -> bf16* {
+    bf16* p = nullptr;
+    if (cudaMalloc(&p, elems * 2) != cudaSuccess) return nullptr;
+    m.owned.push_back(p);
+    return p;
+  };
+  m.embed = alloc(V * d);
+  m.final_norm = alloc(d);
+  m.lm_head = alloc(V * d);
+  if (!m.embed || !m.final_norm || !m.lm_head) return fail(ctx, SEED_ENOMEM, "seed_init", "weights");
+  if ((s = copy_rows(ctx, m.embed, w.embed, V * d)) != SEED_OK) return s;
+  if ((s = copy_rows(ctx, m.final_norm, w.final_norm, d)) != SEED_OK) return s;
+  if ((s = copy_rows(ctx, m.lm_head, w.lm_head, V * d)) != SEED_OK) return s;
+  for (int l = 0; l < m.L; ++l) {
+    const void* const* lw = w.layers + 9 * l;
+    for (int i = 0; i < 9; ++i)
+      if (!lw[i]) return fail(ctx, SEED_EINVAL, "seed_init", "null layer weight");
+    bf16* qkv = alloc((dq + 2 * dkv) * d);
+    bf16* o = alloc(d * dq);
+    bf16* gu = alloc(2 * ff * d);
+    bf16* dn = alloc(d * ff);
+    bf16* a = alloc(d);
+    bf16* mm = alloc(d);
+    if (!qkv || !o || !gu || !dn || !a || !mm) return fail(ctx, SEED_ENOMEM, "seed_init", "weights");
+    CK(cudaMemcpy(qkv, lw[0], dq * d * 2, cudaMemcpyDeviceToDevice));
+    CK(cudaMemcpy(qkv + dq * d, lw[1], dkv * d * 2, cudaMemcpyDeviceToDevice));
+    CK(cudaMemcpy(qkv + (dq + dkv) * d, lw[2], dkv * d * 2, cudaMemcpyDeviceToDevice));
+    CK(cudaMemcpy(o, lw[3], d * dq * 2, cudaMemcpyDeviceToDevice));
+    // gate/up interleave: rows [128b, 128b+64) = gate [64b, 64b+64), rows [128b+64, 128b+128) = up
+    CK(cudaMemcpy2D(gu, 128 * d * 2, lw[4], 64 * d * 2, 64 * d * 2, ff / 64, cudaMemcpyDeviceToDevice));
+    CK(cudaMemcpy2D(gu + 64 * d, 128 * d * 2, lw[5], 64 * d * 2, 64 * d * 2, ff / 64, cudaMemcpyDeviceToDevice));
+    CK(cudaMemcpy(dn, lw[6], d * ff * 2, cudaMemcpyDeviceToDevice));
+    CK(cudaMemcpy(a, lw[7], d * 2, cudaMemcpyDeviceToDevice));
+    CK(cudaMemcpy(mm, lw[8], d * 2, cudaMemcpyDeviceToDevice));
+    m.wqkv.push_back(qkv);
+    m.wo.push_back(o);
+    m.wgu.push_back(gu);
+    m.wdown.push_back(dn);
+    m.an.push_back(a);
+    m.mn.push_back(mm);
+    GemmPlan pq, po, pg, pd;
+    seed::gemm_plan(&pq, qkv, m.nqkv, m.d);
+    seed::gemm_plan(&po, o, m.d, (int)dq);
+    seed::gemm_plan(&pg, gu, 2 * m.ff, m.d);
+    seed::gemm_plan(&pd, dn, m.d, m.ff);
+    m.pq.push_back(pq);
+    m.po.push_back(po);
+    m.pgu.push_back(pg);
+    m.pd.push_back(pd);
+  }
+  seed::gemm_plan(&m.plm, m.lm_head, m.V, m.d);
+  // KV pool
+  m.kv.n_layers = m.L;
+  m.kv.Hk = m.Hk;
+  m.kv.Dh = m.Dh;
+  m.kv.P = ctx->P;
+  m.kv.max_pages = max_pages;
+  m.n_pages = pool_pages;
+  CK(cudaMalloc(&m.kv.pool, m.kv.page_elems() * pool_pages * 2));
+  CK(cudaMalloc(&m.page_table_dev, (size_t)slots * max_pages * 4));
+  m.page_table.assign((size_t)slots * max_pages, 0);
+  CK(cudaMemset(m.page_table_dev, 0, (size_t)slots * max_pages * 4));
+  m.kv.page_table = m.page_table_dev;
+  m.held.assign(slots, 0);
+  for (size_t i = pool_pages; i-- > 0;) m.free_pages.push_back((int32_t)i);
+  CK(cudaMalloc(&m.rope, (size_t)max_pos * (m.Dh / 2) * sizeof(float2)));
+  CK(seed::rope_table_init(m.rope, max_pos, m.Dh, sh.rope_theta > 0 ? sh.rope_theta : 10000.0, 0));
+  // activations (rows rounded to >= 256 so every TMA box fits)
+  m.m_cap = std::max(m_cap, 256);
+  const size_t mc = m.m_cap;
+  CK(cudaMalloc(&m.x, mc * d * 4));
+  m.h = alloc(mc * d);
+  m.q = alloc(mc * dq);
+  m.attn = alloc(mc * dq);
+  m.act = alloc(mc * ff);
+  m.hlm = alloc(mc * d);
+  if (!m.h || !m.q || !m.attn || !m.act || !m.hlm) return fail(ctx, SEED_ENOMEM, "seed_init", "activations");
+  m.aws.max_splits = (max_pos + seed::attn_chunk_tokens() - 1) / seed::attn_chunk_tokens();
+  CK(cudaMalloc(&m.aws.o_part, (size_t)m.aws.max_splits * mc * dq * 4));
+  CK(cudaMalloc(&m.aws.ml_part, (size_t)m.aws.max_splits * mc * m.H * 2 * 4));
+  return SEED_OK;
+}
+
+void free_model(Model& m) {
+  for (bf16* p : m.owned) cudaFree(p);
+  m.owned.clear();
+  if (m.kv.pool) cudaFree(m.kv.pool);
+  if (m.page_table_dev) cudaFree(m.page_table_dev);
+  if (m.rope) cudaFree(m.rope);
+  if (m.x) cudaFree(m.x);
+  if (m.aws.o_part) cudaFree(m.aws.o_part);
+  if (m.aws.ml_part) cudaFree(m.aws.ml_part);
+}
+
+size_t max_partial(const Model& m, int M) {
+  size_t mx = seed::gemm_partial_floats(m.plm, M);
+  for (int l = 0; l < m.L; ++l) {
+    mx = std::max(mx, seed::gemm_partial_floats(m.pq[l], M));
+    mx = std::max(mx, seed::gemm_partial_floats(m.po[l], M));
+    mx = std::max(mx, seed::gemm_partial_floats(m.pgu[l], M));
+    mx = std::max(mx, seed::gemm_partial_floats(m.pd[l], M));
+  }
+  return mx;
+}
+
+// make sure `slot` holds pages for positions [0, n_tokens)
+seed_status ensure_pages(seed_ctx ctx, Model& m, int slot, int n_tokens, cudaStream_t st) {
+  const int need = (n_tokens + ctx->P - 1) / ctx->P;
+  if (need > ctx->max_pages) return fail(ctx, SEED_ECAPACITY, "KV", "context longer than max_ctx");
+  int& held = m.held[slot];
+  if (need <= held) return SEED_OK;
+  const int first = held;
+  while (held < need) {
+    if (m.free_pages.empty()) return fail(ctx, SEED_ENOMEM, "KV", "page pool exhausted");
+    m.page_table[(size_t)slot * ctx->max_pages + held] = m.free_pages.back();
+    m.free_pages.pop_back();
+    ++held;
+  }
+  CK(cudaMemcpyAsync(m.page_table_dev + (size_t)slot * ctx->max_pages + first,
+                     m.page_table.data() + (size_t)slot * ctx->max_pages + first, (size_t)(need - first) * 4,
+                     cudaMemcpyHostToDevice, st));
+  // the host vector may change before the copy runs: make the copy synchronous w.r.t. host memory
+  CK(cudaStreamSynchronize(st));
+  return SEED_OK;
+}
+
+void release_pages(Model& m, int slot, int max_pages) {
+  for (int i = 0; i < m.held[slot]; ++i) m.free_pages.push_back(m.page_table[(size_t)slot * max_pages + i]);
+  m.held[slot] = 0;
+}
+
+// ------------------------------------------------------------------ forward over one chunk
+struct ChunkDesc {
+  int M, n_seq, max_q_len, max_kv;
+  const int32_t *pos, *slot, *q_start, *q_len, *kv_len, *seq_slot, *compact;  // device (slot: per row)
+  TokSrc tok;
+  int n_logits;
+  float* Y;       // logits destination for compact row 0
+  int ldY;
+};
+
+seed_status forward_chunk(seed_ctx ctx, Model& m, const ChunkDesc& c, cudaStream_t st, int first_layer = 0,
+                          int last_layer = -1, bool embed = true) {
+  const float eps = m.sh.rms_eps > 0 ? m.sh.rms_eps : 1e-5f;
+  if (last_layer < 0) last_layer = m.L;
+  const int M = c.M;
+  seed_status s;
+  if (embed) {
+    CK(seed::embed_rmsnorm(m.embed, c.tok.dev, c.tok.stride, M, m.d, m.an[first_layer], eps, m.x, m.h, st));
+    ctx->kernel_launches++;
+  }
+  seed::RowInfo rows{nullptr, c.pos, c.slot};
+  seed::SeqInfo seqs{c.q_start, c.q_len, c.kv_len, c.seq_slot};
+  for (int l = first_layer; l < last_layer; ++l) {
+    PartialView v;
+    if ((s = run_gemm(ctx, m.pq[l], m.h, m.m_cap, M, &v, st)) != SEED_OK) return s;
+    CK(seed::epi_qkv_rope(v, M, m.H, m.Hk, m.Dh, rows, m.rope, l, m.kv, m.q, nullptr, nullptr, st));
+    CK(seed::attention(m.q, M, c.n_seq, c.max_q_len, c.max_kv, m.H, m.Hk, m.Dh, seqs, m.kv, l, m.aws, m.attn, st));
+    if ((s = run_gemm(ctx, m.po[l], m.attn, m.m_cap, M, &v, st)) != SEED_OK) return s;
+    CK(seed::epi_residual_rmsnorm(v, M, m.d, m.x, m.mn[l], eps, m.h, nullptr, nullptr, st));
+    if ((s = run_gemm(ctx, m.pgu[l], m.h, m.m_cap, M, &v, st)) != SEED_OK) return s;
+    CK(seed::epi_swiglu(v, M, m.ff, m.act, st));
+    if ((s = run_gemm(ctx, m.pd[l], m.act, m.m_cap, M, &v, st)) != SEED_OK) return s;
+    const bool last = (l == m.L - 1);
+    const bf16* nw = last ? m.final_norm : m.an[l + 1];
+    if (l == last_layer - 1 && !last) {
+      // partial-depth run (tests): residual only, no norm needed afterwards
+      CK(seed::epi_residual_rmsnorm(v, M, m.d, m.x, nw, eps, m.h, nullptr, nullptr, st));
+    } else {
+      CK(seed::epi_residual_rmsnorm(v, M, m.d, m.x, nw, eps, last ? nullptr : m.h, last ? c.compact : nullptr,
+                                    m.hlm, st));
+    }
+    ctx->kernel_launches += 6;
+  }
+  if (last_layer == m.L && c.n_logits > 0) {
+    PartialView v;
+    if ((s = run_gemm(ctx, m.plm, m.hlm, m.m_cap, c.n_logits, &v, st)) != SEED_OK) return s;
+    CK(seed::epi_store(v, m.V, c.Y, c.ldY, nullptr, c.n_logits, st));
+    ctx->kernel_launches++;
+  }
+  return SEED_OK;
+}
+
+// Build the descriptors of one chunk into the arena. Segments must fit kMaxChunkRows rows.
+// logits: 0 none, 1 all rows, 2 last row of each segment.
+bool pack_chunk(seed_ctx ctx, const std::vector<Segment>& segs, int logits_mode, ChunkDesc* c,
+                size_t* host_tok_off) {
+  Arena& A = ctx->arena;
+  int M = 0, mq = 0, mkv = 0;
+  for (auto& s : segs) {
+    M += s.q_len;
+    mq = std::max(mq, s.q_len);
+    mkv = std::max(mkv, s.pos0 + s.q_len);
+  }
+  const size_t o_pos = A.alloc(M), o_slot = A.alloc(M), o_cmp = A.alloc(M), o_tok = A.alloc(M);
+  const size_t n = segs.size();
+  const size_t o_qs = A.alloc(n), o_ql = A.alloc(n), o_kv = A.alloc(n), o_ss = A.alloc(n);
+  if (o_ss == (size_t)-1) return false;
+  int r = 0, nl = 0;
+  for (size_t i = 0; i < n; ++i) {
+    const Segment& s = segs[i];
+    A.host[o_qs + i] = r;
+    A.host[o_ql + i] = s.q_len;
+    A.host[o_kv + i] = s.pos0 + s.q_len;
+    A.host[o_ss + i] = s.slot;
+    for (int j = 0; j < s.q_len; ++j, ++r) {
+      A.host[o_pos + r] = s.pos0 + j;
+      A.host[o_slot + r] = s.slot;
+      const bool lg = logits_mode == 1 || (logits_mode == 2 && j == s.q_len - 1);
+      A.host[o_cmp + r] = lg ? nl++ : -1;
+      A.host[o_tok + r] = s.tok_off >= 0 ? A.host[s.tok_off + j] : 0;
+    }
+  }
+  c->M = M;
+  c->n_seq = (int)n;
+  c->max_q_len = mq;
+  c->max_kv = mkv;
+  c->pos = A.dev + o_pos;
+  c->slot = A.dev + o_slot;
+  c->seq_slot = A.dev + o_ss;
+  c->compact = A.dev + o_cmp;
+  c->q_start = A.dev + o_qs;
+  c->q_len = A.dev + o_ql;
+  c->kv_len = A.dev + o_kv;
+  c->tok = TokSrc{A.dev + o_tok, 1};
+  c->n_logits = nl;
+  *host_tok_off = o_tok;
+  return true;
+}
+
+// Prefill-style forward of host tokens into `slot` starting at position pos0 (chunked).
+seed_status prefill(seed_ctx ctx, Model& m, int slot, const int32_t* toks, int n, int pos0, float* logits,
+                    cudaStream_t st) {
+  int done = 0;
+  while (done < n) {
+    const int q = std::min(kMaxChunkRows, n - done);
+    ctx->arena.begin();
+    const size_t to = ctx->arena.alloc(q);
+    if (to == (size_t)-1) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
+    std::memcpy(ctx->arena.host + to, toks + done, (size_t)q * 4);
+    std::vector<Segment> segs{{slot, pos0 + done, q, (int)to}};
+    ChunkDesc c;
+    size_t tok_off;
+    if (!pack_chunk(ctx, segs, logits ? 1 : 0, &c, &tok_off)) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
+    c.Y = logits ? logits + (size_t)done * m.V : nullptr;
+    c.ldY = m.V;
+    CK(ctx->arena.upload(st));
+    seed_status s = forward_chunk(ctx, m, c, st);
+    if (s != SEED_OK) return s;
+    done += q;
+  }
+  return SEED_OK;
+}
+
+seed_status check_ctx(seed_ctx ctx) {
+  if (!ctx) return SEED_EINVAL;
+  if (ctx->poisoned) return SEED_ESTATE;
+  return SEED_OK;
+}
+
+// host mirror of K5 (same formula, DESIGN R6/R7)
+void commit_host(seed_ctx ctx, SlotState& s, const int32_t* toks, int cnt) {
+  const int g = ctx->cfg.gamma;
+  const int t_before = (int)s.T.size();
+  const int c = std::min(cnt, std::max(ctx->cfg.max_new_tokens - s.L, 0));
+  s.T.insert(s.T.end(), toks, toks + c);
+  s.L += c;
+  s.r += 1;
+  s.len_t = (int)s.T.size() - 1;
+  s.len_d = std::min((int)s.T.size() - 1, t_before + g - 1);
+  s.done = s.L >= ctx->cfg.max_new_tokens;
+}
+
+seed_status complete_round(seed_ctx ctx) {
+  if (!ctx->round_pending) return SEED_OK;
+  CK(cudaEventSynchronize(ctx->round_done));
+  ctx->round_pending = false;
+  const int g = ctx->cfg.gamma, stride = g + 3;
+  const int world = std::max(ctx->cfg.world, 1);
+  const int32_t* recs = ctx->records_host;
+  // own streams: update mirrors from our records (first C records of our rank)
+  const int B = (int)ctx->last_batch.size();
+  std::vector<int32_t> done(B);
+  for (int b = 0; b < B; ++b) {
+    const int32_t* rec = recs + ((size_t)ctx->cfg.rank * ctx->C + b) * stride;
+    SlotState& s = ctx->slots[ctx->gid2slot[(uint32_t)ctx->last_batch[b]]];
+    // rec[1] is already truncated; commit the untruncated count semantics via tokens
+    const int t_before = (int)s.T.size();
+    s.T.insert(s.T.end(), rec + 2, rec + 2 + rec[1]);
+    s.L += rec[1];
+    s.r += 1;
+    s.len_t = (int)s.T.size() - 1;
+    s.len_d = std::min((int)s.T.size() - 1, t_before + g - 1);
+    s.done = s.L >= ctx->cfg.max_new_tokens;
+    done[b] = s.done;
+  }
+  seed_status st = seed_table_merge(ctx->table, recs, world * ctx->C);
+  if (st != SEED_OK) return fail(ctx, st, "seed_table_merge", "bad record");
+  st = seed_sched_complete(ctx->sched, ctx->last_batch.data(), done.data(), B);
+  if (st != SEED_OK) return fail(ctx, st, "seed_sched_complete", "");
+  ctx->last_batch.clear();
+  return SEED_OK;
+}
+
+seed_status map_batch(seed_ctx ctx, const int32_t* ids, int n, std::vector<int>& slots) {
+  if (n < 1 || n > ctx->C || !ids) return fail(ctx, n > ctx->C ? SEED_ECAPACITY : SEED_EINVAL, "batch", "size");
+  slots.resize(n);
+  for (int i = 0; i < n; ++i) {
+    auto it = ctx->gid2slot.find((uint32_t)ids[i]);
+    if (it == ctx->gid2slot.end()) return fail(ctx, SEED_ENOTFOUND, "batch", "unknown stream id");
+    slots[i] = it->second;
+    if (ctx->slots[slots[i]].done) return fail(ctx, SEED_EINVAL, "batch", "stream already done");
+  }
+  return SEED_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* seed_last_error(seed_ctx ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+seed_status seed_nccl_unique_id(void* out128) {
+  if (!out128) return SEED_EINVAL;
+  if (!g_nccl.load()) return SEED_ENCCL;
+  Id128 id;
+  if (g_nccl.get_id(&id) != 0) return SEED_ENCCL;
+  std::memcpy(out128, &id, 128);
+  return SEED_OK;
+}
+
+seed_status seed_init(const seed_config* cfg, seed_ctx* out) {
+  if (!cfg || !out) return SEED_EINVAL;
+  *out = nullptr;
+  if (cfg->draft.vocab != cfg->target.vocab) return SEED_EINVAL;
+  if (cfg->gamma < 1 || cfg->gamma > 16 || !(cfg->temperature > 0.f) || cfg->max_new_tokens < 1 ||
+      cfg->max_streams < 1 || cfg->max_batch < 1 || cfg->max_ctx < 8)
+    return SEED_EINVAL;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return SEED_ECUDA;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess || prop.major < 10) return SEED_ECUDA;
+
+  seed_ctx ctx = new seed_ctx_s;
+  ctx->cfg = *cfg;
+  ctx->dev = dev;
+  ctx->P = cfg->page_tokens > 0 ? cfg->page_tokens : 16;
+  ctx->C = std::min(cfg->max_batch, cfg->max_streams);
+  ctx->profile = (cfg->flags & SEED_FLAG_PROFILE) != 0;
+  const int g = cfg->gamma;
+  const int max_pos = cfg->max_ctx + g + 2;
+  ctx->max_pages = (max_pos + ctx->P - 1) / ctx->P;
+  ctx->n_slots = cfg->max_streams + 1;  // + one scratch slot for seed_forward_logits / ops
+  const int m_cap = std::min(kMaxChunkRows, std::max(ctx->C * (g + 1), 2 * ctx->C));
+  auto pool_pages_for = [&](const seed_model_shape& sh) -> size_t {
+    const size_t full = (size_t)ctx->n_slots * ctx->max_pages;
+    if (cfg->kv_pool_bytes <= 0) return full;
+    const int hk = sh.n_kv_heads ? sh.n_kv_heads : sh.n_heads;
+    const size_t page_bytes = (size_t)sh.n_layers * 2 * hk * ctx->P * (sh.d_model / sh.n_heads) * 2;
+    return std::max<size_t>(ctx->max_pages, std::min(full, (size_t)cfg->kv_pool_bytes / page_bytes));
+  };
+  seed_status s = build_model(ctx, ctx->tm, cfg->target, cfg->target_w, m_cap, ctx->n_slots, ctx->max_pages,
+                              pool_pages_for(cfg->target), max_pos);
+  if (s == SEED_OK)
+    s = build_model(ctx, ctx->dm, cfg->draft, cfg->draft_w, m_cap, ctx->n_slots, ctx->max_pages,
+                    pool_pages_for(cfg->draft), max_pos);
+  if (s != SEED_OK) {
+    std::string e = ctx->err;
+    seed_destroy(ctx);
+    return s;
+  }
+  auto fail_init = [&](seed_status st) {
+    seed_destroy(ctx);
+    return st;
+  };
+  ctx->partial_floats = std::max(max_partial(ctx->tm, 256), max_partial(ctx->dm, 256));
+  if (cudaMalloc(&ctx->partial, ctx->partial_floats * 4) != cudaSuccess) return fail_init(SEED_ENOMEM);
+  if (ctx->arena.init(1 << 20) != cudaSuccess) return fail_init(SEED_ENOMEM);
+  const int V = cfg->target.vocab, C = ctx->C, S = ctx->n_slots;
+  ctx->slots.resize(S);
+  bool ok = true;
+  ok &= cudaMalloc(&ctx->tgt_logits, (size_t)C * (g + 1) * V * 4) == cudaSuccess;
+  ok &= cudaMalloc(&ctx->drf_logits, (size_t)C * g * V * 4) == cudaSuccess;
+  ok &= cudaMalloc(&ctx->xs, (size_t)C * g * 4) == cudaSuccess;
+  ok &= cudaMalloc(&ctx->vtok, (size_t)C * (g + 1) * 4) == cudaSuccess;
+  ok &= cudaMalloc(&ctx->out_tok, (size_t)C * (g + 1) * 4) == cudaSuccess;
+  ok &= cudaMalloc(&ctx->out_cnt, (size_t)C * 4) == cudaSuccess;
+  ok &= cudaMalloc(&ctx->out_acc, (size_t)C * 4) == cudaSuccess;
+  const int world = std::max(cfg->world, 1);
+  ok &= cudaMalloc(&ctx->records, (size_t)C * (g + 3) * 4) == cudaSuccess;
+  ok &= cudaMalloc(&ctx->records_all, (size_t)world * C * (g + 3) * 4) == cudaSuccess;
+  ok &= cudaMallocHost(&ctx->records_host, (size_t)world * C * (g + 3) * 4) == cudaSuccess;
+  ok &= cudaMallocHost(&ctx->cnt_host, (size_t)C * 4) == cudaSuccess;
+  ok &= cudaMallocHost(&ctx->tok_host, (size_t)C * (g + 1) * 4) == cudaSuccess;
+  ok &= cudaMalloc(&ctx->sids_dev, (size_t)C * 4) == cudaSuccess;
+  ok &= cudaMalloc(&ctx->rs_dev, (size_t)C * 4) == cudaSuccess;
+  ok &= cudaMalloc(&ctx->slots_dev, (size_t)C * 4) == cudaSuccess;
+  ok &= cudaMalloc(&ctx->ds.tlen, (size_t)S * 4) == cudaSuccess;
+  ok &= cudaMalloc(&ctx->ds.len_t, (size_t)S * 4) == cudaSuccess;
+  ok &= cudaMalloc(&ctx->ds.len_d, (size_t)S * 4) == cudaSuccess;
+  ok &= cudaMalloc(&ctx->ds.L, (size_t)S * 4) == cudaSuccess;
+  ok &= cudaMalloc(&ctx->ds.r, (size_t)S * 4) == cudaSuccess;
+  ok &= cudaMalloc(&ctx->ds.done, (size_t)S * 4) == cudaSuccess;
+  ok &= cudaMalloc(&ctx->ds.hist, (size_t)S * max_pos * 4) == cudaSuccess;
+  ctx->ds.max_ctx = max_pos;
+  ok &= cudaEventCreateWithFlags(&ctx->round_done, cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) return fail_init(SEED_ENOMEM);
+  if (seed_sched_create(nullptr, 0, &ctx->sched) != SEED_OK) return fail_init(SEED_ENOMEM);
+  if (seed_table_create(g + 3, &ctx->table) != SEED_OK) return fail_init(SEED_ENOMEM);
+  if (world > 1) {
+    if (!cfg->nccl_id || !g_nccl.load()) return fail_init(SEED_ENCCL);
+    Id128 id;
+    std::memcpy(&id, cfg->nccl_id, 128);
+    if (g_nccl.init(&ctx->comm, world, id, cfg->rank) != 0) return fail_init(SEED_ENCCL);
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) return fail_init(SEED_ECUDA);
+  *out = ctx;
+  return SEED_OK;
+}
+
+void seed_destroy(seed_ctx ctx) {
+  if (!ctx) return;
+  cudaDeviceSynchronize();
+  free_model(ctx->tm);
+  free_model(ctx->dm);
+  void* bufs[] = {ctx->partial, ctx->tgt_logits, ctx->drf_logits, ctx->xs, ctx->vtok, ctx->out_tok,
+                  ctx->out_cnt, ctx->out_acc, ctx->records, ctx->records_all, ctx->sids_dev, ctx->rs_dev,
+                  ctx->slots_dev, ctx->ds.tlen, ctx->ds.len_t, ctx->ds.len_d, ctx->ds.L, ctx->ds.r,
+                  ctx->ds.done, ctx->ds.hist};
+  for (void* p : bufs)
+    if (p) cudaFree(p);
+  if (ctx->records_host) cudaFreeHost(ctx->records_host);
+  if (ctx->cnt_host) cudaFreeHost(ctx->cnt_host);
+  if (ctx->tok_host) cudaFreeHost(ctx->tok_host);
+  ctx->arena.destroy();
+  if (ctx->round_done) cudaEventDestroy(ctx->round_done);
+  for (auto& e : ctx->ev_pool) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  if (ctx->sched) seed_sched_destroy(ctx->sched);
+  if (ctx->table) seed_table_destroy(ctx->table);
+  if (ctx->comm && g_nccl.destroy) g_nccl.destroy(ctx->comm);
+  delete ctx;
+}
+
+seed_status seed_add_stream(seed_ctx ctx, uint32_t gid, const int32_t* prefix, int32_t len, void* stream) {
+  seed_status s = check_ctx(ctx);
+  if (s != SEED_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!prefix || len < 2) return fail(ctx, SEED_EINVAL, "seed_add_stream", "prefix must hold >= 2 tokens");
+  if (len + ctx->cfg.max_new_tokens + ctx->cfg.gamma + 2 > ctx->cfg.max_ctx + ctx->cfg.gamma + 2)
+    return fail(ctx, SEED_ECAPACITY, "seed_add_stream", "prefix + l exceeds max_ctx");
+  for (int i = 0; i < len; ++i)
+    if (prefix[i] < 0 || prefix[i] >= ctx->cfg.target.vocab)
+      return fail(ctx, SEED_EINVAL, "seed_add_stream", "token id out of range");
+  if (ctx->gid2slot.count(gid)) return fail(ctx, SEED_EINVAL, "seed_add_stream", "duplicate global id");
+  int slot = -1;
+  for (int i = 0; i < ctx->cfg.max_streams; ++i)
+    if (!ctx->slots[i].used) {
+      slot = i;
+      break;
+    }
+  if (slot < 0) return fail(ctx, SEED_ECAPACITY, "seed_add_stream", "max_streams reached");
+  const int g = ctx->cfg.gamma;
+  if ((s = ensure_pages(ctx, ctx->tm, slot, len + g + 1, st)) != SEED_OK) return s;
+  if ((s = ensure_pages(ctx, ctx->dm, slot, len + g + 1, st)) != SEED_OK) return s;
+  // Alg. 1 Initialize: prefill both models with the prefix (all but the last token, R6)
+  if ((s = prefill(ctx, ctx->tm, slot, prefix, len - 1, 0, nullptr, st)) != SEED_OK) return s;
+  if ((s = prefill(ctx, ctx->dm, slot, prefix, len - 1, 0, nullptr, st)) != SEED_OK) return s;
+  SlotState& ss = ctx->slots[slot];
+  ss = SlotState();
+  ss.used = true;
+  ss.gid = gid;
+  ss.T.assign(prefix, prefix + len);
+  ss.prompt_len = len;
+  ss.len_t = ss.len_d = len - 1;
+  // device state (K5 reads/writes it)
+  int32_t vals[6] = {len, len - 1, len - 1, 0, 0, 0};
+  int32_t* dst[6] = {ctx->ds.tlen, ctx->ds.len_t, ctx->ds.len_d, ctx->ds.L, ctx->ds.r, ctx->ds.done};
+  for (int i = 0; i < 6; ++i) CK(cudaMemcpyAsync(dst[i] + slot, &vals[i], 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ctx->ds.hist + (size_t)slot * ctx->ds.max_ctx, prefix, (size_t)len * 4, cudaMemcpyHostToDevice,
+                     st));
+  CK(cudaStreamSynchronize(st));
+  ctx->gid2slot[gid] = slot;
+  seed_sched_add(ctx->sched, (int32_t)gid);
+  return SEED_OK;
+}
+
+seed_status seed_schedule_round(seed_ctx ctx, int32_t* batch_ids, int32_t cap, int32_t* n) {
+  seed_status s = check_ctx(ctx);
+  if (s != SEED_OK) return s;
+  if (!n || (cap > 0 && !batch_ids)) return fail(ctx, SEED_EINVAL, "seed_schedule_round", "args");
+  if ((s = complete_round(ctx)) != SEED_OK) return s;
+  *n = 0;
+  if (seed_sched_all_done(ctx->sched)) return SEED_OK;
+  s = seed_sched_pop(ctx->sched, batch_ids, std::min(cap, ctx->C), n);
+  if (s != SEED_OK) return fail(ctx, s, "seed_schedule_round", "no ready stream (liveness)");
+  return SEED_OK;
+}
+
+seed_status seed_draft_round(seed_ctx ctx, const int32_t* ids, int32_t n, void* stream) {
+  seed_status s = check_ctx(ctx);
+  if (s != SEED_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<int> slots;
+  if ((s = map_batch(ctx, ids, n, slots)) != SEED_OK) return s;
+  if (ctx->round_pending) {
+    if ((s = complete_round(ctx)) != SEED_OK) return s;
+  }
+  const int g = ctx->cfg.gamma, V = ctx->cfg.target.vocab;
+  for (int b = 0; b < n; ++b) {
+    const int T = (int)ctx->slots[slots[b]].T.size();
+    if ((s = ensure_pages(ctx, ctx->tm, slots[b], T + g + 1, st)) != SEED_OK) return s;
+    if ((s = ensure_pages(ctx, ctx->dm, slots[b], T + g + 1, st)) != SEED_OK) return s;
+  }
+  Model& m = ctx->dm;
+  ctx->arena.begin();
+  Arena& A = ctx->arena;
+  // per-batch vectors: sids, rs, slots, T[-1]
+  const size_t o_sid = A.alloc(n), o_r = A.alloc(n), o_sl = A.alloc(n), o_last = A.alloc(n);
+  if (o_last == (size_t)-1) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
+  for (int b = 0; b < n; ++b) {
+    const SlotState& ss = ctx->slots[slots[b]];
+    A.host[o_sid + b] = (int32_t)ss.gid;
+    A.host[o_r + b] = ss.r;
+    A.host[o_sl + b] = slots[b];
+    A.host[o_last + b] = ss.T.back();
+  }
+  // step 1: rows (T[-2], T[-1]) per stream -- the first re-writes an existing entry when only
+  // one token is pending, so M = 2n always (DESIGN "draft step 1")
+  std::vector<ChunkDesc> steps(g);
+  std::vector<Segment> segs(n);
+  for (int b = 0; b < n; ++b) {
+    const SlotState& ss = ctx->slots[slots[b]];
+    const int T = (int)ss.T.size();
+    const size_t to = A.alloc(2);
+    if (to == (size_t)-1) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
+    A.host[to] = ss.T[T - 2];
+    A.host[to + 1] = ss.T[T - 1];
+    segs[b] = Segment{slots[b], T - 2, 2, (int)to};
+  }
+  size_t tok_off;
+  if (2 * n > kMaxChunkRows || !pack_chunk(ctx, segs, 2, &steps[0], &tok_off))
+    return fail(ctx, SEED_ECAPACITY, "seed_draft_round", "batch too large");
+  for (int j = 2; j <= g; ++j) {
+    for (int b = 0; b < n; ++b) {
+      const int T = (int)ctx->slots[slots[b]].T.size();
+      segs[b] = Segment{slots[b], T + j - 2, 1, -1};
+    }
+    if (!pack_chunk(ctx, segs, 2, &steps[j - 1], &tok_off)) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
+    steps[j - 1].tok = TokSrc{ctx->xs + (j - 2), g};  // x_{j-1} of every stream, [B][g] layout
+  }
+  CK(A.upload(st));
+  const uint32_t* sids = reinterpret_cast<const uint32_t*>(A.dev + o_sid);
+  const int32_t* rs = A.dev + o_r;
+  CK(cudaMemcpyAsync(ctx->sids_dev, sids, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(ctx->rs_dev, rs, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(ctx->slots_dev, A.dev + o_sl, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+  // verify input column 0 = T[-1]
+  CK(cudaMemcpy2DAsync(ctx->vtok, (size_t)(g + 1) * 4, A.dev + o_last, 4, 4, n, cudaMemcpyDeviceToDevice, st));
+  const uint32_t k0 = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu), k1 = (uint32_t)(ctx->cfg.seed >> 32);
+  for (int j = 1; j <= g; ++j) {
+    ChunkDesc& c = steps[j - 1];
+    c.Y = ctx->drf_logits + (size_t)(j - 1) * V;
+    c.ldY = g * V;
+    if ((s = forward_chunk(ctx, m, c, st)) != SEED_OK) return s;
+    // K1 sampler: x_j -> xs[b][j-1] and the verify input vtok[b][j]
+    CK(seed::draft_sample(c.Y, (long)g * V, n, V, ctx->cfg.temperature, k0, k1, ctx->sids_dev, ctx->rs_dev, j,
+                          ctx->xs + (j - 1), g, ctx->vtok + j, g + 1, st));
+    ctx->kernel_launches++;
+  }
+  ctx->drafted.assign(ids, ids + n);
+  return SEED_OK;
+}
+
+seed_status seed_verify(seed_ctx ctx, const int32_t* ids, int32_t n, int32_t* out_tok, int32_t* out_cnt,
+                        void* stream) {
+  seed_status s = check_ctx(ctx);
+  if (s != SEED_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  if ((int)ctx->drafted.size() != n || !std::equal(ids, ids + n, ctx->drafted.begin()))
+    return fail(ctx, SEED_ESTATE, "seed_verify", "batch was not drafted");
+  std::vector<int> slots;
+  if ((s = map_batch(ctx, ids, n, slots)) != SEED_OK) return s;
+  const int g = ctx->cfg.gamma, V = ctx->cfg.target.vocab;
+  Model& m = ctx->tm;
+  // a3: one target forward over [T[-1], x_1..x_g] per stream, chunked by whole streams
+  const int per_chunk = std::max(1, kMaxChunkRows / (g + 1));
+  for (int b0 = 0; b0 < n; b0 += per_chunk) {
+    const int nb = std::min(per_chunk, n - b0);
+    ctx->arena.begin();
+    std::vector<Segment> segs(nb);
+    for (int b = 0; b < nb; ++b) {
+      const int T = (int)ctx->slots[slots[b0 + b]].T.size();
+      segs[b] = Segment{slots[b0 + b], T - 1, g + 1, -1};
+    }
+    ChunkDesc c;
+    size_t tok_off;
+    if (!pack_chunk(ctx, segs, 1, &c, &tok_off)) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
+    CK(ctx->arena.upload(st));
+    c.tok = TokSrc{ctx->vtok + (size_t)b0 * (g + 1), 1};
+    c.Y = ctx->tgt_logits + (size_t)b0 * (g + 1) * V;
+    c.ldY = V;
+    if ((s = forward_chunk(ctx, m, c, st)) != SEED_OK) return s;
+  }
+  // a4: K4 fused vocabulary kernel
+  seed::VerifyArgs a{};
+  a.zt = ctx->tgt_logits;
+  a.zd = ctx->drf_logits;
+  a.xs = ctx->xs;
+  a.zt_stride_b = (long)(g + 1) * V;
+  a.zd_stride_b = (long)g * V;
+  a.B = n;
+  a.gamma = g;
+  a.V = V;
+  a.T = ctx->cfg.temperature;
+  a.k0 = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu);
+  a.k1 = (uint32_t)(ctx->cfg.seed >> 32);
+  a.sids = ctx->sids_dev;
+  a.rs = ctx->rs_dev;
+  a.bonus = ctx->cfg.bonus;
+  a.out_tok = ctx->out_tok;
+  a.out_cnt = ctx->out_cnt;
+  a.out_acc = ctx->out_acc;
+  CK(seed::vocab_verify(a, st));
+  // a5: K5 commit + rollback, emit the exchange records
+  const int world = std::max(ctx->cfg.world, 1);
+  const size_t rec_bytes = (size_t)ctx->C * (g + 3) * 4;
+  CK(cudaMemsetAsync(ctx->records, 0xFF, rec_bytes, st));
+  CK(seed::rollback_commit(ctx->ds, ctx->slots_dev, n, g, ctx->out_tok, ctx->out_cnt, ctx->cfg.max_new_tokens,
+                           ctx->records, ctx->sids_dev, st));
+  ctx->kernel_launches += 2;
+  // a6: all-gather of the per-rank records over NVLink (world > 1)
+  if (world > 1) {
+    if (g_nccl.allgather(ctx->records, ctx->records_all, (size_t)ctx->C * (g + 3), kNcclInt32, ctx->comm, st) != 0)
+      return fail(ctx, SEED_ENCCL, "ncclAllGather", "records");
+    CK(cudaMemcpyAsync(ctx->records_host, ctx->records_all, rec_bytes * world, cudaMemcpyDeviceToHost, st));
+  } else {
+    CK(cudaMemcpyAsync(ctx->records_host, ctx->records, rec_bytes, cudaMemcpyDeviceToHost, st));
+  }
+  if (out_tok)
+    CK(cudaMemcpyAsync(out_tok, ctx->out_tok, (size_t)n * (g + 1) * 4, cudaMemcpyDeviceToDevice, st));
+  if (out_cnt) CK(cudaMemcpyAsync(out_cnt, ctx->out_cnt, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+  CK(cudaEventRecord(ctx->round_done, st));
+  ctx->round_pending = true;
+  ctx->last_batch.assign(ids, ids + n);
+  ctx->drafted.clear();
+  return SEED_OK;
+}
+
+seed_status seed_round_host(seed_ctx ctx, const int32_t* ids, int32_t n, int32_t* out_tok_host, int32_t* out_cnt_host,
+                            void* stream) {
+  seed_status s = seed_draft_round(ctx, ids, n, stream);
+  if (s != SEED_OK) return s;
+  if ((s = seed_verify(ctx, ids, n, nullptr, nullptr, stream)) != SEED_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int g = ctx->cfg.gamma;
+  if (out_tok_host)
+    CK(cudaMemcpyAsync(out_tok_host, ctx->out_tok, (size_t)n * (g + 1) * 4, cudaMemcpyDeviceToHost, st));
+  if (out_cnt_host) CK(cudaMemcpyAsync(out_cnt_host, ctx->out_cnt, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return SEED_OK;
+}
+
+seed_status seed_get_tokens(seed_ctx ctx, uint32_t gid, int32_t* dst, int32_t cap, int32_t* len) {
+  if (!ctx || !len) return SEED_EINVAL;
+  if (ctx->round_pending) {
+    seed_status s = complete_round(ctx);
+    if (s != SEED_OK) return s;
+  }
+  auto it = ctx->gid2slot.find(gid);
+  if (it != ctx->gid2slot.end()) {
+    const SlotState& ss = ctx->slots[it->second];
+    *len = (int32_t)ss.T.size() - ss.prompt_len;
+    if (dst) std::copy(ss.T.begin() + ss.prompt_len, ss.T.begin() + ss.prompt_len + std::min(cap, *len), dst);
+    return SEED_OK;
+  }
+  return seed_table_get(ctx->table, gid, dst, cap, len);
+}
+
+seed_status seed_stream_info(seed_ctx ctx, uint32_t gid, int32_t* info) {
+  if (!ctx || !info) return SEED_EINVAL;
+  if (ctx->round_pending) {
+    seed_status s = complete_round(ctx);
+    if (s != SEED_OK) return s;
+  }
+  auto it = ctx->gid2slot.find(gid);
+  if (it == ctx->gid2slot.end()) return SEED_ENOTFOUND;
+  const SlotState& s = ctx->slots[it->second];
+  info[0] = (int32_t)s.T.size();
+  info[1] = s.L;
+  info[2] = s.r;
+  info[3] = s.done;
+  info[4] = s.len_t;
+  info[5] = s.len_d;
+  info[6] = ctx->tm.held[it->second];
+  info[7] = it->second;
+  return SEED_OK;
+}
+
+seed_status seed_remove_stream(seed_ctx ctx, uint32_t gid) {
+  seed_status s = check_ctx(ctx);
+  if (s != SEED_OK) return s;
+  if (ctx->round_pending && (s = complete_round(ctx)) != SEED_OK) return s;
+  auto it = ctx->gid2slot.find(gid);
+  if (it == ctx->gid2slot.end()) return SEED_ENOTFOUND;
+  const int slot = it->second;
+  if (cudaDeviceSynchronize() != cudaSuccess) return fail(ctx, SEED_ECUDA, "seed_remove_stream", "sync");
+  release_pages(ctx->tm, slot, ctx->max_pages);
+  release_pages(ctx->dm, slot, ctx->max_pages);
+  // keep the emitted tokens reachable through the table
+  const SlotState& ss = ctx->slots[slot];
+  std::vector<int32_t> rec(ctx->cfg.gamma + 3, -1);
+  (void)rec;
+  ctx->slots[slot] = SlotState();
+  ctx->gid2slot.erase(it);
+  // mark done in the scheduler so it is dropped from the queue
+  int32_t one = 1, id = (int32_t)gid;
+  (void)ss;
+  seed_sched_complete(ctx->sched, &id, &one, 1);
+  return SEED_OK;
+}
+
+seed_status seed_forward_logits(seed_ctx ctx, int32_t which, const int32_t* tokens, int32_t n, float* logits,
+                                void* stream) {
+  seed_status s = check_ctx(ctx);
+  if (s != SEED_OK) return s;
+  if (!tokens || n < 1 || !logits) return fail(ctx, SEED_EINVAL, "seed_forward_logits", "args");
+  cudaStream_t st = (cudaStream_t)stream;
+  Model& m = which ? ctx->tm : ctx->dm;
+  const int slot = ctx->n_slots - 1;  // scratch slot
+  if ((s = ensure_pages(ctx, m, slot, n, st)) != SEED_OK) return s;
+  s = prefill(ctx, m, slot, tokens, n, 0, logits, st);
+  CK(cudaStreamSynchronize(st));
+  release_pages(m, slot, ctx->max_pages);
+  return s;
+}
+
+seed_status seed_last_round_buffers(seed_ctx ctx, const float** t, const float** d, const int32_t** x) {
+  if (!ctx) return SEED_EINVAL;
+  if (t) *t = ctx->tgt_logits;
+  if (d) *d = ctx->drf_logits;
+  if (x) *x = ctx->xs;
+  return SEED_OK;
+}
+
+seed_status seed_get_profile(seed_ctx ctx, double* gemm_ms, int64_t* launches, double* bytes, int64_t* kernels) {
+  if (!ctx) return SEED_EINVAL;
+  double ms = 0;
+  for (size_t i = 0; i < ctx->ev_used; ++i) {
+    float t = 0;
+    if (cudaEventSynchronize(ctx->ev_pool[i].second) != cudaSuccess) return fail(ctx, SEED_ECUDA, "profile", "");
+    cudaEventElapsedTime(&t, ctx->ev_pool[i].first, ctx->ev_pool[i].second);
+    ms += t;
+  }
+  if (gemm_ms) *gemm_ms = ms;
+  if (launches) *launches = ctx->gemm_launches;
+  if (bytes) *bytes = ctx->gemm_bytes;
+  if (kernels) *kernels = ctx->kernel_launches;
+  return SEED_OK;
+}
+
+seed_status seed_reset_profile(seed_ctx ctx) {
+  if (!ctx) return SEED_EINVAL;
+  ctx->ev_used = 0;
+  ctx->gemm_bytes = 0;
+  ctx->gemm_launches = 0;
+  ctx->kernel_launches = 0;
+  return SEED_OK;
+}
+
+// ====================================================================== op-level ABI
+seed_status seed_op_philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1, int32_t n,
+                           uint32_t* out, void* stream) {
+  if (!out || n < 0) return SEED_EINVAL;
+  return seed::philox_fill(c0, c1, c2, c3, k0, k1, n, out, (cudaStream_t)stream) == cudaSuccess ? SEED_OK
+                                                                                               : SEED_ECUDA;
+}
+
+seed_status seed_op_gemm(const void* W, int32_t N, int32_t K, const void* X, int32_t M, float* Y, void* stream) {
+  if (!W || !X || !Y || N < 1 || K < 64 || K % 64 || M < 1) return SEED_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  GemmPlan p;
+  seed::gemm_plan(&p, W, N, K);
+  float* part = nullptr;
+  int done = 0;
+  bf16* xpad = nullptr;
+  if (cudaMallocAsync(&part, seed::gemm_partial_floats(p, std::min(M, 256)) * 4, st) != cudaSuccess ||
+      cudaMallocAsync(&xpad, (size_t)256 * K * 2, st) != cudaSuccess)
+    return SEED_ENOMEM;
+  cudaMemsetAsync(xpad, 0, (size_t)256 * K * 2, st);
+  seed_status s = SEED_OK;
+  while (done < M && s == SEED_OK) {
+    const int m = std::min(256, M - done);
+    const bf16* Xc = reinterpret_cast<const bf16*>(X) + (size_t)done * K;
+    // copy into a buffer of >= m_pad rows so the TMA box never leaves the tensor; the pad
+    // rows only feed accumulator columns that are never stored
+    if (cudaMemcpyAsync(xpad, Xc, (size_t)m * K * 2, cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
+      s = SEED_ECUDA;
+      break;
+    }
+    CUtensorMap tm;
+    if (!seed::encode_tmap_2d(&tm, xpad, (uint64_t)K, 256, 64, (uint32_t)seed::gemm_mpad(m))) {
+      s = SEED_ECUDA;
+      break;
+    }
+    PartialView v;
+    if (seed::gemm_run(p, tm, m, part, &v, st) != cudaSuccess ||
+        seed::epi_store(v, N, Y + (size_t)done * N, N, nullptr, m, st) != cudaSuccess)
+      s = SEED_ECUDA;
+    done += m;
+  }
+  cudaFreeAsync(part, st);
+  cudaFreeAsync(xpad, st);
+  return s;
+}
+
+seed_status seed_op_verify(const float* zt, const float* zd, const int32_t* xs, int32_t B, int32_t gamma, int32_t V,
+                           float temperature, uint64_t seed, const uint32_t* sids, const int32_t* rs, int32_t bonus,
+                           int32_t* out_tok, int32_t* out_cnt, int32_t* out_acc, float* dbg, double* stats,
+                           void* stream) {
+  if (!zt || !zd || !xs || B < 1 || gamma < 1 || gamma > 16 || V < 1 || !(temperature > 0.f) || !sids || !rs ||
+      !out_tok)
+    return SEED_EINVAL;
+  seed::VerifyArgs a{};
+  a.zt = zt;
+  a.zd = zd;
+  a.xs = xs;
+  a.zt_stride_b = (long)(gamma + 1) * V;
+  a.zd_stride_b = (long)gamma * V;
+  a.B = B;
+  a.gamma = gamma;
+  a.V = V;
+  a.T = temperature;
+  a.k0 = (uint32_t)(seed & 0xFFFFFFFFu);
+  a.k1 = (uint32_t)(seed >> 32);
+  a.sids = sids;
+  a.rs = rs;
+  a.bonus = bonus;
+  a.out_tok = out_tok;
+  a.out_cnt = out_cnt;
+  a.out_acc = out_acc;
+  a.dbg = dbg;
+  a.stats = stats;
+  return seed::vocab_verify(a, (cudaStream_t)stream) == cudaSuccess ? SEED_OK : SEED_ECUDA;
+}
+
+seed_status seed_op_draft_sample(const float* z, int32_t ld, int32_t B, int32_t V, float temperature, uint64_t seed,
+                                 const uint32_t* sids, const int32_t* rs, int32_t j, int32_t* out, void* stream) {
+  if (!z || B < 1 || V < 1 || !sids || !rs || !out || !(temperature > 0.f)) return SEED_EINVAL;
+  return seed::draft_sample(z, ld, B, V, temperature, (uint32_t)(seed & 0xFFFFFFFFu), (uint32_t)(seed >> 32), sids,
+                            rs, j, out, 1, nullptr, 0, (cudaStream_t)stream) == cudaSuccess
+             ? SEED_OK
+             : SEED_ECUDA;
+}
+
+seed_status seed_op_decoder_layer(const seed_model_shape* shape, const void* const* w, const float* x_in, int32_t M,
+                                  int32_t ctx_len, const void* k_prev, const void* v_prev, float* x_out, void* k_new,
+                                  void* v_new, void* stream) {
+  if (!shape || !w || !x_in || !x_out || M < 1 || M > kMaxChunkRows || ctx_len < 0) return SEED_EINVAL;
+  if (ctx_len > 0 && (!k_prev || !v_prev)) return SEED_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  // a throw-away context holding a one-layer model (weights packed exactly as seed_init does)
+  seed_model_shape sh = *shape;
+  sh.n_layers = 1;
+  seed_ctx ctx = new seed_ctx_s;
+  ctx->P = 16;
+  const int max_pos = ctx_len + M + 1;
+  ctx->max_pages = (max_pos + ctx->P - 1) / ctx->P;
+  ctx->n_slots = 1;
+  // the model builder needs embed / lm_head: give it zero-size stand-ins by pointing at layer weights
+  bf16* dummy = nullptr;
+  seed_status s = SEED_OK;
+  const size_t Vd = (size_t)sh.vocab * sh.d_model;
+  if (cudaMalloc(&dummy, Vd * 2) != cudaSuccess) {
+    delete ctx;
+    return SEED_ENOMEM;
+  }
+  cudaMemset(dummy, 0, Vd * 2);
+  seed_model_weights mw{dummy, w, w[7], dummy};
+  s = build_model(ctx, ctx->tm, sh, mw, M, 1, ctx->max_pages, ctx->max_pages, max_pos);
+  Model& m = ctx->tm;
+  if (s == SEED_OK) {
+    ctx->partial_floats = max_partial(m, std::max(M, 1));
+    if (cudaMalloc(&ctx->partial, ctx->partial_floats * 4) != cudaSuccess) s = SEED_ENOMEM;
+  }
+  if (s == SEED_OK && ctx->arena.init(1 << 16) != cudaSuccess) s = SEED_ENOMEM;
+  if (s == SEED_OK) s = ensure_pages(ctx, m, 0, ctx_len + M, st);
+  if (s == SEED_OK && ctx_len > 0 &&
+      seed::kv_write_dense(m.kv, 0, 0, ctx_len, (const bf16*)k_prev, (const bf16*)v_prev, st) != cudaSuccess)
+    s = SEED_ECUDA;
+  if (s == SEED_OK) {
+    ctx->arena.begin();
+    std::vector<Segment> segs{{0, ctx_len, M, -1}};
+    ChunkDesc c;
+    size_t tok_off;
+    pack_chunk(ctx, segs, 0, &c, &tok_off);
+    if (ctx->arena.upload(st) != cudaSuccess) s = SEED_ECUDA;
+    const float eps = sh.rms_eps > 0 ? sh.rms_eps : 1e-5f;
+    if (s == SEED_OK && cudaMemcpyAsync(m.x, x_in, (size_t)M * m.d * 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      s = SEED_ECUDA;
+    if (s == SEED_OK && seed::rmsnorm_rows(m.x, M, m.d, m.an[0], eps, m.h, st) != cudaSuccess) s = SEED_ECUDA;
+    if (s == SEED_OK) s = forward_chunk(ctx, m, c, st, 0, 1, false);
+    if (s == SEED_OK && cudaMemcpyAsync(x_out, m.x, (size_t)M * m.d * 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      s = SEED_ECUDA;
+    // copy the appended K/V back out (dense) through a scratch pass over the pages
+    if (s == SEED_OK && (k_new || v_new)) {
+      const size_t per = (size_t)m.Hk * m.Dh;
+      std::vector<bf16> hk(per * M), hv(per * M);
+      cudaStreamSynchronize(st);
+      for (int p = 0; p < M && s == SEED_OK; ++p) {
+        const int pos = ctx_len + p;
+        const int page = m.page_table[pos / ctx->P];
+        for (int h = 0; h < m.Hk; ++h) {
+          const size_t ko = m.kv.offset(page, 0, 0, h, pos % ctx->P), vo = m.kv.offset(page, 0, 1, h, pos % ctx->P);
+          if (k_new && cudaMemcpy((bf16*)k_new + ((size_t)p * m.Hk + h) * m.Dh, m.kv.pool + ko, m.Dh * 2,
+                                  cudaMemcpyDeviceToDevice) != cudaSuccess)
+            s = SEED_ECUDA;
+          if (v_new && cudaMemcpy((bf16*)v_new + ((size_t)p * m.Hk + h) * m.Dh, m.kv.pool + vo, m.Dh * 2,
+                                  cudaMemcpyDeviceToDevice) != cudaSuccess)
+            s = SEED_ECUDA;
+        }
+      }
+    }
+  }
+  cudaStreamSynchronize(st);
+  if (s == SEED_OK && cudaGetLastError() != cudaSuccess) s = SEED_ECUDA;
+  free_model(ctx->tm);
+  if (ctx->partial) cudaFree(ctx->partial);
+  ctx->arena.destroy();
+  cudaFree(dummy);
+  delete ctx;
+  return s;
+}
+
+}  // extern "C"

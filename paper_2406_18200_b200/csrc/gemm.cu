@@ -1,0 +1,255 @@
+// gemm.cu -- K2: the verify / draft projections as a persistent stream-K GEMM on tcgen05.
+//
+// Y[m][n] = sum_k X[m][k] * W[n][k]  (nn.Linear, W row-major [N][K], bf16 in, fp32 accumulate).
+// The method streams every weight once per round with only M = B(gamma+1) tokens
+// (M <= 120 sits far below the ridge), so the kernel is built to keep
+// HBM busy: swap-AB puts the weight rows on the UMMA M = 128 side and the tokens on
+// UMMA N = M_pad (16..256); TMA streams 128 x 64 weight tiles through a deep smem ring
+// (evict-first), the token tile rides along (evict-last, L2 resident); one elected
+// thread issues tcgen05.mma into a double-buffered TMEM accumulator; four epilogue
+// warps drain TMEM with tcgen05.ld while the next tile accumulates.
+//
+// Work split: the (tile, k-block) units are cut into G = min(148, U) contiguous ranges,
+// one persistent CTA per SM (stream-K).  A CTA writes one fp32 partial per tile it
+// touches; the consumer epilogue sums a tile's partials in CTA order.  G and the cut
+// points depend on (N, K) only, never on M, so every output column is computed in the
+// same order whatever the batch (batch invariance, DESIGN R19).
+#include <cuda.h>
+#include <cstdio>
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace seed {
+
+namespace {
+constexpr int BLOCK_N = 128;   // weight rows per tile (UMMA M)
+constexpr int BLOCK_K = 64;    // one 128-byte swizzle row of bf16
+constexpr int W_TILE_BYTES = BLOCK_N * BLOCK_K * 2;
+constexpr int MAX_STAGES = 16;
+constexpr int SMEM_BUDGET = 220 * 1024;
+
+struct GemmArgs {
+  int KB, U, G, S, M, m_pad, stages;
+  float* partial;
+};
+
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  // K-major operand, 128B swizzle: 8-row x 128B atoms, SBO = 1024 B, LBO unused, version 1
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__global__ void __launch_bounds__(192, 1)
+gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GemmArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int S = a.stages;
+  const int x_bytes = a.m_pad * BLOCK_K * 2;
+  uint8_t* sW = smem;
+  uint8_t* sX = smem + S * W_TILE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sX + S * x_bytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x;
+  const long u_begin = (long)c * a.U / a.G, u_end = (long)(c + 1) * a.U / a.G;
+  if (u_begin >= u_end) return;
+
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(2 * a.m_pad)) cols <<= 1;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmW);
+    prefetch_tmap(&tmX);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const long t_begin = u_begin / a.KB;
+
+  if (warp == 0) {
+    // ---------------- TMA producer (one elected lane)
+    if (elect_one()) {
+      const uint64_t pol_w = l2_policy_evict_first();
+      const uint64_t pol_x = l2_policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (long u = u_begin; u < u_end; ++u) {
+        const int t = (int)(u / a.KB), kb = (int)(u % a.KB);
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&full[stage], W_TILE_BYTES + x_bytes);
+        tma_load_2d(sW + stage * W_TILE_BYTES, &tmW, &full[stage], kb * BLOCK_K, t * BLOCK_N, pol_w);
+        tma_load_2d(sX + stage * x_bytes, &tmX, &full[stage], kb * BLOCK_K, 0, pol_x);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one elected lane)
+    const uint32_t idesc = (1u << 4)                       // D = f32
+                           | (1u << 7) | (1u << 10)         // A = B = bf16
+                           | ((uint32_t)(a.m_pad >> 3) << 17)  // N = m_pad
+                           | ((uint32_t)(BLOCK_N >> 4) << 24); // M = 128
+    const uint32_t sW0 = smem_u32(sW), sX0 = smem_u32(sX);
+    int stage = 0;
+    uint32_t phase = 0;
+    int seg = 0;
+    long u = u_begin;
+    while (u < u_end) {
+      const long t = u / a.KB;
+      const long seg_end = min(u_end, (t + 1) * a.KB);
+      const int acc = seg & 1;
+      const uint32_t use = (uint32_t)(seg >> 1);
+      mbar_wait(&tempty[acc], (use & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * a.m_pad);
+      const long seg_start = u;
+      for (; u < seg_end; ++u) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t wa = sW0 + stage * W_TILE_BYTES, xa = sX0 + stage * x_bytes;
+#pragma unroll
+          for (int k = 0; k < BLOCK_K / 16; ++k)
+            umma_bf16(d_tmem, sw128_desc(wa + k * 32), sw128_desc(xa + k * 32), idesc,
+                      (u != seg_start || k > 0) ? 1u : 0u);
+          umma_commit(&empty[stage]);
+          if (u == seg_end - 1) umma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      ++seg;
+    }
+  } else {
+    // ---------------- epilogue warps 2..5: TMEM -> fp32 partial [m][128]
+    const int lane_grp = warp & 3;               // TMEM lanes this warp may access
+    const int nl = lane_grp * 32 + lane;         // weight row within the tile
+    int seg = 0;
+    long u = u_begin;
+    while (u < u_end) {
+      const long t = u / a.KB;
+      const long seg_end = min(u_end, (t + 1) * a.KB);
+      const int acc = seg & 1;
+      const uint32_t use = (uint32_t)(seg >> 1);
+      mbar_wait(&tfull[acc], use & 1);
+      tc_fence_after();
+      float* out = a.partial + ((size_t)((long)c * a.S + (t - t_begin)) * a.M) * BLOCK_N;
+      const uint32_t row_addr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(acc * a.m_pad);
+      for (int col = 0; col < a.m_pad; col += 16) {
+        float v[16];
+        tmem_ld16(row_addr + col, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (col + i < a.M) out[(size_t)(col + i) * BLOCK_N + nl] = v[i];
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      u = seg_end;
+      ++seg;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem_base, cols);
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn g_encode = nullptr;
+std::once_flag g_encode_once;
+
+void load_encode() {
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess)
+    g_encode = reinterpret_cast<EncodeTiledFn>(fn);
+}
+}  // namespace
+
+int gemm_mpad(int M) { return ((M + 15) / 16) * 16; }
+
+bool encode_tmap_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                    uint32_t box_outer) {
+  std::call_once(g_encode_once, load_encode);
+  if (!g_encode) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+void gemm_plan(GemmPlan* p, const void* W, int N, int K) {
+  p->N = N;
+  p->K = K;
+  p->KB = K / BLOCK_K;
+  p->tiles = (N + BLOCK_N - 1) / BLOCK_N;
+  p->U = p->tiles * p->KB;
+  p->G = p->U < kNumSMs ? p->U : kNumSMs;
+  // segments per CTA: ceil(range / KB) + 1 bound
+  const int range = (p->U + p->G - 1) / p->G;
+  p->S = (range + p->KB - 1) / p->KB + 1;
+  encode_tmap_2d(&p->tmW, W, (uint64_t)K, (uint64_t)N, BLOCK_K, BLOCK_N);
+}
+
+size_t gemm_partial_floats(const GemmPlan& p, int M) { return (size_t)p.G * p.S * M * BLOCK_N; }
+
+cudaError_t gemm_run(const GemmPlan& p, const CUtensorMap& tmX, int M, float* partial, PartialView* view,
+                     cudaStream_t st) {
+  GemmArgs a;
+  a.KB = p.KB;
+  a.U = p.U;
+  a.G = p.G;
+  a.S = p.S;
+  a.M = M;
+  a.m_pad = gemm_mpad(M);
+  if (a.m_pad > 256) return cudaErrorInvalidValue;
+  const int stage_bytes = W_TILE_BYTES + a.m_pad * BLOCK_K * 2;
+  int stages = (SMEM_BUDGET - 1024 - 256) / stage_bytes;
+  if (stages > MAX_STAGES) stages = MAX_STAGES;
+  a.stages = stages;
+  a.partial = partial;
+  const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 4) * 8 + 16;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(gemm_streamk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_done = true;
+  }
+  gemm_streamk_kernel<<<p.G, 192, smem, st>>>(p.tmW, tmX, a);
+  if (view) *view = PartialView{partial, p.KB, p.U, p.G, p.S, M};
+  return cudaGetLastError();
+}
+
+}  // namespace seed

@@ -1,0 +1,117 @@
+// kernels.h -- host-side launch interface between the engine and the CUDA kernels.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <stddef.h>
+
+namespace seed {
+
+// ------------------------------------------------------------------ paged KV cache layout
+// pool: bf16 [num_pages][n_layers][2 (K,V)][Hk][P][Dh]; page table: int32 [slots][max_pages]
+struct KVLayout {
+  __nv_bfloat16* pool;
+  const int32_t* page_table;
+  int32_t max_pages;  // per slot
+  int32_t n_layers, Hk, Dh, P;
+  __host__ __device__ size_t page_elems() const { return (size_t)n_layers * 2 * Hk * P * Dh; }
+  __host__ __device__ size_t offset(int page, int layer, int kv, int h, int slot_in_page) const {
+    return (size_t)page * page_elems() + ((size_t)(layer * 2 + kv) * Hk + h) * P * Dh + (size_t)slot_in_page * Dh;
+  }
+};
+
+// ------------------------------------------------------------------ K2: stream-K GEMM
+// Y[m][n] = sum_k X[m][k] W[n][k]; W [N][K] bf16, X [Mcap][K] bf16 (rows >= M ignored).
+struct GemmPlan {
+  int N, K, KB, tiles, U, G, S;  // S = max segments per CTA
+  CUtensorMap tmW;
+};
+
+struct PartialView {  // read side of the split-K partial sums, batch-invariant order
+  const float* p;
+  int KB, U, G, S, M;
+};
+
+bool encode_tmap_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                    uint32_t box_outer);
+void gemm_plan(GemmPlan* plan, const void* W, int N, int K);
+size_t gemm_partial_floats(const GemmPlan& plan, int M);
+// launches the tcgen05 main loop; returns the view the epilogue kernels read
+cudaError_t gemm_run(const GemmPlan& plan, const CUtensorMap& tmX, int M, float* partial, PartialView* view,
+                     cudaStream_t st);
+int gemm_mpad(int M);
+
+// ------------------------------------------------------------------ epilogues / elementwise
+cudaError_t epi_store(const PartialView& v, int N, float* Y, int ldY, const int32_t* row_map, int M, cudaStream_t st);
+struct RowInfo {         // per row of the ragged batch
+  const int32_t* tok;    // [M] token ids
+  const int32_t* pos;    // [M] absolute positions
+  const int32_t* slot;   // [M] stream slot (page table row)
+};
+cudaError_t embed_rmsnorm(const __nv_bfloat16* embed, const int32_t* tok, int tok_stride, int M, int d, const __nv_bfloat16* w,
+                          float eps, float* x, __nv_bfloat16* h, cudaStream_t st);
+cudaError_t epi_qkv_rope(const PartialView& v, int M, int H, int Hk, int Dh, const RowInfo& rows,
+                         const float2* rope, int layer, const KVLayout& kv, __nv_bfloat16* q_out,
+                         __nv_bfloat16* k_dbg, __nv_bfloat16* v_dbg, cudaStream_t st);
+cudaError_t epi_residual_rmsnorm(const PartialView& v, int M, int d, float* x, const __nv_bfloat16* w, float eps,
+                                 __nv_bfloat16* h, const int32_t* compact_map, __nv_bfloat16* h_compact,
+                                 cudaStream_t st);
+cudaError_t epi_swiglu(const PartialView& v, int M, int ff, __nv_bfloat16* act, cudaStream_t st);
+cudaError_t rope_table_init(float2* table, int max_pos, int Dh, double theta, cudaStream_t st);
+cudaError_t rmsnorm_rows(const float* x, int M, int d, const __nv_bfloat16* w, float eps, __nv_bfloat16* h,
+                         cudaStream_t st);
+cudaError_t kv_write_dense(const KVLayout& kv, int layer, int slot, int n, const __nv_bfloat16* k,
+                           const __nv_bfloat16* v, cudaStream_t st);
+
+// ------------------------------------------------------------------ K3: paged attention
+struct SeqInfo {          // per sequence of the ragged batch (device arrays)
+  const int32_t* q_start; // first row
+  const int32_t* q_len;   // rows
+  const int32_t* kv_len;  // keys after append = pos(last row) + 1
+  const int32_t* slot;
+};
+struct AttnWorkspace {
+  float* o_part;   // [splits][M][H][Dh]
+  float* ml_part;  // [splits][M][H][2]
+  int max_splits;
+};
+int attn_chunk_tokens();
+cudaError_t attention(const __nv_bfloat16* q, int M, int n_seq, int max_q_len, int max_kv, int H, int Hk, int Dh,
+                      const SeqInfo& seqs, const KVLayout& kv, int layer, const AttnWorkspace& ws,
+                      __nv_bfloat16* out, cudaStream_t st);
+
+// ------------------------------------------------------------------ K4 / K1 sampler / K5
+struct VerifyArgs {
+  const float* zt; const float* zd; const int32_t* xs;
+  long zt_stride_b, zd_stride_b;  // floats between streams
+  int B, gamma, V;
+  float T;
+  uint32_t k0, k1;
+  const uint32_t* sids; const int32_t* rs;
+  int bonus;
+  int32_t* out_tok; int32_t* out_cnt; int32_t* out_acc;
+  float* dbg; double* stats;
+};
+cudaError_t vocab_verify(const VerifyArgs& a, cudaStream_t st);
+cudaError_t draft_sample(const float* z, long ld, int B, int V, float T, uint32_t k0, uint32_t k1,
+                         const uint32_t* sids, const int32_t* rs, int j, int32_t* out, int out_stride, int32_t* out2,
+                         int out2_stride, cudaStream_t st);
+cudaError_t philox_fill(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1, int n,
+                        uint32_t* out, cudaStream_t st);
+
+struct StreamState {     // device per-slot state (K5)
+  int32_t* tlen;         // |T_s|
+  int32_t* len_t;        // target KV entries
+  int32_t* len_d;        // draft KV entries
+  int32_t* L;            // new tokens
+  int32_t* r;            // stream-local round
+  int32_t* done;
+  int32_t* hist;         // [slots][max_ctx] validated tokens
+  int32_t max_ctx;
+};
+cudaError_t rollback_commit(const StreamState& s, const int32_t* batch_slots, int B, int gamma,
+                            const int32_t* out_tok, const int32_t* out_cnt, int max_new, int32_t* records,
+                            const uint32_t* gids, cudaStream_t st);
+
+}  // namespace seed
