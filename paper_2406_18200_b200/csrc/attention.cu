@@ -36,6 +36,8 @@ attn_chunk_kernel(const __nv_bfloat16* __restrict__ q, int H, int Hk, SeqInfo se
   auto m_s = reinterpret_cast<float(*)[QB]>(tail + QB * DH * 4 + WARPS * QB * 32 * 4);
   auto l_s = reinterpret_cast<float(*)[QB]>(tail + QB * DH * 4 + WARPS * QB * 32 * 4 + WARPS * QB * 4);
 
+  pdl_trigger();
+  pdl_wait();
   const int seq = blockIdx.x / n_qblk, qb = blockIdx.x % n_qblk;
   const int head = blockIdx.y, split = blockIdx.z;
   const int kvh = head / (H / Hk);
@@ -79,20 +81,26 @@ attn_chunk_kernel(const __nv_bfloat16* __restrict__ q, int H, int Hk, SeqInfo se
   for (int kt = c_begin + warp * 32; kt < c_end; kt += WARPS * 32) {
     // ---- stage the K and V tile of keys kt .. kt+31 (16-byte vectors)
     constexpr int VPR = DH / 8;   // 16-byte vectors per key row
+    // all 16-byte pieces of the tile in flight at once (cp.async, no register staging); the
+    // tile's page ids (kt is a multiple of 32, P divides 32 or vice versa) are read once
+    const int pg_first = kt / kv.P;
+    const int npg = (min(kt + 31, c_end - 1)) / kv.P - pg_first + 1;
+    const int my_page = lane < npg ? __ldg(kv.page_table + (size_t)slot * kv.max_pages + pg_first + lane) : 0;
+#pragma unroll 8
     for (int e = lane; e < 32 * VPR; e += 32) {
       const int kk = e / VPR, c16 = e % VPR;
       const int key = kt + kk;
-      uint4 kvv = make_uint4(0, 0, 0, 0), vvv = make_uint4(0, 0, 0, 0);
+      const int page = __shfl_sync(0xffffffffu, my_page, min(31, key / kv.P - pg_first));
       if (key < c_end) {
-        const int page = kv.page_table[(size_t)slot * kv.max_pages + key / kv.P];
         const size_t ko = kv.offset(page, layer, 0, kvh, key % kv.P);
-        const size_t vo = kv.offset(page, layer, 1, kvh, key % kv.P);
-        kvv = __ldg(reinterpret_cast<const uint4*>(kv.pool + ko) + c16);
-        vvv = __ldg(reinterpret_cast<const uint4*>(kv.pool + vo) + c16);
+        cp_async16(&k_s[warp][kk][c16 * 8], reinterpret_cast<const uint4*>(kv.pool + ko) + c16);
+        cp_async16(&v_s[warp][kk][c16 * 8], reinterpret_cast<const uint4*>(kv.pool + ko + kv.vofs()) + c16);
+      } else {
+        *reinterpret_cast<uint4*>(&k_s[warp][kk][c16 * 8]) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(&v_s[warp][kk][c16 * 8]) = make_uint4(0, 0, 0, 0);
       }
-      *reinterpret_cast<uint4*>(&k_s[warp][kk][c16 * 8]) = kvv;
-      *reinterpret_cast<uint4*>(&v_s[warp][kk][c16 * 8]) = vvv;
     }
+    cp_async_wait_all();
     __syncwarp();
     // ---- scores: lane = key
     const int key = kt + lane;
@@ -194,6 +202,8 @@ attn_chunk_kernel(const __nv_bfloat16* __restrict__ q, int H, int Hk, SeqInfo se
 // merge chunk partials in chunk order; grid (M, H), block Dh
 __global__ void attn_combine_kernel(AttnWorkspace ws, int M, int H, int Dh, int splits, const int32_t* row_nsplit,
                                     __nv_bfloat16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int row = blockIdx.x, head = blockIdx.y, d = threadIdx.x;
   const int ns = row_nsplit ? row_nsplit[row] : splits;
   float mx = -INFINITY;
@@ -225,8 +235,8 @@ struct ChunkLauncher {
       cudaFuncSetAttribute(attn_chunk_kernel<DH, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
-    attn_chunk_kernel<DH, NR><<<grid, 128, smem, st>>>(q, H, Hk, seqs, kv, layer, n_qblk, scale, ws, M);
-    return cudaGetLastError();
+    return launch(attn_chunk_kernel<DH, NR>, grid, dim3(128), smem, st, q, H, Hk, seqs, kv, layer, n_qblk, scale, ws,
+                  M);
   }
 };
 
@@ -269,9 +279,7 @@ cudaError_t attention(const __nv_bfloat16* q, int M, int n_seq, int max_q_len, i
   else if (Dh == 32) e = launch_chunks<32>(q, M, n_seq, max_q_len, max_kv, H, Hk, seqs, kv, layer, ws, st);
   else return cudaErrorInvalidValue;
   if (e != cudaSuccess) return e;
-  dim3 grid(M, H);
-  attn_combine_kernel<<<grid, Dh, 0, st>>>(ws, M, H, Dh, splits, nullptr, out);
-  return cudaGetLastError();
+  return launch(attn_combine_kernel, dim3(M, H), dim3(Dh), 0, st, ws, M, H, Dh, splits, (const int32_t*)nullptr, out);
 }
 
 }  // namespace seed

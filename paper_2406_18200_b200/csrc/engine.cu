@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -120,7 +121,7 @@ struct Model {
   // paged KV
   KVLayout kv{};
   int32_t* page_table_dev = nullptr;
-  std::vector<int32_t> page_table;        // host mirror [slots][max_pages]
+  int32_t* page_table = nullptr;          // pinned host mirror [slots][max_pages]
   std::vector<int32_t> free_pages;
   std::vector<int32_t> held;              // pages held per slot
   size_t n_pages = 0;
@@ -138,6 +139,22 @@ struct SlotState {  // host mirror of one stream slot
   bool used = false;
   std::vector<int32_t> T;  // validated tokens
   int prompt_len = 0, L = 0, r = 0, done = 0, len_t = 0, len_d = 0;
+};
+
+struct ChunkDesc {
+  int M, n_seq, max_q_len, max_kv;
+  const int32_t *pos, *slot, *q_start, *q_len, *kv_len, *seq_slot, *compact;  // device (slot: per row)
+  TokSrc tok;
+  int n_logits;
+  float* Y;       // logits destination for compact row 0
+  int ldY;
+};
+
+struct RoundPlan {  // descriptors of one round at batch-size-determined arena offsets
+  int n = 0;
+  size_t o_sid = 0, o_r = 0, o_sl = 0, o_last = 0;
+  std::vector<ChunkDesc> draft, verify;
+  std::vector<int> verify_b0;
 };
 
 constexpr int kMaxChunkRows = 256;
@@ -174,15 +191,26 @@ struct seed_ctx_s {
   cudaEvent_t round_done = nullptr;
   std::vector<int32_t> last_batch;  // global ids of the batch in flight
   std::vector<int32_t> drafted;     // batch drafted and not yet verified
+  RoundPlan plan;
   bool round_pending = false;
   // NCCL
   void* comm = nullptr;
-  // profiling
-  bool profile = false;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
-  size_t ev_used = 0;
-  double gemm_bytes = 0;
-  int64_t gemm_launches = 0, kernel_launches = 0;
+  // CUDA graphs of the round, one pair per batch size (R23)
+  bool use_graphs = true;
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  struct RoundGraphs {
+    cudaGraphExec_t draft = nullptr, verify = nullptr;
+    double gemm_bytes = 0;
+    int64_t gemms = 0, kernels = 0;
+  };
+  std::map<int, RoundGraphs> graphs;
+  // profiling: per-GEMM globaltimer records accumulated on the device
+  bool profile = false, in_round = false;
+  unsigned long long *timing_rec = nullptr, *timing_acc = nullptr;
+  int rec_cap = 0, rec_used = 0;
+  double round_gemm_bytes = 0, gemm_bytes = 0;
+  int64_t round_gemms = 0, gemm_launches = 0, kernel_launches = 0;
 };
 
 namespace {
@@ -221,24 +249,12 @@ seed_status run_gemm(seed_ctx ctx, const GemmPlan& p, const bf16* X, int rows_ca
                      cudaStream_t st) {
   const CUtensorMap* tm = xmap(ctx, X, p.K, rows_cap, M);
   if (!tm) return fail(ctx, SEED_ECUDA, "cuTensorMapEncodeTiled", "X operand");
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (ctx->profile) {
-    if (ctx->ev_used == ctx->ev_pool.size()) {
-      cudaEvent_t a, b;
-      CK(cudaEventCreate(&a));
-      CK(cudaEventCreate(&b));
-      ctx->ev_pool.push_back({a, b});
-    }
-    e0 = ctx->ev_pool[ctx->ev_used].first;
-    e1 = ctx->ev_pool[ctx->ev_used].second;
-    ctx->ev_used++;
-    CK(cudaEventRecord(e0, st));
-  }
-  CK(seed::gemm_run(p, *tm, M, ctx->partial, view, st));
-  if (ctx->profile) {
-    CK(cudaEventRecord(e1, st));
-    ctx->gemm_bytes += (double)p.N * p.K * 2 + (double)M * p.K * 2 + (double)M * p.N * 4;
-    ctx->gemm_launches++;
+  unsigned long long* rec = nullptr;
+  if (ctx->profile && ctx->in_round && ctx->rec_used < ctx->rec_cap) rec = ctx->timing_rec + 2 * ctx->rec_used++;
+  CK(seed::gemm_run(p, *tm, M, ctx->partial, view, st, rec));
+  if (ctx->in_round) {
+    ctx->round_gemm_bytes += (double)p.N * p.K * 2 + (double)M * p.K * 2 + (double)M * p.N * 4;
+    ctx->round_gemms++;
   }
   ctx->kernel_launches++;
   return SEED_OK;
@@ -336,7 +352,8 @@ seed_status build_model(seed_ctx ctx, Model& m, const seed_model_shape& sh, cons
   m.n_pages = pool_pages;
   CK(cudaMalloc(&m.kv.pool, m.kv.page_elems() * pool_pages * 2));
   CK(cudaMalloc(&m.page_table_dev, (size_t)slots * max_pages * 4));
-  m.page_table.assign((size_t)slots * max_pages, 0);
+  CK(cudaMallocHost(&m.page_table, (size_t)slots * max_pages * 4));
+  std::memset(m.page_table, 0, (size_t)slots * max_pages * 4);
   CK(cudaMemset(m.page_table_dev, 0, (size_t)slots * max_pages * 4));
   m.kv.page_table = m.page_table_dev;
   m.held.assign(slots, 0);
@@ -360,6 +377,11 @@ seed_status build_model(seed_ctx ctx, Model& m, const seed_model_shape& sh, cons
 }
 
 void free_model(Model& m) {
+  for (auto* v : {&m.pq, &m.po, &m.pgu, &m.pd})
+    for (auto& p : *v) seed::gemm_plan_free(&p);
+  seed::gemm_plan_free(&m.plm);
+  if (m.page_table) cudaFreeHost(m.page_table);
+  m.page_table = nullptr;
   for (bf16* p : m.owned) cudaFree(p);
   m.owned.clear();
   if (m.kv.pool) cudaFree(m.kv.pool);
@@ -394,11 +416,10 @@ seed_status ensure_pages(seed_ctx ctx, Model& m, int slot, int n_tokens, cudaStr
     m.free_pages.pop_back();
     ++held;
   }
+  // pinned mirror: entries change again only after release_pages, which synchronises first
   CK(cudaMemcpyAsync(m.page_table_dev + (size_t)slot * ctx->max_pages + first,
-                     m.page_table.data() + (size_t)slot * ctx->max_pages + first, (size_t)(need - first) * 4,
+                     m.page_table + (size_t)slot * ctx->max_pages + first, (size_t)(need - first) * 4,
                      cudaMemcpyHostToDevice, st));
-  // the host vector may change before the copy runs: make the copy synchronous w.r.t. host memory
-  CK(cudaStreamSynchronize(st));
   return SEED_OK;
 }
 
@@ -408,14 +429,6 @@ void release_pages(Model& m, int slot, int max_pages) {
 }
 
 // ------------------------------------------------------------------ forward over one chunk
-struct ChunkDesc {
-  int M, n_seq, max_q_len, max_kv;
-  const int32_t *pos, *slot, *q_start, *q_len, *kv_len, *seq_slot, *compact;  // device (slot: per row)
-  TokSrc tok;
-  int n_logits;
-  float* Y;       // logits destination for compact row 0
-  int ldY;
-};
 
 seed_status forward_chunk(seed_ctx ctx, Model& m, const ChunkDesc& c, cudaStream_t st, int first_layer = 0,
                           int last_layer = -1, bool embed = true) {
@@ -580,6 +593,13 @@ seed_status complete_round(seed_ctx ctx) {
   return SEED_OK;
 }
 
+// finish any round work in flight before the descriptor arena is reused outside a round
+seed_status quiesce(seed_ctx ctx) {
+  if (ctx->gstream) CK(cudaStreamSynchronize(ctx->gstream));
+  if (ctx->round_pending) return complete_round(ctx);
+  return SEED_OK;
+}
+
 seed_status map_batch(seed_ctx ctx, const int32_t* ids, int n, std::vector<int>& slots) {
   if (n < 1 || n > ctx->C || !ids) return fail(ctx, n > ctx->C ? SEED_ECAPACITY : SEED_EINVAL, "batch", "size");
   slots.resize(n);
@@ -589,6 +609,207 @@ seed_status map_batch(seed_ctx ctx, const int32_t* ids, int n, std::vector<int>&
     slots[i] = it->second;
     if (ctx->slots[slots[i]].done) return fail(ctx, SEED_EINVAL, "batch", "stream already done");
   }
+  return SEED_OK;
+}
+
+// ------------------------------------------------------------------ one round
+// All descriptors of a round (draft steps and verify chunks) are packed into the arena at
+// offsets that depend on the batch size only, so the captured graph of a batch size can be
+// replayed with fresh descriptor contents (R23).
+seed_status build_round_plan(seed_ctx ctx, const std::vector<int>& slots, int n, RoundPlan& P) {
+  const int g = ctx->cfg.gamma;
+  Arena& A = ctx->arena;
+  A.begin();
+  P.n = n;
+  P.o_sid = A.alloc(n);
+  P.o_r = A.alloc(n);
+  P.o_sl = A.alloc(n);
+  P.o_last = A.alloc(n);
+  if (P.o_last == (size_t)-1) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
+  for (int b = 0; b < n; ++b) {
+    const SlotState& ss = ctx->slots[slots[b]];
+    A.host[P.o_sid + b] = (int32_t)ss.gid;
+    A.host[P.o_r + b] = ss.r;
+    A.host[P.o_sl + b] = slots[b];
+    A.host[P.o_last + b] = ss.T.back();
+  }
+  const int max_pos = ctx->cfg.max_ctx + g + 2;
+  // draft step 1 feeds (T[-2], T[-1]); when one token is pending the first row rewrites an
+  // existing entry with identical values (R22), so M = 2n every round
+  P.draft.assign(g, ChunkDesc{});
+  std::vector<Segment> segs(n);
+  for (int b = 0; b < n; ++b) {
+    const SlotState& ss = ctx->slots[slots[b]];
+    const int T = (int)ss.T.size();
+    const size_t to = A.alloc(2);
+    if (to == (size_t)-1) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
+    A.host[to] = ss.T[T - 2];
+    A.host[to + 1] = ss.T[T - 1];
+    segs[b] = Segment{slots[b], T - 2, 2, (int)to};
+  }
+  size_t tok_off;
+  if (2 * n > kMaxChunkRows || !pack_chunk(ctx, segs, 2, &P.draft[0], &tok_off))
+    return fail(ctx, SEED_ECAPACITY, "seed_draft_round", "batch too large");
+  for (int j = 2; j <= g; ++j) {
+    for (int b = 0; b < n; ++b) {
+      const int T = (int)ctx->slots[slots[b]].T.size();
+      segs[b] = Segment{slots[b], T + j - 2, 1, -1};
+    }
+    if (!pack_chunk(ctx, segs, 2, &P.draft[j - 1], &tok_off)) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
+    P.draft[j - 1].tok = TokSrc{ctx->xs + (j - 2), g};  // x_{j-1} of every stream ([B][g] layout)
+  }
+  // verify chunks of whole streams
+  P.verify.clear();
+  P.verify_b0.clear();
+  const int per_chunk = std::max(1, kMaxChunkRows / (g + 1));
+  for (int b0 = 0; b0 < n; b0 += per_chunk) {
+    const int nb = std::min(per_chunk, n - b0);
+    std::vector<Segment> vs(nb);
+    for (int b = 0; b < nb; ++b) {
+      const int T = (int)ctx->slots[slots[b0 + b]].T.size();
+      vs[b] = Segment{slots[b0 + b], T - 1, g + 1, -1};
+    }
+    ChunkDesc c;
+    if (!pack_chunk(ctx, vs, 1, &c, &tok_off)) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
+    c.tok = TokSrc{ctx->vtok + (size_t)b0 * (g + 1), 1};
+    c.Y = ctx->tgt_logits + (size_t)b0 * (g + 1) * ctx->cfg.target.vocab;
+    c.ldY = ctx->cfg.target.vocab;
+    P.verify.push_back(c);
+    P.verify_b0.push_back(b0);
+  }
+  if (ctx->use_graphs) {  // fixed grids: attention sized for the longest context (R23)
+    for (auto& c : P.draft) c.max_kv = max_pos;
+    for (auto& c : P.verify) c.max_kv = max_pos;
+  }
+  return SEED_OK;
+}
+
+seed_status enqueue_draft(seed_ctx ctx, cudaStream_t st) {
+  RoundPlan& P = ctx->plan;
+  const int n = P.n, g = ctx->cfg.gamma, V = ctx->cfg.target.vocab;
+  Arena& A = ctx->arena;
+  seed_status s;
+  CK(cudaMemcpyAsync(A.dev, A.host, A.used * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ctx->sids_dev, A.dev + P.o_sid, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(ctx->rs_dev, A.dev + P.o_r, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(ctx->slots_dev, A.dev + P.o_sl, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+  // verify input column 0 = T[-1]
+  CK(cudaMemcpy2DAsync(ctx->vtok, (size_t)(g + 1) * 4, A.dev + P.o_last, 4, 4, n, cudaMemcpyDeviceToDevice, st));
+  const uint32_t k0 = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu), k1 = (uint32_t)(ctx->cfg.seed >> 32);
+  for (int j = 1; j <= g; ++j) {
+    ChunkDesc& c = P.draft[j - 1];
+    c.Y = ctx->drf_logits + (size_t)(j - 1) * V;
+    c.ldY = g * V;
+    if ((s = forward_chunk(ctx, ctx->dm, c, st)) != SEED_OK) return s;
+    // K1 sampler: x_j -> xs[b][j-1] and the verify input vtok[b][j]
+    CK(seed::draft_sample(c.Y, (long)g * V, n, V, ctx->cfg.temperature, k0, k1, ctx->sids_dev, ctx->rs_dev, j,
+                          ctx->xs + (j - 1), g, ctx->vtok + j, g + 1, st));
+    ctx->kernel_launches++;
+  }
+  return SEED_OK;
+}
+
+seed_status enqueue_verify(seed_ctx ctx, cudaStream_t st) {
+  RoundPlan& P = ctx->plan;
+  const int n = P.n, g = ctx->cfg.gamma, V = ctx->cfg.target.vocab;
+  seed_status s;
+  for (auto& c : P.verify)
+    if ((s = forward_chunk(ctx, ctx->tm, c, st)) != SEED_OK) return s;
+  // a4: K4 fused vocabulary kernel
+  seed::VerifyArgs a{};
+  a.zt = ctx->tgt_logits;
+  a.zd = ctx->drf_logits;
+  a.xs = ctx->xs;
+  a.zt_stride_b = (long)(g + 1) * V;
+  a.zd_stride_b = (long)g * V;
+  a.B = n;
+  a.gamma = g;
+  a.V = V;
+  a.T = ctx->cfg.temperature;
+  a.k0 = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu);
+  a.k1 = (uint32_t)(ctx->cfg.seed >> 32);
+  a.sids = ctx->sids_dev;
+  a.rs = ctx->rs_dev;
+  a.bonus = ctx->cfg.bonus;
+  a.out_tok = ctx->out_tok;
+  a.out_cnt = ctx->out_cnt;
+  a.out_acc = ctx->out_acc;
+  CK(seed::vocab_verify(a, st));
+  // a5: K5 commit + rollback, emit the exchange records
+  const int world = std::max(ctx->cfg.world, 1);
+  const size_t rec_bytes = (size_t)ctx->C * (g + 3) * 4;
+  CK(cudaMemsetAsync(ctx->records, 0xFF, rec_bytes, st));
+  CK(seed::rollback_commit(ctx->ds, ctx->slots_dev, n, g, ctx->out_tok, ctx->out_cnt, ctx->cfg.max_new_tokens,
+                           ctx->records, ctx->sids_dev, st));
+  ctx->kernel_launches += 2;
+  if (ctx->profile) {
+    CK(seed::timing_accumulate(ctx->timing_rec, ctx->rec_used, ctx->timing_acc, st));
+    ctx->kernel_launches++;
+  }
+  // a6: all-gather of the per-rank records over NVLink (world > 1)
+  if (world > 1) {
+    if (g_nccl.allgather(ctx->records, ctx->records_all, (size_t)ctx->C * (g + 3), kNcclInt32, ctx->comm, st) != 0)
+      return fail(ctx, SEED_ENCCL, "ncclAllGather", "records");
+    CK(cudaMemcpyAsync(ctx->records_host, ctx->records_all, rec_bytes * world, cudaMemcpyDeviceToHost, st));
+  } else {
+    CK(cudaMemcpyAsync(ctx->records_host, ctx->records, rec_bytes, cudaMemcpyDeviceToHost, st));
+  }
+  return SEED_OK;
+}
+
+// Runs the draft (draft = true) or verify phase of the planned round: directly on the caller's
+// stream, or as a CUDA graph captured once per batch size on the library's stream.
+seed_status run_phase(seed_ctx ctx, int n, bool draft, cudaStream_t st) {
+  seed_status s;
+  const int64_t k0 = ctx->kernel_launches;
+  if (draft) {
+    ctx->in_round = true;
+    ctx->rec_used = 0;
+    ctx->round_gemm_bytes = 0;
+    ctx->round_gemms = 0;
+  }
+  if (!ctx->use_graphs) {
+    s = draft ? enqueue_draft(ctx, st) : enqueue_verify(ctx, st);
+    if (s != SEED_OK) return s;
+    if (!draft) {
+      ctx->gemm_bytes += ctx->round_gemm_bytes;
+      ctx->gemm_launches += ctx->round_gemms;
+      ctx->in_round = false;
+      CK(cudaEventRecord(ctx->round_done, st));
+    }
+    return SEED_OK;
+  }
+  auto& G = ctx->graphs[n];
+  cudaGraphExec_t& ex = draft ? G.draft : G.verify;
+  if (!ex) {
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(ctx->gstream, cudaStreamCaptureModeThreadLocal));
+    s = draft ? enqueue_draft(ctx, ctx->gstream) : enqueue_verify(ctx, ctx->gstream);
+    cudaError_t e = cudaStreamEndCapture(ctx->gstream, &graph);
+    if (s != SEED_OK) return s;
+    CK(e);
+    CK(cudaGraphInstantiate(&ex, graph, 0));
+    cudaGraphDestroy(graph);
+    G.kernels += ctx->kernel_launches - k0;
+    if (!draft) {
+      G.gemm_bytes = ctx->round_gemm_bytes;
+      G.gemms = ctx->round_gemms;
+    }
+  } else {
+    ctx->kernel_launches += 0;  // counted below from the captured totals
+  }
+  CK(cudaEventRecord(ctx->ev_in, st));
+  CK(cudaStreamWaitEvent(ctx->gstream, ctx->ev_in, 0));
+  CK(cudaGraphLaunch(ex, ctx->gstream));
+  if (!draft) {
+    CK(cudaEventRecord(ctx->round_done, ctx->gstream));
+    ctx->kernel_launches = k0 + G.kernels;
+    ctx->gemm_bytes += G.gemm_bytes;
+    ctx->gemm_launches += G.gemms;
+    ctx->in_round = false;
+  }
+  CK(cudaEventRecord(ctx->ev_out, ctx->gstream));
+  CK(cudaStreamWaitEvent(st, ctx->ev_out, 0));
   return SEED_OK;
 }
 
@@ -685,6 +906,27 @@ seed_status seed_init(const seed_config* cfg, seed_ctx* out) {
   ok &= cudaMalloc(&ctx->ds.hist, (size_t)S * max_pos * 4) == cudaSuccess;
   ctx->ds.max_ctx = max_pos;
   ok &= cudaEventCreateWithFlags(&ctx->round_done, cudaEventDisableTiming) == cudaSuccess;
+  ok &= cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) == cudaSuccess;
+  ok &= cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming) == cudaSuccess;
+  ok &= cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking) == cudaSuccess;
+  {
+    const char* e = getenv("SEED_GRAPHS");
+    ctx->use_graphs = !(e && e[0] == '0');
+  }
+  if (ctx->profile) {
+    ctx->rec_cap = 8192;
+    ok &= cudaMalloc(&ctx->timing_rec, (size_t)ctx->rec_cap * 2 * 8) == cudaSuccess;
+    ok &= cudaMalloc(&ctx->timing_acc, 2 * 8) == cudaSuccess;
+    if (ok) {
+      std::vector<unsigned long long> init((size_t)ctx->rec_cap * 2);
+      for (int i = 0; i < ctx->rec_cap; ++i) {
+        init[2 * i] = ~0ull;
+        init[2 * i + 1] = 0ull;
+      }
+      ok &= cudaMemcpy(ctx->timing_rec, init.data(), init.size() * 8, cudaMemcpyHostToDevice) == cudaSuccess;
+      ok &= cudaMemset(ctx->timing_acc, 0, 16) == cudaSuccess;
+    }
+  }
   if (!ok) return fail_init(SEED_ENOMEM);
   if (seed_sched_create(nullptr, 0, &ctx->sched) != SEED_OK) return fail_init(SEED_ENOMEM);
   if (seed_table_create(g + 3, &ctx->table) != SEED_OK) return fail_init(SEED_ENOMEM);
@@ -715,10 +957,15 @@ void seed_destroy(seed_ctx ctx) {
   if (ctx->tok_host) cudaFreeHost(ctx->tok_host);
   ctx->arena.destroy();
   if (ctx->round_done) cudaEventDestroy(ctx->round_done);
-  for (auto& e : ctx->ev_pool) {
-    cudaEventDestroy(e.first);
-    cudaEventDestroy(e.second);
+  for (auto& kv : ctx->graphs) {
+    if (kv.second.draft) cudaGraphExecDestroy(kv.second.draft);
+    if (kv.second.verify) cudaGraphExecDestroy(kv.second.verify);
   }
+  if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
+  if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
+  if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
+  if (ctx->timing_rec) cudaFree(ctx->timing_rec);
+  if (ctx->timing_acc) cudaFree(ctx->timing_acc);
   if (ctx->sched) seed_sched_destroy(ctx->sched);
   if (ctx->table) seed_table_destroy(ctx->table);
   if (ctx->comm && g_nccl.destroy) g_nccl.destroy(ctx->comm);
@@ -730,6 +977,7 @@ seed_status seed_add_stream(seed_ctx ctx, uint32_t gid, const int32_t* prefix, i
   if (s != SEED_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
   if (!prefix || len < 2) return fail(ctx, SEED_EINVAL, "seed_add_stream", "prefix must hold >= 2 tokens");
+  if ((s = quiesce(ctx)) != SEED_OK) return s;
   if (len + ctx->cfg.max_new_tokens + ctx->cfg.gamma + 2 > ctx->cfg.max_ctx + ctx->cfg.gamma + 2)
     return fail(ctx, SEED_ECAPACITY, "seed_add_stream", "prefix + l exceeds max_ctx");
   for (int i = 0; i < len; ++i)
@@ -786,71 +1034,16 @@ seed_status seed_draft_round(seed_ctx ctx, const int32_t* ids, int32_t n, void* 
   cudaStream_t st = (cudaStream_t)stream;
   std::vector<int> slots;
   if ((s = map_batch(ctx, ids, n, slots)) != SEED_OK) return s;
-  if (ctx->round_pending) {
-    if ((s = complete_round(ctx)) != SEED_OK) return s;
-  }
-  const int g = ctx->cfg.gamma, V = ctx->cfg.target.vocab;
+  if (ctx->round_pending && (s = complete_round(ctx)) != SEED_OK) return s;
+  const int g = ctx->cfg.gamma;
   for (int b = 0; b < n; ++b) {
     const int T = (int)ctx->slots[slots[b]].T.size();
     if ((s = ensure_pages(ctx, ctx->tm, slots[b], T + g + 1, st)) != SEED_OK) return s;
     if ((s = ensure_pages(ctx, ctx->dm, slots[b], T + g + 1, st)) != SEED_OK) return s;
   }
-  Model& m = ctx->dm;
-  ctx->arena.begin();
-  Arena& A = ctx->arena;
-  // per-batch vectors: sids, rs, slots, T[-1]
-  const size_t o_sid = A.alloc(n), o_r = A.alloc(n), o_sl = A.alloc(n), o_last = A.alloc(n);
-  if (o_last == (size_t)-1) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
-  for (int b = 0; b < n; ++b) {
-    const SlotState& ss = ctx->slots[slots[b]];
-    A.host[o_sid + b] = (int32_t)ss.gid;
-    A.host[o_r + b] = ss.r;
-    A.host[o_sl + b] = slots[b];
-    A.host[o_last + b] = ss.T.back();
-  }
-  // step 1: rows (T[-2], T[-1]) per stream -- the first re-writes an existing entry when only
-  // one token is pending, so M = 2n always (DESIGN "draft step 1")
-  std::vector<ChunkDesc> steps(g);
-  std::vector<Segment> segs(n);
-  for (int b = 0; b < n; ++b) {
-    const SlotState& ss = ctx->slots[slots[b]];
-    const int T = (int)ss.T.size();
-    const size_t to = A.alloc(2);
-    if (to == (size_t)-1) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
-    A.host[to] = ss.T[T - 2];
-    A.host[to + 1] = ss.T[T - 1];
-    segs[b] = Segment{slots[b], T - 2, 2, (int)to};
-  }
-  size_t tok_off;
-  if (2 * n > kMaxChunkRows || !pack_chunk(ctx, segs, 2, &steps[0], &tok_off))
-    return fail(ctx, SEED_ECAPACITY, "seed_draft_round", "batch too large");
-  for (int j = 2; j <= g; ++j) {
-    for (int b = 0; b < n; ++b) {
-      const int T = (int)ctx->slots[slots[b]].T.size();
-      segs[b] = Segment{slots[b], T + j - 2, 1, -1};
-    }
-    if (!pack_chunk(ctx, segs, 2, &steps[j - 1], &tok_off)) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
-    steps[j - 1].tok = TokSrc{ctx->xs + (j - 2), g};  // x_{j-1} of every stream, [B][g] layout
-  }
-  CK(A.upload(st));
-  const uint32_t* sids = reinterpret_cast<const uint32_t*>(A.dev + o_sid);
-  const int32_t* rs = A.dev + o_r;
-  CK(cudaMemcpyAsync(ctx->sids_dev, sids, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
-  CK(cudaMemcpyAsync(ctx->rs_dev, rs, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
-  CK(cudaMemcpyAsync(ctx->slots_dev, A.dev + o_sl, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
-  // verify input column 0 = T[-1]
-  CK(cudaMemcpy2DAsync(ctx->vtok, (size_t)(g + 1) * 4, A.dev + o_last, 4, 4, n, cudaMemcpyDeviceToDevice, st));
-  const uint32_t k0 = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu), k1 = (uint32_t)(ctx->cfg.seed >> 32);
-  for (int j = 1; j <= g; ++j) {
-    ChunkDesc& c = steps[j - 1];
-    c.Y = ctx->drf_logits + (size_t)(j - 1) * V;
-    c.ldY = g * V;
-    if ((s = forward_chunk(ctx, m, c, st)) != SEED_OK) return s;
-    // K1 sampler: x_j -> xs[b][j-1] and the verify input vtok[b][j]
-    CK(seed::draft_sample(c.Y, (long)g * V, n, V, ctx->cfg.temperature, k0, k1, ctx->sids_dev, ctx->rs_dev, j,
-                          ctx->xs + (j - 1), g, ctx->vtok + j, g + 1, st));
-    ctx->kernel_launches++;
-  }
+  RoundPlan& P = ctx->plan;
+  if ((s = build_round_plan(ctx, slots, n, P)) != SEED_OK) return s;
+  if ((s = run_phase(ctx, n, true, st)) != SEED_OK) return s;
   ctx->drafted.assign(ids, ids + n);
   return SEED_OK;
 }
@@ -862,68 +1055,11 @@ seed_status seed_verify(seed_ctx ctx, const int32_t* ids, int32_t n, int32_t* ou
   cudaStream_t st = (cudaStream_t)stream;
   if ((int)ctx->drafted.size() != n || !std::equal(ids, ids + n, ctx->drafted.begin()))
     return fail(ctx, SEED_ESTATE, "seed_verify", "batch was not drafted");
-  std::vector<int> slots;
-  if ((s = map_batch(ctx, ids, n, slots)) != SEED_OK) return s;
-  const int g = ctx->cfg.gamma, V = ctx->cfg.target.vocab;
-  Model& m = ctx->tm;
-  // a3: one target forward over [T[-1], x_1..x_g] per stream, chunked by whole streams
-  const int per_chunk = std::max(1, kMaxChunkRows / (g + 1));
-  for (int b0 = 0; b0 < n; b0 += per_chunk) {
-    const int nb = std::min(per_chunk, n - b0);
-    ctx->arena.begin();
-    std::vector<Segment> segs(nb);
-    for (int b = 0; b < nb; ++b) {
-      const int T = (int)ctx->slots[slots[b0 + b]].T.size();
-      segs[b] = Segment{slots[b0 + b], T - 1, g + 1, -1};
-    }
-    ChunkDesc c;
-    size_t tok_off;
-    if (!pack_chunk(ctx, segs, 1, &c, &tok_off)) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
-    CK(ctx->arena.upload(st));
-    c.tok = TokSrc{ctx->vtok + (size_t)b0 * (g + 1), 1};
-    c.Y = ctx->tgt_logits + (size_t)b0 * (g + 1) * V;
-    c.ldY = V;
-    if ((s = forward_chunk(ctx, m, c, st)) != SEED_OK) return s;
-  }
-  // a4: K4 fused vocabulary kernel
-  seed::VerifyArgs a{};
-  a.zt = ctx->tgt_logits;
-  a.zd = ctx->drf_logits;
-  a.xs = ctx->xs;
-  a.zt_stride_b = (long)(g + 1) * V;
-  a.zd_stride_b = (long)g * V;
-  a.B = n;
-  a.gamma = g;
-  a.V = V;
-  a.T = ctx->cfg.temperature;
-  a.k0 = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu);
-  a.k1 = (uint32_t)(ctx->cfg.seed >> 32);
-  a.sids = ctx->sids_dev;
-  a.rs = ctx->rs_dev;
-  a.bonus = ctx->cfg.bonus;
-  a.out_tok = ctx->out_tok;
-  a.out_cnt = ctx->out_cnt;
-  a.out_acc = ctx->out_acc;
-  CK(seed::vocab_verify(a, st));
-  // a5: K5 commit + rollback, emit the exchange records
-  const int world = std::max(ctx->cfg.world, 1);
-  const size_t rec_bytes = (size_t)ctx->C * (g + 3) * 4;
-  CK(cudaMemsetAsync(ctx->records, 0xFF, rec_bytes, st));
-  CK(seed::rollback_commit(ctx->ds, ctx->slots_dev, n, g, ctx->out_tok, ctx->out_cnt, ctx->cfg.max_new_tokens,
-                           ctx->records, ctx->sids_dev, st));
-  ctx->kernel_launches += 2;
-  // a6: all-gather of the per-rank records over NVLink (world > 1)
-  if (world > 1) {
-    if (g_nccl.allgather(ctx->records, ctx->records_all, (size_t)ctx->C * (g + 3), kNcclInt32, ctx->comm, st) != 0)
-      return fail(ctx, SEED_ENCCL, "ncclAllGather", "records");
-    CK(cudaMemcpyAsync(ctx->records_host, ctx->records_all, rec_bytes * world, cudaMemcpyDeviceToHost, st));
-  } else {
-    CK(cudaMemcpyAsync(ctx->records_host, ctx->records, rec_bytes, cudaMemcpyDeviceToHost, st));
-  }
+  if ((s = run_phase(ctx, n, false, st)) != SEED_OK) return s;
+  const int g = ctx->cfg.gamma;
   if (out_tok)
     CK(cudaMemcpyAsync(out_tok, ctx->out_tok, (size_t)n * (g + 1) * 4, cudaMemcpyDeviceToDevice, st));
   if (out_cnt) CK(cudaMemcpyAsync(out_cnt, ctx->out_cnt, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
-  CK(cudaEventRecord(ctx->round_done, st));
   ctx->round_pending = true;
   ctx->last_batch.assign(ids, ids + n);
   ctx->drafted.clear();
@@ -1009,6 +1145,7 @@ seed_status seed_forward_logits(seed_ctx ctx, int32_t which, const int32_t* toke
   if (s != SEED_OK) return s;
   if (!tokens || n < 1 || !logits) return fail(ctx, SEED_EINVAL, "seed_forward_logits", "args");
   cudaStream_t st = (cudaStream_t)stream;
+  if ((s = quiesce(ctx)) != SEED_OK) return s;
   Model& m = which ? ctx->tm : ctx->dm;
   const int slot = ctx->n_slots - 1;  // scratch slot
   if ((s = ensure_pages(ctx, m, slot, n, st)) != SEED_OK) return s;
@@ -1029,11 +1166,12 @@ seed_status seed_last_round_buffers(seed_ctx ctx, const float** t, const float**
 seed_status seed_get_profile(seed_ctx ctx, double* gemm_ms, int64_t* launches, double* bytes, int64_t* kernels) {
   if (!ctx) return SEED_EINVAL;
   double ms = 0;
-  for (size_t i = 0; i < ctx->ev_used; ++i) {
-    float t = 0;
-    if (cudaEventSynchronize(ctx->ev_pool[i].second) != cudaSuccess) return fail(ctx, SEED_ECUDA, "profile", "");
-    cudaEventElapsedTime(&t, ctx->ev_pool[i].first, ctx->ev_pool[i].second);
-    ms += t;
+  if (ctx->timing_acc) {
+    unsigned long long acc[2] = {0, 0};
+    if (cudaDeviceSynchronize() != cudaSuccess ||
+        cudaMemcpy(acc, ctx->timing_acc, sizeof(acc), cudaMemcpyDeviceToHost) != cudaSuccess)
+      return fail(ctx, SEED_ECUDA, "seed_get_profile", "");
+    ms = acc[0] * 1e-6;
   }
   if (gemm_ms) *gemm_ms = ms;
   if (launches) *launches = ctx->gemm_launches;
@@ -1044,7 +1182,8 @@ seed_status seed_get_profile(seed_ctx ctx, double* gemm_ms, int64_t* launches, d
 
 seed_status seed_reset_profile(seed_ctx ctx) {
   if (!ctx) return SEED_EINVAL;
-  ctx->ev_used = 0;
+  if (ctx->timing_acc && cudaMemset(ctx->timing_acc, 0, 2 * sizeof(unsigned long long)) != cudaSuccess)
+    return fail(ctx, SEED_ECUDA, "seed_reset_profile", "");
   ctx->gemm_bytes = 0;
   ctx->gemm_launches = 0;
   ctx->kernel_launches = 0;
@@ -1094,6 +1233,8 @@ seed_status seed_op_gemm(const void* W, int32_t N, int32_t K, const void* X, int
   }
   cudaFreeAsync(part, st);
   cudaFreeAsync(xpad, st);
+  cudaStreamSynchronize(st);
+  seed::gemm_plan_free(&p);
   return s;
 }
 

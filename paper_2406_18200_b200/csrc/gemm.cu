@@ -15,8 +15,11 @@
 // points depend on (N, K) only, never on M, so every output column is computed in the
 // same order whatever the batch (batch invariance, DESIGN R19).
 #include <cuda.h>
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -33,7 +36,14 @@ constexpr int SMEM_BUDGET = 220 * 1024;
 struct GemmArgs {
   int KB, U, G, S, M, m_pad, stages;
   float* partial;
+  unsigned long long* timing;  // optional [2]: min CTA start, max CTA end (globaltimer ns)
 };
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   // K-major operand, 128B swizzle: 8-row x 128B atoms, SBO = 1024 B, LBO unused, version 1
@@ -62,6 +72,8 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
   const int c = blockIdx.x;
   const long u_begin = (long)c * a.U / a.G, u_end = (long)(c + 1) * a.U / a.G;
   if (u_begin >= u_end) return;
+  pdl_trigger();
+  if (a.timing && threadIdx.x == 0) atomicMin(&a.timing[0], globaltimer());
 
   uint32_t cols = 32;
   while (cols < (uint32_t)(2 * a.m_pad)) cols <<= 1;
@@ -91,9 +103,23 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
     if (elect_one()) {
       const uint64_t pol_w = l2_policy_evict_first();
       const uint64_t pol_x = l2_policy_evict_last();
-      int stage = 0;
-      uint32_t phase = 0;
-      for (long u = u_begin; u < u_end; ++u) {
+      // The weights do not depend on the previous kernel: fill the whole ring with weight
+      // tiles before waiting on it (PDL), so weight streaming overlaps the predecessor.
+      const long n_pre = min((long)S, u_end - u_begin);
+      for (long i = 0; i < n_pre; ++i) {
+        const long u = u_begin + i;
+        const int t = (int)(u / a.KB), kb = (int)(u % a.KB);
+        mbar_arrive_expect_tx(&full[i], W_TILE_BYTES + x_bytes);
+        tma_load_2d(sW + i * W_TILE_BYTES, &tmW, &full[i], kb * BLOCK_K, t * BLOCK_N, pol_w);
+      }
+      pdl_wait();  // X (the activations) is written by the previous kernel
+      for (long i = 0; i < n_pre; ++i) {
+        const long u = u_begin + i;
+        tma_load_2d(sX + i * x_bytes, &tmX, &full[i], (int)(u % a.KB) * BLOCK_K, 0, pol_x);
+      }
+      int stage = (int)(n_pre % S);
+      uint32_t phase = n_pre == S ? 1u : 0u;
+      for (long u = u_begin + n_pre; u < u_end; ++u) {
         const int t = (int)(u / a.KB), kb = (int)(u % a.KB);
         mbar_wait(&empty[stage], phase ^ 1);
         mbar_arrive_expect_tx(&full[stage], W_TILE_BYTES + x_bytes);
@@ -149,6 +175,7 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
     // ---------------- epilogue warps 2..5: TMEM -> fp32 partial [m][128]
     const int lane_grp = warp & 3;               // TMEM lanes this warp may access
     const int nl = lane_grp * 32 + lane;         // weight row within the tile
+    pdl_wait();                                  // the partial buffer is read by the predecessor
     int seg = 0;
     long u = u_begin;
     while (u < u_end) {
@@ -178,6 +205,20 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
   __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc(tmem_base, cols);
+  if (a.timing && threadIdx.x == 0) atomicMax(&a.timing[1], globaltimer());
+}
+
+// adds the span of every recorded launch to acc[0] (ns) and the count to acc[1]; resets records
+__global__ void timing_accumulate_kernel(unsigned long long* rec, int n, unsigned long long* acc) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const unsigned long long s = rec[2 * i], e = rec[2 * i + 1];
+    if (e > s && s != ~0ull) {
+      atomicAdd(&acc[0], e - s);
+      atomicAdd(&acc[1], 1ull);
+    }
+    rec[2 * i] = ~0ull;
+    rec[2 * i + 1] = 0ull;
+  }
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -217,17 +258,57 @@ void gemm_plan(GemmPlan* p, const void* W, int N, int K) {
   p->KB = K / BLOCK_K;
   p->tiles = (N + BLOCK_N - 1) / BLOCK_N;
   p->U = p->tiles * p->KB;
-  p->G = p->U < kNumSMs ? p->U : kNumSMs;
+  // at least 4 k-blocks per CTA so a tile meets few partial segments (small draft GEMMs)
+  p->G = std::max(1, std::min(kNumSMs, p->U / 4));
   // segments per CTA: ceil(range / KB) + 1 bound
   const int range = (p->U + p->G - 1) / p->G;
   p->S = (range + p->KB - 1) / p->KB + 1;
   encode_tmap_2d(&p->tmW, W, (uint64_t)K, (uint64_t)N, BLOCK_K, BLOCK_N);
+  // per tile: the partial-segment indices (c * S + j) in CTA order -- the fixed, M-independent
+  // reduction order every consumer uses (R19)
+  std::vector<std::vector<int>> lists(p->tiles);
+  for (int c = 0; c < p->G; ++c) {
+    const long ub = (long)c * p->U / p->G, ue = (long)(c + 1) * p->U / p->G;
+    if (ub >= ue) continue;
+    const long tb = ub / p->KB;
+    for (long t = tb; t <= (ue - 1) / p->KB; ++t) lists[t].push_back(c * p->S + (int)(t - tb));
+  }
+  p->maxseg = 0;
+  for (auto& l : lists) p->maxseg = std::max<int>(p->maxseg, (int)l.size());
+  std::vector<int> flat((size_t)p->tiles * (p->maxseg + 1), -1);
+  for (int t = 0; t < p->tiles; ++t) {
+    flat[(size_t)t * (p->maxseg + 1)] = (int)lists[t].size();
+    for (size_t k = 0; k < lists[t].size(); ++k) flat[(size_t)t * (p->maxseg + 1) + 1 + k] = lists[t][k];
+  }
+  p->seg = nullptr;
+  if (cudaMalloc(&p->seg, flat.size() * sizeof(int)) == cudaSuccess)
+    cudaMemcpy(p->seg, flat.data(), flat.size() * sizeof(int), cudaMemcpyHostToDevice);
+}
+
+void gemm_plan_free(GemmPlan* p) {
+  if (p->seg) cudaFree(p->seg);
+  p->seg = nullptr;
+}
+
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("SEED_PDL");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
 }
 
 size_t gemm_partial_floats(const GemmPlan& p, int M) { return (size_t)p.G * p.S * M * BLOCK_N; }
 
+cudaError_t timing_accumulate(unsigned long long* rec, int n, unsigned long long* acc, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  timing_accumulate_kernel<<<1, 256, 0, st>>>(rec, n, acc);
+  return cudaGetLastError();
+}
+
 cudaError_t gemm_run(const GemmPlan& p, const CUtensorMap& tmX, int M, float* partial, PartialView* view,
-                     cudaStream_t st) {
+                     cudaStream_t st, unsigned long long* timing) {
   GemmArgs a;
   a.KB = p.KB;
   a.U = p.U;
@@ -241,15 +322,16 @@ cudaError_t gemm_run(const GemmPlan& p, const CUtensorMap& tmX, int M, float* pa
   if (stages > MAX_STAGES) stages = MAX_STAGES;
   a.stages = stages;
   a.partial = partial;
+  a.timing = timing;
   const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 4) * 8 + 16;
   static bool attr_done = false;
   if (!attr_done) {
     cudaFuncSetAttribute(gemm_streamk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_done = true;
   }
-  gemm_streamk_kernel<<<p.G, 192, smem, st>>>(p.tmW, tmX, a);
-  if (view) *view = PartialView{partial, p.KB, p.U, p.G, p.S, M};
-  return cudaGetLastError();
+  cudaError_t e = launch(gemm_streamk_kernel, dim3(p.G), dim3(192), smem, st, p.tmW, tmX, a);
+  if (view) *view = PartialView{partial, p.seg, p.maxseg, M};
+  return e;
 }
 
 }  // namespace seed

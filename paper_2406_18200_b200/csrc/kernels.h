@@ -16,6 +16,7 @@ struct KVLayout {
   int32_t max_pages;  // per slot
   int32_t n_layers, Hk, Dh, P;
   __host__ __device__ size_t page_elems() const { return (size_t)n_layers * 2 * Hk * P * Dh; }
+  __host__ __device__ size_t vofs() const { return (size_t)Hk * P * Dh; }  // K -> V of the same layer
   __host__ __device__ size_t offset(int page, int layer, int kv, int h, int slot_in_page) const {
     return (size_t)page * page_elems() + ((size_t)(layer * 2 + kv) * Hk + h) * P * Dh + (size_t)slot_in_page * Dh;
   }
@@ -25,21 +26,26 @@ struct KVLayout {
 // Y[m][n] = sum_k X[m][k] W[n][k]; W [N][K] bf16, X [Mcap][K] bf16 (rows >= M ignored).
 struct GemmPlan {
   int N, K, KB, tiles, U, G, S;  // S = max segments per CTA
+  int maxseg;                    // max partial segments per tile
+  int* seg;                      // device [tiles][maxseg + 1]: count, then segment ids in CTA order
   CUtensorMap tmW;
 };
 
 struct PartialView {  // read side of the split-K partial sums, batch-invariant order
   const float* p;
-  int KB, U, G, S, M;
+  const int* seg;
+  int maxseg, M;
 };
 
 bool encode_tmap_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
                     uint32_t box_outer);
 void gemm_plan(GemmPlan* plan, const void* W, int N, int K);
+void gemm_plan_free(GemmPlan* plan);
 size_t gemm_partial_floats(const GemmPlan& plan, int M);
 // launches the tcgen05 main loop; returns the view the epilogue kernels read
 cudaError_t gemm_run(const GemmPlan& plan, const CUtensorMap& tmX, int M, float* partial, PartialView* view,
-                     cudaStream_t st);
+                     cudaStream_t st, unsigned long long* timing = nullptr);
+cudaError_t timing_accumulate(unsigned long long* rec, int n, unsigned long long* acc, cudaStream_t st);
 int gemm_mpad(int M);
 
 // ------------------------------------------------------------------ epilogues / elementwise

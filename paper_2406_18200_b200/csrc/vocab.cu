@@ -12,6 +12,8 @@
 // it (DESIGN "decision precision"), so accepted lengths and token ids match bit for bit.
 #include <cooperative_groups.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "philox.cuh"
@@ -88,69 +90,177 @@ __device__ Best block_best(Best b, Best* red) {
   return r;
 }
 
-__device__ __forceinline__ float scaled(const float* z, int v, float T) { return __fdiv_rn(__ldg(z + v), T); }
+__device__ __forceinline__ float scaled_v(float z, float T) { return __fdiv_rn(z, T); }
 
 // -log(E), E = -log1p(-u): the exponential-race offset, fp64
 __device__ __forceinline__ double neg_log_exp(double u) { return -log(-log1p(-u)); }
 
-// race over this CTA's slice with weights given by `wfn(v)` (fp64, -inf = excluded)
-template <class WFn>
-__device__ Best race_slice(int v0, int v1, uint32_t c1, uint32_t r, uint32_t sid, uint32_t k0, uint32_t k1,
-                           WFn wfn) {
-  Best b{-INFINITY, -1};
-  for (int g = v0 + 4 * (int)threadIdx.x; g < v1; g += 4 * VT) {
+// Stage rows of this CTA's vocabulary slice into shared memory: one bulk TMA copy per row
+// when the slice is 16-byte aligned, coalesced loads otherwise.  All threads call it.
+struct Stager {
+  float* buf;       // [nbuf][slice]
+  uint64_t* bar;
+  uint32_t phase;
+  int slice, v0, n; // n = valid elements of this CTA's slice
+  bool bulk;
+  template <class RowPtr>
+  __device__ void stage(int first, int k, RowPtr rowptr) {
+    if (n <= 0) return;
+    if (bulk) {
+      if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(bar, (uint32_t)(k * n * 4));
+        for (int i = 0; i < k; ++i) bulk_g2s(buf + (size_t)i * slice, rowptr(first + i) + v0, (uint32_t)(n * 4), bar);
+      }
+      mbar_wait(bar, phase);
+      phase ^= 1;
+    } else {
+      for (int i = 0; i < k; ++i) {
+        const float* src = rowptr(first + i) + v0;
+        for (int l = threadIdx.x; l < n; l += VT) buf[(size_t)i * slice + l] = __ldg(src + l);
+      }
+      __syncthreads();
+    }
+  }
+};
+
+constexpr int SMEM_ROWS_BYTES = 200 * 1024;
+
+__device__ __forceinline__ Best cluster_best(cg::cluster_group& cluster, Best* cta_best, Best mine) {
+  if (threadIdx.x == 0) *cta_best = mine;
+  cluster.sync();
+  Best acc = *cluster.map_shared_rank(cta_best, 0);
+  for (int c = 1; c < CS; ++c) acc = best_merge(acc, *cluster.map_shared_rank(cta_best, c));
+  cluster.sync();  // every peer has read cta_best before it may change
+  return acc;
+}
+
+
+// Exponential race over this CTA's slice, decided exactly as in fp64 (R21): pass A scores every
+// id in fp32 (w32 returns NAN where fp32 is not accurate enough; those ids are scored in fp64),
+// the cluster agrees on the best fp32 key; pass B rescoring in fp64 every id within RACE_MARGIN
+// of it (>= 100x the fp32 error bound) and takes the exact argmax, ties to the smallest id.
+constexpr float RACE_MARGIN = 1e-3f;
+
+template <class W32, class W64>
+__device__ Best race_exact(cg::cluster_group& cluster, int v0, int n, uint32_t c1, uint32_t r, uint32_t sid,
+                           uint32_t k0, uint32_t k1, float* keys, float* red_f, float* cta_f, Best* red_b,
+                           Best* cta_best, W32 w32, W64 w64) {
+  float best32 = -INFINITY;
+  for (int l = 4 * (int)threadIdx.x; l < n; l += 4 * VT) {
+    const int g = v0 + l;
     const Philox4 ph = philox4x32_10((uint32_t)(g >> 2), c1, r, sid, k0, k1);
     const uint32_t words[4] = {ph.x, ph.y, ph.z, ph.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int v = g + e;
-      if (v >= v1) break;
-      const double w = wfn(v);
-      if (w == -INFINITY) continue;
-      const double key = w + neg_log_exp(philox_uniform(words[e]));
-      if (b.v < 0 || key > b.k) b = Best{key, v};
+      if (l + e >= n) break;
+      const float w = w32(l + e);
+      float key = -INFINITY;
+      if (w != w) {  // NaN: fp64 needed
+        const double wd = w64(l + e);
+        if (wd != -INFINITY) key = (float)(wd + neg_log_exp(philox_uniform(words[e])));
+      } else if (w != -INFINITY) {
+        const float u = (float)philox_uniform(words[e]);
+        key = w - logf(-log1pf(-u));
+      }
+      keys[l + e] = key;
+      best32 = fmaxf(best32, key);
     }
   }
-  return b;
+  // cluster-wide max of the fp32 keys
+  best32 = warp_max(best32);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red_f[threadIdx.x >> 5] = best32;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = red_f[0];
+    for (int i = 1; i < VT / 32; ++i) m = fmaxf(m, red_f[i]);
+    *cta_f = m;
+  }
+  cluster.sync();
+  float gmax = -INFINITY;
+  for (int c = 0; c < CS; ++c) gmax = fmaxf(gmax, *cluster.map_shared_rank(cta_f, c));
+  Best b{-INFINITY, -1};
+  if (gmax != -INFINITY) {
+    const float thr = gmax - RACE_MARGIN;
+    for (int l = threadIdx.x; l < n; l += VT) {
+      if (keys[l] < thr) continue;
+      const int g = v0 + l;
+      const Philox4 ph = philox4x32_10((uint32_t)(g >> 2), c1, r, sid, k0, k1);
+      const uint32_t words[4] = {ph.x, ph.y, ph.z, ph.w};
+      const double wd = w64(l);
+      if (wd == -INFINITY) continue;
+      const double key = wd + neg_log_exp(philox_uniform(words[g & 3]));
+      if (b.v < 0 || key > b.k || (key == b.k && g < b.v)) b = Best{key, g};
+    }
+  }
+  b = block_best(b, red_b);
+  return cluster_best(cluster, cta_best, b);
 }
 
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(VT)
-vocab_verify_kernel(VerifyArgs A) {
+vocab_verify_kernel(VerifyArgs A, int nbuf) {
+  extern __shared__ __align__(128) float rows_s[];  // [nbuf][slice] rows, then [slice] race keys
+  __shared__ float red_f[VT / 32];
+  __shared__ float cta_f;
   __shared__ Stat red_s[VT / 32];
   __shared__ Best red_b[VT / 32];
   __shared__ Stat cta_stat[MAX_ROWS];
   __shared__ Stat glob[MAX_ROWS];
   __shared__ Best cta_best;
-  __shared__ int s_a, s_y;
+  __shared__ int s_a;
+  __shared__ __align__(8) uint64_t bar;
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int b = blockIdx.x / CS;
   const int g = A.gamma, V = A.V;
   const int R = 2 * g + 1;
   const int slice = ((V + CS - 1) / CS + 3) & ~3;
-  const int v0 = min(V, rank * slice), v1 = min(V, v0 + slice);
+  const int v0 = min(V, rank * slice), n = min(V, v0 + slice) - v0;
   const float* zt = A.zt + (size_t)b * A.zt_stride_b;
   const float* zd = A.zd + (size_t)b * A.zd_stride_b;
   const uint32_t sid = A.sids[b], rr = (uint32_t)A.rs[b];
+  auto rowptr = [&](int row) -> const float* {
+    return row <= g ? zt + (size_t)row * V : zd + (size_t)(row - g - 1) * V;
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_trigger();
+  pdl_wait();   // the logits are written by the previous kernels
+  Stager sg{rows_s, &bar, 0u, slice, v0, n, (V % 4 == 0) && (n % 4 == 0)};
+  float* keys_s = rows_s + (size_t)nbuf * slice;
 
   // ---- phase 1: per-row statistics over the slice (rows 0..g target, g+1..2g draft)
-  for (int row = 0; row < R; ++row) {
-    const float* z = row <= g ? zt + (size_t)row * V : zd + (size_t)(row - g - 1) * V;
-    Stat s{-INFINITY, 0.0, -1};
-    for (int v = v0 + threadIdx.x; v < v1; v += VT) {
-      const double x = (double)scaled(z, v, A.T);
-      if (s.i < 0) {
-        s = Stat{x, 0.0, v};
-      } else if (x > s.m) {
-        s.S = (s.S + 1.0) * exp(s.m - x);  // the old maximum joins the tail
-        s.m = x;
-        s.i = v;
-      } else {
-        s.S += exp(x - s.m);
+  int resident0 = -1, resident_k = 0;
+  for (int r0 = 0; r0 < R; r0 += nbuf) {
+    const int k = min(nbuf, R - r0);
+    if (r0 > 0) __syncthreads();
+    sg.stage(r0, k, rowptr);
+    resident0 = r0;
+    resident_k = k;
+    for (int i = 0; i < k; ++i) {
+      const float* zs = rows_s + (size_t)i * slice;
+      Stat s{-INFINITY, 0.0, -1};
+      float mf = -INFINITY;  // fp32 copy of s.m (the maxima are fp32 values)
+      for (int l = threadIdx.x; l < n; l += VT) {
+        const float xf = scaled_v(zs[l], A.T);
+        if (s.i < 0) {
+          s = Stat{(double)xf, 0.0, v0 + l};
+          mf = xf;
+        } else if (xf > mf) {
+          s.S = (s.S + 1.0) * exp(s.m - (double)xf);  // the old maximum joins the tail
+          s.m = (double)xf;
+          s.i = v0 + l;
+          mf = xf;
+        } else {
+          s.S += (double)expf(xf - mf);  // terms <= 1 in fp32, summed in fp64 (R21)
+        }
       }
+      const Stat t = block_stat(s, red_s);
+      if (threadIdx.x == 0) cta_stat[r0 + i] = t;
     }
-    const Stat t = block_stat(s, red_s);
-    if (threadIdx.x == 0) cta_stat[row] = t;
   }
   cluster.sync();
   // ---- cluster merge in rank order (identical result in every CTA)
@@ -168,8 +278,8 @@ vocab_verify_kernel(VerifyArgs A) {
     for (int j = 1; j <= g; ++j) {
       const int x = A.xs[(size_t)b * g + (j - 1)];
       const Stat st = glob[j - 1], sq = glob[g + j];
-      const double lp = ((double)scaled(zt + (size_t)(j - 1) * V, x, A.T) - st.m) - log1p(st.S);
-      const double lq = ((double)scaled(zd + (size_t)(j - 1) * V, x, A.T) - sq.m) - log1p(sq.S);
+      const double lp = ((double)scaled_v(__ldg(zt + (size_t)(j - 1) * V + x), A.T) - st.m) - log1p(st.S);
+      const double lq = ((double)scaled_v(__ldg(zd + (size_t)(j - 1) * V + x), A.T) - sq.m) - log1p(sq.S);
       const double rho = exp(fmin(0.0, lp - lq));
       const Philox4 ph = philox4x32_10(0u, (kTagAccept << 24) | (uint32_t)j, rr, sid, A.k0, A.k1);
       const double u = philox_uniform(ph.x);
@@ -188,59 +298,75 @@ vocab_verify_kernel(VerifyArgs A) {
   __syncthreads();
   const int a = s_a;
 
-  // ---- phase 3: residual race on row a (0-based) or bonus race on row g
+  // ---- phase 3: residual race on row a (0-based) or bonus race on row g, from shared memory
+  auto resident = [&](int row) -> const float* {
+    return (row >= resident0 && row < resident0 + resident_k) ? rows_s + (size_t)(row - resident0) * slice : nullptr;
+  };
   const uint32_t c1 = (kTagResample << 24) | (uint32_t)(a + 1);
   int y = -1;
   if (a < g || A.bonus) {
-    Best bb;
-    if (a < g) {
-      const Stat st = glob[a], sq = glob[g + 1 + a];
-      const double l1t = log1p(st.S), l1q = log1p(sq.S);
-      const float* zta = zt + (size_t)a * V;
-      const float* zda = zd + (size_t)a * V;
-      bb = race_slice(v0, v1, c1, rr, sid, A.k0, A.k1, [&](int v) -> double {
-        const double lp = ((double)scaled(zta, v, A.T) - st.m) - l1t;
-        const double lq = ((double)scaled(zda, v, A.T) - sq.m) - l1q;
-        return lq < lp ? lp + log(-expm1(lq - lp)) : -INFINITY;
-      });
-    } else {
-      const float* ztg = zt + (size_t)g * V;
-      bb = race_slice(v0, v1, c1, rr, sid, A.k0, A.k1, [&](int v) -> double { return (double)scaled(ztg, v, A.T); });
-    }
-    bb = block_best(bb, red_b);
-    if (threadIdx.x == 0) cta_best = bb;
-    cluster.sync();
-    if (threadIdx.x == 0) {
-      Best acc = *cluster.map_shared_rank(&cta_best, 0);
-      for (int c = 1; c < CS; ++c) acc = best_merge(acc, *cluster.map_shared_rank(&cta_best, c));
-      s_y = acc.v;
-    }
-    __syncthreads();
-    y = s_y;
-    if (y < 0 && a < g) {
-      // empty residual (rounding only): bonus rule on the same row, same uniforms
-      const float* zta = zt + (size_t)a * V;
-      Best fb = race_slice(v0, v1, c1, rr, sid, A.k0, A.k1, [&](int v) -> double { return (double)scaled(zta, v, A.T); });
-      fb = block_best(fb, red_b);
-      cluster.sync();   // everyone finished reading cta_best
-      if (threadIdx.x == 0) cta_best = fb;
-      cluster.sync();
-      if (threadIdx.x == 0) {
-        Best acc = *cluster.map_shared_rank(&cta_best, 0);
-        for (int c = 1; c < CS; ++c) acc = best_merge(acc, *cluster.map_shared_rank(&cta_best, c));
-        s_y = acc.v;
-      }
+    const int rt = a < g ? a : g;           // target row of the race
+    const int rd = g + 1 + a;               // draft row (residual only)
+    const float* zt_s = resident(rt);
+    const float* zd_s = a < g ? resident(rd) : nullptr;
+    if (!zt_s || (a < g && !zd_s)) {        // not resident: stage the rows into buffers 0 / 1
       __syncthreads();
-      y = s_y;
+      sg.stage(rt, 1, rowptr);
+      resident0 = rt;
+      resident_k = 1;
+      zt_s = rows_s;
+      if (a < g) {
+        if (threadIdx.x == 0 && sg.bulk && n > 0) {
+          mbar_arrive_expect_tx(&bar, (uint32_t)(n * 4));
+          bulk_g2s(rows_s + slice, rowptr(rd) + v0, (uint32_t)(n * 4), &bar);
+        }
+        if (sg.bulk && n > 0) {
+          mbar_wait(&bar, sg.phase);
+          sg.phase ^= 1;
+        } else {
+          for (int l = threadIdx.x; l < n; l += VT) rows_s[slice + l] = __ldg(rowptr(rd) + v0 + l);
+          __syncthreads();
+        }
+        zd_s = rows_s + slice;
+      }
+    }
+    const Stat st = glob[rt];
+    const double l1t = log1p(st.S);
+    const float mt = (float)st.m, l1tf = (float)l1t;
+    auto bonus32 = [&](int l) -> float { return scaled_v(zt_s[l], A.T); };
+    auto bonus64 = [&](int l) -> double { return (double)scaled_v(zt_s[l], A.T); };
+    if (a < g) {
+      const Stat sq = glob[g + 1 + a];
+      const double l1q = log1p(sq.S);
+      const float mq = (float)sq.m, l1qf = (float)l1q;
+      auto res32 = [&](int l) -> float {
+        const float lp = (scaled_v(zt_s[l], A.T) - mt) - l1tf;
+        const float lq = (scaled_v(zd_s[l], A.T) - mq) - l1qf;
+        const float dlt = lq - lp;
+        if (dlt > -0.05f) return dlt >= 0.05f ? -INFINITY : NAN;  // near-equal p, q: fp64
+        return lp + logf(-expm1f(dlt));
+      };
+      auto res64 = [&](int l) -> double {
+        const double lp = ((double)scaled_v(zt_s[l], A.T) - st.m) - l1t;
+        const double lq = ((double)scaled_v(zd_s[l], A.T) - sq.m) - l1q;
+        return lq < lp ? lp + log(-expm1(lq - lp)) : -INFINITY;
+      };
+      y = race_exact(cluster, v0, n, c1, rr, sid, A.k0, A.k1, keys_s, red_f, &cta_f, red_b, &cta_best, res32, res64).v;
+      if (y < 0)  // empty residual (rounding only): bonus rule on the same row, same uniforms
+        y = race_exact(cluster, v0, n, c1, rr, sid, A.k0, A.k1, keys_s, red_f, &cta_f, red_b, &cta_best, bonus32,
+                       bonus64).v;
+    } else {
+      y = race_exact(cluster, v0, n, c1, rr, sid, A.k0, A.k1, keys_s, red_f, &cta_f, red_b, &cta_best, bonus32,
+                     bonus64).v;
     }
   }
   if (rank == 0 && threadIdx.x == 0) {
     int32_t* ot = A.out_tok + (size_t)b * (g + 1);
     for (int j = 0; j < a; ++j) ot[j] = A.xs[(size_t)b * g + j];
-    int n = a;
-    if (y >= 0) ot[n++] = y;
-    for (int j = n; j <= g; ++j) ot[j] = -1;
-    if (A.out_cnt) A.out_cnt[b] = n;
+    int cnt = a;
+    if (y >= 0) ot[cnt++] = y;
+    for (int j = cnt; j <= g; ++j) ot[j] = -1;
+    if (A.out_cnt) A.out_cnt[b] = cnt;
     if (A.out_acc) A.out_acc[b] = a;
   }
   if (A.stats && rank == 0) {
@@ -256,26 +382,35 @@ vocab_verify_kernel(VerifyArgs A) {
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(VT)
 draft_sample_kernel(const float* z, long ld, int V, float T, uint32_t k0, uint32_t k1, const uint32_t* sids,
                     const int32_t* rs, int j, int32_t* out, int out_stride, int32_t* out2, int out2_stride) {
+  extern __shared__ __align__(128) float rows_s[];  // [slice] row, then [slice] race keys
+  __shared__ float red_f[VT / 32];
+  __shared__ float cta_f;
   __shared__ Best red_b[VT / 32];
   __shared__ Best cta_best;
+  __shared__ __align__(8) uint64_t bar;
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int b = blockIdx.x / CS;
   const int slice = ((V + CS - 1) / CS + 3) & ~3;
-  const int v0 = min(V, rank * slice), v1 = min(V, v0 + slice);
+  const int v0 = min(V, rank * slice), n = min(V, v0 + slice) - v0;
   const float* zr = z + (size_t)b * ld;
-  Best bb = race_slice(v0, v1, (kTagDraft << 24) | (uint32_t)j, (uint32_t)rs[b], sids[b], k0, k1,
-                       [&](int v) -> double { return (double)scaled(zr, v, T); });
-  bb = block_best(bb, red_b);
-  if (threadIdx.x == 0) cta_best = bb;
-  cluster.sync();
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_trigger();
+  pdl_wait();
+  Stager sg{rows_s, &bar, 0u, slice, v0, n, (V % 4 == 0) && (n % 4 == 0) && (ld % 4 == 0)};
+  sg.stage(0, 1, [&](int) { return zr; });
+  auto w32 = [&](int l) -> float { return scaled_v(rows_s[l], T); };
+  auto w64 = [&](int l) -> double { return (double)scaled_v(rows_s[l], T); };
+  const Best acc = race_exact(cluster, v0, n, (kTagDraft << 24) | (uint32_t)j, (uint32_t)rs[b], sids[b], k0, k1,
+                              rows_s + slice, red_f, &cta_f, red_b, &cta_best, w32, w64);
   if (rank == 0 && threadIdx.x == 0) {
-    Best acc = *cluster.map_shared_rank(&cta_best, 0);
-    for (int c = 1; c < CS; ++c) acc = best_merge(acc, *cluster.map_shared_rank(&cta_best, c));
     out[(size_t)b * out_stride] = acc.v;
     if (out2) out2[(size_t)b * out2_stride] = acc.v;
   }
-  cluster.sync();
 }
 
 __global__ void philox_fill_kernel(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1, int n,
@@ -290,6 +425,8 @@ __global__ void philox_fill_kernel(uint32_t c0, uint32_t c1, uint32_t c2, uint32
 __global__ void rollback_commit_kernel(StreamState s, const int32_t* batch_slots, int B, int gamma,
                                        const int32_t* out_tok, const int32_t* out_cnt, int max_new, int32_t* records,
                                        const uint32_t* gids) {
+  pdl_trigger();
+  pdl_wait();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   const int slot = batch_slots[b];
@@ -315,16 +452,33 @@ __global__ void rollback_commit_kernel(StreamState s, const int32_t* batch_slots
 }  // namespace
 
 cudaError_t vocab_verify(const VerifyArgs& a, cudaStream_t st) {
-  if (2 * a.gamma + 1 > MAX_ROWS) return cudaErrorInvalidValue;
-  vocab_verify_kernel<<<a.B * CS, VT, 0, st>>>(a);
-  return cudaGetLastError();
+  const int R = 2 * a.gamma + 1;
+  if (R > MAX_ROWS) return cudaErrorInvalidValue;
+  const int slice = ((a.V + CS - 1) / CS + 3) & ~3;
+  const int nbuf = std::max(2, std::min(R, SMEM_ROWS_BYTES / (slice * 4) - 1));
+  const size_t smem = (size_t)(nbuf + 1) * slice * 4;
+  if (smem > 220 * 1024) return cudaErrorInvalidValue;
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(vocab_verify_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  return launch(vocab_verify_kernel, dim3(a.B * CS), dim3(VT), smem, st, a, nbuf);
 }
 
 cudaError_t draft_sample(const float* z, long ld, int B, int V, float T, uint32_t k0, uint32_t k1,
                          const uint32_t* sids, const int32_t* rs, int j, int32_t* out, int out_stride, int32_t* out2,
                          int out2_stride, cudaStream_t st) {
-  draft_sample_kernel<<<B * CS, VT, 0, st>>>(z, ld, V, T, k0, k1, sids, rs, j, out, out_stride, out2, out2_stride);
-  return cudaGetLastError();
+  const int slice = ((V + CS - 1) / CS + 3) & ~3;
+  const size_t smem = (size_t)2 * slice * 4;
+  if (smem > 220 * 1024) return cudaErrorInvalidValue;
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(draft_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  return launch(draft_sample_kernel, dim3(B * CS), dim3(VT), smem, st, z, ld, V, T, k0, k1, sids, rs, j, out,
+                out_stride, out2, out2_stride);
 }
 
 cudaError_t philox_fill(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1, int n,
@@ -336,9 +490,8 @@ cudaError_t philox_fill(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint
 cudaError_t rollback_commit(const StreamState& s, const int32_t* batch_slots, int B, int gamma,
                             const int32_t* out_tok, const int32_t* out_cnt, int max_new, int32_t* records,
                             const uint32_t* gids, cudaStream_t st) {
-  rollback_commit_kernel<<<(B + 127) / 128, 128, 0, st>>>(s, batch_slots, B, gamma, out_tok, out_cnt, max_new,
-                                                          records, gids);
-  return cudaGetLastError();
+  return launch(rollback_commit_kernel, dim3((B + 127) / 128), dim3(128), 0, st, s, batch_slots, B, gamma, out_tok,
+                out_cnt, max_new, records, gids);
 }
 
 }  // namespace seed
