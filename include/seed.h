@@ -160,6 +160,10 @@ SEED_API seed_status seed_last_round_buffers(seed_ctx ctx, const float** tgt_log
 SEED_API seed_status seed_get_profile(seed_ctx ctx, double* gemm_ms, int64_t* gemm_launches,
                              double* gemm_bytes, int64_t* kernel_launches);
 SEED_API seed_status seed_reset_profile(seed_ctx ctx);
+/* GEMM trace of the most recent round (SEED_FLAG_PROFILE): out[4*i..4*i+3] = globaltimer ns of
+ * launch i: first CTA start, dependency release (PDL wait returned), last CTA end, 0.
+ * out: host buffer of 4*cap uint64; *n = launches written (in round launch order). */
+SEED_API seed_status seed_gemm_trace(seed_ctx ctx, uint64_t* out, int32_t cap, int32_t* n);
 
 SEED_API const char* seed_last_error(seed_ctx ctx);
 SEED_API void seed_destroy(seed_ctx ctx);

@@ -157,6 +157,14 @@ class SeedEngine:
         self._check(self.lib.seed_get_profile(self.ctx, C.byref(ms), C.byref(n), C.byref(by), C.byref(k)), "profile")
         return {"gemm_ms": ms.value, "gemm_launches": n.value, "gemm_bytes": by.value, "kernel_launches": k.value}
 
+    def gemm_trace(self, cap=4096):
+        """[(start, release, end)] globaltimer ns of each GEMM launch of the last round (profile=True)."""
+        buf = np.zeros(4 * cap, dtype=np.uint64)
+        n = C.c_int32(0)
+        self._check(self.lib.seed_gemm_trace(self.ctx, buf.ctypes.data_as(C.POINTER(C.c_uint64)), cap, C.byref(n)),
+                    "seed_gemm_trace")
+        return buf[:4 * n.value].reshape(-1, 4)[:, :3].astype(np.int64)
+
     def reset_profile(self):
         self._check(self.lib.seed_reset_profile(self.ctx), "reset_profile")
 

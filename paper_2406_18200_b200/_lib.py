@@ -57,6 +57,7 @@ _SIGS = {
     "seed_get_profile": [_P, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_double),
                          C.POINTER(C.c_int64)],
     "seed_reset_profile": [_P],
+    "seed_gemm_trace": [_P, C.POINTER(C.c_uint64), C.c_int32, _I32P],
     "seed_last_error": [_P],
     "seed_destroy": [_P],
     "seed_nccl_unique_id": [_P],

@@ -1,285 +1,376 @@
-// attention.cu -- K3: causal attention of the verify / draft / prefill rows over the paged KV cache.
+// attention.cu -- K3: the QKV epilogue, causal attention over the paged KV cache, and the
+// split-KV merge, fused in one kernel.
 //
 // For each sequence of the ragged batch, rows q_start .. q_start + q_len - 1 sit at positions
-// kv_len - q_len .. kv_len - 1 and attend to keys 0 .. pos (R15: causal MHA).  The new rows'
-// K/V were already appended to the pages by the QKV epilogue, so every key is read from the
-// cache the same way.  Memory-bound on K/V; the work is split over
-// (sequence x 8-row query block, head, 128-key chunk) so that N = 3 streams still fill the
-// GPU ("flash-decoding"), with a fixed chunk grid so a row's result never depends on the
-// batch (R19).  Each warp stages a 32-key K/V tile in shared memory, scores it with fp32
-// FMAs (lane = key), keeps an online softmax per row and accumulates P.V (lane = dims).
-// A second kernel merges the chunk partials in chunk order and rounds the output to bf16 (B3).
+// kv_len - q_len .. kv_len - 1 and attend to keys 0 .. pos (R15: causal MHA).  One CTA of 4
+// warps owns (sequence x 16-row query block, head, 128-key chunk):
+//   * it reads the QKV GEMM's fp32 output for its query rows, applies RoPE and rounds Q to bf16
+//     (B2) -- no separate epilogue kernel;
+//   * cached keys/values stream into shared memory with cp.async; the new rows' K (RoPE) and V
+//     are formed from the QKV output straight into the tiles and appended to the cache pages
+//     (one writer per position);
+//   * warp w owns the 32-key tile c_begin + 32 w: S = Q K^T and O = P V run as bf16
+//     mma.sync.m16n8k16 tiles (Q padded to 16 rows; ldmatrix from padded, conflict-free tiles;
+//     P re-packed from the S accumulators as the A operand, B5);
+//   * the 4 warps merge (m, l, O) in a fixed order; with several chunks the last CTA of a
+//     (sequence block, head) to finish (atomic ticket) merges the chunk partials in chunk
+//     order; the output is rounded to bf16 (B3).
+// The chunk grid is fixed (128 keys), so a row's result never depends on the batch (R19).
+// Memory-bound on the cached K/V.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace seed {
 
 namespace {
-constexpr int CHUNK = 128;      // keys per CTA (4 warps x 32)
 constexpr int WARPS = 4;
-constexpr int QB = 8;           // query rows per CTA
+constexpr int CHUNK = WARPS * 32;        // keys per CTA
+constexpr int QB = 16;                   // query rows per CTA (one m16 MMA tile)
 
-template <int DH, int NR>
-__global__ void __launch_bounds__(128)
-attn_chunk_kernel(const __nv_bfloat16* __restrict__ q, int H, int Hk, SeqInfo seqs, KVLayout kv, int layer,
-                  int n_qblk, float scale, AttnWorkspace ws, int M) {
-  constexpr int DPL = DH / 32;          // dims per lane in P.V
-  constexpr int KPAD = DH + 8;          // bf16 row pitch of the K tile (16-byte pad)
-  extern __shared__ __align__(16) uint8_t attn_smem[];
-  // carve: K tiles | V tiles (aliased by o_s after the key loop) | q | p | m, l
-  auto k_s = reinterpret_cast<__nv_bfloat16(*)[32][KPAD]>(attn_smem);
-  auto v_s = reinterpret_cast<__nv_bfloat16(*)[32][DH]>(attn_smem + WARPS * 32 * KPAD * 2);
-  auto o_s = reinterpret_cast<float(*)[QB][DH]>(attn_smem);
-  uint8_t* tail = attn_smem + WARPS * 32 * (KPAD + DH) * 2;
-  auto q_s = reinterpret_cast<float(*)[DH]>(tail);
-  auto p_s = reinterpret_cast<float(*)[QB][32]>(tail + QB * DH * 4);
-  auto m_s = reinterpret_cast<float(*)[QB]>(tail + QB * DH * 4 + WARPS * QB * 32 * 4);
-  auto l_s = reinterpret_cast<float(*)[QB]>(tail + QB * DH * 4 + WARPS * QB * 32 * 4 + WARPS * QB * 4);
+template <int DH>
+struct Smem {
+  static constexpr int PITCH = DH + 8;   // bf16 row pitch (16-byte pad: conflict-free ldmatrix)
+  static constexpr size_t Q = 0;                                     // bf16 [16][PITCH]
+  static constexpr size_t K = Q + (size_t)QB * PITCH * 2;            // bf16 [WARPS][32][PITCH]
+  static constexpr size_t V = K + (size_t)WARPS * 32 * PITCH * 2;    // bf16 [WARPS][32][PITCH]
+  static constexpr size_t ML = V + (size_t)WARPS * 32 * PITCH * 2;   // fp32 [2][WARPS][QB]
+  static constexpr size_t TK = ML + (size_t)2 * WARPS * QB * 4;      // ticket
+  static constexpr size_t BYTES = TK + 16;
+  // o merge scratch fp32 [WARPS][QB][DH] aliases K|V after the MMAs
+};
+
+SEED_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+SEED_DEV void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+SEED_DEV void mma_bf16(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+SEED_DEV uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+template <int DH>
+__global__ void __launch_bounds__(WARPS * 32)
+attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, const float2* __restrict__ rope,
+                  KVLayout kv, int layer, int n_qblk, float scale, AttnWorkspace ws, int M,
+                  __nv_bfloat16* __restrict__ out) {
+  using L = Smem<DH>;
+  constexpr int P = L::PITCH;
+  constexpr int HALF = DH / 2;
+  constexpr int VPR = DH / 8;            // 16-byte pieces per row
+  constexpr int NT = WARPS * 32;
+  constexpr int DT = DH / 8;             // 8-dim n-tiles of the output
+  extern __shared__ __align__(16) uint8_t smem[];
+  __nv_bfloat16* q_s = reinterpret_cast<__nv_bfloat16*>(smem + L::Q);
+  __nv_bfloat16* k_s = reinterpret_cast<__nv_bfloat16*>(smem + L::K);
+  __nv_bfloat16* v_s = reinterpret_cast<__nv_bfloat16*>(smem + L::V);
+  float* m_s = reinterpret_cast<float*>(smem + L::ML);
+  float* l_s = m_s + WARPS * QB;
+  float* o_s = reinterpret_cast<float*>(smem + L::K);
+  int* ticket_s = reinterpret_cast<int*>(smem + L::TK);
 
   pdl_trigger();
+  if (ws.timing && threadIdx.x == 0) atomicMin(&ws.timing[0], globaltimer_ns());
   pdl_wait();
+  if (ws.timing && threadIdx.x == 0) atomicMin(&ws.timing[1], globaltimer_ns());
+  auto done = [&]() {
+    if (ws.timing && threadIdx.x == 0) atomicMax(&ws.timing[2], globaltimer_ns());
+  };
   const int seq = blockIdx.x / n_qblk, qb = blockIdx.x % n_qblk;
-  const int head = blockIdx.y, split = blockIdx.z;
+  const int head = blockIdx.y, split = blockIdx.z, nsplit = gridDim.z;
   const int kvh = head / (H / Hk);
   const int q0 = seqs.q_start[seq], ql = seqs.q_len[seq], kvl = seqs.kv_len[seq];
   const int slot = seqs.slot[seq];
   const int r0 = qb * QB;
-  if (r0 >= ql) return;
-  const int nr = min(QB, ql - r0);
-  const int pos0 = kvl - ql + r0;                  // position of the first row of this block
-  const int key_end = pos0 + nr;                   // keys [0, key_end) are visible to some row
-  const int c_begin = split * CHUNK;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const size_t ws_row = (size_t)(q0 + r0);
-
-  if (c_begin >= key_end) {
-    // empty chunk for this block: mark the partials invalid
-    for (int e = tid; e < nr; e += 128) {
-      float* ml = ws.ml_part + (((size_t)split * M + ws_row + e) * H + head) * 2;
-      ml[0] = -INFINITY;
-      ml[1] = 0.f;
-    }
+  if (r0 >= ql) {
+    done();
     return;
   }
-
-  for (int e = tid; e < QB * DH; e += 128) {
-    const int r = e / DH, d = e % DH;
-    q_s[r][d] = r < nr ? bf2f(q[((size_t)(q0 + r0 + r) * H + head) * DH + d]) : 0.f;
-  }
-  __syncthreads();
-
-  float m_r[NR], l_r[NR], o_r[NR][DPL];
-#pragma unroll
-  for (int r = 0; r < NR; ++r) {
-    m_r[r] = -INFINITY;
-    l_r[r] = 0.f;
-#pragma unroll
-    for (int j = 0; j < DPL; ++j) o_r[r][j] = 0.f;
-  }
-
+  const int nr = min(QB, ql - r0);
+  const int new_first = kvl - ql;                  // position of the sequence's first new row
+  const int pos0 = new_first + r0;                 // position of the first row of this block
+  const int key_end = pos0 + nr;                   // keys [0, key_end) are visible to some row
+  const int c_begin = split * CHUNK;
   const int c_end = min(c_begin + CHUNK, key_end);
-  for (int kt = c_begin + warp * 32; kt < c_end; kt += WARPS * 32) {
-    // ---- stage the K and V tile of keys kt .. kt+31 (16-byte vectors)
-    constexpr int VPR = DH / 8;   // 16-byte vectors per key row
-    // all 16-byte pieces of the tile in flight at once (cp.async, no register staging); the
-    // tile's page ids (kt is a multiple of 32, P divides 32 or vice versa) are read once
-    const int pg_first = kt / kv.P;
-    const int npg = (min(kt + 31, c_end - 1)) / kv.P - pg_first + 1;
-    const int my_page = lane < npg ? __ldg(kv.page_table + (size_t)slot * kv.max_pages + pg_first + lane) : 0;
-#pragma unroll 8
-    for (int e = lane; e < 32 * VPR; e += 32) {
-      const int kk = e / VPR, c16 = e % VPR;
-      const int key = kt + kk;
-      const int page = __shfl_sync(0xffffffffu, my_page, min(31, key / kv.P - pg_first));
-      if (key < c_end) {
-        const size_t ko = kv.offset(page, layer, 0, kvh, key % kv.P);
-        cp_async16(&k_s[warp][kk][c16 * 8], reinterpret_cast<const uint4*>(kv.pool + ko) + c16);
-        cp_async16(&v_s[warp][kk][c16 * 8], reinterpret_cast<const uint4*>(kv.pool + ko + kv.vofs()) + c16);
-      } else {
-        *reinterpret_cast<uint4*>(&k_s[warp][kk][c16 * 8]) = make_uint4(0, 0, 0, 0);
-        *reinterpret_cast<uint4*>(&v_s[warp][kk][c16 * 8]) = make_uint4(0, 0, 0, 0);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;          // MMA fragment coordinates
+  const size_t ws_row = (size_t)(q0 + r0);
+  const int ldq = (H + 2 * Hk) * DH;               // row stride of the QKV GEMM output
+
+  float o_acc[DT][4];
+  float m_row[2] = {-INFINITY, -INFINITY}, l_row[2] = {0.f, 0.f};   // rows g, g + 8
+#pragma unroll
+  for (int j = 0; j < DT; ++j) o_acc[j][0] = o_acc[j][1] = o_acc[j][2] = o_acc[j][3] = 0.f;
+
+  if (c_begin < key_end) {
+    // ---- cached keys of this warp's tile: cp.async into the K / V tiles
+    const int kt = c_begin + warp * 32;
+    const int old_end = min(c_end, new_first);
+    __nv_bfloat16* kw = k_s + (size_t)warp * 32 * P;
+    __nv_bfloat16* vw = v_s + (size_t)warp * 32 * P;
+    {
+      const int pg_first = kt / kv.P;
+      const int my_page = (kt + lane < old_end) ? __ldg(kv.page_table + (size_t)slot * kv.max_pages + (kt + lane) / kv.P)
+                                                : 0;
+#pragma unroll 4
+      for (int e = lane; e < 32 * VPR; e += 32) {
+        const int kk = e / VPR, c16 = e % VPR;
+        const int key = kt + kk;
+        const int page = __shfl_sync(0xffffffffu, my_page, kk);
+        if (key < old_end) {
+          const size_t ko = kv.offset(page, layer, 0, kvh, key % kv.P);
+          cp_async16(kw + kk * P + c16 * 8, reinterpret_cast<const uint4*>(kv.pool + ko) + c16);
+          cp_async16(vw + kk * P + c16 * 8, reinterpret_cast<const uint4*>(kv.pool + ko + kv.vofs()) + c16);
+        } else if (key >= c_end || key >= key_end) {
+          *reinterpret_cast<uint4*>(kw + kk * P + c16 * 8) = make_uint4(0, 0, 0, 0);
+          *reinterpret_cast<uint4*>(vw + kk * P + c16 * 8) = make_uint4(0, 0, 0, 0);
+        }
+        (void)pg_first;
+      }
+    }
+    // ---- Q of this block's rows and head: RoPE, bf16 rounding (B2); padding rows are zero
+    for (int e = tid; e < QB * HALF; e += NT) {
+      const int r = e / HALF, i = e % HALF;
+      float a = 0.f, b = 0.f;
+      if (r < nr) {
+        const float* yr = qkv + (size_t)(q0 + r0 + r) * ldq + head * DH;
+        const float2 cs = rope[(size_t)(pos0 + r) * HALF + i];
+        const float x0 = yr[i], x1 = yr[i + HALF];
+        a = x0 * cs.x - x1 * cs.y;
+        b = x1 * cs.x + x0 * cs.y;
+      }
+      q_s[r * P + i] = f2bf(a);
+      q_s[r * P + i + HALF] = f2bf(b);
+    }
+    // ---- new rows of the sequence inside this chunk: K (RoPE) and V from the QKV output into
+    // the tiles; the owning query block appends them to the cache
+    const int nk0 = max(c_begin, new_first), nk1 = c_end;
+    for (int e = tid; e < (nk1 - nk0) * HALF; e += NT) {
+      const int key = nk0 + e / HALF, i = e % HALF;
+      const int m = q0 + (key - new_first);
+      const float* yk = qkv + (size_t)m * ldq + (H + kvh) * DH;
+      const float* yv = qkv + (size_t)m * ldq + (H + Hk + kvh) * DH;
+      const float2 cs = rope[(size_t)key * HALF + i];
+      const float a = yk[i], b = yk[i + HALF];
+      const __nv_bfloat16 ka = f2bf(a * cs.x - b * cs.y), kb = f2bf(b * cs.x + a * cs.y);
+      const __nv_bfloat16 va = f2bf(yv[i]), vb = f2bf(yv[i + HALF]);
+      const int w = (key - c_begin) >> 5, kk = (key - c_begin) & 31;
+      __nv_bfloat16* kr = k_s + ((size_t)w * 32 + kk) * P;
+      __nv_bfloat16* vr = v_s + ((size_t)w * 32 + kk) * P;
+      kr[i] = ka;
+      kr[i + HALF] = kb;
+      vr[i] = va;
+      vr[i + HALF] = vb;
+      if (head % (H / Hk) == 0 && qb == (key - new_first) / QB) {  // one writer per kv head, position
+        const int page = __ldg(kv.page_table + (size_t)slot * kv.max_pages + key / kv.P);
+        __nv_bfloat16* kdst = kv.pool + kv.offset(page, layer, 0, kvh, key % kv.P);
+        kdst[i] = ka;
+        kdst[i + HALF] = kb;
+        kdst[kv.vofs() + i] = va;
+        kdst[kv.vofs() + i + HALF] = vb;
       }
     }
     cp_async_wait_all();
-    __syncwarp();
-    // ---- scores: lane = key
-    const int key = kt + lane;
-    float s[NR];
+    __syncthreads();
+
+    if (kt < c_end) {
+      // ---- S = Q K^T for this warp's 32 keys: 4 n-tiles of 8 keys, DH/16 k-steps
+      float s[4][4];
 #pragma unroll
-    for (int r = 0; r < NR; ++r) s[r] = 0.f;
-#pragma unroll 4
-    for (int d = 0; d < DH; d += 8) {
-      float kf[8];
-      bf16x8_to_f32(*reinterpret_cast<const uint4*>(&k_s[warp][lane][d]), kf);
+      for (int j = 0; j < 4; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+      const uint32_t qa = smem_u32(q_s), kb = smem_u32(kw);
 #pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        const float4 qa = *reinterpret_cast<const float4*>(&q_s[r][d]);
-        const float4 qc = *reinterpret_cast<const float4*>(&q_s[r][d + 4]);
-        s[r] += qa.x * kf[0] + qa.y * kf[1] + qa.z * kf[2] + qa.w * kf[3] + qc.x * kf[4] + qc.y * kf[5] +
-                qc.z * kf[6] + qc.w * kf[7];
+      for (int ks = 0; ks < DH / 16; ++ks) {
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4(qa + ((lane & 15) * P + ks * 16 + (lane >> 4) * 8) * 2, a0, a1, a2, a3);
+#pragma unroll
+        for (int nt = 0; nt < 4; nt += 2) {
+          uint32_t b0, b1, b2, b3;
+          const int key = nt * 8 + (lane >> 4) * 8 + (lane & 7);
+          ldsm_x4(kb + (key * P + ks * 16 + ((lane >> 3) & 1) * 8) * 2, b0, b1, b2, b3);
+          mma_bf16(s[nt], a0, a1, a2, a3, b0, b1);
+          mma_bf16(s[nt + 1], a0, a1, a2, a3, b2, b3);
+        }
+      }
+      // ---- mask + softmax over the tile (rows g, g + 8; lane holds keys 8 nt + 2 t4, +1)
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int r = g + 8 * h2;
+        float mx = -INFINITY;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const int key = kt + nt * 8 + 2 * t4 + c;
+            const bool ok = r < nr && key < c_end && key <= pos0 + r;
+            float& v = s[nt][2 * h2 + c];
+            v = ok ? v * scale : -INFINITY;
+            mx = fmaxf(mx, v);
+          }
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        float sum = 0.f;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            float& v = s[nt][2 * h2 + c];
+            v = (mx == -INFINITY) ? 0.f : expf(v - mx);
+            sum += v;
+          }
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        m_row[h2] = mx;
+        l_row[h2] = sum;
+      }
+      // ---- O = P V: P (bf16, B5) re-packed from the S accumulators; V via ldmatrix.trans
+      const uint32_t vb = smem_u32(vw);
+#pragma unroll
+      for (int kc = 0; kc < 2; ++kc) {   // keys 16 kc .. 16 kc + 15
+        const uint32_t pa0 = pack_bf16(s[2 * kc][0], s[2 * kc][1]);
+        const uint32_t pa1 = pack_bf16(s[2 * kc][2], s[2 * kc][3]);
+        const uint32_t pa2 = pack_bf16(s[2 * kc + 1][0], s[2 * kc + 1][1]);
+        const uint32_t pa3 = pack_bf16(s[2 * kc + 1][2], s[2 * kc + 1][3]);
+#pragma unroll
+        for (int dt = 0; dt < DT; dt += 2) {
+          uint32_t b0, b1, b2, b3;
+          const int key = kc * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+          const int dim = dt * 8 + (lane >> 4) * 8;
+          ldsm_x4_t(vb + (key * P + dim) * 2, b0, b1, b2, b3);
+          mma_bf16(o_acc[dt], pa0, pa1, pa2, pa3, b0, b1);
+          mma_bf16(o_acc[dt + 1], pa0, pa1, pa2, pa3, b2, b3);
+        }
       }
     }
-    // ---- online softmax per row (causal mask: key <= pos(row))
-#pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      const bool valid = (r < nr) && (key < c_end) && (key <= pos0 + r);
-      const float sc = valid ? s[r] * scale : -INFINITY;
-      const float tmax = warp_max(sc);
-      const float m_new = fmaxf(m_r[r], tmax);
-      float p = 0.f, corr = 1.f;
-      if (m_new != -INFINITY) {
-        p = valid ? expf(sc - m_new) : 0.f;
-        corr = (m_r[r] == -INFINITY) ? 0.f : expf(m_r[r] - m_new);
-      }
-      l_r[r] = l_r[r] * corr + warp_sum(p);
-      m_r[r] = m_new;
-#pragma unroll
-      for (int j = 0; j < DPL; ++j) o_r[r][j] *= corr;
-      p_s[warp][r][lane] = p;
-    }
-    __syncwarp();
-    // ---- P.V: lane owns dims lane*DPL .. +DPL
-#pragma unroll 4
-    for (int kk = 0; kk < 32; ++kk) {
-      float vf[DPL];
-      if constexpr (DPL == 4) {
-        const uint2 raw = *reinterpret_cast<const uint2*>(&v_s[warp][kk][lane * 4]);
-        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
-        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
-        vf[0] = a.x; vf[1] = a.y; vf[2] = b.x; vf[3] = b.y;
-      } else if constexpr (DPL == 2) {
-        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v_s[warp][kk][lane * 2]));
-        vf[0] = a.x; vf[1] = a.y;
-      } else {
-        vf[0] = bf2f(v_s[warp][kk][lane]);
-      }
-#pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        const float p = p_s[warp][r][kk];
-#pragma unroll
-        for (int j = 0; j < DPL; ++j) o_r[r][j] += p * vf[j];
-      }
-    }
-    __syncwarp();
   }
-  // ---- merge the 4 warps of the CTA (fixed order); o_s aliases the K/V tiles
-  __syncthreads();
+
+  // ---- merge the 4 warps (fixed order) into this chunk's result
+  __syncthreads();   // o_s aliases the K / V tiles
+  if (t4 == 0) {
+    m_s[warp * QB + g] = m_row[0];
+    m_s[warp * QB + g + 8] = m_row[1];
+    l_s[warp * QB + g] = l_row[0];
+    l_s[warp * QB + g + 8] = l_row[1];
+  }
 #pragma unroll
-  for (int r = 0; r < NR; ++r) {
-    if (lane == 0) {
-      m_s[warp][r] = m_r[r];
-      l_s[warp][r] = l_r[r];
-    }
-#pragma unroll
-    for (int j = 0; j < DPL; ++j) o_s[warp][r][lane * DPL + j] = o_r[r][j];
+  for (int dt = 0; dt < DT; ++dt) {
+    float* o0 = o_s + ((size_t)warp * QB + g) * DH + dt * 8 + 2 * t4;
+    float* o1 = o_s + ((size_t)warp * QB + g + 8) * DH + dt * 8 + 2 * t4;
+    o0[0] = o_acc[dt][0];
+    o0[1] = o_acc[dt][1];
+    o1[0] = o_acc[dt][2];
+    o1[1] = o_acc[dt][3];
   }
   __syncthreads();
-  for (int e = tid; e < nr * DH; e += 128) {
+  const bool single = nsplit == 1;
+  for (int e = tid; e < nr * DH; e += NT) {
     const int r = e / DH, d = e % DH;
     float mx = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < WARPS; ++w) mx = fmaxf(mx, m_s[w][r]);
+    for (int w = 0; w < WARPS; ++w) mx = fmaxf(mx, m_s[w * QB + r]);
     float o = 0.f, l = 0.f;
     if (mx != -INFINITY) {
 #pragma unroll
       for (int w = 0; w < WARPS; ++w) {
-        if (m_s[w][r] == -INFINITY) continue;
-        const float f = expf(m_s[w][r] - mx);
-        o += o_s[w][r][d] * f;
-        l += l_s[w][r] * f;
+        const float mw = m_s[w * QB + r];
+        if (mw == -INFINITY) continue;
+        const float f = expf(mw - mx);
+        o += o_s[((size_t)w * QB + r) * DH + d] * f;
+        l += l_s[w * QB + r] * f;
       }
     }
     const size_t row = ws_row + r;
-    ws.o_part[(((size_t)split * M + row) * H + head) * DH + d] = o;
-    if (d == 0) {
-      float* ml = ws.ml_part + (((size_t)split * M + row) * H + head) * 2;
-      ml[0] = mx;
-      ml[1] = l;
+    if (single) {
+      out[(row * H + head) * DH + d] = f2bf(o / l);
+    } else {
+      ws.o_part[(((size_t)split * M + row) * H + head) * DH + d] = o;
+      if (d == 0) {
+        float* ml = ws.ml_part + (((size_t)split * M + row) * H + head) * 2;
+        ml[0] = mx;
+        ml[1] = l;
+      }
     }
   }
-}
-
-// merge chunk partials in chunk order; grid (M, H), block Dh
-__global__ void attn_combine_kernel(AttnWorkspace ws, int M, int H, int Dh, int splits, const int32_t* row_nsplit,
-                                    __nv_bfloat16* __restrict__ out) {
-  pdl_trigger();
-  pdl_wait();
-  const int row = blockIdx.x, head = blockIdx.y, d = threadIdx.x;
-  const int ns = row_nsplit ? row_nsplit[row] : splits;
-  float mx = -INFINITY;
-  for (int s = 0; s < ns; ++s) mx = fmaxf(mx, ws.ml_part[(((size_t)s * M + row) * H + head) * 2]);
-  float o = 0.f, l = 0.f;
-  for (int s = 0; s < ns; ++s) {
-    const float* ml = ws.ml_part + (((size_t)s * M + row) * H + head) * 2;
-    if (ml[0] == -INFINITY) continue;
-    const float f = expf(ml[0] - mx);
-    o += ws.o_part[(((size_t)s * M + row) * H + head) * Dh + d] * f;
-    l += ml[1] * f;
+  if (single) {
+    done();
+    return;
   }
-  out[((size_t)row * H + head) * Dh + d] = f2bf(o / l);
-}
 
-
-template <int DH>
-constexpr size_t attn_smem_bytes() {
-  return (size_t)WARPS * 32 * (DH + 8 + DH) * 2 + QB * DH * 4 + WARPS * QB * 32 * 4 + 2 * WARPS * QB * 4;
-}
-
-template <int DH, int NR>
-struct ChunkLauncher {
-  static cudaError_t go(dim3 grid, size_t smem, cudaStream_t st, const __nv_bfloat16* q, int H, int Hk,
-                        const SeqInfo& seqs, const KVLayout& kv, int layer, int n_qblk, float scale,
-                        const AttnWorkspace& ws, int M) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(attn_chunk_kernel<DH, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
+  // ---- the last chunk CTA of (sequence block, head) merges all chunks in chunk order
+  __syncthreads();
+  int* ctr = ws.counters + ((size_t)(seq * n_qblk + qb) * H + head);
+  if (tid == 0) {
+    __threadfence();
+    *ticket_s = atomicAdd(ctr, 1);
+    __threadfence();
+  }
+  __syncthreads();
+  if (*ticket_s != nsplit - 1) {
+    done();
+    return;
+  }
+  for (int e = tid; e < nr * DH; e += NT) {
+    const int r = e / DH, d = e % DH;
+    const size_t row = ws_row + r;
+    float mx = -INFINITY;
+    for (int s = 0; s < nsplit; ++s) mx = fmaxf(mx, __ldcg(ws.ml_part + (((size_t)s * M + row) * H + head) * 2));
+    float o = 0.f, l = 0.f;
+    for (int s = 0; s < nsplit; ++s) {
+      const float* ml = ws.ml_part + (((size_t)s * M + row) * H + head) * 2;
+      const float ms = __ldcg(ml);
+      if (ms == -INFINITY) continue;
+      const float f = expf(ms - mx);
+      o += __ldcg(ws.o_part + (((size_t)s * M + row) * H + head) * DH + d) * f;
+      l += __ldcg(ml + 1) * f;
     }
-    return launch(attn_chunk_kernel<DH, NR>, grid, dim3(128), smem, st, q, H, Hk, seqs, kv, layer, n_qblk, scale, ws,
-                  M);
+    out[(row * H + head) * DH + d] = f2bf(o / l);
   }
-};
+  if (tid == 0) *ctr = 0;  // ready for the next launch (graph replay)
+  done();
+}
 
 template <int DH>
-cudaError_t launch_chunks(const __nv_bfloat16* q, int M, int n_seq, int max_q_len, int max_kv, int H, int Hk,
-                          const SeqInfo& seqs, const KVLayout& kv, int layer, const AttnWorkspace& ws,
-                          cudaStream_t st) {
+cudaError_t launch_dh(int M, int n_seq, int max_q_len, int max_kv, int H, int Hk, const float* qkv,
+                      const SeqInfo& seqs, const float2* rope, const KVLayout& kv, int layer, const AttnWorkspace& ws,
+                      __nv_bfloat16* out, cudaStream_t st) {
   const int n_qblk = (max_q_len + QB - 1) / QB;
   const int splits = (max_kv + CHUNK - 1) / CHUNK;
-  dim3 grid(n_seq * n_qblk, H, splits);
+  const size_t smem = Smem<DH>::BYTES;
+  static_assert((size_t)WARPS * QB * DH * 4 <= 2 * (size_t)WARPS * 32 * (DH + 8) * 2, "o merge scratch fits");
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_fused_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
   const float scale = 1.0f / sqrtf((float)DH);
-  const size_t smem = attn_smem_bytes<DH>();
-  if (max_q_len == 1)
-    return ChunkLauncher<DH, 1>::go(grid, smem, st, q, H, Hk, seqs, kv, layer, n_qblk, scale, ws, M);
-  else if (max_q_len == 2)
-    return ChunkLauncher<DH, 2>::go(grid, smem, st, q, H, Hk, seqs, kv, layer, n_qblk, scale, ws, M);
-  else if (max_q_len <= 4)
-    return ChunkLauncher<DH, 4>::go(grid, smem, st, q, H, Hk, seqs, kv, layer, n_qblk, scale, ws, M);
-  else if (max_q_len <= 5)
-    return ChunkLauncher<DH, 5>::go(grid, smem, st, q, H, Hk, seqs, kv, layer, n_qblk, scale, ws, M);
-  else if (max_q_len <= 6)
-    return ChunkLauncher<DH, 6>::go(grid, smem, st, q, H, Hk, seqs, kv, layer, n_qblk, scale, ws, M);
-  else if (max_q_len <= 7)
-    return ChunkLauncher<DH, 7>::go(grid, smem, st, q, H, Hk, seqs, kv, layer, n_qblk, scale, ws, M);
-  else
-    return ChunkLauncher<DH, 8>::go(grid, smem, st, q, H, Hk, seqs, kv, layer, n_qblk, scale, ws, M);
+  return launch(attn_fused_kernel<DH>, dim3(n_seq * n_qblk, H, splits), dim3(WARPS * 32), smem, st, qkv, H, Hk,
+                seqs, rope, kv, layer, n_qblk, scale, ws, M, out);
 }
 }  // namespace
 
 int attn_chunk_tokens() { return CHUNK; }
+int attn_query_block() { return QB; }
 
-cudaError_t attention(const __nv_bfloat16* q, int M, int n_seq, int max_q_len, int max_kv, int H, int Hk, int Dh,
-                      const SeqInfo& seqs, const KVLayout& kv, int layer, const AttnWorkspace& ws,
-                      __nv_bfloat16* out, cudaStream_t st) {
+cudaError_t attention(const float* qkv, int M, int n_seq, int max_q_len, int max_kv, int H, int Hk, int Dh,
+                      const SeqInfo& seqs, const float2* rope, const KVLayout& kv, int layer,
+                      const AttnWorkspace& ws, __nv_bfloat16* out, cudaStream_t st) {
   const int splits = (max_kv + CHUNK - 1) / CHUNK;
   if (splits > ws.max_splits) return cudaErrorInvalidValue;
-  cudaError_t e;
-  if (Dh == 128) e = launch_chunks<128>(q, M, n_seq, max_q_len, max_kv, H, Hk, seqs, kv, layer, ws, st);
-  else if (Dh == 64) e = launch_chunks<64>(q, M, n_seq, max_q_len, max_kv, H, Hk, seqs, kv, layer, ws, st);
-  else if (Dh == 32) e = launch_chunks<32>(q, M, n_seq, max_q_len, max_kv, H, Hk, seqs, kv, layer, ws, st);
-  else return cudaErrorInvalidValue;
-  if (e != cudaSuccess) return e;
-  return launch(attn_combine_kernel, dim3(M, H), dim3(Dh), 0, st, ws, M, H, Dh, splits, (const int32_t*)nullptr, out);
+  if ((size_t)n_seq * ((max_q_len + QB - 1) / QB) * H > (size_t)ws.max_counters) return cudaErrorInvalidValue;
+  if (Dh == 128) return launch_dh<128>(M, n_seq, max_q_len, max_kv, H, Hk, qkv, seqs, rope, kv, layer, ws, out, st);
+  if (Dh == 64) return launch_dh<64>(M, n_seq, max_q_len, max_kv, H, Hk, qkv, seqs, rope, kv, layer, ws, out, st);
+  if (Dh == 32) return launch_dh<32>(M, n_seq, max_q_len, max_kv, H, Hk, qkv, seqs, rope, kv, layer, ws, out, st);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace seed

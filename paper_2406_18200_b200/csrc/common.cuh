@@ -157,6 +157,12 @@ SEED_DEV void cp_async16(void* smem_dst, const void* gsrc) {
 }
 SEED_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+SEED_DEV unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 SEED_DEV bool elect_one() {
   uint32_t pred = 0;
   asm volatile(
@@ -170,8 +176,13 @@ SEED_DEV bool elect_one() {
 // ---------------------------------------------------------------- host: launches with PDL
 bool pdl_enabled();
 
+// every kernel runs with the maximum shared-memory carveout, so CTAs of consecutive kernels can
+// share an SM without an L1/shared reconfiguration (which would drain the SM and defeat PDL)
+void carveout_once(const void* kern);
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  carveout_once(reinterpret_cast<const void*>(kern));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;

@@ -25,7 +25,6 @@
 
 using seed::GemmPlan;
 using seed::KVLayout;
-using seed::PartialView;
 typedef __nv_bfloat16 bf16;
 
 namespace {
@@ -129,6 +128,7 @@ struct Model {
   // activations for up to m_cap rows per forward chunk
   int m_cap = 0;
   float* x = nullptr;
+  float* y = nullptr;   // fp32 GEMM output [m_cap][max(nqkv, 2 ff, d)]
   bf16 *h = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr, *hlm = nullptr;
   seed::AttnWorkspace aws{};
   std::vector<bf16*> owned;
@@ -152,6 +152,7 @@ struct ChunkDesc {
 
 struct RoundPlan {  // descriptors of one round at batch-size-determined arena offsets
   int n = 0;
+  int64_t key_draft = 0, key_verify = 0;  // graph keys: batch size and attention chunk counts
   size_t o_sid = 0, o_r = 0, o_sl = 0, o_last = 0;
   std::vector<ChunkDesc> draft, verify;
   std::vector<int> verify_b0;
@@ -199,15 +200,19 @@ struct seed_ctx_s {
   bool use_graphs = true;
   cudaStream_t gstream = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
-  struct RoundGraphs {
-    cudaGraphExec_t draft = nullptr, verify = nullptr;
+  struct PhaseGraph {
+    cudaGraphExec_t exec = nullptr;
     double gemm_bytes = 0;
     int64_t gemms = 0, kernels = 0;
   };
-  std::map<int, RoundGraphs> graphs;
+  std::map<int64_t, PhaseGraph> draft_graphs, verify_graphs;
   // profiling: per-GEMM globaltimer records accumulated on the device
   bool profile = false, in_round = false;
-  unsigned long long *timing_rec = nullptr, *timing_acc = nullptr;
+  unsigned long long *timing_rec = nullptr, *timing_acc = nullptr, *timing_last = nullptr;
+  int last_draft_recs = 0, last_verify_recs = 0;
+  std::map<int, int> draft_recs;  // records of the draft phase per batch size
+  double draft_gemm_bytes = 0;
+  int64_t draft_gemms = 0;
   int rec_cap = 0, rec_used = 0;
   double round_gemm_bytes = 0, gemm_bytes = 0;
   int64_t round_gemms = 0, gemm_launches = 0, kernel_launches = 0;
@@ -245,13 +250,13 @@ const CUtensorMap* xmap(seed_ctx ctx, const bf16* buf, int K, int rows_cap, int 
   return &(ctx->xmaps[key] = m);
 }
 
-seed_status run_gemm(seed_ctx ctx, const GemmPlan& p, const bf16* X, int rows_cap, int M, PartialView* view,
+seed_status run_gemm(seed_ctx ctx, const GemmPlan& p, const bf16* X, int rows_cap, int M, float* Y, int ldY,
                      cudaStream_t st) {
   const CUtensorMap* tm = xmap(ctx, X, p.K, rows_cap, M);
   if (!tm) return fail(ctx, SEED_ECUDA, "cuTensorMapEncodeTiled", "X operand");
   unsigned long long* rec = nullptr;
-  if (ctx->profile && ctx->in_round && ctx->rec_used < ctx->rec_cap) rec = ctx->timing_rec + 2 * ctx->rec_used++;
-  CK(seed::gemm_run(p, *tm, M, ctx->partial, view, st, rec));
+  if (ctx->profile && ctx->in_round && ctx->rec_used < ctx->rec_cap) rec = ctx->timing_rec + 4 * ctx->rec_used++;
+  CK(seed::gemm_run(p, *tm, M, ctx->partial, Y, ldY, st, rec));
   if (ctx->in_round) {
     ctx->round_gemm_bytes += (double)p.N * p.K * 2 + (double)M * p.K * 2 + (double)M * p.N * 4;
     ctx->round_gemms++;
@@ -364,6 +369,7 @@ seed_status build_model(seed_ctx ctx, Model& m, const seed_model_shape& sh, cons
   m.m_cap = std::max(m_cap, 256);
   const size_t mc = m.m_cap;
   CK(cudaMalloc(&m.x, mc * d * 4));
+  CK(cudaMalloc(&m.y, mc * std::max<size_t>({(size_t)m.nqkv, 2 * ff, d}) * 4));
   m.h = alloc(mc * d);
   m.q = alloc(mc * dq);
   m.attn = alloc(mc * dq);
@@ -373,6 +379,9 @@ seed_status build_model(seed_ctx ctx, Model& m, const seed_model_shape& sh, cons
   m.aws.max_splits = (max_pos + seed::attn_chunk_tokens() - 1) / seed::attn_chunk_tokens();
   CK(cudaMalloc(&m.aws.o_part, (size_t)m.aws.max_splits * mc * dq * 4));
   CK(cudaMalloc(&m.aws.ml_part, (size_t)m.aws.max_splits * mc * m.H * 2 * 4));
+  m.aws.max_counters = (int)(mc * m.H);
+  CK(cudaMalloc(&m.aws.counters, (size_t)m.aws.max_counters * 4));
+  CK(cudaMemset(m.aws.counters, 0, (size_t)m.aws.max_counters * 4));
   return SEED_OK;
 }
 
@@ -388,8 +397,10 @@ void free_model(Model& m) {
   if (m.page_table_dev) cudaFree(m.page_table_dev);
   if (m.rope) cudaFree(m.rope);
   if (m.x) cudaFree(m.x);
+  if (m.y) cudaFree(m.y);
   if (m.aws.o_part) cudaFree(m.aws.o_part);
   if (m.aws.ml_part) cudaFree(m.aws.ml_part);
+  if (m.aws.counters) cudaFree(m.aws.counters);
 }
 
 size_t max_partial(const Model& m, int M) {
@@ -440,34 +451,35 @@ seed_status forward_chunk(seed_ctx ctx, Model& m, const ChunkDesc& c, cudaStream
     CK(seed::embed_rmsnorm(m.embed, c.tok.dev, c.tok.stride, M, m.d, m.an[first_layer], eps, m.x, m.h, st));
     ctx->kernel_launches++;
   }
-  seed::RowInfo rows{nullptr, c.pos, c.slot};
   seed::SeqInfo seqs{c.q_start, c.q_len, c.kv_len, c.seq_slot};
   for (int l = first_layer; l < last_layer; ++l) {
-    PartialView v;
-    if ((s = run_gemm(ctx, m.pq[l], m.h, m.m_cap, M, &v, st)) != SEED_OK) return s;
-    CK(seed::epi_qkv_rope(v, M, m.H, m.Hk, m.Dh, rows, m.rope, l, m.kv, m.q, nullptr, nullptr, st));
-    CK(seed::attention(m.q, M, c.n_seq, c.max_q_len, c.max_kv, m.H, m.Hk, m.Dh, seqs, m.kv, l, m.aws, m.attn, st));
-    if ((s = run_gemm(ctx, m.po[l], m.attn, m.m_cap, M, &v, st)) != SEED_OK) return s;
-    CK(seed::epi_residual_rmsnorm(v, M, m.d, m.x, m.mn[l], eps, m.h, nullptr, nullptr, st));
-    if ((s = run_gemm(ctx, m.pgu[l], m.h, m.m_cap, M, &v, st)) != SEED_OK) return s;
-    CK(seed::epi_swiglu(v, M, m.ff, m.act, st));
-    if ((s = run_gemm(ctx, m.pd[l], m.act, m.m_cap, M, &v, st)) != SEED_OK) return s;
+    if ((s = run_gemm(ctx, m.pq[l], m.h, m.m_cap, M, m.y, m.nqkv, st)) != SEED_OK) return s;
+    {
+      seed::AttnWorkspace aws = m.aws;
+      aws.timing = nullptr;
+      if (ctx->profile && ctx->in_round && ctx->rec_used < ctx->rec_cap) aws.timing = ctx->timing_rec + 4 * ctx->rec_used++;
+      CK(seed::attention(m.y, M, c.n_seq, c.max_q_len, c.max_kv, m.H, m.Hk, m.Dh, seqs, m.rope, m.kv, l, aws,
+                         m.attn, st));
+    }
+    if ((s = run_gemm(ctx, m.po[l], m.attn, m.m_cap, M, m.y, m.d, st)) != SEED_OK) return s;
+    CK(seed::residual_rmsnorm(m.y, M, m.d, m.x, m.mn[l], eps, m.h, nullptr, nullptr, st));
+    if ((s = run_gemm(ctx, m.pgu[l], m.h, m.m_cap, M, m.y, 2 * m.ff, st)) != SEED_OK) return s;
+    CK(seed::swiglu(m.y, M, m.ff, m.act, st));
+    if ((s = run_gemm(ctx, m.pd[l], m.act, m.m_cap, M, m.y, m.d, st)) != SEED_OK) return s;
     const bool last = (l == m.L - 1);
     const bf16* nw = last ? m.final_norm : m.an[l + 1];
     if (l == last_layer - 1 && !last) {
       // partial-depth run (tests): residual only, no norm needed afterwards
-      CK(seed::epi_residual_rmsnorm(v, M, m.d, m.x, nw, eps, m.h, nullptr, nullptr, st));
+      CK(seed::residual_rmsnorm(m.y, M, m.d, m.x, nw, eps, m.h, nullptr, nullptr, st));
     } else {
-      CK(seed::epi_residual_rmsnorm(v, M, m.d, m.x, nw, eps, last ? nullptr : m.h, last ? c.compact : nullptr,
-                                    m.hlm, st));
+      CK(seed::residual_rmsnorm(m.y, M, m.d, m.x, nw, eps, last ? nullptr : m.h, last ? c.compact : nullptr,
+                                m.hlm, st));
     }
-    ctx->kernel_launches += 6;
+    ctx->kernel_launches += 4;
   }
   if (last_layer == m.L && c.n_logits > 0) {
-    PartialView v;
-    if ((s = run_gemm(ctx, m.plm, m.hlm, m.m_cap, c.n_logits, &v, st)) != SEED_OK) return s;
-    CK(seed::epi_store(v, m.V, c.Y, c.ldY, nullptr, c.n_logits, st));
-    ctx->kernel_launches++;
+    // the LM head writes the fp32 logits straight into the caller's rows (F2)
+    if ((s = run_gemm(ctx, m.plm, m.hlm, m.m_cap, c.n_logits, c.Y, c.ldY, st)) != SEED_OK) return s;
   }
   return SEED_OK;
 }
@@ -677,10 +689,19 @@ seed_status build_round_plan(seed_ctx ctx, const std::vector<int>& slots, int n,
     P.verify.push_back(c);
     P.verify_b0.push_back(b0);
   }
-  if (ctx->use_graphs) {  // fixed grids: attention sized for the longest context (R23)
-    for (auto& c : P.draft) c.max_kv = max_pos;
-    for (auto& c : P.verify) c.max_kv = max_pos;
-  }
+  // attention grids sized by the round's longest context, rounded up to whole chunks; the
+  // graphs are keyed by (batch size, chunk counts), so a graph is re-captured only when a
+  // context crosses a chunk boundary (R23)
+  const int ch = seed::attn_chunk_tokens();
+  int dk = 0, vk = 0;
+  for (auto& c : P.draft) dk = std::max(dk, c.max_kv);
+  for (auto& c : P.verify) vk = std::max(vk, c.max_kv);
+  dk = std::min(max_pos, (dk + ch - 1) / ch * ch);
+  vk = std::min(max_pos, (vk + ch - 1) / ch * ch);
+  for (auto& c : P.draft) c.max_kv = dk;
+  for (auto& c : P.verify) c.max_kv = vk;
+  P.key_draft = ((int64_t)n << 32) | (dk / ch);
+  P.key_verify = ((int64_t)n << 32) | (vk / ch);
   return SEED_OK;
 }
 
@@ -743,8 +764,15 @@ seed_status enqueue_verify(seed_ctx ctx, cudaStream_t st) {
                            ctx->records, ctx->sids_dev, st));
   ctx->kernel_launches += 2;
   if (ctx->profile) {
-    CK(seed::timing_accumulate(ctx->timing_rec, ctx->rec_used, ctx->timing_acc, st));
-    ctx->kernel_launches++;
+    // draft records live in [0, half), verify records in [half, ...)
+    const int half = ctx->rec_cap / 2;
+    const int nd = ctx->draft_recs[n], nv = ctx->rec_used - half;
+    ctx->last_draft_recs = nd;
+    ctx->last_verify_recs = nv;
+    CK(seed::timing_accumulate(ctx->timing_rec, nd, ctx->timing_acc, ctx->timing_last, st));
+    CK(seed::timing_accumulate(ctx->timing_rec + 4 * (size_t)half, nv, ctx->timing_acc,
+                               ctx->timing_last + 4 * (size_t)half, st));
+    ctx->kernel_launches += 2;
   }
   // a6: all-gather of the per-rank records over NVLink (world > 1)
   if (world > 1) {
@@ -762,25 +790,25 @@ seed_status enqueue_verify(seed_ctx ctx, cudaStream_t st) {
 seed_status run_phase(seed_ctx ctx, int n, bool draft, cudaStream_t st) {
   seed_status s;
   const int64_t k0 = ctx->kernel_launches;
-  if (draft) {
-    ctx->in_round = true;
-    ctx->rec_used = 0;
-    ctx->round_gemm_bytes = 0;
-    ctx->round_gemms = 0;
-  }
+  ctx->in_round = true;
+  ctx->rec_used = draft ? 0 : ctx->rec_cap / 2;
+  ctx->round_gemm_bytes = 0;
+  ctx->round_gemms = 0;
   if (!ctx->use_graphs) {
     s = draft ? enqueue_draft(ctx, st) : enqueue_verify(ctx, st);
     if (s != SEED_OK) return s;
-    if (!draft) {
-      ctx->gemm_bytes += ctx->round_gemm_bytes;
-      ctx->gemm_launches += ctx->round_gemms;
+    ctx->gemm_bytes += ctx->round_gemm_bytes;
+    ctx->gemm_launches += ctx->round_gemms;
+    if (draft) {
+      ctx->draft_recs[n] = ctx->rec_used;
+    } else {
       ctx->in_round = false;
       CK(cudaEventRecord(ctx->round_done, st));
     }
     return SEED_OK;
   }
-  auto& G = ctx->graphs[n];
-  cudaGraphExec_t& ex = draft ? G.draft : G.verify;
+  auto& G = draft ? ctx->draft_graphs[ctx->plan.key_draft] : ctx->verify_graphs[ctx->plan.key_verify];
+  cudaGraphExec_t& ex = G.exec;
   if (!ex) {
     cudaGraph_t graph;
     CK(cudaStreamBeginCapture(ctx->gstream, cudaStreamCaptureModeThreadLocal));
@@ -790,22 +818,22 @@ seed_status run_phase(seed_ctx ctx, int n, bool draft, cudaStream_t st) {
     CK(e);
     CK(cudaGraphInstantiate(&ex, graph, 0));
     cudaGraphDestroy(graph);
-    G.kernels += ctx->kernel_launches - k0;
-    if (!draft) {
-      G.gemm_bytes = ctx->round_gemm_bytes;
-      G.gemms = ctx->round_gemms;
-    }
-  } else {
-    ctx->kernel_launches += 0;  // counted below from the captured totals
+    G.kernels = ctx->kernel_launches - k0;
+    G.gemm_bytes = ctx->round_gemm_bytes;
+    G.gemms = ctx->round_gemms;
+    if (draft) ctx->draft_recs[n] = ctx->rec_used;
   }
   CK(cudaEventRecord(ctx->ev_in, st));
   CK(cudaStreamWaitEvent(ctx->gstream, ctx->ev_in, 0));
   CK(cudaGraphLaunch(ex, ctx->gstream));
-  if (!draft) {
+  ctx->kernel_launches = k0 + G.kernels;
+  if (draft) {
+    ctx->draft_gemm_bytes = G.gemm_bytes;
+    ctx->draft_gemms = G.gemms;
+  } else {
     CK(cudaEventRecord(ctx->round_done, ctx->gstream));
-    ctx->kernel_launches = k0 + G.kernels;
-    ctx->gemm_bytes += G.gemm_bytes;
-    ctx->gemm_launches += G.gemms;
+    ctx->gemm_bytes += ctx->draft_gemm_bytes + G.gemm_bytes;
+    ctx->gemm_launches += ctx->draft_gemms + G.gemms;
     ctx->in_round = false;
   }
   CK(cudaEventRecord(ctx->ev_out, ctx->gstream));
@@ -915,13 +943,16 @@ seed_status seed_init(const seed_config* cfg, seed_ctx* out) {
   }
   if (ctx->profile) {
     ctx->rec_cap = 8192;
-    ok &= cudaMalloc(&ctx->timing_rec, (size_t)ctx->rec_cap * 2 * 8) == cudaSuccess;
+    ok &= cudaMalloc(&ctx->timing_rec, (size_t)ctx->rec_cap * 4 * 8) == cudaSuccess;
+    ok &= cudaMalloc(&ctx->timing_last, (size_t)ctx->rec_cap * 4 * 8) == cudaSuccess;
     ok &= cudaMalloc(&ctx->timing_acc, 2 * 8) == cudaSuccess;
     if (ok) {
-      std::vector<unsigned long long> init((size_t)ctx->rec_cap * 2);
+      std::vector<unsigned long long> init((size_t)ctx->rec_cap * 4);
       for (int i = 0; i < ctx->rec_cap; ++i) {
-        init[2 * i] = ~0ull;
-        init[2 * i + 1] = 0ull;
+        init[4 * i] = ~0ull;
+        init[4 * i + 1] = ~0ull;
+        init[4 * i + 2] = 0ull;
+        init[4 * i + 3] = 0ull;
       }
       ok &= cudaMemcpy(ctx->timing_rec, init.data(), init.size() * 8, cudaMemcpyHostToDevice) == cudaSuccess;
       ok &= cudaMemset(ctx->timing_acc, 0, 16) == cudaSuccess;
@@ -957,15 +988,15 @@ void seed_destroy(seed_ctx ctx) {
   if (ctx->tok_host) cudaFreeHost(ctx->tok_host);
   ctx->arena.destroy();
   if (ctx->round_done) cudaEventDestroy(ctx->round_done);
-  for (auto& kv : ctx->graphs) {
-    if (kv.second.draft) cudaGraphExecDestroy(kv.second.draft);
-    if (kv.second.verify) cudaGraphExecDestroy(kv.second.verify);
-  }
+  for (auto* gm : {&ctx->draft_graphs, &ctx->verify_graphs})
+    for (auto& kv : *gm)
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
   if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
   if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
   if (ctx->timing_rec) cudaFree(ctx->timing_rec);
   if (ctx->timing_acc) cudaFree(ctx->timing_acc);
+  if (ctx->timing_last) cudaFree(ctx->timing_last);
   if (ctx->sched) seed_sched_destroy(ctx->sched);
   if (ctx->table) seed_table_destroy(ctx->table);
   if (ctx->comm && g_nccl.destroy) g_nccl.destroy(ctx->comm);
@@ -1180,6 +1211,22 @@ seed_status seed_get_profile(seed_ctx ctx, double* gemm_ms, int64_t* launches, d
   return SEED_OK;
 }
 
+seed_status seed_gemm_trace(seed_ctx ctx, uint64_t* out, int32_t cap, int32_t* n) {
+  if (!ctx || !n) return SEED_EINVAL;
+  *n = 0;
+  if (!ctx->timing_last) return SEED_OK;
+  const int nd = std::min(cap, ctx->last_draft_recs);
+  const int nv = std::min(cap - nd, ctx->last_verify_recs);
+  const size_t half = (size_t)ctx->rec_cap / 2;
+  if (cudaDeviceSynchronize() != cudaSuccess ||
+      (nd > 0 && cudaMemcpy(out, ctx->timing_last, (size_t)nd * 32, cudaMemcpyDeviceToHost) != cudaSuccess) ||
+      (nv > 0 && cudaMemcpy(out + 4 * (size_t)nd, ctx->timing_last + 4 * half, (size_t)nv * 32,
+                            cudaMemcpyDeviceToHost) != cudaSuccess))
+    return fail(ctx, SEED_ECUDA, "seed_gemm_trace", "");
+  *n = nd + nv;
+  return SEED_OK;
+}
+
 seed_status seed_reset_profile(seed_ctx ctx) {
   if (!ctx) return SEED_EINVAL;
   if (ctx->timing_acc && cudaMemset(ctx->timing_acc, 0, 2 * sizeof(unsigned long long)) != cudaSuccess)
@@ -1225,10 +1272,7 @@ seed_status seed_op_gemm(const void* W, int32_t N, int32_t K, const void* X, int
       s = SEED_ECUDA;
       break;
     }
-    PartialView v;
-    if (seed::gemm_run(p, tm, m, part, &v, st) != cudaSuccess ||
-        seed::epi_store(v, N, Y + (size_t)done * N, N, nullptr, m, st) != cudaSuccess)
-      s = SEED_ECUDA;
+    if (seed::gemm_run(p, tm, m, part, Y + (size_t)done * N, N, st) != cudaSuccess) s = SEED_ECUDA;
     done += m;
   }
   cudaFreeAsync(part, st);
@@ -1322,7 +1366,9 @@ seed_status seed_op_decoder_layer(const seed_model_shape* shape, const void* con
     const float eps = sh.rms_eps > 0 ? sh.rms_eps : 1e-5f;
     if (s == SEED_OK && cudaMemcpyAsync(m.x, x_in, (size_t)M * m.d * 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
       s = SEED_ECUDA;
-    if (s == SEED_OK && seed::rmsnorm_rows(m.x, M, m.d, m.an[0], eps, m.h, st) != cudaSuccess) s = SEED_ECUDA;
+    if (s == SEED_OK && seed::residual_rmsnorm(nullptr, M, m.d, m.x, m.an[0], eps, m.h, nullptr, nullptr, st) !=
+                             cudaSuccess)
+      s = SEED_ECUDA;
     if (s == SEED_OK) s = forward_chunk(ctx, m, c, st, 0, 1, false);
     if (s == SEED_OK && cudaMemcpyAsync(x_out, m.x, (size_t)M * m.d * 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
       s = SEED_ECUDA;

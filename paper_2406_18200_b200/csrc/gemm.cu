@@ -9,11 +9,12 @@
 // thread issues tcgen05.mma into a double-buffered TMEM accumulator; four epilogue
 // warps drain TMEM with tcgen05.ld while the next tile accumulates.
 //
-// Work split: the (tile, k-block) units are cut into G = min(148, U) contiguous ranges,
-// one persistent CTA per SM (stream-K).  A CTA writes one fp32 partial per tile it
-// touches; the consumer epilogue sums a tile's partials in CTA order.  G and the cut
-// points depend on (N, K) only, never on M, so every output column is computed in the
-// same order whatever the batch (batch invariance, DESIGN R19).
+// Work split: the (tile, k-block) units are cut into G = min(148, U / 4) contiguous ranges,
+// one persistent CTA per SM (stream-K).  A tile owned by one CTA goes straight from TMEM to Y;
+// a tile shared by several CTAs is written as fp32 partials and the last CTA to finish it
+// (atomic ticket) sums them in CTA order and writes Y.  G and the cut points depend on
+// (N, K) only, never on M, so every output column is computed in the same order whatever the
+// batch (batch invariance, DESIGN R19).
 #include <cuda.h>
 #include <algorithm>
 #include <cstdio>
@@ -31,12 +32,17 @@ constexpr int BLOCK_N = 128;   // weight rows per tile (UMMA M)
 constexpr int BLOCK_K = 64;    // one 128-byte swizzle row of bf16
 constexpr int W_TILE_BYTES = BLOCK_N * BLOCK_K * 2;
 constexpr int MAX_STAGES = 16;
-constexpr int SMEM_BUDGET = 220 * 1024;
+// 8 weight stages (128 KB in flight per SM) saturate HBM; the smem cap leaves room for an
+// attention / epilogue CTA to co-reside, so the next GEMM's weight prefetch overlaps it (PDL)
+constexpr int SMEM_BUDGET = 150 * 1024;
 
 struct GemmArgs {
-  int KB, U, G, S, M, m_pad, stages;
-  float* partial;
-  unsigned long long* timing;  // optional [2]: min CTA start, max CTA end (globaltimer ns)
+  int KB, U, G, S, M, m_pad, stages, N, ldY, maxseg;
+  float* partial;              // split-K partials of tiles shared by several CTAs
+  float* Y;                    // output fp32 [M][ldY]
+  const int* seg;              // per tile: count, partial-segment ids in CTA order
+  int* counters;               // per tile: finished segments (zero between launches)
+  unsigned long long* timing;  // optional [4]: min CTA start, min release (PDL), max CTA end (ns)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -52,6 +58,42 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)2 << 61;
   return d;
+}
+
+// Sum the partial segments of one tile column (weight row nl) for all M rows, in CTA order.
+// 16 rows per batch and two segments per step: every load is independent (ILP), the adds
+// keep the fixed k order.
+__device__ __forceinline__ void reduce_tile(const float* __restrict__ P, const int* __restrict__ sl, int M, int nl,
+                                            float* __restrict__ Y, int ldY, int n, int N) {
+  const int cnt = sl[0];
+  for (int m0 = 0; m0 < M; m0 += 16) {
+    float acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+    int k = 0;
+    for (; k + 1 < cnt; k += 2) {
+      const float* s0 = P + ((size_t)sl[1 + k] * M + m0) * BLOCK_N + nl;
+      const float* s1 = P + ((size_t)sl[2 + k] * M + m0) * BLOCK_N + nl;
+      float v0[16], v1[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        v0[j] = m0 + j < M ? __ldcg(s0 + (size_t)j * BLOCK_N) : 0.f;
+        v1[j] = m0 + j < M ? __ldcg(s1 + (size_t)j * BLOCK_N) : 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] = (acc[j] + v0[j]) + v1[j];
+    }
+    if (k < cnt) {
+      const float* s0 = P + ((size_t)sl[1 + k] * M + m0) * BLOCK_N + nl;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] += m0 + j < M ? __ldcg(s0 + (size_t)j * BLOCK_N) : 0.f;
+    }
+    if (n < N) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (m0 + j < M) Y[(size_t)(m0 + j) * ldY + n] = acc[j];
+    }
+  }
 }
 
 __global__ void __launch_bounds__(192, 1)
@@ -113,6 +155,7 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
         tma_load_2d(sW + i * W_TILE_BYTES, &tmW, &full[i], kb * BLOCK_K, t * BLOCK_N, pol_w);
       }
       pdl_wait();  // X (the activations) is written by the previous kernel
+      if (a.timing) atomicMin(&a.timing[1], globaltimer());
       for (long i = 0; i < n_pre; ++i) {
         const long u = u_begin + i;
         tma_load_2d(sX + i * x_bytes, &tmX, &full[i], (int)(u % a.KB) * BLOCK_K, 0, pol_x);
@@ -172,31 +215,54 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
       ++seg;
     }
   } else {
-    // ---------------- epilogue warps 2..5: TMEM -> fp32 partial [m][128]
+    // ---------------- epilogue warps 2..5: TMEM -> Y (whole tiles) or -> split-K partial; the
+    // last CTA to finish a shared tile sums its partials in CTA order and writes Y (R19)
     const int lane_grp = warp & 3;               // TMEM lanes this warp may access
     const int nl = lane_grp * 32 + lane;         // weight row within the tile
-    pdl_wait();                                  // the partial buffer is read by the predecessor
+    const int et = threadIdx.x - 64;             // 0..127 among the epilogue threads
+    volatile int* s_last = reinterpret_cast<volatile int*>(tmem_slot + 1);
+    pdl_wait();                                  // Y and the partials are read by the predecessor
     int seg = 0;
     long u = u_begin;
     while (u < u_end) {
       const long t = u / a.KB;
       const long seg_end = min(u_end, (t + 1) * a.KB);
+      const bool whole = (u == t * a.KB) && (seg_end == (t + 1) * a.KB);
+      const int n = (int)t * BLOCK_N + nl;
       const int acc = seg & 1;
       const uint32_t use = (uint32_t)(seg >> 1);
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
-      float* out = a.partial + ((size_t)((long)c * a.S + (t - t_begin)) * a.M) * BLOCK_N;
+      float* out = whole ? a.Y + n : a.partial + ((size_t)((long)c * a.S + (t - t_begin)) * a.M) * BLOCK_N + nl;
+      const size_t ld = whole ? (size_t)a.ldY : (size_t)BLOCK_N;
+      const bool keep = !whole || n < a.N;
       const uint32_t row_addr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(acc * a.m_pad);
       for (int col = 0; col < a.m_pad; col += 16) {
         float v[16];
         tmem_ld16(row_addr + col, v);
 #pragma unroll
         for (int i = 0; i < 16; ++i)
-          if (col + i < a.M) out[(size_t)(col + i) * BLOCK_N + nl] = v[i];
+          if (col + i < a.M && keep) out[(size_t)(col + i) * ld] = v[i];
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (!whole) {
+        // publish: barrier over the epilogue warps, then one thread fences and takes a ticket
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const int* sl = a.seg + t * (a.maxseg + 1);
+        if (et == 0) {
+          __threadfence();
+          *s_last = (atomicAdd(&a.counters[t], 1) == sl[0] - 1) ? 1 : 0;
+          __threadfence();
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (*s_last) {
+          reduce_tile(a.partial, sl, a.M, nl, a.Y, a.ldY, n, a.N);
+          if (et == 0) a.counters[t] = 0;   // ready for the next launch (graph replay)
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // s_last is reused by the next segment
+      }
       u = seg_end;
       ++seg;
     }
@@ -205,19 +271,29 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
   __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc(tmem_base, cols);
-  if (a.timing && threadIdx.x == 0) atomicMax(&a.timing[1], globaltimer());
+  if (a.timing && threadIdx.x == 0) atomicMax(&a.timing[2], globaltimer());
 }
 
-// adds the span of every recorded launch to acc[0] (ns) and the count to acc[1]; resets records
-__global__ void timing_accumulate_kernel(unsigned long long* rec, int n, unsigned long long* acc) {
+// adds the span of every recorded launch to acc[0] (ns) and the count to acc[1], copies the
+// records to `last` (the most recent round, for the trace ABI) and resets them
+__global__ void timing_accumulate_kernel(unsigned long long* rec, int n, unsigned long long* acc,
+                                         unsigned long long* last) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const unsigned long long s = rec[2 * i], e = rec[2 * i + 1];
+    const unsigned long long s = rec[4 * i], e = rec[4 * i + 2];
     if (e > s && s != ~0ull) {
       atomicAdd(&acc[0], e - s);
       atomicAdd(&acc[1], 1ull);
     }
-    rec[2 * i] = ~0ull;
-    rec[2 * i + 1] = 0ull;
+    if (last) {
+      last[4 * i] = rec[4 * i];
+      last[4 * i + 1] = rec[4 * i + 1];
+      last[4 * i + 2] = rec[4 * i + 2];
+      last[4 * i + 3] = rec[4 * i + 3];
+    }
+    rec[4 * i] = ~0ull;
+    rec[4 * i + 1] = ~0ull;
+    rec[4 * i + 2] = 0ull;
+    rec[4 * i + 3] = 0ull;
   }
 }
 
@@ -283,11 +359,26 @@ void gemm_plan(GemmPlan* p, const void* W, int N, int K) {
   p->seg = nullptr;
   if (cudaMalloc(&p->seg, flat.size() * sizeof(int)) == cudaSuccess)
     cudaMemcpy(p->seg, flat.data(), flat.size() * sizeof(int), cudaMemcpyHostToDevice);
+  p->counters = nullptr;
+  if (cudaMalloc(&p->counters, (size_t)p->tiles * sizeof(int)) == cudaSuccess)
+    cudaMemset(p->counters, 0, (size_t)p->tiles * sizeof(int));
 }
 
 void gemm_plan_free(GemmPlan* p) {
   if (p->seg) cudaFree(p->seg);
+  if (p->counters) cudaFree(p->counters);
   p->seg = nullptr;
+  p->counters = nullptr;
+}
+
+void carveout_once(const void* kern) {
+  static std::vector<const void*> done;
+  for (const void* k : done)
+    if (k == kern) return;
+  done.push_back(kern);
+  const char* e = getenv("SEED_CARVEOUT");
+  const int pct = e ? atoi(e) : 100;
+  if (pct >= 0) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
 }
 
 bool pdl_enabled() {
@@ -301,13 +392,14 @@ bool pdl_enabled() {
 
 size_t gemm_partial_floats(const GemmPlan& p, int M) { return (size_t)p.G * p.S * M * BLOCK_N; }
 
-cudaError_t timing_accumulate(unsigned long long* rec, int n, unsigned long long* acc, cudaStream_t st) {
+cudaError_t timing_accumulate(unsigned long long* rec, int n, unsigned long long* acc, unsigned long long* last,
+                              cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  timing_accumulate_kernel<<<1, 256, 0, st>>>(rec, n, acc);
+  timing_accumulate_kernel<<<1, 256, 0, st>>>(rec, n, acc, last);
   return cudaGetLastError();
 }
 
-cudaError_t gemm_run(const GemmPlan& p, const CUtensorMap& tmX, int M, float* partial, PartialView* view,
+cudaError_t gemm_run(const GemmPlan& p, const CUtensorMap& tmX, int M, float* partial, float* Y, int ldY,
                      cudaStream_t st, unsigned long long* timing) {
   GemmArgs a;
   a.KB = p.KB;
@@ -322,16 +414,20 @@ cudaError_t gemm_run(const GemmPlan& p, const CUtensorMap& tmX, int M, float* pa
   if (stages > MAX_STAGES) stages = MAX_STAGES;
   a.stages = stages;
   a.partial = partial;
+  a.Y = Y;
+  a.ldY = ldY;
+  a.N = p.N;
+  a.seg = p.seg;
+  a.maxseg = p.maxseg;
+  a.counters = p.counters;
   a.timing = timing;
-  const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 4) * 8 + 16;
+  const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 4) * 8 + 32;
   static bool attr_done = false;
   if (!attr_done) {
     cudaFuncSetAttribute(gemm_streamk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_done = true;
   }
-  cudaError_t e = launch(gemm_streamk_kernel, dim3(p.G), dim3(192), smem, st, p.tmW, tmX, a);
-  if (view) *view = PartialView{partial, p.seg, p.maxseg, M};
-  return e;
+  return launch(gemm_streamk_kernel, dim3(p.G), dim3(192), smem, st, p.tmW, tmX, a);
 }
 
 }  // namespace seed

@@ -28,13 +28,8 @@ struct GemmPlan {
   int N, K, KB, tiles, U, G, S;  // S = max segments per CTA
   int maxseg;                    // max partial segments per tile
   int* seg;                      // device [tiles][maxseg + 1]: count, then segment ids in CTA order
+  int* counters;                 // device [tiles]: split-K tickets (zero between launches)
   CUtensorMap tmW;
-};
-
-struct PartialView {  // read side of the split-K partial sums, batch-invariant order
-  const float* p;
-  const int* seg;
-  int maxseg, M;
 };
 
 bool encode_tmap_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
@@ -42,14 +37,14 @@ bool encode_tmap_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t 
 void gemm_plan(GemmPlan* plan, const void* W, int N, int K);
 void gemm_plan_free(GemmPlan* plan);
 size_t gemm_partial_floats(const GemmPlan& plan, int M);
-// launches the tcgen05 main loop; returns the view the epilogue kernels read
-cudaError_t gemm_run(const GemmPlan& plan, const CUtensorMap& tmX, int M, float* partial, PartialView* view,
+// Y[m][n] (row stride ldY) = sum_k X[m][k] W[n][k], fp32; `partial` is split-K scratch
+cudaError_t gemm_run(const GemmPlan& plan, const CUtensorMap& tmX, int M, float* partial, float* Y, int ldY,
                      cudaStream_t st, unsigned long long* timing = nullptr);
-cudaError_t timing_accumulate(unsigned long long* rec, int n, unsigned long long* acc, cudaStream_t st);
+cudaError_t timing_accumulate(unsigned long long* rec, int n, unsigned long long* acc, unsigned long long* last,
+                              cudaStream_t st);
 int gemm_mpad(int M);
 
 // ------------------------------------------------------------------ epilogues / elementwise
-cudaError_t epi_store(const PartialView& v, int N, float* Y, int ldY, const int32_t* row_map, int M, cudaStream_t st);
 struct RowInfo {         // per row of the ragged batch
   const int32_t* tok;    // [M] token ids
   const int32_t* pos;    // [M] absolute positions
@@ -57,16 +52,13 @@ struct RowInfo {         // per row of the ragged batch
 };
 cudaError_t embed_rmsnorm(const __nv_bfloat16* embed, const int32_t* tok, int tok_stride, int M, int d, const __nv_bfloat16* w,
                           float eps, float* x, __nv_bfloat16* h, cudaStream_t st);
-cudaError_t epi_qkv_rope(const PartialView& v, int M, int H, int Hk, int Dh, const RowInfo& rows,
-                         const float2* rope, int layer, const KVLayout& kv, __nv_bfloat16* q_out,
-                         __nv_bfloat16* k_dbg, __nv_bfloat16* v_dbg, cudaStream_t st);
-cudaError_t epi_residual_rmsnorm(const PartialView& v, int M, int d, float* x, const __nv_bfloat16* w, float eps,
-                                 __nv_bfloat16* h, const int32_t* compact_map, __nv_bfloat16* h_compact,
-                                 cudaStream_t st);
-cudaError_t epi_swiglu(const PartialView& v, int M, int ff, __nv_bfloat16* act, cudaStream_t st);
+// x[m] += Y[m] (Y may be null), h = bf16(rmsnorm(x[m]) * w); compact rows also to h_compact
+cudaError_t residual_rmsnorm(const float* Y, int M, int d, float* x, const __nv_bfloat16* w, float eps,
+                             __nv_bfloat16* h, const int32_t* compact_map, __nv_bfloat16* h_compact,
+                             cudaStream_t st);
+// act[m][i] = bf16(silu(g) * u), g/u from the interleaved gate/up GEMM output Y [M][2ff]
+cudaError_t swiglu(const float* Y, int M, int ff, __nv_bfloat16* act, cudaStream_t st);
 cudaError_t rope_table_init(float2* table, int max_pos, int Dh, double theta, cudaStream_t st);
-cudaError_t rmsnorm_rows(const float* x, int M, int d, const __nv_bfloat16* w, float eps, __nv_bfloat16* h,
-                         cudaStream_t st);
 cudaError_t kv_write_dense(const KVLayout& kv, int layer, int slot, int n, const __nv_bfloat16* k,
                            const __nv_bfloat16* v, cudaStream_t st);
 
@@ -80,12 +72,16 @@ struct SeqInfo {          // per sequence of the ragged batch (device arrays)
 struct AttnWorkspace {
   float* o_part;   // [splits][M][H][Dh]
   float* ml_part;  // [splits][M][H][2]
-  int max_splits;
+  int* counters;   // [max_counters] chunk tickets per (sequence block, head), zero between launches
+  int max_splits, max_counters;
+  unsigned long long* timing;  // optional profile record [4] (start, release, end)
 };
 int attn_chunk_tokens();
-cudaError_t attention(const __nv_bfloat16* q, int M, int n_seq, int max_q_len, int max_kv, int H, int Hk, int Dh,
-                      const SeqInfo& seqs, const KVLayout& kv, int layer, const AttnWorkspace& ws,
-                      __nv_bfloat16* out, cudaStream_t st);
+int attn_query_block();
+// fused: QKV epilogue (RoPE, bf16, KV append) + paged attention + split-KV merge; qkv = Y [M][(H+2Hk)Dh]
+cudaError_t attention(const float* qkv, int M, int n_seq, int max_q_len, int max_kv, int H, int Hk, int Dh,
+                      const SeqInfo& seqs, const float2* rope, const KVLayout& kv, int layer,
+                      const AttnWorkspace& ws, __nv_bfloat16* out, cudaStream_t st);
 
 // ------------------------------------------------------------------ K4 / K1 sampler / K5
 struct VerifyArgs {
