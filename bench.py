@@ -290,7 +290,10 @@ def run_ours(args):
                      "unit": "GB/s", "frac": achieved / hbm, "peak_source": peak_src,
                      "traffic": traffic_from_profiles(), "launches": prof["gemm_launches"],
                      "gemm_share_of_step": prof["gemm_ms"] / ms if world == 1 else None,
-                     "bytes_per_launch": gemm_bytes, "avg_launch_us": gemm_avg_ms * 1e3},
+                     "bytes_per_launch": gemm_bytes, "avg_launch_us": gemm_avg_ms * 1e3,
+                     "timing": "device %globaltimer per launch: dependency release -> last CTA end "
+                               "(the weight prefetch overlapped with the predecessor under PDL is not counted)",
+                     "avg_span_us": prof["gemm_span_ms"] / max(prof["gemm_launches"], 1) * 1e3},
         "e2e": {"value": emitted_e2e / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d // steps,
                 "d2h_bytes_per_step": d2h // steps},
         "clocks": clk,

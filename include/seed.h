@@ -155,10 +155,14 @@ SEED_API seed_status seed_forward_logits(seed_ctx ctx, int32_t which, const int3
 SEED_API seed_status seed_last_round_buffers(seed_ctx ctx, const float** tgt_logits, const float** drf_logits,
                                     const int32_t** draft_tokens);
 
-/* Profiling (SEED_FLAG_PROFILE): total device ms and launch count of the GEMM kernel since
- * the last reset, measured with CUDA events on the launching stream. */
+/* Profiling (SEED_FLAG_PROFILE), since the last reset, measured on the device with %globaltimer
+ * inside the GEMM kernel (launches inside CUDA graphs with PDL have no stream events between them):
+ * gemm_ms = sum over GEMM launches of (last CTA end - dependency release), i.e. the time each GEMM
+ * holds the critical path; gemm_span_ms = sum of (last CTA end - first CTA start), which also
+ * counts the weight prefetch overlapped with the predecessor; gemm_bytes = algorithmic bytes
+ * (weights + activations + fp32 outputs); kernel_launches = libseed kernels launched. */
 SEED_API seed_status seed_get_profile(seed_ctx ctx, double* gemm_ms, int64_t* gemm_launches,
-                             double* gemm_bytes, int64_t* kernel_launches);
+                             double* gemm_bytes, int64_t* kernel_launches, double* gemm_span_ms);
 SEED_API seed_status seed_reset_profile(seed_ctx ctx);
 /* GEMM trace of the most recent round (SEED_FLAG_PROFILE): out[4*i..4*i+3] = globaltimer ns of
  * launch i: first CTA start, dependency release (PDL wait returned), last CTA end, 0.

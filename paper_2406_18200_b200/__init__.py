@@ -153,9 +153,11 @@ class SeedEngine:
                 _wrap(x.value, (n, g), torch.int32))
 
     def profile(self):
-        ms, n, by, k = C.c_double(), C.c_int64(), C.c_double(), C.c_int64()
-        self._check(self.lib.seed_get_profile(self.ctx, C.byref(ms), C.byref(n), C.byref(by), C.byref(k)), "profile")
-        return {"gemm_ms": ms.value, "gemm_launches": n.value, "gemm_bytes": by.value, "kernel_launches": k.value}
+        ms, n, by, k, sp = C.c_double(), C.c_int64(), C.c_double(), C.c_int64(), C.c_double()
+        self._check(self.lib.seed_get_profile(self.ctx, C.byref(ms), C.byref(n), C.byref(by), C.byref(k), C.byref(sp)),
+                    "profile")
+        return {"gemm_ms": ms.value, "gemm_launches": n.value, "gemm_bytes": by.value, "kernel_launches": k.value,
+                "gemm_span_ms": sp.value}
 
     def gemm_trace(self, cap=4096):
         """[(start, release, end)] globaltimer ns of each GEMM launch of the last round (profile=True)."""

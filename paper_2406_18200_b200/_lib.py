@@ -55,7 +55,7 @@ _SIGS = {
     "seed_forward_logits": [_P, C.c_int32, _I32P, C.c_int32, _P, _P],
     "seed_last_round_buffers": [_P, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)],
     "seed_get_profile": [_P, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_double),
-                         C.POINTER(C.c_int64)],
+                         C.POINTER(C.c_int64), C.POINTER(C.c_double)],
     "seed_reset_profile": [_P],
     "seed_gemm_trace": [_P, C.POINTER(C.c_uint64), C.c_int32, _I32P],
     "seed_last_error": [_P],

@@ -81,16 +81,33 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
 
   pdl_trigger();
   if (ws.timing && threadIdx.x == 0) atomicMin(&ws.timing[0], globaltimer_ns());
-  pdl_wait();
-  if (ws.timing && threadIdx.x == 0) atomicMin(&ws.timing[1], globaltimer_ns());
-  auto done = [&]() {
-    if (ws.timing && threadIdx.x == 0) atomicMax(&ws.timing[2], globaltimer_ns());
-  };
   const int seq = blockIdx.x / n_qblk, qb = blockIdx.x % n_qblk;
   const int head = blockIdx.y, split = blockIdx.z, nsplit = gridDim.z;
   const int kvh = head / (H / Hk);
+  // the descriptors were uploaded before the round's first kernel: safe before pdl_wait()
   const int q0 = seqs.q_start[seq], ql = seqs.q_len[seq], kvl = seqs.kv_len[seq];
   const int slot = seqs.slot[seq];
+  if (seqs.stable && threadIdx.x < 32) {
+    // keys below `stable` were written before this round: pull this chunk's cached K / V into
+    // L2 while our predecessor (the QKV GEMM) still runs
+    const int p0 = (split * CHUNK) / kv.P;
+    const int p1 = (min(seqs.stable[seq], split * CHUNK + CHUNK) + kv.P - 1) / kv.P;
+    const uint32_t blk = (uint32_t)kv.P * DH * 2;
+    for (int i = p0 + (int)threadIdx.x; i < p1; i += 32) {
+      const int page = __ldg(kv.page_table + (size_t)slot * kv.max_pages + i);
+      const __nv_bfloat16* kb0 = kv.pool + kv.offset(page, layer, 0, kvh, 0);
+      prefetch_l2(kb0, blk);
+      prefetch_l2(kb0 + kv.vofs(), blk);
+    }
+  }
+  pdl_wait();
+  if (ws.timing && threadIdx.x == 0) atomicMin(&ws.timing[1], globaltimer_ns());
+  auto done = [&]() {
+    if (ws.timing && threadIdx.x == 0) {
+      atomicMax(&ws.timing[2], globaltimer_ns());
+      ws.timing[3] = 2;  // record kind: attention
+    }
+  };
   const int r0 = qb * QB;
   if (r0 >= ql) {
     done();
@@ -310,9 +327,9 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
   __syncthreads();
   int* ctr = ws.counters + ((size_t)(seq * n_qblk + qb) * H + head);
   if (tid == 0) {
-    __threadfence();
+    fence_acq_rel_gpu();
     *ticket_s = atomicAdd(ctr, 1);
-    __threadfence();
+    fence_acq_rel_gpu();
   }
   __syncthreads();
   if (*ticket_s != nsplit - 1) {

@@ -157,6 +157,13 @@ SEED_DEV void cp_async16(void* smem_dst, const void* gsrc) {
 }
 SEED_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// L2 prefetch of a contiguous global range (TMA non-tensor), bytes % 16 == 0
+SEED_DEV void prefetch_l2(const void* gsrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gsrc), "r"(bytes) : "memory");
+}
+// release/acquire fence at GPU scope (cheaper than the sequentially consistent __threadfence)
+SEED_DEV void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 SEED_DEV unsigned long long globaltimer_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

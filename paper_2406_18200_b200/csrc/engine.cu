@@ -103,6 +103,7 @@ struct Arena {
 struct Segment {  // rows of one sequence in a forward chunk
   int slot, pos0, q_len;
   int tok_off;    // offset of host tokens in the arena (-1: tokens from a device source)
+  int stable = 0; // cache positions written before this round (attention may prefetch them early)
 };
 
 struct TokSrc {   // device token source for rows (row m reads dev[m * stride])
@@ -143,7 +144,7 @@ struct SlotState {  // host mirror of one stream slot
 
 struct ChunkDesc {
   int M, n_seq, max_q_len, max_kv;
-  const int32_t *pos, *slot, *q_start, *q_len, *kv_len, *seq_slot, *compact;  // device (slot: per row)
+  const int32_t *pos, *slot, *q_start, *q_len, *kv_len, *seq_slot, *seq_stable, *compact;  // device (slot: per row)
   TokSrc tok;
   int n_logits;
   float* Y;       // logits destination for compact row 0
@@ -451,7 +452,7 @@ seed_status forward_chunk(seed_ctx ctx, Model& m, const ChunkDesc& c, cudaStream
     CK(seed::embed_rmsnorm(m.embed, c.tok.dev, c.tok.stride, M, m.d, m.an[first_layer], eps, m.x, m.h, st));
     ctx->kernel_launches++;
   }
-  seed::SeqInfo seqs{c.q_start, c.q_len, c.kv_len, c.seq_slot};
+  seed::SeqInfo seqs{c.q_start, c.q_len, c.kv_len, c.seq_slot, c.seq_stable};
   for (int l = first_layer; l < last_layer; ++l) {
     if ((s = run_gemm(ctx, m.pq[l], m.h, m.m_cap, M, m.y, m.nqkv, st)) != SEED_OK) return s;
     {
@@ -497,8 +498,8 @@ bool pack_chunk(seed_ctx ctx, const std::vector<Segment>& segs, int logits_mode,
   }
   const size_t o_pos = A.alloc(M), o_slot = A.alloc(M), o_cmp = A.alloc(M), o_tok = A.alloc(M);
   const size_t n = segs.size();
-  const size_t o_qs = A.alloc(n), o_ql = A.alloc(n), o_kv = A.alloc(n), o_ss = A.alloc(n);
-  if (o_ss == (size_t)-1) return false;
+  const size_t o_qs = A.alloc(n), o_ql = A.alloc(n), o_kv = A.alloc(n), o_ss = A.alloc(n), o_st = A.alloc(n);
+  if (o_st == (size_t)-1) return false;
   int r = 0, nl = 0;
   for (size_t i = 0; i < n; ++i) {
     const Segment& s = segs[i];
@@ -506,6 +507,7 @@ bool pack_chunk(seed_ctx ctx, const std::vector<Segment>& segs, int logits_mode,
     A.host[o_ql + i] = s.q_len;
     A.host[o_kv + i] = s.pos0 + s.q_len;
     A.host[o_ss + i] = s.slot;
+    A.host[o_st + i] = s.stable;
     for (int j = 0; j < s.q_len; ++j, ++r) {
       A.host[o_pos + r] = s.pos0 + j;
       A.host[o_slot + r] = s.slot;
@@ -521,6 +523,7 @@ bool pack_chunk(seed_ctx ctx, const std::vector<Segment>& segs, int logits_mode,
   c->pos = A.dev + o_pos;
   c->slot = A.dev + o_slot;
   c->seq_slot = A.dev + o_ss;
+  c->seq_stable = A.dev + o_st;
   c->compact = A.dev + o_cmp;
   c->q_start = A.dev + o_qs;
   c->q_len = A.dev + o_ql;
@@ -657,7 +660,7 @@ seed_status build_round_plan(seed_ctx ctx, const std::vector<int>& slots, int n,
     if (to == (size_t)-1) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
     A.host[to] = ss.T[T - 2];
     A.host[to + 1] = ss.T[T - 1];
-    segs[b] = Segment{slots[b], T - 2, 2, (int)to};
+    segs[b] = Segment{slots[b], T - 2, 2, (int)to, T - 2};
   }
   size_t tok_off;
   if (2 * n > kMaxChunkRows || !pack_chunk(ctx, segs, 2, &P.draft[0], &tok_off))
@@ -665,7 +668,7 @@ seed_status build_round_plan(seed_ctx ctx, const std::vector<int>& slots, int n,
   for (int j = 2; j <= g; ++j) {
     for (int b = 0; b < n; ++b) {
       const int T = (int)ctx->slots[slots[b]].T.size();
-      segs[b] = Segment{slots[b], T + j - 2, 1, -1};
+      segs[b] = Segment{slots[b], T + j - 2, 1, -1, T - 2};
     }
     if (!pack_chunk(ctx, segs, 2, &P.draft[j - 1], &tok_off)) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
     P.draft[j - 1].tok = TokSrc{ctx->xs + (j - 2), g};  // x_{j-1} of every stream ([B][g] layout)
@@ -679,7 +682,7 @@ seed_status build_round_plan(seed_ctx ctx, const std::vector<int>& slots, int n,
     std::vector<Segment> vs(nb);
     for (int b = 0; b < nb; ++b) {
       const int T = (int)ctx->slots[slots[b0 + b]].T.size();
-      vs[b] = Segment{slots[b0 + b], T - 1, g + 1, -1};
+      vs[b] = Segment{slots[b0 + b], T - 1, g + 1, -1, T - 1};
     }
     ChunkDesc c;
     if (!pack_chunk(ctx, vs, 1, &c, &tok_off)) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
@@ -945,7 +948,7 @@ seed_status seed_init(const seed_config* cfg, seed_ctx* out) {
     ctx->rec_cap = 8192;
     ok &= cudaMalloc(&ctx->timing_rec, (size_t)ctx->rec_cap * 4 * 8) == cudaSuccess;
     ok &= cudaMalloc(&ctx->timing_last, (size_t)ctx->rec_cap * 4 * 8) == cudaSuccess;
-    ok &= cudaMalloc(&ctx->timing_acc, 2 * 8) == cudaSuccess;
+    ok &= cudaMalloc(&ctx->timing_acc, 4 * 8) == cudaSuccess;
     if (ok) {
       std::vector<unsigned long long> init((size_t)ctx->rec_cap * 4);
       for (int i = 0; i < ctx->rec_cap; ++i) {
@@ -955,7 +958,7 @@ seed_status seed_init(const seed_config* cfg, seed_ctx* out) {
         init[4 * i + 3] = 0ull;
       }
       ok &= cudaMemcpy(ctx->timing_rec, init.data(), init.size() * 8, cudaMemcpyHostToDevice) == cudaSuccess;
-      ok &= cudaMemset(ctx->timing_acc, 0, 16) == cudaSuccess;
+      ok &= cudaMemset(ctx->timing_acc, 0, 32) == cudaSuccess;
     }
   }
   if (!ok) return fail_init(SEED_ENOMEM);
@@ -1194,17 +1197,20 @@ seed_status seed_last_round_buffers(seed_ctx ctx, const float** t, const float**
   return SEED_OK;
 }
 
-seed_status seed_get_profile(seed_ctx ctx, double* gemm_ms, int64_t* launches, double* bytes, int64_t* kernels) {
+seed_status seed_get_profile(seed_ctx ctx, double* gemm_ms, int64_t* launches, double* bytes, int64_t* kernels,
+                             double* gemm_span_ms) {
   if (!ctx) return SEED_EINVAL;
-  double ms = 0;
+  double ms = 0, span = 0;
   if (ctx->timing_acc) {
-    unsigned long long acc[2] = {0, 0};
+    unsigned long long acc[4] = {0, 0, 0, 0};
     if (cudaDeviceSynchronize() != cudaSuccess ||
         cudaMemcpy(acc, ctx->timing_acc, sizeof(acc), cudaMemcpyDeviceToHost) != cudaSuccess)
       return fail(ctx, SEED_ECUDA, "seed_get_profile", "");
     ms = acc[0] * 1e-6;
+    span = acc[2] * 1e-6;
   }
   if (gemm_ms) *gemm_ms = ms;
+  if (gemm_span_ms) *gemm_span_ms = span;
   if (launches) *launches = ctx->gemm_launches;
   if (bytes) *bytes = ctx->gemm_bytes;
   if (kernels) *kernels = ctx->kernel_launches;
@@ -1229,7 +1235,7 @@ seed_status seed_gemm_trace(seed_ctx ctx, uint64_t* out, int32_t cap, int32_t* n
 
 seed_status seed_reset_profile(seed_ctx ctx) {
   if (!ctx) return SEED_EINVAL;
-  if (ctx->timing_acc && cudaMemset(ctx->timing_acc, 0, 2 * sizeof(unsigned long long)) != cudaSuccess)
+  if (ctx->timing_acc && cudaMemset(ctx->timing_acc, 0, 4 * sizeof(unsigned long long)) != cudaSuccess)
     return fail(ctx, SEED_ECUDA, "seed_reset_profile", "");
   ctx->gemm_bytes = 0;
   ctx->gemm_launches = 0;

@@ -252,9 +252,9 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
         asm volatile("bar.sync 1, 128;" ::: "memory");
         const int* sl = a.seg + t * (a.maxseg + 1);
         if (et == 0) {
-          __threadfence();
+          fence_acq_rel_gpu();
           *s_last = (atomicAdd(&a.counters[t], 1) == sl[0] - 1) ? 1 : 0;
-          __threadfence();
+          fence_acq_rel_gpu();
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (*s_last) {
@@ -271,18 +271,23 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
   __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc(tmem_base, cols);
-  if (a.timing && threadIdx.x == 0) atomicMax(&a.timing[2], globaltimer());
+  if (a.timing && threadIdx.x == 0) {
+    atomicMax(&a.timing[2], globaltimer());
+    a.timing[3] = 1;  // record kind: GEMM
+  }
 }
 
-// adds the span of every recorded launch to acc[0] (ns) and the count to acc[1], copies the
-// records to `last` (the most recent round, for the trace ABI) and resets them
+// GEMM records (kind 1): acc[0] += end - release (ns on the critical path), acc[1] += 1,
+// acc[2] += end - start (span, including the PDL overlap with the predecessor); copies all records
+// to `last` (the most recent round, for the trace ABI) and resets them
 __global__ void timing_accumulate_kernel(unsigned long long* rec, int n, unsigned long long* acc,
                                          unsigned long long* last) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const unsigned long long s = rec[4 * i], e = rec[4 * i + 2];
-    if (e > s && s != ~0ull) {
-      atomicAdd(&acc[0], e - s);
+    const unsigned long long s = rec[4 * i], r = rec[4 * i + 1], e = rec[4 * i + 2];
+    if (rec[4 * i + 3] == 1 && e > s && s != ~0ull) {
+      atomicAdd(&acc[0], e - (r != ~0ull && r < e ? r : s));
       atomicAdd(&acc[1], 1ull);
+      atomicAdd(&acc[2], e - s);
     }
     if (last) {
       last[4 * i] = rec[4 * i];

@@ -68,6 +68,7 @@ struct SeqInfo {          // per sequence of the ragged batch (device arrays)
   const int32_t* q_len;   // rows
   const int32_t* kv_len;  // keys after append = pos(last row) + 1
   const int32_t* slot;
+  const int32_t* stable;  // keys written before the round (safe to prefetch early); may be null
 };
 struct AttnWorkspace {
   float* o_part;   // [splits][M][H][Dh]
