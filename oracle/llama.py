@@ -13,7 +13,9 @@ Two modes:
   "bf16"  -- bf16-faithful: fp64 arithmetic, rounded to bf16 (RNE) exactly at the
              points where the CUDA path stores bf16, and to fp32 where it keeps
              fp32 (DESIGN.md "bf16 rounding points"):
-               B1 RMSNorm output (operand of QKV, gate/up and LM-head GEMMs)
+               B1 RMSNorm operand of the QKV, gate/up and LM-head GEMMs: bf16(x * w);
+                  the 1/rms(x) row scale is applied to the fp32 GEMM output
+                  (R24; the same linear map, rounded at another point)
                B2 Q and K after RoPE, and V (the KV cache is bf16)
                B3 attention output (operand of the O GEMM)
                B4 SwiGLU product silu(g) * u (operand of the down GEMM)
@@ -84,6 +86,18 @@ def apply_rope(x, cos, sin):
     return x * cos[:, None, :] + rot * sin[:, None, :]
 
 
+def norm_matmul(x, w, mats, eps, faithful):
+    """rmsnorm(x, w) @ M^T for each M in mats.  fp64: the definition.  bf16-faithful (R24):
+    (bf16(x * w) @ M^T) * 1/sqrt(mean(x^2) + eps) -- equal in exact arithmetic, since the
+    row scale 1/rms(x) commutes with the matrix product."""
+    if not faithful:
+        h = rmsnorm(x, w, eps)
+        return [h @ M.T for M in mats]
+    hw = bf16_round(x * w)                                                      # B1
+    inv = 1.0 / np.sqrt(np.mean(x * x, axis=-1, keepdims=True) + eps)
+    return [(hw @ M.T) * inv for M in mats]
+
+
 def silu(x):
     return x / (1.0 + np.exp(-x))
 
@@ -133,10 +147,8 @@ def _layer(sh, Lc, x, positions, K_prev, V_prev, faithful):
     rf = f32_round if faithful else (lambda a: a)
     H, Hk, Dh = sh.n_heads, sh.kv_heads, sh.head_dim
     q_len = x.shape[0]
-    h = rb(rmsnorm(x, Lc["attn_norm"], sh.rms_eps))                  # B1
-    q = (h @ Lc["wq"].T).reshape(q_len, H, Dh)
-    k = (h @ Lc["wk"].T).reshape(q_len, Hk, Dh)
-    v = (h @ Lc["wv"].T).reshape(q_len, Hk, Dh)
+    q, k, v = norm_matmul(x, Lc["attn_norm"], [Lc["wq"], Lc["wk"], Lc["wv"]], sh.rms_eps, faithful)   # B1
+    q, k, v = q.reshape(q_len, H, Dh), k.reshape(q_len, Hk, Dh), v.reshape(q_len, Hk, Dh)
     cos, sin = rope_cos_sin(positions, Dh, sh.rope_theta)
     q = rb(apply_rope(q, cos, sin))                                   # B2
     k = rb(apply_rope(k, cos, sin))
@@ -145,8 +157,7 @@ def _layer(sh, Lc, x, positions, K_prev, V_prev, faithful):
     Vc = np.concatenate([V_prev, v], axis=0)
     o = rb(_attention(q, K, Vc, positions, H // Hk).reshape(q_len, H * Dh))   # B3
     x = rf(x + o @ Lc["wo"].T)                                        # F1
-    h2 = rb(rmsnorm(x, Lc["mlp_norm"], sh.rms_eps))                   # B1
-    g, u = h2 @ Lc["w_gate"].T, h2 @ Lc["w_up"].T
+    g, u = norm_matmul(x, Lc["mlp_norm"], [Lc["w_gate"], Lc["w_up"]], sh.rms_eps, faithful)        # B1
     if faithful:
         g, u = rf(g), rf(u)
     act = rb(silu(g) * u)                                             # B4
@@ -164,7 +175,6 @@ def forward_batch(shape: LlamaShape, W, seqs, mode="bf16", logits_rows=None, cap
     Layers are the outer loop so each weight matrix is converted once.
     """
     faithful = mode == "bf16"
-    rb = bf16_round if faithful else (lambda a: a)
     rf = f32_round if faithful else (lambda a: a)
     xs, poss = [], []
     for toks, cache in seqs:
@@ -187,8 +197,7 @@ def forward_batch(shape: LlamaShape, W, seqs, mode="bf16", logits_rows=None, cap
         x = xs[s]
         if logits_rows is not None and logits_rows[s] is not None:
             x = x[logits_rows[s]]
-        h = rb(rmsnorm(x, fn, shape.rms_eps))                         # B1
-        out.append(rf(h @ head.T))                                    # F2
+        out.append(rf(norm_matmul(x, fn, [head], shape.rms_eps, faithful)[0]))   # B1, F2
     return out
 
 

@@ -129,8 +129,11 @@ struct Model {
   // activations for up to m_cap rows per forward chunk
   int m_cap = 0;
   float* x = nullptr;
-  float* y = nullptr;   // fp32 GEMM output [m_cap][max(nqkv, 2 ff, d)]
-  bf16 *h = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr, *hlm = nullptr;
+  float* y = nullptr;    // fp32 QKV output [m_cap][nqkv]
+  float *ssq_a = nullptr, *ssq_b = nullptr;  // per-tile sums of squares of the residual [d/128][m_cap]
+  bf16* h = nullptr;     // bf16(x * w_norm): operand of QKV / gate-up / LM head (B1, R24)
+  bf16* act = nullptr;   // bf16(silu(g) * u): operand of the down projection (B4)
+  bf16* attn = nullptr;  // attention output (bf16 operand of the O projection, B3)
   seed::AttnWorkspace aws{};
   std::vector<bf16*> owned;
 };
@@ -147,6 +150,7 @@ struct ChunkDesc {
   const int32_t *pos, *slot, *q_start, *q_len, *kv_len, *seq_slot, *seq_stable, *compact;  // device (slot: per row)
   TokSrc tok;
   int n_logits;
+  const int32_t* logit_rows;  // device [n_logits]: chunk row of each logits row
   float* Y;       // logits destination for compact row 0
   int ldY;
 };
@@ -251,19 +255,28 @@ const CUtensorMap* xmap(seed_ctx ctx, const bf16* buf, int K, int rows_cap, int 
   return &(ctx->xmaps[key] = m);
 }
 
-seed_status run_gemm(seed_ctx ctx, const GemmPlan& p, const bf16* X, int rows_cap, int M, float* Y, int ldY,
-                     cudaStream_t st) {
-  const CUtensorMap* tm = xmap(ctx, X, p.K, rows_cap, M);
-  if (!tm) return fail(ctx, SEED_ECUDA, "cuTensorMapEncodeTiled", "X operand");
+seed_status run_gemm(seed_ctx ctx, const GemmPlan& p, int M, const seed::GemmIO& io, cudaStream_t st) {
   unsigned long long* rec = nullptr;
   if (ctx->profile && ctx->in_round && ctx->rec_used < ctx->rec_cap) rec = ctx->timing_rec + 4 * ctx->rec_used++;
-  CK(seed::gemm_run(p, *tm, M, ctx->partial, Y, ldY, st, rec));
+  CK(seed::gemm_run(p, M, io, ctx->partial, st, rec));
   if (ctx->in_round) {
-    ctx->round_gemm_bytes += (double)p.N * p.K * 2 + (double)M * p.K * 2 + (double)M * p.N * 4;
+    // algorithmic bytes: weights + bf16 X + output (fp32 Y; residual: read + write x, write bf16 h;
+    // SwiGLU: bf16 act of half the width)
+    const double yout = io.ymode == 0 ? 4.0 : (io.ymode == 1 ? 10.0 : 1.0);
+    ctx->round_gemm_bytes += (double)p.N * p.K * 2 + (double)M * p.K * 2 + (double)M * p.N * yout;
     ctx->round_gemms++;
   }
   ctx->kernel_launches++;
   return SEED_OK;
+}
+
+// X operand from a bf16 activation buffer by TMA
+seed::GemmIO io_tma(seed_ctx ctx, const bf16* X, int K, int rows_cap, int M, float* Y, int ldY) {
+  seed::GemmIO io;
+  io.tmX = xmap(ctx, X, K, rows_cap, M);
+  io.Y = Y;
+  io.ldY = ldY;
+  return io;
 }
 
 // ------------------------------------------------------------------ model setup
@@ -370,13 +383,13 @@ seed_status build_model(seed_ctx ctx, Model& m, const seed_model_shape& sh, cons
   m.m_cap = std::max(m_cap, 256);
   const size_t mc = m.m_cap;
   CK(cudaMalloc(&m.x, mc * d * 4));
-  CK(cudaMalloc(&m.y, mc * std::max<size_t>({(size_t)m.nqkv, 2 * ff, d}) * 4));
-  m.h = alloc(mc * d);
-  m.q = alloc(mc * dq);
+  CK(cudaMalloc(&m.ssq_a, ((d + 127) / 128) * mc * 4));
+  CK(cudaMalloc(&m.ssq_b, ((d + 127) / 128) * mc * 4));
+  CK(cudaMalloc(&m.y, mc * std::max<size_t>((size_t)m.nqkv, d) * 4));
   m.attn = alloc(mc * dq);
+  m.h = alloc(mc * d);
   m.act = alloc(mc * ff);
-  m.hlm = alloc(mc * d);
-  if (!m.h || !m.q || !m.attn || !m.act || !m.hlm) return fail(ctx, SEED_ENOMEM, "seed_init", "activations");
+  if (!m.attn || !m.h || !m.act) return fail(ctx, SEED_ENOMEM, "seed_init", "activations");
   m.aws.max_splits = (max_pos + seed::attn_chunk_tokens() - 1) / seed::attn_chunk_tokens();
   CK(cudaMalloc(&m.aws.o_part, (size_t)m.aws.max_splits * mc * dq * 4));
   CK(cudaMalloc(&m.aws.ml_part, (size_t)m.aws.max_splits * mc * m.H * 2 * 4));
@@ -399,6 +412,8 @@ void free_model(Model& m) {
   if (m.rope) cudaFree(m.rope);
   if (m.x) cudaFree(m.x);
   if (m.y) cudaFree(m.y);
+  if (m.ssq_a) cudaFree(m.ssq_a);
+  if (m.ssq_b) cudaFree(m.ssq_b);
   if (m.aws.o_part) cudaFree(m.aws.o_part);
   if (m.aws.ml_part) cudaFree(m.aws.ml_part);
   if (m.aws.counters) cudaFree(m.aws.counters);
@@ -448,13 +463,34 @@ seed_status forward_chunk(seed_ctx ctx, Model& m, const ChunkDesc& c, cudaStream
   if (last_layer < 0) last_layer = m.L;
   const int M = c.M;
   seed_status s;
-  if (embed) {
-    CK(seed::embed_rmsnorm(m.embed, c.tok.dev, c.tok.stride, M, m.d, m.an[first_layer], eps, m.x, m.h, st));
-    ctx->kernel_launches++;
-  }
+  // the RMSNorm weight applied to the residual after layer l (B1, R24)
+  auto next_norm = [&](int l) { return l + 1 < m.L ? m.an[l + 1] : m.final_norm; };
+  // embedding (or the given residual), its per-tile sums of squares and h = bf16(x * attn_norm)
+  CK(seed::embed_stats(embed ? m.embed : nullptr, c.tok.dev, c.tok.stride, M, m.d, m.x, m.ssq_b,
+                       first_layer < m.L ? m.an[first_layer] : m.final_norm, m.h, st));
+  ctx->kernel_launches++;
   seed::SeqInfo seqs{c.q_start, c.q_len, c.kv_len, c.seq_slot, c.seq_stable};
+  const CUtensorMap* tm_h = xmap(ctx, m.h, m.d, m.m_cap, M);
+  const CUtensorMap* tm_attn = xmap(ctx, m.attn, m.H * m.Dh, m.m_cap, M);
+  const CUtensorMap* tm_act = xmap(ctx, m.act, m.ff, m.m_cap, M);
+  if (!tm_h || !tm_attn || !tm_act) return fail(ctx, SEED_ECUDA, "cuTensorMapEncodeTiled", "activations");
+  // X = h, output rows scaled by 1/rms from the per-tile sums of squares `ssq`
+  auto norm_io = [&](const float* ssq) {
+    seed::GemmIO io;
+    io.tmX = tm_h;
+    io.ssq_in = ssq;
+    io.ssq_in_ld = M;
+    io.eps = eps;
+    return io;
+  };
   for (int l = first_layer; l < last_layer; ++l) {
-    if ((s = run_gemm(ctx, m.pq[l], m.h, m.m_cap, M, m.y, m.nqkv, st)) != SEED_OK) return s;
+    // QKV: y = (h Wqkv^T) / rms(x)
+    {
+      seed::GemmIO io = norm_io(m.ssq_b);
+      io.Y = m.y;
+      io.ldY = m.nqkv;
+      if ((s = run_gemm(ctx, m.pq[l], M, io, st)) != SEED_OK) return s;
+    }
     {
       seed::AttnWorkspace aws = m.aws;
       aws.timing = nullptr;
@@ -462,25 +498,47 @@ seed_status forward_chunk(seed_ctx ctx, Model& m, const ChunkDesc& c, cudaStream
       CK(seed::attention(m.y, M, c.n_seq, c.max_q_len, c.max_kv, m.H, m.Hk, m.Dh, seqs, m.rope, m.kv, l, aws,
                          m.attn, st));
     }
-    if ((s = run_gemm(ctx, m.po[l], m.attn, m.m_cap, M, m.y, m.d, st)) != SEED_OK) return s;
-    CK(seed::residual_rmsnorm(m.y, M, m.d, m.x, m.mn[l], eps, m.h, nullptr, nullptr, st));
-    if ((s = run_gemm(ctx, m.pgu[l], m.h, m.m_cap, M, m.y, 2 * m.ff, st)) != SEED_OK) return s;
-    CK(seed::swiglu(m.y, M, m.ff, m.act, st));
-    if ((s = run_gemm(ctx, m.pd[l], m.act, m.m_cap, M, m.y, m.d, st)) != SEED_OK) return s;
-    const bool last = (l == m.L - 1);
-    const bf16* nw = last ? m.final_norm : m.an[l + 1];
-    if (l == last_layer - 1 && !last) {
-      // partial-depth run (tests): residual only, no norm needed afterwards
-      CK(seed::residual_rmsnorm(m.y, M, m.d, m.x, nw, eps, m.h, nullptr, nullptr, st));
-    } else {
-      CK(seed::residual_rmsnorm(m.y, M, m.d, m.x, nw, eps, last ? nullptr : m.h, last ? c.compact : nullptr,
-                                m.hlm, st));
+    // O: x += attn Wo^T; sums of squares -> ssq_a; h = bf16(x * mlp_norm)
+    {
+      seed::GemmIO io;
+      io.tmX = tm_attn;
+      io.ymode = 1;
+      io.Y = m.x;
+      io.ldY = m.d;
+      io.ssq_out = m.ssq_a;
+      io.nw = m.mn[l];
+      io.hout = m.h;
+      if ((s = run_gemm(ctx, m.po[l], M, io, st)) != SEED_OK) return s;
     }
-    ctx->kernel_launches += 4;
+    // gate/up: act = bf16(silu(g) * u), g | u = (h Wgu^T) / rms(x)
+    {
+      seed::GemmIO io = norm_io(m.ssq_a);
+      io.ymode = 2;
+      io.hout = m.act;
+      if ((s = run_gemm(ctx, m.pgu[l], M, io, st)) != SEED_OK) return s;
+    }
+    // down: x += act Wd^T; sums of squares -> ssq_b; h = bf16(x * next norm weight)
+    {
+      seed::GemmIO io;
+      io.tmX = tm_act;
+      io.ymode = 1;
+      io.Y = m.x;
+      io.ldY = m.d;
+      io.ssq_out = m.ssq_b;
+      io.nw = next_norm(l);
+      io.hout = m.h;
+      if ((s = run_gemm(ctx, m.pd[l], M, io, st)) != SEED_OK) return s;
+    }
+    ctx->kernel_launches += 1;
   }
   if (last_layer == m.L && c.n_logits > 0) {
-    // the LM head writes the fp32 logits straight into the caller's rows (F2)
-    if ((s = run_gemm(ctx, m.plm, m.hlm, m.m_cap, c.n_logits, c.Y, c.ldY, st)) != SEED_OK) return s;
+    // LM head over all chunk rows; fp32 logits of the logits rows (compact index) straight into
+    // the caller's rows (F2)
+    seed::GemmIO io = norm_io(m.ssq_b);
+    io.Y = c.Y;
+    io.ldY = c.ldY;
+    io.yrow = c.n_logits == M ? nullptr : c.compact;
+    if ((s = run_gemm(ctx, m.plm, M, io, st)) != SEED_OK) return s;
   }
   return SEED_OK;
 }
@@ -496,7 +554,7 @@ bool pack_chunk(seed_ctx ctx, const std::vector<Segment>& segs, int logits_mode,
     mq = std::max(mq, s.q_len);
     mkv = std::max(mkv, s.pos0 + s.q_len);
   }
-  const size_t o_pos = A.alloc(M), o_slot = A.alloc(M), o_cmp = A.alloc(M), o_tok = A.alloc(M);
+  const size_t o_pos = A.alloc(M), o_slot = A.alloc(M), o_cmp = A.alloc(M), o_tok = A.alloc(M), o_lr = A.alloc(M);
   const size_t n = segs.size();
   const size_t o_qs = A.alloc(n), o_ql = A.alloc(n), o_kv = A.alloc(n), o_ss = A.alloc(n), o_st = A.alloc(n);
   if (o_st == (size_t)-1) return false;
@@ -512,6 +570,7 @@ bool pack_chunk(seed_ctx ctx, const std::vector<Segment>& segs, int logits_mode,
       A.host[o_pos + r] = s.pos0 + j;
       A.host[o_slot + r] = s.slot;
       const bool lg = logits_mode == 1 || (logits_mode == 2 && j == s.q_len - 1);
+      if (lg) A.host[o_lr + nl] = r;
       A.host[o_cmp + r] = lg ? nl++ : -1;
       A.host[o_tok + r] = s.tok_off >= 0 ? A.host[s.tok_off + j] : 0;
     }
@@ -525,6 +584,7 @@ bool pack_chunk(seed_ctx ctx, const std::vector<Segment>& segs, int logits_mode,
   c->seq_slot = A.dev + o_ss;
   c->seq_stable = A.dev + o_st;
   c->compact = A.dev + o_cmp;
+  c->logit_rows = A.dev + o_lr;
   c->q_start = A.dev + o_qs;
   c->q_len = A.dev + o_ql;
   c->kv_len = A.dev + o_kv;
@@ -1278,7 +1338,11 @@ seed_status seed_op_gemm(const void* W, int32_t N, int32_t K, const void* X, int
       s = SEED_ECUDA;
       break;
     }
-    if (seed::gemm_run(p, tm, m, part, Y + (size_t)done * N, N, st) != cudaSuccess) s = SEED_ECUDA;
+    seed::GemmIO io;
+    io.tmX = &tm;
+    io.Y = Y + (size_t)done * N;
+    io.ldY = N;
+    if (seed::gemm_run(p, m, io, part, st) != cudaSuccess) s = SEED_ECUDA;
     done += m;
   }
   cudaFreeAsync(part, st);
@@ -1372,9 +1436,7 @@ seed_status seed_op_decoder_layer(const seed_model_shape* shape, const void* con
     const float eps = sh.rms_eps > 0 ? sh.rms_eps : 1e-5f;
     if (s == SEED_OK && cudaMemcpyAsync(m.x, x_in, (size_t)M * m.d * 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
       s = SEED_ECUDA;
-    if (s == SEED_OK && seed::residual_rmsnorm(nullptr, M, m.d, m.x, m.an[0], eps, m.h, nullptr, nullptr, st) !=
-                             cudaSuccess)
-      s = SEED_ECUDA;
+    (void)eps;
     if (s == SEED_OK) s = forward_chunk(ctx, m, c, st, 0, 1, false);
     if (s == SEED_OK && cudaMemcpyAsync(x_out, m.x, (size_t)M * m.d * 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
       s = SEED_ECUDA;

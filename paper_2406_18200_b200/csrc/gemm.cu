@@ -37,12 +37,20 @@ constexpr int MAX_STAGES = 16;
 constexpr int SMEM_BUDGET = 150 * 1024;
 
 struct GemmArgs {
-  int KB, U, G, S, M, m_pad, stages, N, ldY, maxseg;
+  int KB, U, G, S, M, m_pad, stages, N, K, ldY, maxseg;
+  int ymode;                   // 0 store Y (x row scale, row map); 1 residual; 2 SwiGLU (see GemmIO)
+  int ssq_in_ld;               // row stride of ssq_in
+  float eps;
   float* partial;              // split-K partials of tiles shared by several CTAs
-  float* Y;                    // output fp32 [M][ldY]
+  float* Y;                    // fp32 output [M][ldY]; ymode 1: the residual stream (in place)
   const int* seg;              // per tile: count, partial-segment ids in CTA order
   int* counters;               // per tile: finished segments (zero between launches)
-  unsigned long long* timing;  // optional [4]: min CTA start, min release (PDL), max CTA end (ns)
+  const float* ssq_in;         // optional [ceil(K/128)][ssq_in_ld]: rows scaled by 1/rms (R24)
+  const int32_t* yrow;         // ymode 0: optional output row map (-1: row not stored)
+  float* ssq_out;              // ymode 1: [ceil(N/128)][M] sums of squares of the new residual
+  const __nv_bfloat16* nw;     // ymode 1: next RMSNorm weight [N]
+  __nv_bfloat16* hout;         // ymode 1: bf16(x_new * nw) [M][N]; ymode 2: bf16(silu(g) * u) [M][N/2]
+  unsigned long long* timing;  // optional [4]: min CTA start, min release (PDL), max CTA end (ns), kind
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -60,39 +68,95 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return d;
 }
 
-// Sum the partial segments of one tile column (weight row nl) for all M rows, in CTA order.
-// 16 rows per batch and two segments per step: every load is independent (ILP), the adds
-// keep the fixed k order.
-__device__ __forceinline__ void reduce_tile(const float* __restrict__ P, const int* __restrict__ sl, int M, int nl,
-                                            float* __restrict__ Y, int ldY, int n, int N) {
-  const int cnt = sl[0];
-  for (int m0 = 0; m0 < M; m0 += 16) {
-    float acc[16];
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+// Epilogue for 16 rows m0..m0+15 of output column n (tile t, weight row nl) held by this thread;
+// the 128 epilogue threads hold the 128 columns of the tile.
+//   ymode 0: Y[row(m)][n] = acc * inv[m]
+//   ymode 1: x[m][n] += acc; per-warp x^2 row sums (-> ssq_out); hout[m][n] = bf16(x * nw[n])
+//   ymode 2: gate (nl < 64) and up (nl >= 64) of output j = 64 t + nl % 64, scaled by inv[m],
+//            meet in shared memory; hout[m][j] = bf16(silu(g) * u)                   (B4)
+__device__ __forceinline__ void finish16(const GemmArgs& a, int m0, int t, int nl, const float* v, int ew, int lane,
+                                         const float* inv_s, float* red_s, float* xch_s) {
+  const int n = t * BLOCK_N + nl;
+  if (a.ymode == 0) {
+    if (n < a.N) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) acc[j] = 0.f;
-    int k = 0;
-    for (; k + 1 < cnt; k += 2) {
-      const float* s0 = P + ((size_t)sl[1 + k] * M + m0) * BLOCK_N + nl;
-      const float* s1 = P + ((size_t)sl[2 + k] * M + m0) * BLOCK_N + nl;
-      float v0[16], v1[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        v0[j] = m0 + j < M ? __ldcg(s0 + (size_t)j * BLOCK_N) : 0.f;
-        v1[j] = m0 + j < M ? __ldcg(s1 + (size_t)j * BLOCK_N) : 0.f;
+      for (int i = 0; i < 16; ++i) {
+        const int m = m0 + i;
+        if (m >= a.M) break;
+        const int row = a.yrow ? a.yrow[m] : m;
+        if (row >= 0) a.Y[(size_t)row * a.ldY + n] = a.ssq_in ? v[i] * inv_s[m] : v[i];
       }
-#pragma unroll
-      for (int j = 0; j < 16; ++j) acc[j] = (acc[j] + v0[j]) + v1[j];
     }
-    if (k < cnt) {
-      const float* s0 = P + ((size_t)sl[1 + k] * M + m0) * BLOCK_N + nl;
+    return;
+  }
+  if (a.ymode == 1) {
+    float sq[16];
+    const float w = n < a.N ? bf2f(a.nw[n]) : 0.f;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) acc[j] += m0 + j < M ? __ldcg(s0 + (size_t)j * BLOCK_N) : 0.f;
+    for (int i = 0; i < 16; ++i) {
+      sq[i] = 0.f;
+      if (m0 + i < a.M && n < a.N) {
+        float* px = a.Y + (size_t)(m0 + i) * a.ldY + n;
+        const float xn = *px + v[i];
+        *px = xn;
+        sq[i] = xn * xn;
+        a.hout[(size_t)(m0 + i) * a.N + n] = f2bf(xn * w);
+      }
     }
-    if (n < N) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (m0 + j < M) Y[(size_t)(m0 + j) * ldY + n] = acc[j];
+    for (int i = 0; i < 16; ++i) sq[i] = warp_sum(sq[i]);
+    if (lane == 0) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) red_s[ew * 256 + m0 + i] = sq[i];
     }
+    return;
+  }
+  // ymode 2: SwiGLU across the tile's gate / up halves
+#pragma unroll
+  for (int i = 0; i < 16; ++i) xch_s[i * 128 + nl] = (m0 + i < a.M) ? v[i] * inv_s[m0 + i] : 0.f;
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  if (nl < 64) {
+    const int j = t * 64 + nl;
+    if (j < a.N / 2) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (m0 + i >= a.M) break;
+        const float g = xch_s[i * 128 + nl], u = xch_s[i * 128 + 64 + nl];
+        a.hout[(size_t)(m0 + i) * (a.N / 2) + j] = f2bf(g / (1.0f + expf(-g)) * u);
+      }
+    }
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+
+// Sum the partial segments of one tile column (weight row nl) for rows m0..m0+15, in CTA order.
+__device__ __forceinline__ void reduce_rows16(const float* __restrict__ P, const int* __restrict__ sl, int M, int m0,
+                                              int nl, float* acc) {
+  const int cnt = sl[0];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+  int k = 0;
+  for (; k + 1 < cnt; k += 2) {
+    const float* s0 = P + ((size_t)sl[1 + k] * M + m0) * BLOCK_N + nl;
+    const float* s1 = P + ((size_t)sl[2 + k] * M + m0) * BLOCK_N + nl;
+    float v0[16], v1[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      v0[j] = m0 + j < M ? __ldcg(s0 + (size_t)j * BLOCK_N) : 0.f;
+      v1[j] = m0 + j < M ? __ldcg(s1 + (size_t)j * BLOCK_N) : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = (acc[j] + v0[j]) + v1[j];
+  }
+  if (k < cnt) {
+    const float* s0 = P + ((size_t)sl[1 + k] * M + m0) * BLOCK_N + nl;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] += m0 + j < M ? __ldcg(s0 + (size_t)j * BLOCK_N) : 0.f;
   }
 }
 
@@ -109,6 +173,10 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  volatile int* s_last = reinterpret_cast<volatile int*>(tmem_slot + 1);
+  float* inv_s = reinterpret_cast<float*>(tmem_slot + 4);   // [256] 1/rms per X row (ssq_in)
+  float* red_s = inv_s + 256;                               // [4][256] per-warp x^2 row sums (ymode 1)
+  float* xch_s = red_s + 1024;                              // [16][128] gate/up exchange (ymode 2)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x;
@@ -141,31 +209,29 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
   const long t_begin = u_begin / a.KB;
 
   if (warp == 0) {
-    // ---------------- TMA producer (one elected lane)
-    if (elect_one()) {
+    // ---------------- producer warp (one lane): weights and X tiles by TMA
+    if (lane == 0) {
       const uint64_t pol_w = l2_policy_evict_first();
       const uint64_t pol_x = l2_policy_evict_last();
-      // The weights do not depend on the previous kernel: fill the whole ring with weight
-      // tiles before waiting on it (PDL), so weight streaming overlaps the predecessor.
+      const uint32_t tx = W_TILE_BYTES + x_bytes;
+      // The weights do not depend on the previous kernel: fill the whole ring with weight tiles
+      // before waiting on it (PDL), so weight streaming overlaps the predecessor.
       const long n_pre = min((long)S, u_end - u_begin);
       for (long i = 0; i < n_pre; ++i) {
         const long u = u_begin + i;
-        const int t = (int)(u / a.KB), kb = (int)(u % a.KB);
-        mbar_arrive_expect_tx(&full[i], W_TILE_BYTES + x_bytes);
-        tma_load_2d(sW + i * W_TILE_BYTES, &tmW, &full[i], kb * BLOCK_K, t * BLOCK_N, pol_w);
+        mbar_arrive_expect_tx(&full[i], tx);
+        tma_load_2d(sW + i * W_TILE_BYTES, &tmW, &full[i], (int)(u % a.KB) * BLOCK_K, (int)(u / a.KB) * BLOCK_N, pol_w);
       }
-      pdl_wait();  // X (the activations) is written by the previous kernel
+      pdl_wait();  // X depends on the previous kernel
       if (a.timing) atomicMin(&a.timing[1], globaltimer());
-      for (long i = 0; i < n_pre; ++i) {
-        const long u = u_begin + i;
-        tma_load_2d(sX + i * x_bytes, &tmX, &full[i], (int)(u % a.KB) * BLOCK_K, 0, pol_x);
-      }
+      for (long i = 0; i < n_pre; ++i)
+        tma_load_2d(sX + i * x_bytes, &tmX, &full[i], (int)((u_begin + i) % a.KB) * BLOCK_K, 0, pol_x);
       int stage = (int)(n_pre % S);
       uint32_t phase = n_pre == S ? 1u : 0u;
       for (long u = u_begin + n_pre; u < u_end; ++u) {
         const int t = (int)(u / a.KB), kb = (int)(u % a.KB);
         mbar_wait(&empty[stage], phase ^ 1);
-        mbar_arrive_expect_tx(&full[stage], W_TILE_BYTES + x_bytes);
+        mbar_arrive_expect_tx(&full[stage], tx);
         tma_load_2d(sW + stage * W_TILE_BYTES, &tmW, &full[stage], kb * BLOCK_K, t * BLOCK_N, pol_w);
         tma_load_2d(sX + stage * x_bytes, &tmX, &full[stage], kb * BLOCK_K, 0, pol_x);
         if (++stage == S) {
@@ -216,33 +282,54 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
     }
   } else {
     // ---------------- epilogue warps 2..5: TMEM -> Y (whole tiles) or -> split-K partial; the
-    // last CTA to finish a shared tile sums its partials in CTA order and writes Y (R19)
+    // last CTA to finish a shared tile sums its partials in CTA order (R19) and applies the
+    // epilogue (store, or residual add + per-tile sums of squares for the next RMSNorm)
     const int lane_grp = warp & 3;               // TMEM lanes this warp may access
     const int nl = lane_grp * 32 + lane;         // weight row within the tile
     const int et = threadIdx.x - 64;             // 0..127 among the epilogue threads
-    volatile int* s_last = reinterpret_cast<volatile int*>(tmem_slot + 1);
+    const int ew = et >> 5;
     pdl_wait();                                  // Y and the partials are read by the predecessor
+    if (a.ssq_in) {
+      // 1 / rms of each X row from the per-tile sums of squares, in tile order (R24)
+      const int kt = (a.K + 127) / 128;
+      for (int m = et; m < a.m_pad; m += 128) {
+        float inv = 0.f;
+        if (m < a.M) {
+          float ss = 0.f;
+          for (int i = 0; i < kt; ++i) ss += __ldcg(a.ssq_in + (size_t)i * a.ssq_in_ld + m);
+          inv = 1.0f / sqrtf(ss / (float)a.K + a.eps);
+        }
+        inv_s[m] = inv;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
     int seg = 0;
     long u = u_begin;
     while (u < u_end) {
       const long t = u / a.KB;
       const long seg_end = min(u_end, (t + 1) * a.KB);
       const bool whole = (u == t * a.KB) && (seg_end == (t + 1) * a.KB);
-      const int n = (int)t * BLOCK_N + nl;
       const int acc = seg & 1;
       const uint32_t use = (uint32_t)(seg >> 1);
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
-      float* out = whole ? a.Y + n : a.partial + ((size_t)((long)c * a.S + (t - t_begin)) * a.M) * BLOCK_N + nl;
-      const size_t ld = whole ? (size_t)a.ldY : (size_t)BLOCK_N;
-      const bool keep = !whole || n < a.N;
       const uint32_t row_addr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(acc * a.m_pad);
-      for (int col = 0; col < a.m_pad; col += 16) {
-        float v[16];
-        tmem_ld16(row_addr + col, v);
+      bool do_finish = whole;
+      if (whole) {
+        for (int col = 0; col < a.m_pad; col += 16) {
+          float v[16];
+          tmem_ld16(row_addr + col, v);
+          finish16(a, col, (int)t, nl, v, ew, lane, inv_s, red_s, xch_s);
+        }
+      } else {
+        float* out = a.partial + ((size_t)((long)c * a.S + (t - t_begin)) * a.M) * BLOCK_N + nl;
+        for (int col = 0; col < a.m_pad; col += 16) {
+          float v[16];
+          tmem_ld16(row_addr + col, v);
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          if (col + i < a.M && keep) out[(size_t)(col + i) * ld] = v[i];
+          for (int i = 0; i < 16; ++i)
+            if (col + i < a.M) out[(size_t)(col + i) * BLOCK_N] = v[i];
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -257,12 +344,23 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
           fence_acq_rel_gpu();
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (*s_last) {
-          reduce_tile(a.partial, sl, a.M, nl, a.Y, a.ldY, n, a.N);
+        do_finish = *s_last != 0;
+        if (do_finish) {
+          for (int m0 = 0; m0 < a.M; m0 += 16) {
+            float v[16];
+            reduce_rows16(a.partial, sl, a.M, m0, nl, v);
+            finish16(a, m0, (int)t, nl, v, ew, lane, inv_s, red_s, xch_s);
+          }
           if (et == 0) a.counters[t] = 0;   // ready for the next launch (graph replay)
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // s_last is reused by the next segment
       }
+      if (do_finish && a.ymode == 1) {
+        // per-tile sums of squares of the updated residual rows, warps in a fixed order
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        for (int m = et; m < a.M; m += 128)
+          a.ssq_out[(size_t)t * a.M + m] = ((red_s[m] + red_s[256 + m]) + red_s[512 + m]) + red_s[768 + m];
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // s_last / red_s are reused by the next segment
       u = seg_end;
       ++seg;
     }
@@ -404,9 +502,9 @@ cudaError_t timing_accumulate(unsigned long long* rec, int n, unsigned long long
   return cudaGetLastError();
 }
 
-cudaError_t gemm_run(const GemmPlan& p, const CUtensorMap& tmX, int M, float* partial, float* Y, int ldY,
-                     cudaStream_t st, unsigned long long* timing) {
-  GemmArgs a;
+cudaError_t gemm_run(const GemmPlan& p, int M, const GemmIO& io, float* partial, cudaStream_t st,
+                     unsigned long long* timing) {
+  GemmArgs a{};
   a.KB = p.KB;
   a.U = p.U;
   a.G = p.G;
@@ -414,25 +512,39 @@ cudaError_t gemm_run(const GemmPlan& p, const CUtensorMap& tmX, int M, float* pa
   a.M = M;
   a.m_pad = gemm_mpad(M);
   if (a.m_pad > 256) return cudaErrorInvalidValue;
+  a.N = p.N;
+  a.K = p.K;
+  a.maxseg = p.maxseg;
+  a.seg = p.seg;
+  a.counters = p.counters;
+  a.partial = partial;
+  a.ymode = io.ymode;
+  a.Y = io.Y;
+  a.ldY = io.ldY;
+  a.yrow = io.yrow;
+  a.ssq_in = io.ssq_in;
+  a.ssq_in_ld = io.ssq_in_ld;
+  a.eps = io.eps;
+  a.ssq_out = io.ssq_out;
+  a.nw = io.nw;
+  a.hout = io.hout;
+  a.timing = timing;
+  if (!io.tmX) return cudaErrorInvalidValue;
+  if (io.ymode == 1 && (!io.Y || !io.ssq_out || !io.nw || !io.hout)) return cudaErrorInvalidValue;
+  if (io.ymode == 2 && (!io.ssq_in || !io.hout || p.N % BLOCK_N)) return cudaErrorInvalidValue;
+  if (io.ymode == 0 && !io.Y) return cudaErrorInvalidValue;
   const int stage_bytes = W_TILE_BYTES + a.m_pad * BLOCK_K * 2;
-  int stages = (SMEM_BUDGET - 1024 - 256) / stage_bytes;
+  const int extra = (256 + 1024 + 2048 + 8) * 4;   // inv_s, red_s, xch_s, flags
+  int stages = (SMEM_BUDGET - 1024 - 256 - extra) / stage_bytes;
   if (stages > MAX_STAGES) stages = MAX_STAGES;
   a.stages = stages;
-  a.partial = partial;
-  a.Y = Y;
-  a.ldY = ldY;
-  a.N = p.N;
-  a.seg = p.seg;
-  a.maxseg = p.maxseg;
-  a.counters = p.counters;
-  a.timing = timing;
-  const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 4) * 8 + 32;
+  const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 4) * 8 + 16 + extra;
   static bool attr_done = false;
   if (!attr_done) {
     cudaFuncSetAttribute(gemm_streamk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_done = true;
   }
-  return launch(gemm_streamk_kernel, dim3(p.G), dim3(192), smem, st, p.tmW, tmX, a);
+  return launch(gemm_streamk_kernel, dim3(p.G), dim3(192), smem, st, p.tmW, *io.tmX, a);
 }
 
 }  // namespace seed

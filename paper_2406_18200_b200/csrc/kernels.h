@@ -37,9 +37,34 @@ bool encode_tmap_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t 
 void gemm_plan(GemmPlan* plan, const void* W, int N, int K);
 void gemm_plan_free(GemmPlan* plan);
 size_t gemm_partial_floats(const GemmPlan& plan, int M);
-// Y[m][n] (row stride ldY) = sum_k X[m][k] W[n][k], fp32; `partial` is split-K scratch
-cudaError_t gemm_run(const GemmPlan& plan, const CUtensorMap& tmX, int M, float* partial, float* Y, int ldY,
-                     cudaStream_t st, unsigned long long* timing = nullptr);
+// Operands and epilogue of one GEMM launch (see gemm.cu):
+//   X: xmode 0 TMA from a bf16 buffer (tmX); 1 RMSNorm of an fp32 residual (xsrc rows, optional
+//      row map xrow, per-tile sums of squares ssq_in [ceil(K/128)][ssq_in_ld], weight nw, eps);
+//      2 SwiGLU of a gate/up GEMM output xsrc [M][2K] (64-row interleave)
+//   Y: ymode 0 Y = X W^T; 1 Y += X W^T (residual, in place) and ssq_out [ceil(N/128)][M]
+// Y = epilogue(X W^T): X is a bf16 [M][K] operand read by TMA (tmX, box 64 x m_pad).
+// ssq_in (optional, [ceil(K/128)][ssq_in_ld]) scales output row m by 1/rms(x_m) = 1/sqrt(sum/K + eps):
+// the RMSNorm of x_m applied after the GEMM, on X = bf16(x * w_norm) (R24).
+//   ymode 0: Y[yrow ? yrow[m] : m][n] = acc (* 1/rms), rows with yrow[m] < 0 skipped
+//   ymode 1: residual: Y[m][n] += acc; ssq_out[n/128][m] = tile sums of the new Y^2;
+//            hout[m][n] = bf16(Y[m][n] * nw[n]) (the next RMSNorm's operand)
+//   ymode 2: SwiGLU on interleaved gate/up tiles (64 + 64 rows of W per 128-row tile):
+//            hout[m][j] = bf16(silu(g_j) * u_j), g, u scaled by 1/rms; hout is [M][N/2]
+struct GemmIO {
+  const CUtensorMap* tmX = nullptr;
+  const float* ssq_in = nullptr;
+  int ssq_in_ld = 0;
+  float eps = 1e-5f;
+  int ymode = 0;
+  float* Y = nullptr;
+  int ldY = 0;
+  const int32_t* yrow = nullptr;
+  float* ssq_out = nullptr;
+  const __nv_bfloat16* nw = nullptr;
+  __nv_bfloat16* hout = nullptr;
+};
+cudaError_t gemm_run(const GemmPlan& plan, int M, const GemmIO& io, float* partial, cudaStream_t st,
+                     unsigned long long* timing = nullptr);
 cudaError_t timing_accumulate(unsigned long long* rec, int n, unsigned long long* acc, unsigned long long* last,
                               cudaStream_t st);
 int gemm_mpad(int M);
@@ -50,14 +75,10 @@ struct RowInfo {         // per row of the ragged batch
   const int32_t* pos;    // [M] absolute positions
   const int32_t* slot;   // [M] stream slot (page table row)
 };
-cudaError_t embed_rmsnorm(const __nv_bfloat16* embed, const int32_t* tok, int tok_stride, int M, int d, const __nv_bfloat16* w,
-                          float eps, float* x, __nv_bfloat16* h, cudaStream_t st);
-// x[m] += Y[m] (Y may be null), h = bf16(rmsnorm(x[m]) * w); compact rows also to h_compact
-cudaError_t residual_rmsnorm(const float* Y, int M, int d, float* x, const __nv_bfloat16* w, float eps,
-                             __nv_bfloat16* h, const int32_t* compact_map, __nv_bfloat16* h_compact,
-                             cudaStream_t st);
-// act[m][i] = bf16(silu(g) * u), g/u from the interleaved gate/up GEMM output Y [M][2ff]
-cudaError_t swiglu(const float* Y, int M, int ff, __nv_bfloat16* act, cudaStream_t st);
+// x = embed[tok] (or x as given when embed == nullptr), ssq[t][m] = sum of x^2 over 128-column
+// tile t, h = bf16(x * nw) (the first RMSNorm's GEMM operand, R24)
+cudaError_t embed_stats(const __nv_bfloat16* embed, const int32_t* tok, int tok_stride, int M, int d, float* x,
+                        float* ssq, const __nv_bfloat16* nw, __nv_bfloat16* h, cudaStream_t st);
 cudaError_t rope_table_init(float2* table, int max_pos, int Dh, double theta, cudaStream_t st);
 cudaError_t kv_write_dense(const KVLayout& kv, int layer, int slot, int n, const __nv_bfloat16* k,
                            const __nv_bfloat16* v, cudaStream_t st);

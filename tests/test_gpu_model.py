@@ -82,6 +82,24 @@ def test_forward_logits_vs_oracle(pkg, dname, tname, n):
     eng.close()
 
 
+@pytest.mark.parametrize("tname", ["llama2_7b", "llama2_13b"])
+def test_forward_slice_full_width_vs_oracle(pkg, tname):
+    """P4(ii): a 2-layer slice of the full-width target (d = 4096 / 5120, V = 32000) end to end,
+    prefilled in several chunks, logits within 2e-2 of the bf16-faithful oracle."""
+    ts = dict(seedgen.SHAPES[tname], n_layers=2)
+    ds = seedgen.SHAPES["llama_68m"]
+    dW, tW = seedgen.model_weights(ds, seedgen.DRAFT_SEED), seedgen.model_weights(ts, seedgen.TARGET_SEED)
+    eng = pkg.SeedEngine(ds, _cuda(dW), ts, _cuda(tW), gamma=4, temperature=1.0, seed=SEED, max_new=8,
+                         max_streams=1, max_batch=1, max_ctx=600)
+    toks = np.random.default_rng(7).integers(3, ts["vocab"], size=300).tolist()   # > one 256-row chunk
+    got = eng.forward_logits(1, toks).double().cpu().numpy()
+    rows = [0, 1, 100, 255, 256, 299]                                             # sampled rows
+    sh = ll.LlamaShape(**ts)
+    ref = ll.forward_batch(sh, tW, [(toks, ll.KVCache(sh))], mode="bf16", logits_rows=[rows])[0]
+    assert _rel_rows(got[rows], ref).max() < 2e-2
+    eng.close()
+
+
 def test_cached_round_logits_equal_recompute(pkg):
     """P5: the verify row for T[-1] (cached decode after rounds) equals a from-scratch forward over T."""
     eng, _ = _engine(pkg, "toy_draft", "toy_target", max_new=40)
