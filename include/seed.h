@@ -168,6 +168,13 @@ SEED_API seed_status seed_reset_profile(seed_ctx ctx);
  * launch i: first CTA start, dependency release (PDL wait returned), last CTA end, 0.
  * out: host buffer of 4*cap uint64; *n = launches written (in round launch order). */
 SEED_API seed_status seed_gemm_trace(seed_ctx ctx, uint64_t* out, int32_t cap, int32_t* n);
+/* Diagnostics (SEED_FLAG_PROFILE and env SEED_CTA_TRACE=1 at seed_init): per-CTA phase
+ * timestamps (globaltimer ns) of GEMM launch `launch` (index as in seed_gemm_trace) of the most
+ * recent round. out: host buffer of 148*16 uint64, row c = CTA c: start, producer release,
+ * producer done, first stage full, MMA done, first accumulator ready, epilogue done, end,
+ * last partial stored, last ticket taken, reduce done, finish done, 4 spare (0 / stale for CTAs
+ * and phases the launch did not reach). *n_cta = 148, or 0 when tracing is off. */
+SEED_API seed_status seed_gemm_cta_trace(seed_ctx ctx, int32_t launch, uint64_t* out, int32_t* n_cta);
 
 SEED_API const char* seed_last_error(seed_ctx ctx);
 SEED_API void seed_destroy(seed_ctx ctx);

@@ -58,6 +58,7 @@ _SIGS = {
                          C.POINTER(C.c_int64), C.POINTER(C.c_double)],
     "seed_reset_profile": [_P],
     "seed_gemm_trace": [_P, C.POINTER(C.c_uint64), C.c_int32, _I32P],
+    "seed_gemm_cta_trace": [_P, C.c_int32, C.POINTER(C.c_uint64), _I32P],
     "seed_last_error": [_P],
     "seed_destroy": [_P],
     "seed_nccl_unique_id": [_P],

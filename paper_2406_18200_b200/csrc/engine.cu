@@ -214,6 +214,7 @@ struct seed_ctx_s {
   // profiling: per-GEMM globaltimer records accumulated on the device
   bool profile = false, in_round = false;
   unsigned long long *timing_rec = nullptr, *timing_acc = nullptr, *timing_last = nullptr;
+  unsigned long long* cta_rec = nullptr;  // SEED_CTA_TRACE=1: [rec_cap][148][16] per-CTA GEMM phases
   int last_draft_recs = 0, last_verify_recs = 0;
   std::map<int, int> draft_recs;  // records of the draft phase per batch size
   double draft_gemm_bytes = 0;
@@ -257,8 +258,12 @@ const CUtensorMap* xmap(seed_ctx ctx, const bf16* buf, int K, int rows_cap, int 
 
 seed_status run_gemm(seed_ctx ctx, const GemmPlan& p, int M, const seed::GemmIO& io, cudaStream_t st) {
   unsigned long long* rec = nullptr;
-  if (ctx->profile && ctx->in_round && ctx->rec_used < ctx->rec_cap) rec = ctx->timing_rec + 4 * ctx->rec_used++;
-  CK(seed::gemm_run(p, M, io, ctx->partial, st, rec));
+  unsigned long long* cta = nullptr;
+  if (ctx->profile && ctx->in_round && ctx->rec_used < ctx->rec_cap) {
+    if (ctx->cta_rec) cta = ctx->cta_rec + (size_t)ctx->rec_used * 148 * 16;
+    rec = ctx->timing_rec + 4 * ctx->rec_used++;
+  }
+  CK(seed::gemm_run(p, M, io, ctx->partial, st, rec, cta));
   if (ctx->in_round) {
     // algorithmic bytes: weights + bf16 X + output (fp32 Y; residual: read + write x, write bf16 h;
     // SwiGLU: bf16 act of half the width)
@@ -1009,6 +1014,8 @@ seed_status seed_init(const seed_config* cfg, seed_ctx* out) {
     ok &= cudaMalloc(&ctx->timing_rec, (size_t)ctx->rec_cap * 4 * 8) == cudaSuccess;
     ok &= cudaMalloc(&ctx->timing_last, (size_t)ctx->rec_cap * 4 * 8) == cudaSuccess;
     ok &= cudaMalloc(&ctx->timing_acc, 4 * 8) == cudaSuccess;
+    const char* ce = getenv("SEED_CTA_TRACE");
+    if (ce && ce[0] == '1') ok &= cudaMalloc(&ctx->cta_rec, (size_t)ctx->rec_cap * 148 * 16 * 8) == cudaSuccess;
     if (ok) {
       std::vector<unsigned long long> init((size_t)ctx->rec_cap * 4);
       for (int i = 0; i < ctx->rec_cap; ++i) {
@@ -1060,6 +1067,7 @@ void seed_destroy(seed_ctx ctx) {
   if (ctx->timing_rec) cudaFree(ctx->timing_rec);
   if (ctx->timing_acc) cudaFree(ctx->timing_acc);
   if (ctx->timing_last) cudaFree(ctx->timing_last);
+  if (ctx->cta_rec) cudaFree(ctx->cta_rec);
   if (ctx->sched) seed_sched_destroy(ctx->sched);
   if (ctx->table) seed_table_destroy(ctx->table);
   if (ctx->comm && g_nccl.destroy) g_nccl.destroy(ctx->comm);
@@ -1290,6 +1298,20 @@ seed_status seed_gemm_trace(seed_ctx ctx, uint64_t* out, int32_t cap, int32_t* n
                             cudaMemcpyDeviceToHost) != cudaSuccess))
     return fail(ctx, SEED_ECUDA, "seed_gemm_trace", "");
   *n = nd + nv;
+  return SEED_OK;
+}
+
+seed_status seed_gemm_cta_trace(seed_ctx ctx, int32_t launch, uint64_t* out, int32_t* n_cta) {
+  if (!ctx || !out || !n_cta || launch < 0) return SEED_EINVAL;
+  *n_cta = 0;
+  if (!ctx->cta_rec) return SEED_OK;
+  const int nd = ctx->last_draft_recs, nv = ctx->last_verify_recs;
+  if (launch >= nd + nv) return SEED_EINVAL;
+  const size_t idx = launch < nd ? (size_t)launch : (size_t)ctx->rec_cap / 2 + (launch - nd);
+  if (cudaDeviceSynchronize() != cudaSuccess ||
+      cudaMemcpy(out, ctx->cta_rec + idx * 148 * 16, 148 * 16 * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(ctx, SEED_ECUDA, "seed_gemm_cta_trace", "");
+  *n_cta = 148;
   return SEED_OK;
 }
 

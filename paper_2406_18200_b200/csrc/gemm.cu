@@ -34,7 +34,6 @@ constexpr int W_TILE_BYTES = BLOCK_N * BLOCK_K * 2;
 constexpr int MAX_STAGES = 16;
 // 8 weight stages (128 KB in flight per SM) saturate HBM; the smem cap leaves room for an
 // attention / epilogue CTA to co-reside, so the next GEMM's weight prefetch overlaps it (PDL)
-constexpr int SMEM_BUDGET = 150 * 1024;
 
 struct GemmArgs {
   int KB, U, G, S, M, m_pad, stages, N, K, ldY, maxseg;
@@ -51,6 +50,7 @@ struct GemmArgs {
   const __nv_bfloat16* nw;     // ymode 1: next RMSNorm weight [N]
   __nv_bfloat16* hout;         // ymode 1: bf16(x_new * nw) [M][N]; ymode 2: bf16(silu(g) * u) [M][N/2]
   unsigned long long* timing;  // optional [4]: min CTA start, min release (PDL), max CTA end (ns), kind
+  unsigned long long* cta;     // optional [G][8] per-CTA phase timestamps (diagnostics, see gemm_run)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -80,30 +80,37 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
 //   ymode 2: gate (nl < 64) and up (nl >= 64) of output j = 64 t + nl % 64, scaled by inv[m],
 //            meet in shared memory; hout[m][j] = bf16(silu(g) * u)                   (B4)
 __device__ __forceinline__ void finish16(const GemmArgs& a, int m0, int t, int nl, const float* v, int ew, int lane,
-                                         const float* inv_s, float* red_s, float* xch_s) {
+                                         const float* inv_s, float* red_s, float* xch_s,
+                                         const float* xpre = nullptr, float wpre = 0.f) {
   const int n = t * BLOCK_N + nl;
   if (a.ymode == 0) {
     if (n < a.N) {
+      int row[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int m = m0 + i;
-        if (m >= a.M) break;
-        const int row = a.yrow ? a.yrow[m] : m;
-        if (row >= 0) a.Y[(size_t)row * a.ldY + n] = a.ssq_in ? v[i] * inv_s[m] : v[i];
-      }
+      for (int i = 0; i < 16; ++i) row[i] = m0 + i >= a.M ? -1 : (a.yrow ? __ldg(a.yrow + m0 + i) : m0 + i);
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (row[i] >= 0) a.Y[(size_t)row[i] * a.ldY + n] = a.ssq_in ? v[i] * inv_s[m0 + i] : v[i];
     }
     return;
   }
   if (a.ymode == 1) {
-    float sq[16];
-    const float w = n < a.N ? bf2f(a.nw[n]) : 0.f;
+    float sq[16], xo[16];
+    const float w = xpre ? wpre : (n < a.N ? bf2f(a.nw[n]) : 0.f);
+    // all residual loads first (one round trip), then the stores
+    if (xpre) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) xo[i] = xpre[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) xo[i] = (m0 + i < a.M && n < a.N) ? a.Y[(size_t)(m0 + i) * a.ldY + n] : 0.f;
+    }
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       sq[i] = 0.f;
       if (m0 + i < a.M && n < a.N) {
-        float* px = a.Y + (size_t)(m0 + i) * a.ldY + n;
-        const float xn = *px + v[i];
-        *px = xn;
+        const float xn = xo[i] + v[i];
+        a.Y[(size_t)(m0 + i) * a.ldY + n] = xn;
         sq[i] = xn * xn;
         a.hout[(size_t)(m0 + i) * a.N + n] = f2bf(xn * w);
       }
@@ -134,33 +141,32 @@ __device__ __forceinline__ void finish16(const GemmArgs& a, int m0, int t, int n
   asm volatile("bar.sync 1, 128;" ::: "memory");
 }
 
-// Sum the partial segments of one tile column (weight row nl) for rows m0..m0+15, in CTA order.
-__device__ __forceinline__ void reduce_rows16(const float* __restrict__ P, const int* __restrict__ sl, int M, int m0,
-                                              int nl, float* acc) {
-  const int cnt = sl[0];
+// Add the other contributors' partials (segments 1..cnt-1 of the tile, in CTA order, R19) to the
+// reducer's own accumulator rows m0..m0+15 of tile column nl; loads go four segments at a time.
+__device__ __forceinline__ void add_partials16(const float* __restrict__ P, const int* __restrict__ sl, int cnt, int M,
+                                               int m0, int nl, float* acc, const int* id0) {
+  for (int k = 1; k < cnt; k += 4) {
+    int id[4];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) acc[j] = 0.f;
-  int k = 0;
-  for (; k + 1 < cnt; k += 2) {
-    const float* s0 = P + ((size_t)sl[1 + k] * M + m0) * BLOCK_N + nl;
-    const float* s1 = P + ((size_t)sl[2 + k] * M + m0) * BLOCK_N + nl;
-    float v0[16], v1[16];
+    for (int q = 0; q < 4; ++q) id[q] = k == 1 ? id0[q] : (k + q < cnt ? __ldg(sl + 1 + k + q) : -1);
+    float v[4][16];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      v0[j] = m0 + j < M ? __ldcg(s0 + (size_t)j * BLOCK_N) : 0.f;
-      v1[j] = m0 + j < M ? __ldcg(s1 + (size_t)j * BLOCK_N) : 0.f;
+    for (int q = 0; q < 4; ++q) {
+      const float* src = P + ((size_t)(id[q] < 0 ? 0 : id[q]) * M + m0) * BLOCK_N + nl;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[q][j] = (id[q] >= 0 && m0 + j < M) ? __ldcg(src + (size_t)j * BLOCK_N) : 0.f;
     }
 #pragma unroll
-    for (int j = 0; j < 16; ++j) acc[j] = (acc[j] + v0[j]) + v1[j];
-  }
-  if (k < cnt) {
-    const float* s0 = P + ((size_t)sl[1 + k] * M + m0) * BLOCK_N + nl;
+    for (int q = 0; q < 4; ++q)
+      if (id[q] >= 0) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) acc[j] += m0 + j < M ? __ldcg(s0 + (size_t)j * BLOCK_N) : 0.f;
+        for (int j = 0; j < 16; ++j) acc[j] += v[q][j];
+      }
   }
 }
 
-__global__ void __launch_bounds__(192, 1)
+// __launch_bounds__(192, 2) keeps registers low enough for two CTAs per SM (SEED_GEMM_SMEM_KB <= 110)
+__global__ void __launch_bounds__(192, 2)
 gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GemmArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -173,10 +179,9 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  volatile int* s_last = reinterpret_cast<volatile int*>(tmem_slot + 1);
   float* inv_s = reinterpret_cast<float*>(tmem_slot + 4);   // [256] 1/rms per X row (ssq_in)
   float* red_s = inv_s + 256;                               // [4][256] per-warp x^2 row sums (ymode 1)
-  float* xch_s = red_s + 1024;                              // [16][128] gate/up exchange (ymode 2)
+  float* xch_s = red_s;                                     // [16][128] gate/up exchange (ymode 2)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x;
@@ -184,9 +189,15 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
   if (u_begin >= u_end) return;
   pdl_trigger();
   if (a.timing && threadIdx.x == 0) atomicMin(&a.timing[0], globaltimer());
+  unsigned long long* ct = a.cta ? a.cta + (size_t)c * 16 : nullptr;
+  if (ct && threadIdx.x == 0) ct[0] = globaltimer();
 
+  // TMEM: two accumulator buffers while they fit in 256 columns, else one -- at most 256 columns
+  // per CTA, so the two CTAs an SM can hold never wait on each other's allocation (a reducer
+  // waits on other CTAs of its grid, which may share its SM)
+  const int nacc = 2 * a.m_pad <= 256 ? 2 : 1;
   uint32_t cols = 32;
-  while (cols < (uint32_t)(2 * a.m_pad)) cols <<= 1;
+  while (cols < (uint32_t)(nacc * a.m_pad)) cols <<= 1;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmW);
@@ -224,6 +235,7 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
       }
       pdl_wait();  // X depends on the previous kernel
       if (a.timing) atomicMin(&a.timing[1], globaltimer());
+      if (ct) ct[1] = globaltimer();
       for (long i = 0; i < n_pre; ++i)
         tma_load_2d(sX + i * x_bytes, &tmX, &full[i], (int)((u_begin + i) % a.KB) * BLOCK_K, 0, pol_x);
       int stage = (int)(n_pre % S);
@@ -231,6 +243,7 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
       for (long u = u_begin + n_pre; u < u_end; ++u) {
         const int t = (int)(u / a.KB), kb = (int)(u % a.KB);
         mbar_wait(&empty[stage], phase ^ 1);
+        if (ct && u == u_begin + n_pre) ct[13] = globaltimer();
         mbar_arrive_expect_tx(&full[stage], tx);
         tma_load_2d(sW + stage * W_TILE_BYTES, &tmW, &full[stage], kb * BLOCK_K, t * BLOCK_N, pol_w);
         tma_load_2d(sX + stage * x_bytes, &tmX, &full[stage], kb * BLOCK_K, 0, pol_x);
@@ -239,6 +252,7 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
           phase ^= 1;
         }
       }
+      if (ct) ct[2] = globaltimer();
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (one elected lane)
@@ -254,8 +268,8 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
     while (u < u_end) {
       const long t = u / a.KB;
       const long seg_end = min(u_end, (t + 1) * a.KB);
-      const int acc = seg & 1;
-      const uint32_t use = (uint32_t)(seg >> 1);
+      const int acc = seg % nacc;
+      const uint32_t use = (uint32_t)(seg / nacc);
       mbar_wait(&tempty[acc], (use & 1) ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + (uint32_t)(acc * a.m_pad);
@@ -263,6 +277,8 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
       for (; u < seg_end; ++u) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
+        if (ct && u == u_begin && lane == 0) ct[3] = globaltimer();
+        if (ct && u == u_begin + S - 1 && lane == 0) ct[12] = globaltimer();
         if (elect_one()) {
           const uint32_t wa = sW0 + stage * W_TILE_BYTES, xa = sX0 + stage * x_bytes;
 #pragma unroll
@@ -280,6 +296,7 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
       }
       ++seg;
     }
+    if (ct && lane == 0) ct[4] = globaltimer();
   } else {
     // ---------------- epilogue warps 2..5: TMEM -> Y (whole tiles) or -> split-K partial; the
     // last CTA to finish a shared tile sums its partials in CTA order (R19) and applies the
@@ -309,19 +326,23 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
       const long t = u / a.KB;
       const long seg_end = min(u_end, (t + 1) * a.KB);
       const bool whole = (u == t * a.KB) && (seg_end == (t + 1) * a.KB);
-      const int acc = seg & 1;
-      const uint32_t use = (uint32_t)(seg >> 1);
+      const int acc = seg % nacc;
+      const uint32_t use = (uint32_t)(seg / nacc);
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
+      if (ct && et == 0 && seg == 0) ct[5] = globaltimer();
       const uint32_t row_addr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(acc * a.m_pad);
-      bool do_finish = whole;
+      // Split tile: the CTA holding the tile's first k-blocks (its range's last segment, the first
+      // contributor in CTA order) reduces; the others publish their partials and move on.
+      const bool reducer = !whole && u == t * a.KB;
+      const bool do_finish = whole || reducer;
       if (whole) {
         for (int col = 0; col < a.m_pad; col += 16) {
           float v[16];
           tmem_ld16(row_addr + col, v);
           finish16(a, col, (int)t, nl, v, ew, lane, inv_s, red_s, xch_s);
         }
-      } else {
+      } else if (!reducer) {
         float* out = a.partial + ((size_t)((long)c * a.S + (t - t_begin)) * a.M) * BLOCK_N + nl;
         for (int col = 0; col < a.m_pad; col += 16) {
           float v[16];
@@ -330,45 +351,66 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
           for (int i = 0; i < 16; ++i)
             if (col + i < a.M) out[(size_t)(col + i) * BLOCK_N] = v[i];
         }
+        if (ct && et == 0) ct[8] = globaltimer();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (et == 0) {
+          fence_acq_rel_gpu();                  // release the CTA's partial (bar.sync + cumulativity)
+          atomicAdd(&a.counters[t], 1);
+        }
+      } else {
+        const int* sl = a.seg + t * (a.maxseg + 1);
+        const int cnt = __ldg(sl);
+        // what does not depend on the other contributors is loaded before waiting: the residual
+        // rows and the next norm weight (ymode 1)
+        int id0[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) id0[q] = 1 + q < cnt ? __ldg(sl + 2 + q) : -1;
+        float xo[16];
+        float wn = 0.f;
+        if (a.ymode == 1) {
+          const int n = (int)t * BLOCK_N + nl;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) xo[i] = (i < a.M && n < a.N) ? a.Y[(size_t)i * a.ldY + n] : 0.f;
+          wn = n < a.N ? bf2f(a.nw[n]) : 0.f;
+        }
+        if (et == 0) {
+          volatile int* ctr = a.counters + t;
+          while (*ctr < cnt - 1) {
+          }
+          fence_acq_rel_gpu();                  // acquire the other partials
+          *ctr = 0;                              // ready for the next launch (graph replay)
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (ct && et == 0) ct[9] = globaltimer() + (xo[0] == 1.2345e-30f ? 1 : 0);
+        for (int m0 = 0; m0 < a.m_pad; m0 += 16) {
+          float v[16];
+          tmem_ld16(row_addr + m0, v);
+          add_partials16(a.partial, sl, cnt, a.M, m0, nl, v, id0);
+          if (ct && et == 0) ct[10] = globaltimer() + (v[0] == 1.2345e-30f ? 1 : 0);   // waits for the loads
+          finish16(a, m0, (int)t, nl, v, ew, lane, inv_s, red_s, xch_s, (a.ymode == 1 && m0 == 0) ? xo : nullptr, wn);
+          if (ct && et == 0) ct[11] = globaltimer();
+        }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (!whole) {
-        // publish: barrier over the epilogue warps, then one thread fences and takes a ticket
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        const int* sl = a.seg + t * (a.maxseg + 1);
-        if (et == 0) {
-          fence_acq_rel_gpu();
-          *s_last = (atomicAdd(&a.counters[t], 1) == sl[0] - 1) ? 1 : 0;
-          fence_acq_rel_gpu();
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        do_finish = *s_last != 0;
-        if (do_finish) {
-          for (int m0 = 0; m0 < a.M; m0 += 16) {
-            float v[16];
-            reduce_rows16(a.partial, sl, a.M, m0, nl, v);
-            finish16(a, m0, (int)t, nl, v, ew, lane, inv_s, red_s, xch_s);
-          }
-          if (et == 0) a.counters[t] = 0;   // ready for the next launch (graph replay)
-        }
-      }
       if (do_finish && a.ymode == 1) {
         // per-tile sums of squares of the updated residual rows, warps in a fixed order
         asm volatile("bar.sync 1, 128;" ::: "memory");
         for (int m = et; m < a.M; m += 128)
           a.ssq_out[(size_t)t * a.M + m] = ((red_s[m] + red_s[256 + m]) + red_s[512 + m]) + red_s[768 + m];
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // s_last / red_s are reused by the next segment
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // red_s / xch_s are reused by the next segment
       u = seg_end;
       ++seg;
     }
+    if (ct && et == 0) ct[6] = globaltimer();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc(tmem_base, cols);
+  if (ct && threadIdx.x == 0) ct[7] = globaltimer();
   if (a.timing && threadIdx.x == 0) {
     atomicMax(&a.timing[2], globaltimer());
     a.timing[3] = 1;  // record kind: GEMM
@@ -493,6 +535,17 @@ bool pdl_enabled() {
   return on == 1;
 }
 
+// dynamic smem per GEMM CTA (env SEED_GEMM_SMEM_KB).  150 KB (one GEMM CTA per SM, ~8 stages)
+// measured faster than 100 KB (two per SM, the next GEMM prefetching beside the running one).
+int smem_budget() {
+  static int b = -1;
+  if (b < 0) {
+    const char* e = getenv("SEED_GEMM_SMEM_KB");
+    b = (e ? atoi(e) : 150) * 1024;
+  }
+  return b;
+}
+
 size_t gemm_partial_floats(const GemmPlan& p, int M) { return (size_t)p.G * p.S * M * BLOCK_N; }
 
 cudaError_t timing_accumulate(unsigned long long* rec, int n, unsigned long long* acc, unsigned long long* last,
@@ -503,7 +556,7 @@ cudaError_t timing_accumulate(unsigned long long* rec, int n, unsigned long long
 }
 
 cudaError_t gemm_run(const GemmPlan& p, int M, const GemmIO& io, float* partial, cudaStream_t st,
-                     unsigned long long* timing) {
+                     unsigned long long* timing, unsigned long long* cta) {
   GemmArgs a{};
   a.KB = p.KB;
   a.U = p.U;
@@ -529,13 +582,15 @@ cudaError_t gemm_run(const GemmPlan& p, int M, const GemmIO& io, float* partial,
   a.nw = io.nw;
   a.hout = io.hout;
   a.timing = timing;
+  a.cta = cta;
   if (!io.tmX) return cudaErrorInvalidValue;
   if (io.ymode == 1 && (!io.Y || !io.ssq_out || !io.nw || !io.hout)) return cudaErrorInvalidValue;
   if (io.ymode == 2 && (!io.ssq_in || !io.hout || p.N % BLOCK_N)) return cudaErrorInvalidValue;
   if (io.ymode == 0 && !io.Y) return cudaErrorInvalidValue;
   const int stage_bytes = W_TILE_BYTES + a.m_pad * BLOCK_K * 2;
-  const int extra = (256 + 1024 + 2048 + 8) * 4;   // inv_s, red_s, xch_s, flags
-  int stages = (SMEM_BUDGET - 1024 - 256 - extra) / stage_bytes;
+  const int extra = (256 + 2048 + 8) * 4;   // inv_s, red_s | xch_s, flags
+  int stages = (smem_budget() - 1024 - 256 - extra) / stage_bytes;
+  if (stages < 2) stages = 2;
   if (stages > MAX_STAGES) stages = MAX_STAGES;
   a.stages = stages;
   const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 4) * 8 + 16 + extra;

@@ -38,10 +38,6 @@ void gemm_plan(GemmPlan* plan, const void* W, int N, int K);
 void gemm_plan_free(GemmPlan* plan);
 size_t gemm_partial_floats(const GemmPlan& plan, int M);
 // Operands and epilogue of one GEMM launch (see gemm.cu):
-//   X: xmode 0 TMA from a bf16 buffer (tmX); 1 RMSNorm of an fp32 residual (xsrc rows, optional
-//      row map xrow, per-tile sums of squares ssq_in [ceil(K/128)][ssq_in_ld], weight nw, eps);
-//      2 SwiGLU of a gate/up GEMM output xsrc [M][2K] (64-row interleave)
-//   Y: ymode 0 Y = X W^T; 1 Y += X W^T (residual, in place) and ssq_out [ceil(N/128)][M]
 // Y = epilogue(X W^T): X is a bf16 [M][K] operand read by TMA (tmX, box 64 x m_pad).
 // ssq_in (optional, [ceil(K/128)][ssq_in_ld]) scales output row m by 1/rms(x_m) = 1/sqrt(sum/K + eps):
 // the RMSNorm of x_m applied after the GEMM, on X = bf16(x * w_norm) (R24).
@@ -63,8 +59,11 @@ struct GemmIO {
   const __nv_bfloat16* nw = nullptr;
   __nv_bfloat16* hout = nullptr;
 };
+// timing: optional [4] launch record (kind 1); cta: optional [G][16] per-CTA globaltimer ns:
+// start, producer release, producer done, first stage full, MMA done, first accumulator ready,
+// epilogue done, end, last partial stored, last ticket taken, reduce done, finish done
 cudaError_t gemm_run(const GemmPlan& plan, int M, const GemmIO& io, float* partial, cudaStream_t st,
-                     unsigned long long* timing = nullptr);
+                     unsigned long long* timing = nullptr, unsigned long long* cta = nullptr);
 cudaError_t timing_accumulate(unsigned long long* rec, int n, unsigned long long* acc, unsigned long long* last,
                               cudaStream_t st);
 int gemm_mpad(int M);

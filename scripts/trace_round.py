@@ -75,3 +75,22 @@ for k, v in kinds.items():
     print(f"  {k:5s} n={len(v):3d} span {v[:,0].mean():7.2f} exposed {v[:,1].mean():7.2f} gap-before {v[:,2].mean():7.2f} us")
 for r in rows[nd:nd + 15]:
     print("   ", " ".join(f"{x:9.2f}" if isinstance(x, float) else f"{x:12s}" for x in r))
+if os.environ.get("SEED_CTA_TRACE") == "1":
+    # per-CTA phases of the layer-1 verify GEMMs and the LM head, relative to the launch release
+    ph = ["release", "prod_done", "first_full", "mma_done", "acc0_ready", "epi_done", "end", "part_stored",
+          "ticket", "reduced", "finished", "ring_used", "first_refill"]
+    for want in ["t.L1.qkv", "t.L1.o", "t.L1.gu", "t.L1.down", "t.lm", "d1.L0.gu"]:
+        i = names.index(want)
+        ct = eng.gemm_cta_trace(i)
+        rel = tr[i, 1]
+        used = ct[:, 7] >= tr[i, 0]
+        ct = ct[used]
+        print(f"{want}: {used.sum()} CTAs; release->end {(tr[i,2]-rel)/1e3:.2f} us; phase - release (us): min / med / max")
+        for k, name in enumerate(ph):
+            v = (ct[:, k + 1] - rel) / 1e3
+            v = v[ct[:, k + 1] >= tr[i, 0]]
+            if len(v) == 0:
+                continue
+            print(f"    {name:11s} {v.min():8.2f} {np.median(v):8.2f} {v.max():8.2f}")
+        last = np.argmax(ct[:, 7])
+        print("    last CTA:", " ".join(f"{(ct[last, k + 1] - rel)/1e3:.2f}" for k in range(len(ph))))
