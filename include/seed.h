@@ -169,11 +169,13 @@ SEED_API seed_status seed_reset_profile(seed_ctx ctx);
  * out: host buffer of 4*cap uint64; *n = launches written (in round launch order). */
 SEED_API seed_status seed_gemm_trace(seed_ctx ctx, uint64_t* out, int32_t cap, int32_t* n);
 /* Diagnostics (SEED_FLAG_PROFILE and env SEED_CTA_TRACE=1 at seed_init): per-CTA phase
- * timestamps (globaltimer ns) of GEMM launch `launch` (index as in seed_gemm_trace) of the most
- * recent round. out: host buffer of 148*16 uint64, row c = CTA c: start, producer release,
- * producer done, first stage full, MMA done, first accumulator ready, epilogue done, end,
- * last partial stored, last ticket taken, reduce done, finish done, 4 spare (0 / stale for CTAs
- * and phases the launch did not reach). *n_cta = 148, or 0 when tracing is off. */
+ * timestamps (globaltimer ns) of launch `launch` (index as in seed_gemm_trace) of the most recent
+ * round.  out: host buffer of 8192 uint64.  GEMM launches: row c (16 words) = CTA c: start,
+ * producer release, producer done, first stage full, MMA done, first accumulator ready, epilogue
+ * done, end, partial stored, contributors seen, reduce done, finish done, ring consumed, first
+ * refill.  Attention launches: row b (8 words) = linear block b: start, release, tiles ready,
+ * chunk result stored, merge ticket, end.  Words a launch did not reach are 0 or stale.
+ * *n_cta = 8192 (words written), or 0 when tracing is off. */
 SEED_API seed_status seed_gemm_cta_trace(seed_ctx ctx, int32_t launch, uint64_t* out, int32_t* n_cta);
 
 SEED_API const char* seed_last_error(seed_ctx ctx);

@@ -168,12 +168,12 @@ class SeedEngine:
         return buf[:4 * n.value].reshape(-1, 4)[:, :3].astype(np.int64)
 
     def gemm_cta_trace(self, launch):
-        """[148][16] per-CTA phase timestamps of one GEMM launch (profile=True, SEED_CTA_TRACE=1)."""
-        buf = np.zeros(148 * 16, dtype=np.uint64)
+        """Raw per-CTA phase words (8192) of one launch (profile=True, SEED_CTA_TRACE=1); see seed.h."""
+        buf = np.zeros(8192, dtype=np.uint64)
         n = C.c_int32(0)
         self._check(self.lib.seed_gemm_cta_trace(self.ctx, int(launch), buf.ctypes.data_as(C.POINTER(C.c_uint64)),
                                                  C.byref(n)), "seed_gemm_cta_trace")
-        return buf.reshape(148, 16)[:n.value].astype(np.int64)
+        return buf[:n.value].astype(np.int64)
 
     def reset_profile(self):
         self._check(self.lib.seed_reset_profile(self.ctx), "reset_profile")

@@ -81,6 +81,12 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
 
   pdl_trigger();
   if (ws.timing && threadIdx.x == 0) atomicMin(&ws.timing[0], globaltimer_ns());
+  unsigned long long* ct =
+      ws.cta ? ws.cta + 8 * (size_t)(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) : nullptr;
+  auto stamp = [&](int k) {
+    if (ct && threadIdx.x == 0) ct[k] = globaltimer_ns();
+  };
+  stamp(0);
   const int seq = blockIdx.x / n_qblk, qb = blockIdx.x % n_qblk;
   const int head = blockIdx.y, split = blockIdx.z, nsplit = gridDim.z;
   const int kvh = head / (H / Hk);
@@ -102,7 +108,9 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
   }
   pdl_wait();
   if (ws.timing && threadIdx.x == 0) atomicMin(&ws.timing[1], globaltimer_ns());
+  stamp(1);
   auto done = [&]() {
+    stamp(5);
     if (ws.timing && threadIdx.x == 0) {
       atomicMax(&ws.timing[2], globaltimer_ns());
       ws.timing[3] = 2;  // record kind: attention
@@ -155,50 +163,97 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
         (void)pg_first;
       }
     }
-    // ---- Q of this block's rows and head: RoPE, bf16 rounding (B2); padding rows are zero
-    for (int e = tid; e < QB * HALF; e += NT) {
-      const int r = e / HALF, i = e % HALF;
-      float a = 0.f, b = 0.f;
-      if (r < nr) {
-        const float* yr = qkv + (size_t)(q0 + r0 + r) * ldq + head * DH;
-        const float2 cs = rope[(size_t)(pos0 + r) * HALF + i];
-        const float x0 = yr[i], x1 = yr[i + HALF];
-        a = x0 * cs.x - x1 * cs.y;
-        b = x1 * cs.x + x0 * cs.y;
+    // ---- Q of this block's rows and head: RoPE, bf16 rounding (B2); padding rows are zero.
+    // Items of 4 rotation pairs; every load of the loop is issued before the first use.
+    {
+      constexpr int QI = QB * HALF / 4, QIT = (QI + NT - 1) / NT;
+      float4 x0[QIT], x1[QIT], c0[QIT], c1[QIT];
+#pragma unroll
+      for (int k = 0; k < QIT; ++k) {
+        const int it = tid + k * NT, r = it / (HALF / 4), i = (it % (HALF / 4)) * 4;
+        x0[k] = x1[k] = c0[k] = c1[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (it < QI && r < nr) {
+          const float* yr = qkv + (size_t)(q0 + r0 + r) * ldq + head * DH;
+          const float4* cs = reinterpret_cast<const float4*>(rope + (size_t)(pos0 + r) * HALF + i);
+          x0[k] = *reinterpret_cast<const float4*>(yr + i);
+          x1[k] = *reinterpret_cast<const float4*>(yr + i + HALF);
+          c0[k] = __ldg(cs);
+          c1[k] = __ldg(cs + 1);
+        }
       }
-      q_s[r * P + i] = f2bf(a);
-      q_s[r * P + i + HALF] = f2bf(b);
+#pragma unroll
+      for (int k = 0; k < QIT; ++k) {
+        const int it = tid + k * NT, r = it / (HALF / 4), i = (it % (HALF / 4)) * 4;
+        if (it < QI) {
+          // c0 = (cos_i, sin_i, cos_i+1, sin_i+1), c1 = (cos_i+2, sin_i+2, cos_i+3, sin_i+3)
+          const float a0 = x0[k].x * c0[k].x - x1[k].x * c0[k].y, b0 = x1[k].x * c0[k].x + x0[k].x * c0[k].y;
+          const float a1 = x0[k].y * c0[k].z - x1[k].y * c0[k].w, b1 = x1[k].y * c0[k].z + x0[k].y * c0[k].w;
+          const float a2 = x0[k].z * c1[k].x - x1[k].z * c1[k].y, b2 = x1[k].z * c1[k].x + x0[k].z * c1[k].y;
+          const float a3 = x0[k].w * c1[k].z - x1[k].w * c1[k].w, b3 = x1[k].w * c1[k].z + x0[k].w * c1[k].w;
+          *reinterpret_cast<uint2*>(q_s + r * P + i) = make_uint2(pack_bf16(a0, a1), pack_bf16(a2, a3));
+          *reinterpret_cast<uint2*>(q_s + r * P + i + HALF) = make_uint2(pack_bf16(b0, b1), pack_bf16(b2, b3));
+        }
+      }
     }
     // ---- new rows of the sequence inside this chunk: K (RoPE) and V from the QKV output into
-    // the tiles; the owning query block appends them to the cache
-    const int nk0 = max(c_begin, new_first), nk1 = c_end;
-    for (int e = tid; e < (nk1 - nk0) * HALF; e += NT) {
-      const int key = nk0 + e / HALF, i = e % HALF;
-      const int m = q0 + (key - new_first);
-      const float* yk = qkv + (size_t)m * ldq + (H + kvh) * DH;
-      const float* yv = qkv + (size_t)m * ldq + (H + Hk + kvh) * DH;
-      const float2 cs = rope[(size_t)key * HALF + i];
-      const float a = yk[i], b = yk[i + HALF];
-      const __nv_bfloat16 ka = f2bf(a * cs.x - b * cs.y), kb = f2bf(b * cs.x + a * cs.y);
-      const __nv_bfloat16 va = f2bf(yv[i]), vb = f2bf(yv[i + HALF]);
-      const int w = (key - c_begin) >> 5, kk = (key - c_begin) & 31;
-      __nv_bfloat16* kr = k_s + ((size_t)w * 32 + kk) * P;
-      __nv_bfloat16* vr = v_s + ((size_t)w * 32 + kk) * P;
-      kr[i] = ka;
-      kr[i + HALF] = kb;
-      vr[i] = va;
-      vr[i + HALF] = vb;
-      if (head % (H / Hk) == 0 && qb == (key - new_first) / QB) {  // one writer per kv head, position
-        const int page = __ldg(kv.page_table + (size_t)slot * kv.max_pages + key / kv.P);
-        __nv_bfloat16* kdst = kv.pool + kv.offset(page, layer, 0, kvh, key % kv.P);
-        kdst[i] = ka;
-        kdst[i + HALF] = kb;
-        kdst[kv.vofs() + i] = va;
-        kdst[kv.vofs() + i + HALF] = vb;
+    // the tiles; the owning query block appends them to the cache (one writer per kv head and
+    // position).  Same 4-pair items, loads first.
+    {
+      const int nk0 = max(c_begin, new_first), nk1 = c_end;
+      const int NI = (nk1 - nk0) * (HALF / 4);
+      for (int base = 0; base < NI; base += 2 * NT) {
+        float4 ka[2], kb[2], va[2], vb[2], c0[2], c1[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int it = base + tid + k * NT;
+          ka[k] = kb[k] = va[k] = vb[k] = c0[k] = c1[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (it < NI) {
+            const int key = nk0 + it / (HALF / 4), i = (it % (HALF / 4)) * 4;
+            const int m = q0 + (key - new_first);
+            const float* yk = qkv + (size_t)m * ldq + (H + kvh) * DH;
+            const float* yv = qkv + (size_t)m * ldq + (H + Hk + kvh) * DH;
+            const float4* cs = reinterpret_cast<const float4*>(rope + (size_t)key * HALF + i);
+            ka[k] = *reinterpret_cast<const float4*>(yk + i);
+            kb[k] = *reinterpret_cast<const float4*>(yk + i + HALF);
+            va[k] = *reinterpret_cast<const float4*>(yv + i);
+            vb[k] = *reinterpret_cast<const float4*>(yv + i + HALF);
+            c0[k] = __ldg(cs);
+            c1[k] = __ldg(cs + 1);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int it = base + tid + k * NT;
+          if (it >= NI) continue;
+          const int key = nk0 + it / (HALF / 4), i = (it % (HALF / 4)) * 4;
+          const float4 x0 = ka[k], x1 = kb[k];
+          const uint2 klo = make_uint2(pack_bf16(x0.x * c0[k].x - x1.x * c0[k].y, x0.y * c0[k].z - x1.y * c0[k].w),
+                                       pack_bf16(x0.z * c1[k].x - x1.z * c1[k].y, x0.w * c1[k].z - x1.w * c1[k].w));
+          const uint2 khi = make_uint2(pack_bf16(x1.x * c0[k].x + x0.x * c0[k].y, x1.y * c0[k].z + x0.y * c0[k].w),
+                                       pack_bf16(x1.z * c1[k].x + x0.z * c1[k].y, x1.w * c1[k].z + x0.w * c1[k].w));
+          const uint2 vlo = make_uint2(pack_bf16(va[k].x, va[k].y), pack_bf16(va[k].z, va[k].w));
+          const uint2 vhi = make_uint2(pack_bf16(vb[k].x, vb[k].y), pack_bf16(vb[k].z, vb[k].w));
+          const int w = (key - c_begin) >> 5, kk = (key - c_begin) & 31;
+          __nv_bfloat16* kr = k_s + ((size_t)w * 32 + kk) * P;
+          __nv_bfloat16* vr = v_s + ((size_t)w * 32 + kk) * P;
+          *reinterpret_cast<uint2*>(kr + i) = klo;
+          *reinterpret_cast<uint2*>(kr + i + HALF) = khi;
+          *reinterpret_cast<uint2*>(vr + i) = vlo;
+          *reinterpret_cast<uint2*>(vr + i + HALF) = vhi;
+          if (head % (H / Hk) == 0 && qb == (key - new_first) / QB) {
+            const int page = __ldg(kv.page_table + (size_t)slot * kv.max_pages + key / kv.P);
+            __nv_bfloat16* kdst = kv.pool + kv.offset(page, layer, 0, kvh, key % kv.P);
+            *reinterpret_cast<uint2*>(kdst + i) = klo;
+            *reinterpret_cast<uint2*>(kdst + i + HALF) = khi;
+            *reinterpret_cast<uint2*>(kdst + kv.vofs() + i) = vlo;
+            *reinterpret_cast<uint2*>(kdst + kv.vofs() + i + HALF) = vhi;
+          }
+        }
       }
     }
     cp_async_wait_all();
     __syncthreads();
+    stamp(2);
 
     if (kt < c_end) {
       // ---- S = Q K^T for this warp's 32 keys: 4 n-tiles of 8 keys, DH/16 k-steps
@@ -290,6 +345,13 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
   }
   __syncthreads();
   const bool single = nsplit == 1;
+  // With several chunks the last one (it holds the new keys) merges: its own result stays in
+  // shared memory, the other chunks publish theirs and leave.
+  const bool reducer = split == nsplit - 1;
+  float* own = o_s + (size_t)WARPS * QB * DH;      // [QB][DH] after the warp scratch, inside K|V
+  float* cm = own + QB * DH;                        // [QB] own chunk max and sum
+  float* cl = cm + QB;
+  float* oml = cl + QB;                             // [nsplit - 1][QB][2] other chunks' (max, sum)
   for (int e = tid; e < nr * DH; e += NT) {
     const int r = e / DH, d = e % DH;
     float mx = -INFINITY;
@@ -309,6 +371,12 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
     const size_t row = ws_row + r;
     if (single) {
       out[(row * H + head) * DH + d] = f2bf(o / l);
+    } else if (reducer) {
+      own[r * DH + d] = o;
+      if (d == 0) {
+        cm[r] = mx;
+        cl[r] = l;
+      }
     } else {
       ws.o_part[(((size_t)split * M + row) * H + head) * DH + d] = o;
       if (d == 0) {
@@ -318,41 +386,79 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
       }
     }
   }
+  stamp(3);
   if (single) {
     done();
     return;
   }
-
-  // ---- the last chunk CTA of (sequence block, head) merges all chunks in chunk order
-  __syncthreads();
   int* ctr = ws.counters + ((size_t)(seq * n_qblk + qb) * H + head);
-  if (tid == 0) {
-    fence_acq_rel_gpu();
-    *ticket_s = atomicAdd(ctr, 1);
-    fence_acq_rel_gpu();
-  }
-  __syncthreads();
-  if (*ticket_s != nsplit - 1) {
+  if (!reducer) {
+    __syncthreads();
+    if (tid == 0) {
+      fence_acq_rel_gpu();   // release this chunk's partial (bar.sync + cumulativity)
+      atomicAdd(ctr, 1);
+    }
     done();
     return;
   }
-  for (int e = tid; e < nr * DH; e += NT) {
-    const int r = e / DH, d = e % DH;
-    const size_t row = ws_row + r;
-    float mx = -INFINITY;
-    for (int s = 0; s < nsplit; ++s) mx = fmaxf(mx, __ldcg(ws.ml_part + (((size_t)s * M + row) * H + head) * 2));
-    float o = 0.f, l = 0.f;
-    for (int s = 0; s < nsplit; ++s) {
-      const float* ml = ws.ml_part + (((size_t)s * M + row) * H + head) * 2;
-      const float ms = __ldcg(ml);
-      if (ms == -INFINITY) continue;
-      const float f = expf(ms - mx);
-      o += __ldcg(ws.o_part + (((size_t)s * M + row) * H + head) * DH + d) * f;
-      l += __ldcg(ml + 1) * f;
+  if (tid == 0) {
+    volatile int* vc = ctr;
+    while (*vc < nsplit - 1) {
     }
-    out[(row * H + head) * DH + d] = f2bf(o / l);
+    fence_acq_rel_gpu();     // acquire the other chunks' partials
+    *vc = 0;                 // ready for the next launch (graph replay)
   }
-  if (tid == 0) *ctr = 0;  // ready for the next launch (graph replay)
+  __syncthreads();
+  stamp(4);
+  for (int e = tid; e < (nsplit - 1) * nr; e += NT) {
+    const int sp = e / nr, r = e % nr;
+    const float2 v = __ldcg(reinterpret_cast<const float2*>(ws.ml_part + (((size_t)sp * M + ws_row + r) * H + head) * 2));
+    oml[(sp * QB + r) * 2] = v.x;
+    oml[(sp * QB + r) * 2 + 1] = v.y;
+  }
+  __syncthreads();
+  // chunks in chunk order 0 .. nsplit - 1 (this one last), as one fixed sum (R19); items of 4 dims
+  constexpr int MI = QB * DH / 4, MIT = (MI + NT - 1) / NT;
+#pragma unroll
+  for (int k = 0; k < MIT; ++k) {
+    const int it = tid + k * NT, r = it / (DH / 4), d = (it % (DH / 4)) * 4;
+    if (it >= MI || r >= nr) continue;
+    float mx = cm[r];
+    for (int sp = 0; sp < nsplit - 1; ++sp) mx = fmaxf(mx, oml[(sp * QB + r) * 2]);
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    float l = 0.f;
+    const size_t row = ws_row + r;
+    for (int s0 = 0; s0 < nsplit - 1; s0 += 4) {
+      float4 v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        v[q] = s0 + q < nsplit - 1
+                   ? __ldcg(reinterpret_cast<const float4*>(ws.o_part + (((size_t)(s0 + q) * M + row) * H + head) * DH + d))
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (s0 + q >= nsplit - 1) break;
+        const float ms = oml[((s0 + q) * QB + r) * 2];
+        if (ms == -INFINITY) continue;
+        const float f = expf(ms - mx);
+        o.x += v[q].x * f;
+        o.y += v[q].y * f;
+        o.z += v[q].z * f;
+        o.w += v[q].w * f;
+        l += oml[((s0 + q) * QB + r) * 2 + 1] * f;
+      }
+    }
+    if (cm[r] != -INFINITY) {
+      const float f = expf(cm[r] - mx);
+      o.x += own[r * DH + d] * f;
+      o.y += own[r * DH + d + 1] * f;
+      o.z += own[r * DH + d + 2] * f;
+      o.w += own[r * DH + d + 3] * f;
+      l += cl[r] * f;
+    }
+    *reinterpret_cast<uint2*>(out + (row * H + head) * DH + d) =
+        make_uint2(pack_bf16(o.x / l, o.y / l), pack_bf16(o.z / l, o.w / l));
+  }
   done();
 }
 
@@ -364,6 +470,10 @@ cudaError_t launch_dh(int M, int n_seq, int max_q_len, int max_kv, int H, int Hk
   const int splits = (max_kv + CHUNK - 1) / CHUNK;
   const size_t smem = Smem<DH>::BYTES;
   static_assert((size_t)WARPS * QB * DH * 4 <= 2 * (size_t)WARPS * 32 * (DH + 8) * 2, "o merge scratch fits");
+  // reducer scratch after the warp scratch: own [QB][DH] + (max, sum) of every chunk
+  const size_t kv_bytes = 2 * (size_t)WARPS * 32 * (DH + 8) * 2;
+  if (((size_t)WARPS * QB * DH + (size_t)QB * DH + 2 * QB + (size_t)2 * QB * splits) * 4 > kv_bytes)
+    return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn_fused_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -164,6 +164,7 @@ struct RoundPlan {  // descriptors of one round at batch-size-determined arena o
 };
 
 constexpr int kMaxChunkRows = 256;
+constexpr size_t kCtaRec = 8192;  // per-launch per-CTA trace words (GEMM: 148 x 16, attention: grid x 8)
 
 }  // namespace
 
@@ -214,7 +215,7 @@ struct seed_ctx_s {
   // profiling: per-GEMM globaltimer records accumulated on the device
   bool profile = false, in_round = false;
   unsigned long long *timing_rec = nullptr, *timing_acc = nullptr, *timing_last = nullptr;
-  unsigned long long* cta_rec = nullptr;  // SEED_CTA_TRACE=1: [rec_cap][148][16] per-CTA GEMM phases
+  unsigned long long* cta_rec = nullptr;  // SEED_CTA_TRACE=1: [rec_cap][kCtaRec] per-CTA phases
   int last_draft_recs = 0, last_verify_recs = 0;
   std::map<int, int> draft_recs;  // records of the draft phase per batch size
   double draft_gemm_bytes = 0;
@@ -260,7 +261,7 @@ seed_status run_gemm(seed_ctx ctx, const GemmPlan& p, int M, const seed::GemmIO&
   unsigned long long* rec = nullptr;
   unsigned long long* cta = nullptr;
   if (ctx->profile && ctx->in_round && ctx->rec_used < ctx->rec_cap) {
-    if (ctx->cta_rec) cta = ctx->cta_rec + (size_t)ctx->rec_used * 148 * 16;
+    if (ctx->cta_rec) cta = ctx->cta_rec + (size_t)ctx->rec_used * kCtaRec;
     rec = ctx->timing_rec + 4 * ctx->rec_used++;
   }
   CK(seed::gemm_run(p, M, io, ctx->partial, st, rec, cta));
@@ -499,7 +500,10 @@ seed_status forward_chunk(seed_ctx ctx, Model& m, const ChunkDesc& c, cudaStream
     {
       seed::AttnWorkspace aws = m.aws;
       aws.timing = nullptr;
-      if (ctx->profile && ctx->in_round && ctx->rec_used < ctx->rec_cap) aws.timing = ctx->timing_rec + 4 * ctx->rec_used++;
+      if (ctx->profile && ctx->in_round && ctx->rec_used < ctx->rec_cap) {
+        if (ctx->cta_rec) aws.cta = ctx->cta_rec + (size_t)ctx->rec_used * kCtaRec;
+        aws.timing = ctx->timing_rec + 4 * ctx->rec_used++;
+      }
       CK(seed::attention(m.y, M, c.n_seq, c.max_q_len, c.max_kv, m.H, m.Hk, m.Dh, seqs, m.rope, m.kv, l, aws,
                          m.attn, st));
     }
@@ -1015,7 +1019,7 @@ seed_status seed_init(const seed_config* cfg, seed_ctx* out) {
     ok &= cudaMalloc(&ctx->timing_last, (size_t)ctx->rec_cap * 4 * 8) == cudaSuccess;
     ok &= cudaMalloc(&ctx->timing_acc, 4 * 8) == cudaSuccess;
     const char* ce = getenv("SEED_CTA_TRACE");
-    if (ce && ce[0] == '1') ok &= cudaMalloc(&ctx->cta_rec, (size_t)ctx->rec_cap * 148 * 16 * 8) == cudaSuccess;
+    if (ce && ce[0] == '1') ok &= cudaMalloc(&ctx->cta_rec, (size_t)ctx->rec_cap * kCtaRec * 8) == cudaSuccess;
     if (ok) {
       std::vector<unsigned long long> init((size_t)ctx->rec_cap * 4);
       for (int i = 0; i < ctx->rec_cap; ++i) {
@@ -1309,9 +1313,9 @@ seed_status seed_gemm_cta_trace(seed_ctx ctx, int32_t launch, uint64_t* out, int
   if (launch >= nd + nv) return SEED_EINVAL;
   const size_t idx = launch < nd ? (size_t)launch : (size_t)ctx->rec_cap / 2 + (launch - nd);
   if (cudaDeviceSynchronize() != cudaSuccess ||
-      cudaMemcpy(out, ctx->cta_rec + idx * 148 * 16, 148 * 16 * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+      cudaMemcpy(out, ctx->cta_rec + idx * kCtaRec, kCtaRec * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
     return fail(ctx, SEED_ECUDA, "seed_gemm_cta_trace", "");
-  *n_cta = 148;
+  *n_cta = (int32_t)kCtaRec;
   return SEED_OK;
 }
 

@@ -535,13 +535,13 @@ bool pdl_enabled() {
   return on == 1;
 }
 
-// dynamic smem per GEMM CTA (env SEED_GEMM_SMEM_KB).  150 KB (one GEMM CTA per SM, ~8 stages)
+// dynamic smem per GEMM CTA (env SEED_GEMM_SMEM_KB).  180 KB (one GEMM CTA per SM, 9 stages at M <= 16)
 // measured faster than 100 KB (two per SM, the next GEMM prefetching beside the running one).
 int smem_budget() {
   static int b = -1;
   if (b < 0) {
     const char* e = getenv("SEED_GEMM_SMEM_KB");
-    b = (e ? atoi(e) : 150) * 1024;
+    b = (e ? atoi(e) : 180) * 1024;
   }
   return b;
 }

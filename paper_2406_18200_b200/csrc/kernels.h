@@ -96,6 +96,7 @@ struct AttnWorkspace {
   int* counters;   // [max_counters] chunk tickets per (sequence block, head), zero between launches
   int max_splits, max_counters;
   unsigned long long* timing;  // optional profile record [4] (start, release, end)
+  unsigned long long* cta = nullptr;  // optional per-block phase words [grid][8] (diagnostics)
 };
 int attn_chunk_tokens();
 int attn_query_block();

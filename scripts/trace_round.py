@@ -73,6 +73,14 @@ for r in rows[nd:]:
 for k, v in kinds.items():
     v = np.array(v)
     print(f"  {k:5s} n={len(v):3d} span {v[:,0].mean():7.2f} exposed {v[:,1].mean():7.2f} gap-before {v[:,2].mean():7.2f} us")
+dk = {}
+for r in rows[:nd]:
+    k = r[0].split(".")[-1]
+    dk.setdefault(k, []).append((r[4], r[5], r[6]))
+print("draft phase per kind:")
+for k, v in dk.items():
+    v = np.array(v)
+    print(f"  {k:5s} n={len(v):3d} span {v[:,0].mean():7.2f} exposed {v[:,1].mean():7.2f} gap-before {v[:,2].mean():7.2f} us")
 for r in rows[nd:nd + 15]:
     print("   ", " ".join(f"{x:9.2f}" if isinstance(x, float) else f"{x:12s}" for x in r))
 if os.environ.get("SEED_CTA_TRACE") == "1":
@@ -81,7 +89,7 @@ if os.environ.get("SEED_CTA_TRACE") == "1":
           "ticket", "reduced", "finished", "ring_used", "first_refill"]
     for want in ["t.L1.qkv", "t.L1.o", "t.L1.gu", "t.L1.down", "t.lm", "d1.L0.gu"]:
         i = names.index(want)
-        ct = eng.gemm_cta_trace(i)
+        ct = eng.gemm_cta_trace(i)[:148 * 16].reshape(148, 16)
         rel = tr[i, 1]
         used = ct[:, 7] >= tr[i, 0]
         ct = ct[used]
@@ -94,3 +102,15 @@ if os.environ.get("SEED_CTA_TRACE") == "1":
             print(f"    {name:11s} {v.min():8.2f} {np.median(v):8.2f} {v.max():8.2f}")
         last = np.argmax(ct[:, 7])
         print("    last CTA:", " ".join(f"{(ct[last, k + 1] - rel)/1e3:.2f}" for k in range(len(ph))))
+    # attention CTA phases (layer 1): start, release, tiles ready, chunk stored, ticket, end
+    i = names.index("t.L1.attn")
+    raw = eng.gemm_cta_trace(i).reshape(-1, 8)
+    rel = tr[i, 1]
+    used = raw[:, 5] >= tr[i, 0]
+    ct = raw[used]
+    print(f"t.L1.attn: {used.sum()} CTAs; release->end {(tr[i,2]-rel)/1e3:.2f} us; phase - release (us): min / med / max")
+    for k, name in enumerate(["start", "release", "tiles", "stored", "ticket", "end"]):
+        v = (ct[:, k] - rel) / 1e3
+        v = v[ct[:, k] >= tr[i, 0]]
+        if len(v):
+            print(f"    {name:11s} {v.min():8.2f} {np.median(v):8.2f} {v.max():8.2f}")
