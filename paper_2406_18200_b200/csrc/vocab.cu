@@ -24,7 +24,7 @@ namespace seed {
 
 namespace {
 constexpr int CS = 8;         // CTAs per cluster (portable maximum)
-constexpr int VT = 256;       // threads per CTA
+constexpr int VT = 512;       // threads per CTA
 constexpr int MAX_ROWS = 2 * 16 + 1;
 
 struct Stat {  // log-softmax running statistic over a set of indices
@@ -33,24 +33,14 @@ struct Stat {  // log-softmax running statistic over a set of indices
   int i;       // first argmax (-1: empty)
 };
 
-__device__ __forceinline__ Stat stat_merge(Stat A, Stat B) {
+struct MaxI {   // fp32 maximum and its first index (-1: empty)
+  float m;
+  int i;
+};
+__device__ __forceinline__ MaxI maxi_merge(MaxI A, MaxI B) {
   if (B.i < 0) return A;
   if (A.i < 0) return B;
-  if (B.m > A.m || (B.m == A.m && B.i < A.i)) {
-    Stat t = A;
-    A = B;
-    B = t;
-  }
-  A.S = A.S + (B.S + 1.0) * exp(B.m - A.m);
-  return A;
-}
-
-__device__ __forceinline__ Stat stat_shfl(const Stat& s, int o) {
-  Stat r;
-  r.m = __shfl_xor_sync(0xffffffffu, s.m, o);
-  r.S = __shfl_xor_sync(0xffffffffu, s.S, o);
-  r.i = __shfl_xor_sync(0xffffffffu, s.i, o);
-  return r;
+  return (B.m > A.m || (B.m == A.m && B.i < A.i)) ? B : A;
 }
 
 struct Best {  // race winner
@@ -67,15 +57,27 @@ __device__ __forceinline__ Best best_shfl(const Best& b, int o) {
 }
 
 // block-wide deterministic reductions (warp butterflies, then warps in order)
-__device__ Stat block_stat(Stat s, Stat* red) {
+__device__ MaxI block_maxi(MaxI s, MaxI* red) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s = stat_merge(s, stat_shfl(s, o));
+  for (int o = 16; o > 0; o >>= 1)
+    s = maxi_merge(s, MaxI{__shfl_xor_sync(0xffffffffu, s.m, o), __shfl_xor_sync(0xffffffffu, s.i, o)});
   const int w = threadIdx.x >> 5;
   __syncthreads();
   if ((threadIdx.x & 31) == 0) red[w] = s;
   __syncthreads();
-  Stat r = red[0];
-  for (int i = 1; i < VT / 32; ++i) r = stat_merge(r, red[i]);
+  MaxI r = red[0];
+  for (int i = 1; i < VT / 32; ++i) r = maxi_merge(r, red[i]);
+  return r;
+}
+__device__ double block_sum(double s, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const int w = threadIdx.x >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[w] = s;
+  __syncthreads();
+  double r = red[0];
+  for (int i = 1; i < VT / 32; ++i) r += red[i];
   return r;
 }
 __device__ Best block_best(Best b, Best* red) {
@@ -90,7 +92,8 @@ __device__ Best block_best(Best b, Best* red) {
   return r;
 }
 
-__device__ __forceinline__ float scaled_v(float z, float T) { return __fdiv_rn(z, T); }
+// a = fl32(z / T) (R4); z / 1 is z exactly
+__device__ __forceinline__ float scaled_v(float z, float T) { return T == 1.0f ? z : __fdiv_rn(z, T); }
 
 // -log(E), E = -log1p(-u): the exponential-race offset, fp64
 __device__ __forceinline__ double neg_log_exp(double u) { return -log(-log1p(-u)); }
@@ -202,9 +205,11 @@ vocab_verify_kernel(VerifyArgs A, int nbuf) {
   extern __shared__ __align__(128) float rows_s[];  // [nbuf][slice] rows, then [slice] race keys
   __shared__ float red_f[VT / 32];
   __shared__ float cta_f;
-  __shared__ Stat red_s[VT / 32];
+  __shared__ MaxI red_m[VT / 32];
+  __shared__ double red_d[VT / 32];
   __shared__ Best red_b[VT / 32];
-  __shared__ Stat cta_stat[MAX_ROWS];
+  __shared__ MaxI cta_max[MAX_ROWS];
+  __shared__ double cta_sum[MAX_ROWS];
   __shared__ Stat glob[MAX_ROWS];
   __shared__ Best cta_best;
   __shared__ int s_a;
@@ -232,7 +237,10 @@ vocab_verify_kernel(VerifyArgs A, int nbuf) {
   Stager sg{rows_s, &bar, 0u, slice, v0, n, (V % 4 == 0) && (n % 4 == 0)};
   float* keys_s = rows_s + (size_t)nbuf * slice;
 
-  // ---- phase 1: per-row statistics over the slice (rows 0..g target, g+1..2g draft)
+  // ---- phase 1: per-row statistics over the slice (rows 0..g target, g+1..2g draft), two passes
+  // per staged group of rows: (a) the fp32 maximum and its first index, merged over the cluster in
+  // rank order; (b) S' = sum over v != argmax of exp(a_v - m), fp32 terms summed in fp64 (R13, R21)
+  // in a fixed thread / warp / rank order -- no rescaling, so no fp64 exponentials.
   int resident0 = -1, resident_k = 0;
   for (int r0 = 0; r0 < R; r0 += nbuf) {
     const int k = min(nbuf, R - r0);
@@ -242,34 +250,41 @@ vocab_verify_kernel(VerifyArgs A, int nbuf) {
     resident_k = k;
     for (int i = 0; i < k; ++i) {
       const float* zs = rows_s + (size_t)i * slice;
-      Stat s{-INFINITY, 0.0, -1};
-      float mf = -INFINITY;  // fp32 copy of s.m (the maxima are fp32 values)
+      MaxI mi{-INFINITY, -1};
       for (int l = threadIdx.x; l < n; l += VT) {
         const float xf = scaled_v(zs[l], A.T);
-        if (s.i < 0) {
-          s = Stat{(double)xf, 0.0, v0 + l};
-          mf = xf;
-        } else if (xf > mf) {
-          s.S = (s.S + 1.0) * exp(s.m - (double)xf);  // the old maximum joins the tail
-          s.m = (double)xf;
-          s.i = v0 + l;
-          mf = xf;
-        } else {
-          s.S += (double)expf(xf - mf);  // terms <= 1 in fp32, summed in fp64 (R21)
-        }
+        if (mi.i < 0 || xf > mi.m) mi = MaxI{xf, v0 + l};
       }
-      const Stat t = block_stat(s, red_s);
-      if (threadIdx.x == 0) cta_stat[r0 + i] = t;
+      mi = block_maxi(mi, red_m);
+      if (threadIdx.x == 0) cta_max[r0 + i] = mi;
     }
+    cluster.sync();
+    for (int row = r0 + (int)threadIdx.x; row < r0 + k; row += VT) {
+      MaxI acc = *cluster.map_shared_rank(&cta_max[row], 0);
+      for (int c = 1; c < CS; ++c) acc = maxi_merge(acc, *cluster.map_shared_rank(&cta_max[row], c));
+      glob[row] = Stat{(double)acc.m, 0.0, acc.i};
+    }
+    __syncthreads();
+    for (int i = 0; i < k; ++i) {
+      const float* zs = rows_s + (size_t)i * slice;
+      const float m = (float)glob[r0 + i].m;
+      const int im = glob[r0 + i].i;
+      double S = 0.0;
+      if (im >= 0)
+        for (int l = threadIdx.x; l < n; l += VT)
+          if (v0 + l != im) S += (double)expf(scaled_v(zs[l], A.T) - m);
+      S = block_sum(S, red_d);
+      if (threadIdx.x == 0) cta_sum[r0 + i] = S;
+    }
+    cluster.sync();
+    for (int row = r0 + (int)threadIdx.x; row < r0 + k; row += VT) {
+      double acc = *cluster.map_shared_rank(&cta_sum[row], 0);
+      for (int c = 1; c < CS; ++c) acc += *cluster.map_shared_rank(&cta_sum[row], c);
+      glob[row].S = acc;
+    }
+    __syncthreads();
   }
-  cluster.sync();
-  // ---- cluster merge in rank order (identical result in every CTA)
-  for (int row = threadIdx.x; row < R; row += VT) {
-    Stat acc = *cluster.map_shared_rank(&cta_stat[row], 0);
-    for (int c = 1; c < CS; ++c) acc = stat_merge(acc, *cluster.map_shared_rank(&cta_stat[row], c));
-    glob[row] = acc;
-  }
-  __syncthreads();
+  cluster.sync();   // peers may still read cta_max / cta_sum of this CTA
 
   // ---- phase 2: accept / reject chain
   if (threadIdx.x == 0) {
