@@ -142,25 +142,33 @@ __device__ __forceinline__ void finish16(const GemmArgs& a, int m0, int t, int n
 }
 
 // Add the other contributors' partials (segments 1..cnt-1 of the tile, in CTA order, R19) to the
-// reducer's own accumulator rows m0..m0+15 of tile column nl; loads go four segments at a time.
-__device__ __forceinline__ void add_partials16(const float* __restrict__ P, const int* __restrict__ sl, int cnt, int M,
-                                               int m0, int nl, float* acc, const int* id0) {
+// reducer's own accumulator rows m0..m0+15 of tile column nl.  Partials are laid out
+// [segment][column][m_pad] so a thread's 16 rows are 64 contiguous bytes; loads go four segments
+// at a time.
+__device__ __forceinline__ void add_partials16(const float* __restrict__ P, const int* __restrict__ sl, int cnt,
+                                               int m_pad, int m0, int nl, float* acc, const int* id0) {
   for (int k = 1; k < cnt; k += 4) {
     int id[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) id[q] = k == 1 ? id0[q] : (k + q < cnt ? __ldg(sl + 1 + k + q) : -1);
-    float v[4][16];
+    float4 v[4][4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const float* src = P + ((size_t)(id[q] < 0 ? 0 : id[q]) * M + m0) * BLOCK_N + nl;
+      const float4* src =
+          reinterpret_cast<const float4*>(P + ((size_t)(id[q] < 0 ? 0 : id[q]) * BLOCK_N + nl) * m_pad + m0);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) v[q][j] = (id[q] >= 0 && m0 + j < M) ? __ldcg(src + (size_t)j * BLOCK_N) : 0.f;
+      for (int j = 0; j < 4; ++j) v[q][j] = id[q] >= 0 ? __ldcg(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       if (id[q] >= 0) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) acc[j] += v[q][j];
+        for (int j = 0; j < 4; ++j) {
+          acc[4 * j] += v[q][j].x;
+          acc[4 * j + 1] += v[q][j].y;
+          acc[4 * j + 2] += v[q][j].z;
+          acc[4 * j + 3] += v[q][j].w;
+        }
       }
   }
 }
@@ -343,13 +351,13 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
           finish16(a, col, (int)t, nl, v, ew, lane, inv_s, red_s, xch_s);
         }
       } else if (!reducer) {
-        float* out = a.partial + ((size_t)((long)c * a.S + (t - t_begin)) * a.M) * BLOCK_N + nl;
+        float4* out = reinterpret_cast<float4*>(
+            a.partial + ((size_t)((long)c * a.S + (t - t_begin)) * BLOCK_N + nl) * a.m_pad);
         for (int col = 0; col < a.m_pad; col += 16) {
           float v[16];
           tmem_ld16(row_addr + col, v);
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (col + i < a.M) out[(size_t)(col + i) * BLOCK_N] = v[i];
+          for (int j = 0; j < 4; ++j) out[col / 4 + j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
         }
         if (ct && et == 0) ct[8] = globaltimer();
         asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -385,7 +393,7 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
         for (int m0 = 0; m0 < a.m_pad; m0 += 16) {
           float v[16];
           tmem_ld16(row_addr + m0, v);
-          add_partials16(a.partial, sl, cnt, a.M, m0, nl, v, id0);
+          add_partials16(a.partial, sl, cnt, a.m_pad, m0, nl, v, id0);
           if (ct && et == 0) ct[10] = globaltimer() + (v[0] == 1.2345e-30f ? 1 : 0);   // waits for the loads
           finish16(a, m0, (int)t, nl, v, ew, lane, inv_s, red_s, xch_s, (a.ymode == 1 && m0 == 0) ? xo : nullptr, wn);
           if (ct && et == 0) ct[11] = globaltimer();
@@ -546,7 +554,7 @@ int smem_budget() {
   return b;
 }
 
-size_t gemm_partial_floats(const GemmPlan& p, int M) { return (size_t)p.G * p.S * M * BLOCK_N; }
+size_t gemm_partial_floats(const GemmPlan& p, int M) { return (size_t)p.G * p.S * gemm_mpad(M) * BLOCK_N; }
 
 cudaError_t timing_accumulate(unsigned long long* rec, int n, unsigned long long* acc, unsigned long long* last,
                               cudaStream_t st) {
