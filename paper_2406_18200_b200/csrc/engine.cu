@@ -316,6 +316,14 @@ seed_status build_model(seed_ctx ctx, Model& m, const seed_model_shape& sh, cons
   m.V = sh.vocab;
   m.L = sh.n_layers;
   m.nqkv = (m.H + 2 * m.Hk) * m.Dh;
+  // k-blocks per CTA at least: small models (the draft) trade split-K parallelism for fewer
+  // partial reductions (env SEED_MIN_UNITS_SMALL for models with d_model < 2048); a function of
+  // the shape only, so batch invariance (R19) holds
+  int min_units = 4;
+  if (m.d < 2048) {
+    const char* e = getenv("SEED_MIN_UNITS_SMALL");
+    min_units = e ? atoi(e) : 12;   // measured: 12 (whole 768-wide k-rows) beats 4 and 24
+  }
   const size_t d = m.d, ff = m.ff, V = m.V, dkv = (size_t)m.Hk * m.Dh, dq = (size_t)m.H * m.Dh;
   auto alloc = [&](size_t elems) -> bf16* {
     bf16* p = nullptr;
@@ -358,16 +366,16 @@ seed_status build_model(seed_ctx ctx, Model& m, const seed_model_shape& sh, cons
     m.an.push_back(a);
     m.mn.push_back(mm);
     GemmPlan pq, po, pg, pd;
-    seed::gemm_plan(&pq, qkv, m.nqkv, m.d);
-    seed::gemm_plan(&po, o, m.d, (int)dq);
-    seed::gemm_plan(&pg, gu, 2 * m.ff, m.d);
-    seed::gemm_plan(&pd, dn, m.d, m.ff);
+    seed::gemm_plan(&pq, qkv, m.nqkv, m.d, min_units);
+    seed::gemm_plan(&po, o, m.d, (int)dq, min_units);
+    seed::gemm_plan(&pg, gu, 2 * m.ff, m.d, min_units);
+    seed::gemm_plan(&pd, dn, m.d, m.ff, min_units);
     m.pq.push_back(pq);
     m.po.push_back(po);
     m.pgu.push_back(pg);
     m.pd.push_back(pd);
   }
-  seed::gemm_plan(&m.plm, m.lm_head, m.V, m.d);
+  seed::gemm_plan(&m.plm, m.lm_head, m.V, m.d, min_units);
   // KV pool
   m.kv.n_layers = m.L;
   m.kv.Hk = m.Hk;

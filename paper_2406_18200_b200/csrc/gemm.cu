@@ -481,14 +481,14 @@ bool encode_tmap_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t 
   return r == CUDA_SUCCESS;
 }
 
-void gemm_plan(GemmPlan* p, const void* W, int N, int K) {
+void gemm_plan(GemmPlan* p, const void* W, int N, int K, int min_units) {
   p->N = N;
   p->K = K;
   p->KB = K / BLOCK_K;
   p->tiles = (N + BLOCK_N - 1) / BLOCK_N;
   p->U = p->tiles * p->KB;
-  // at least 4 k-blocks per CTA so a tile meets few partial segments (small draft GEMMs)
-  p->G = std::max(1, std::min(kNumSMs, p->U / 4));
+  // at least min_units k-blocks per CTA, so a small GEMM's tiles meet few partial segments
+  p->G = std::max(1, std::min(kNumSMs, p->U / std::max(1, min_units)));
   // segments per CTA: ceil(range / KB) + 1 bound
   const int range = (p->U + p->G - 1) / p->G;
   p->S = (range + p->KB - 1) / p->KB + 1;

@@ -34,7 +34,7 @@ struct GemmPlan {
 
 bool encode_tmap_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
                     uint32_t box_outer);
-void gemm_plan(GemmPlan* plan, const void* W, int N, int K);
+void gemm_plan(GemmPlan* plan, const void* W, int N, int K, int min_units = 4);
 void gemm_plan_free(GemmPlan* plan);
 size_t gemm_partial_floats(const GemmPlan& plan, int M);
 // Operands and epilogue of one GEMM launch (see gemm.cu):
