@@ -33,9 +33,11 @@ struct Smem {
   static constexpr size_t Q = 0;                                     // bf16 [16][PITCH]
   static constexpr size_t K = Q + (size_t)QB * PITCH * 2;            // bf16 [WARPS][32][PITCH]
   static constexpr size_t V = K + (size_t)WARPS * 32 * PITCH * 2;    // bf16 [WARPS][32][PITCH]
-  static constexpr size_t ML = V + (size_t)WARPS * 32 * PITCH * 2;   // fp32 [2][WARPS][QB]
-  static constexpr size_t TK = ML + (size_t)2 * WARPS * QB * 4;      // ticket
-  static constexpr size_t BYTES = TK + 16;
+  static constexpr size_t ML = V + (size_t)WARPS * 32 * PITCH * 2;   // fp32 m, l [2][WARPS][QB], merge
+                                                                     // factors [WARPS][QB], row m, l [2][QB]
+  static constexpr size_t TK = ML + (size_t)(3 * WARPS + 2) * QB * 4; // ticket
+  static constexpr size_t BAR = TK + 16;                             // mbarrier per warp (K / V tile)
+  static constexpr size_t BYTES = BAR + WARPS * 8;
   // o merge scratch fp32 [WARPS][QB][DH] aliases K|V after the MMAs
 };
 
@@ -77,8 +79,16 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
   float* m_s = reinterpret_cast<float*>(smem + L::ML);
   float* l_s = m_s + WARPS * QB;
   float* o_s = reinterpret_cast<float*>(smem + L::K);
-  int* ticket_s = reinterpret_cast<int*>(smem + L::TK);
+  float* fw_s = l_s + WARPS * QB;                 // [WARPS][QB] warp merge factors
+  float* rm_s = fw_s + WARPS * QB;                // [QB] row max, then row sum
+  float* rl_s = rm_s + QB;
+  uint64_t* bar_s = reinterpret_cast<uint64_t*>(smem + L::BAR);
 
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < WARPS; ++w) mbar_init(&bar_s[w], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
   pdl_trigger();
   if (ws.timing && threadIdx.x == 0) atomicMin(&ws.timing[0], globaltimer_ns());
   unsigned long long* ct =
@@ -138,29 +148,28 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
   for (int j = 0; j < DT; ++j) o_acc[j][0] = o_acc[j][1] = o_acc[j][2] = o_acc[j][3] = 0.f;
 
   if (c_begin < key_end) {
-    // ---- cached keys of this warp's tile: cp.async into the K / V tiles
+    // ---- cached keys of this warp's tile: one bulk copy (TMA) per K and V row into the padded
+    // tiles, completing on the warp's mbarrier; rows past the chunk are zero
     const int kt = c_begin + warp * 32;
     const int old_end = min(c_end, new_first);
     __nv_bfloat16* kw = k_s + (size_t)warp * 32 * P;
     __nv_bfloat16* vw = v_s + (size_t)warp * 32 * P;
     {
-      const int pg_first = kt / kv.P;
-      const int my_page = (kt + lane < old_end) ? __ldg(kv.page_table + (size_t)slot * kv.max_pages + (kt + lane) / kv.P)
-                                                : 0;
-#pragma unroll 4
-      for (int e = lane; e < 32 * VPR; e += 32) {
-        const int kk = e / VPR, c16 = e % VPR;
-        const int key = kt + kk;
-        const int page = __shfl_sync(0xffffffffu, my_page, kk);
-        if (key < old_end) {
-          const size_t ko = kv.offset(page, layer, 0, kvh, key % kv.P);
-          cp_async16(kw + kk * P + c16 * 8, reinterpret_cast<const uint4*>(kv.pool + ko) + c16);
-          cp_async16(vw + kk * P + c16 * 8, reinterpret_cast<const uint4*>(kv.pool + ko + kv.vofs()) + c16);
-        } else if (key >= c_end || key >= key_end) {
-          *reinterpret_cast<uint4*>(kw + kk * P + c16 * 8) = make_uint4(0, 0, 0, 0);
-          *reinterpret_cast<uint4*>(vw + kk * P + c16 * 8) = make_uint4(0, 0, 0, 0);
+      const int key = kt + lane;
+      const int n_old = max(0, min(32, old_end - kt));
+      if (lane == 0) mbar_arrive_expect_tx(&bar_s[warp], (uint32_t)n_old * DH * 2 * 2);
+      __syncwarp();
+      if (lane < n_old) {
+        const int page = __ldg(kv.page_table + (size_t)slot * kv.max_pages + key / kv.P);
+        const __nv_bfloat16* src = kv.pool + kv.offset(page, layer, 0, kvh, key % kv.P);
+        bulk_g2s(kw + lane * P, src, DH * 2, &bar_s[warp]);
+        bulk_g2s(vw + lane * P, src + kv.vofs(), DH * 2, &bar_s[warp]);
+      } else if (key >= c_end || key >= key_end) {
+#pragma unroll
+        for (int c16 = 0; c16 < VPR; ++c16) {
+          *reinterpret_cast<uint4*>(kw + lane * P + c16 * 8) = make_uint4(0, 0, 0, 0);
+          *reinterpret_cast<uint4*>(vw + lane * P + c16 * 8) = make_uint4(0, 0, 0, 0);
         }
-        (void)pg_first;
       }
     }
     // ---- Q of this block's rows and head: RoPE, bf16 rounding (B2); padding rows are zero.
@@ -251,7 +260,7 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
         }
       }
     }
-    cp_async_wait_all();
+    mbar_wait(&bar_s[warp], 0);
     __syncthreads();
     stamp(2);
 
@@ -352,38 +361,53 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
   float* cm = own + QB * DH;                        // [QB] own chunk max and sum
   float* cl = cm + QB;
   float* oml = cl + QB;                             // [nsplit - 1][QB][2] other chunks' (max, sum)
-  for (int e = tid; e < nr * DH; e += NT) {
-    const int r = e / DH, d = e % DH;
+  // per row: the 4 warps' merge factors exp(m_w - m) and the row sum, warps in a fixed order
+  if (tid < nr) {
+    const int r = tid;
     float mx = -INFINITY;
 #pragma unroll
     for (int w = 0; w < WARPS; ++w) mx = fmaxf(mx, m_s[w * QB + r]);
-    float o = 0.f, l = 0.f;
-    if (mx != -INFINITY) {
+    float l = 0.f;
 #pragma unroll
-      for (int w = 0; w < WARPS; ++w) {
-        const float mw = m_s[w * QB + r];
-        if (mw == -INFINITY) continue;
-        const float f = expf(mw - mx);
-        o += o_s[((size_t)w * QB + r) * DH + d] * f;
-        l += l_s[w * QB + r] * f;
-      }
+    for (int w = 0; w < WARPS; ++w) {
+      const float mw = m_s[w * QB + r];
+      const float f = (mx == -INFINITY || mw == -INFINITY) ? 0.f : expf(mw - mx);
+      fw_s[w * QB + r] = f;
+      l += l_s[w * QB + r] * f;
+    }
+    rm_s[r] = mx;
+    rl_s[r] = l;
+    if (!single && reducer) {
+      cm[r] = mx;
+      cl[r] = l;
+    } else if (!single) {
+      float* ml = ws.ml_part + (((size_t)split * M + ws_row + r) * H + head) * 2;
+      ml[0] = mx;
+      ml[1] = l;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < nr * (DH / 4); e += NT) {
+    const int r = e / (DH / 4), d = (e % (DH / 4)) * 4;
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) {
+      const float f = fw_s[w * QB + r];
+      const float4 v = *reinterpret_cast<const float4*>(o_s + ((size_t)w * QB + r) * DH + d);
+      o.x += v.x * f;
+      o.y += v.y * f;
+      o.z += v.z * f;
+      o.w += v.w * f;
     }
     const size_t row = ws_row + r;
     if (single) {
-      out[(row * H + head) * DH + d] = f2bf(o / l);
+      const float l = rl_s[r];
+      *reinterpret_cast<uint2*>(out + (row * H + head) * DH + d) =
+          make_uint2(pack_bf16(o.x / l, o.y / l), pack_bf16(o.z / l, o.w / l));
     } else if (reducer) {
-      own[r * DH + d] = o;
-      if (d == 0) {
-        cm[r] = mx;
-        cl[r] = l;
-      }
+      *reinterpret_cast<float4*>(own + r * DH + d) = o;
     } else {
-      ws.o_part[(((size_t)split * M + row) * H + head) * DH + d] = o;
-      if (d == 0) {
-        float* ml = ws.ml_part + (((size_t)split * M + row) * H + head) * 2;
-        ml[0] = mx;
-        ml[1] = l;
-      }
+      *reinterpret_cast<float4*>(ws.o_part + (((size_t)split * M + row) * H + head) * DH + d) = o;
     }
   }
   stamp(3);
