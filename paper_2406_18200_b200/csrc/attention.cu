@@ -17,8 +17,12 @@
 //     order; the output is rounded to bf16 (B3).
 // The chunk grid is fixed (128 keys), so a row's result never depends on the batch (R19).
 // Memory-bound on the cached K/V.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace seed {
 
@@ -65,7 +69,7 @@ template <int DH>
 __global__ void __launch_bounds__(WARPS * 32)
 attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, const float2* __restrict__ rope,
                   KVLayout kv, int layer, int n_qblk, float scale, AttnWorkspace ws, int M,
-                  __nv_bfloat16* __restrict__ out) {
+                  __nv_bfloat16* __restrict__ out, int clustered) {
   using L = Smem<DH>;
   constexpr int P = L::PITCH;
   constexpr int HALF = DH / 2;
@@ -354,9 +358,11 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
   }
   __syncthreads();
   const bool single = nsplit == 1;
-  // With several chunks the last one (it holds the new keys) merges: its own result stays in
-  // shared memory, the other chunks publish theirs and leave.
-  const bool reducer = split == nsplit - 1;
+  // With several chunks: launched as one thread-block cluster per (sequence block, head)
+  // (clustered, <= 8 chunks), every chunk keeps its result in shared memory and the cluster
+  // merges through distributed shared memory; otherwise the last chunk (it holds the new keys)
+  // merges from global memory after the others published theirs.
+  const bool reducer = clustered || split == nsplit - 1;
   float* own = o_s + (size_t)WARPS * QB * DH;      // [QB][DH] after the warp scratch, inside K|V
   float* cm = own + QB * DH;                        // [QB] own chunk max and sum
   float* cl = cm + QB;
@@ -412,6 +418,36 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
   }
   stamp(3);
   if (single) {
+    done();
+    return;
+  }
+  if (clustered) {
+    // every rank merges a slice of the (row, 4-dim) items from all ranks' results, chunk order
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();   // release this CTA's result, acquire the peers'
+    stamp(4);
+    for (int e = tid + split * NT; e < nr * (DH / 4); e += NT * nsplit) {
+      const int r = e / (DH / 4), d = (e % (DH / 4)) * 4;
+      float mx = -INFINITY;
+      for (int sp = 0; sp < nsplit; ++sp) mx = fmaxf(mx, *cluster.map_shared_rank(cm + r, sp));
+      float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+      float l = 0.f;
+      for (int sp = 0; sp < nsplit; ++sp) {
+        const float ms = *cluster.map_shared_rank(cm + r, sp);
+        if (ms == -INFINITY) continue;
+        const float f = expf(ms - mx);
+        const float4 v = *reinterpret_cast<const float4*>(cluster.map_shared_rank(own + r * DH + d, sp));
+        o.x += v.x * f;
+        o.y += v.y * f;
+        o.z += v.z * f;
+        o.w += v.w * f;
+        l += *cluster.map_shared_rank(cl + r, sp) * f;
+      }
+      const size_t row = ws_row + r;
+      *reinterpret_cast<uint2*>(out + (row * H + head) * DH + d) =
+          make_uint2(pack_bf16(o.x / l, o.y / l), pack_bf16(o.z / l, o.w / l));
+    }
+    cluster.sync();   // peers finished reading this CTA's shared memory
     done();
     return;
   }
@@ -486,6 +522,16 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
   done();
 }
 
+// env SEED_ATTN_CLUSTER=0 forces the global-memory merge (both give identical results)
+bool attn_cluster_merge() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("SEED_ATTN_CLUSTER");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 template <int DH>
 cudaError_t launch_dh(int M, int n_seq, int max_q_len, int max_kv, int H, int Hk, const float* qkv,
                       const SeqInfo& seqs, const float2* rope, const KVLayout& kv, int layer, const AttnWorkspace& ws,
@@ -504,8 +550,11 @@ cudaError_t launch_dh(int M, int n_seq, int max_q_len, int max_kv, int H, int Hk
     attr = true;
   }
   const float scale = 1.0f / sqrtf((float)DH);
-  return launch(attn_fused_kernel<DH>, dim3(n_seq * n_qblk, H, splits), dim3(WARPS * 32), smem, st, qkv, H, Hk,
-                seqs, rope, kv, layer, n_qblk, scale, ws, M, out);
+  // <= 8 chunks: one cluster per (sequence block, head) along z, merged through DSMEM
+  const int clustered = (splits > 1 && splits <= 8 && attn_cluster_merge()) ? 1 : 0;
+  return launch_clustered(attn_fused_kernel<DH>, dim3(n_seq * n_qblk, H, splits), dim3(WARPS * 32), smem, st,
+                          dim3(1, 1, clustered ? splits : 1), qkv, H, Hk, seqs, rope, kv, layer, n_qblk, scale, ws, M,
+                          out, clustered);
 }
 }  // namespace
 
