@@ -60,6 +60,12 @@ SEED_DEV void mma_bf16(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
+// 2^x on the SFU (ex2.approx: ~2 ulp; the attention probabilities are rounded to bf16 anyway, B5)
+SEED_DEV float exp2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 SEED_DEV uint32_t pack_bf16(float lo, float hi) {
   const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<const uint32_t*>(&v);
@@ -270,23 +276,30 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
 
     if (kt < c_end) {
       // ---- S = Q K^T for this warp's 32 keys: 4 n-tiles of 8 keys, DH/16 k-steps
-      float s[4][4];
+      // two accumulator sets (even / odd k-steps) halve the dependent mma chain
+      float s[4][4], s2[4][4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+      for (int j = 0; j < 4; ++j)
+        s[j][0] = s[j][1] = s[j][2] = s[j][3] = s2[j][0] = s2[j][1] = s2[j][2] = s2[j][3] = 0.f;
       const uint32_t qa = smem_u32(q_s), kb = smem_u32(kw);
 #pragma unroll
       for (int ks = 0; ks < DH / 16; ++ks) {
         uint32_t a0, a1, a2, a3;
         ldsm_x4(qa + ((lane & 15) * P + ks * 16 + (lane >> 4) * 8) * 2, a0, a1, a2, a3);
+        float (*acc)[4] = (ks & 1) ? s2 : s;
 #pragma unroll
         for (int nt = 0; nt < 4; nt += 2) {
           uint32_t b0, b1, b2, b3;
           const int key = nt * 8 + (lane >> 4) * 8 + (lane & 7);
           ldsm_x4(kb + (key * P + ks * 16 + ((lane >> 3) & 1) * 8) * 2, b0, b1, b2, b3);
-          mma_bf16(s[nt], a0, a1, a2, a3, b0, b1);
-          mma_bf16(s[nt + 1], a0, a1, a2, a3, b2, b3);
+          mma_bf16(acc[nt], a0, a1, a2, a3, b0, b1);
+          mma_bf16(acc[nt + 1], a0, a1, a2, a3, b2, b3);
         }
       }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) s[j][c] += s2[j][c];
       // ---- mask + softmax over the tile (rows g, g + 8; lane holds keys 8 nt + 2 t4, +1)
 #pragma unroll
       for (int h2 = 0; h2 < 2; ++h2) {
@@ -310,7 +323,7 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
             float& v = s[nt][2 * h2 + c];
-            v = (mx == -INFINITY) ? 0.f : expf(v - mx);
+            v = (mx == -INFINITY) ? 0.f : exp2_approx(v - mx);
             sum += v;
           }
         sum += __shfl_xor_sync(0xffffffffu, sum, 1);
@@ -377,7 +390,7 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
 #pragma unroll
     for (int w = 0; w < WARPS; ++w) {
       const float mw = m_s[w * QB + r];
-      const float f = (mx == -INFINITY || mw == -INFINITY) ? 0.f : expf(mw - mx);
+      const float f = (mx == -INFINITY || mw == -INFINITY) ? 0.f : exp2_approx(mw - mx);
       fw_s[w * QB + r] = f;
       l += l_s[w * QB + r] * f;
     }
@@ -435,7 +448,7 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
       for (int sp = 0; sp < nsplit; ++sp) {
         const float ms = *cluster.map_shared_rank(cm + r, sp);
         if (ms == -INFINITY) continue;
-        const float f = expf(ms - mx);
+        const float f = exp2_approx(ms - mx);
         const float4 v = *reinterpret_cast<const float4*>(cluster.map_shared_rank(own + r * DH + d, sp));
         o.x += v.x * f;
         o.y += v.y * f;
@@ -500,7 +513,7 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
         if (s0 + q >= nsplit - 1) break;
         const float ms = oml[((s0 + q) * QB + r) * 2];
         if (ms == -INFINITY) continue;
-        const float f = expf(ms - mx);
+        const float f = exp2_approx(ms - mx);
         o.x += v[q].x * f;
         o.y += v[q].y * f;
         o.z += v[q].z * f;
@@ -509,7 +522,7 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
       }
     }
     if (cm[r] != -INFINITY) {
-      const float f = expf(cm[r] - mx);
+      const float f = exp2_approx(cm[r] - mx);
       o.x += own[r * DH + d] * f;
       o.y += own[r * DH + d + 1] * f;
       o.z += own[r * DH + d + 2] * f;
@@ -549,7 +562,8 @@ cudaError_t launch_dh(int M, int n_seq, int max_q_len, int max_kv, int H, int Hk
     cudaFuncSetAttribute(attn_fused_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  const float scale = 1.0f / sqrtf((float)DH);
+  // scores are kept in the base-2 domain: s = q.k / sqrt(Dh) * log2(e), p = 2^(s - max)
+  const float scale = 1.0f / sqrtf((float)DH) * 1.4426950408889634f;
   // <= 8 chunks: one cluster per (sequence block, head) along z, merged through DSMEM
   const int clustered = (splits > 1 && splits <= 8 && attn_cluster_merge()) ? 1 : 0;
   return launch_clustered(attn_fused_kernel<DH>, dim3(n_seq * n_qblk, H, splits), dim3(WARPS * 32), smem, st,
