@@ -190,6 +190,7 @@ struct seed_ctx_s {
   int C = 0, G = 0;
   float *tgt_logits = nullptr, *drf_logits = nullptr;
   int32_t *xs = nullptr, *vtok = nullptr, *out_tok = nullptr, *out_cnt = nullptr, *out_acc = nullptr;
+  int32_t* verify_work = nullptr;  // K4 scratch [C][2 (gamma + 1) + 1] (tickets zero between launches)
   int32_t *records = nullptr, *records_all = nullptr, *records_host = nullptr, *cnt_host = nullptr,
           *tok_host = nullptr;
   uint32_t* sids_dev = nullptr;
@@ -835,6 +836,7 @@ seed_status enqueue_verify(seed_ctx ctx, cudaStream_t st) {
   a.out_tok = ctx->out_tok;
   a.out_cnt = ctx->out_cnt;
   a.out_acc = ctx->out_acc;
+  a.work = ctx->verify_work;
   CK(seed::vocab_verify(a, st));
   // a5: K5 commit + rollback, emit the exchange records
   const int world = std::max(ctx->cfg.world, 1);
@@ -996,6 +998,8 @@ seed_status seed_init(const seed_config* cfg, seed_ctx* out) {
   ok &= cudaMalloc(&ctx->out_tok, (size_t)C * (g + 1) * 4) == cudaSuccess;
   ok &= cudaMalloc(&ctx->out_cnt, (size_t)C * 4) == cudaSuccess;
   ok &= cudaMalloc(&ctx->out_acc, (size_t)C * 4) == cudaSuccess;
+  ok &= cudaMalloc(&ctx->verify_work, (size_t)C * (2 * (g + 1) + 1) * 4) == cudaSuccess;
+  if (ok) ok &= cudaMemset(ctx->verify_work, 0, (size_t)C * (2 * (g + 1) + 1) * 4) == cudaSuccess;
   const int world = std::max(cfg->world, 1);
   ok &= cudaMalloc(&ctx->records, (size_t)C * (g + 3) * 4) == cudaSuccess;
   ok &= cudaMalloc(&ctx->records_all, (size_t)world * C * (g + 3) * 4) == cudaSuccess;
@@ -1060,7 +1064,7 @@ void seed_destroy(seed_ctx ctx) {
   free_model(ctx->tm);
   free_model(ctx->dm);
   void* bufs[] = {ctx->partial, ctx->tgt_logits, ctx->drf_logits, ctx->xs, ctx->vtok, ctx->out_tok,
-                  ctx->out_cnt, ctx->out_acc, ctx->records, ctx->records_all, ctx->sids_dev, ctx->rs_dev,
+                  ctx->out_cnt, ctx->out_acc, ctx->verify_work, ctx->records, ctx->records_all, ctx->sids_dev, ctx->rs_dev,
                   ctx->slots_dev, ctx->ds.tlen, ctx->ds.len_t, ctx->ds.len_d, ctx->ds.L, ctx->ds.r,
                   ctx->ds.done, ctx->ds.hist};
   for (void* p : bufs)
@@ -1413,7 +1417,12 @@ seed_status seed_op_verify(const float* zt, const float* zd, const int32_t* xs, 
   a.out_acc = out_acc;
   a.dbg = dbg;
   a.stats = stats;
-  return seed::vocab_verify(a, (cudaStream_t)stream) == cudaSuccess ? SEED_OK : SEED_ECUDA;
+  const size_t wb = (size_t)B * (2 * (gamma + 1) + 1) * 4;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMallocAsync(&a.work, wb, st) != cudaSuccess) return SEED_ENOMEM;
+  bool ok = cudaMemsetAsync(a.work, 0, wb, st) == cudaSuccess && seed::vocab_verify(a, st) == cudaSuccess;
+  ok &= cudaFreeAsync(a.work, st) == cudaSuccess;
+  return ok ? SEED_OK : SEED_ECUDA;
 }
 
 seed_status seed_op_draft_sample(const float* z, int32_t ld, int32_t B, int32_t V, float temperature, uint64_t seed,

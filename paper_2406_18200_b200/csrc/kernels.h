@@ -116,6 +116,8 @@ struct VerifyArgs {
   int bonus;
   int32_t* out_tok; int32_t* out_cnt; int32_t* out_acc;
   float* dbg; double* stats;
+  int32_t* work;   // device [B][2 (gamma + 1) + 1] scratch (accept flags, candidate tokens, ticket);
+                   // the ticket words must be zero before the first launch (the kernel re-zeroes them)
 };
 cudaError_t vocab_verify(const VerifyArgs& a, cudaStream_t st);
 cudaError_t draft_sample(const float* z, long ld, int B, int V, float T, uint32_t k0, uint32_t k1,

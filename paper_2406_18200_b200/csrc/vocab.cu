@@ -25,7 +25,6 @@ namespace seed {
 namespace {
 constexpr int CS = 8;         // CTAs per cluster (portable maximum)
 constexpr int VT = 512;       // threads per CTA
-constexpr int MAX_ROWS = 2 * 16 + 1;
 
 struct Stat {  // log-softmax running statistic over a set of indices
   double m;    // max of a (as fp64)
@@ -126,7 +125,6 @@ struct Stager {
   }
 };
 
-constexpr int SMEM_ROWS_BYTES = 200 * 1024;
 
 __device__ __forceinline__ Best cluster_best(cg::cluster_group& cluster, Best* cta_best, Best mine) {
   if (threadIdx.x == 0) *cta_best = mine;
@@ -200,33 +198,38 @@ __device__ Best race_exact(cg::cluster_group& cluster, int v0, int n, uint32_t c
   return cluster_best(cluster, cta_best, b);
 }
 
+// K4: one 8-CTA cluster per (stream b, position j = 0..gamma).  Cluster (b, j) computes the
+// statistics of target row j and draft row j, the accept decision for x_{j+1} (j < gamma), and the
+// token that would be emitted if j were the first rejected position: the residual race on row j
+// (slot j + 1), or for j = gamma the bonus race on the last target row.  The last cluster of the
+// stream to finish (ticket) counts the leading accepts a and emits x_1..x_a, y_a -- the same
+// decisions, counters and races as the sequential Alg. 1, evaluated in parallel.
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(VT)
-vocab_verify_kernel(VerifyArgs A, int nbuf) {
-  extern __shared__ __align__(128) float rows_s[];  // [nbuf][slice] rows, then [slice] race keys
+vocab_verify_kernel(VerifyArgs A) {
+  extern __shared__ __align__(128) float rows_s[];  // [2][slice] target / draft row, [slice] race keys
   __shared__ float red_f[VT / 32];
   __shared__ float cta_f;
   __shared__ MaxI red_m[VT / 32];
   __shared__ double red_d[VT / 32];
   __shared__ Best red_b[VT / 32];
-  __shared__ MaxI cta_max[MAX_ROWS];
-  __shared__ double cta_sum[MAX_ROWS];
-  __shared__ Stat glob[MAX_ROWS];
+  __shared__ MaxI cta_max[2];
+  __shared__ double cta_sum[2];
+  __shared__ Stat glob[2];
   __shared__ Best cta_best;
-  __shared__ int s_a;
   __shared__ __align__(8) uint64_t bar;
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
-  const int b = blockIdx.x / CS;
   const int g = A.gamma, V = A.V;
-  const int R = 2 * g + 1;
+  const int cid = blockIdx.x / CS;
+  const int b = cid / (g + 1), j = cid % (g + 1);
+  const bool has_d = j < g;                          // draft row j exists
+  const int nrows = has_d ? 2 : 1;
   const int slice = ((V + CS - 1) / CS + 3) & ~3;
   const int v0 = min(V, rank * slice), n = min(V, v0 + slice) - v0;
   const float* zt = A.zt + (size_t)b * A.zt_stride_b;
   const float* zd = A.zd + (size_t)b * A.zd_stride_b;
   const uint32_t sid = A.sids[b], rr = (uint32_t)A.rs[b];
-  auto rowptr = [&](int row) -> const float* {
-    return row <= g ? zt + (size_t)row * V : zd + (size_t)(row - g - 1) * V;
-  };
+  auto rowptr = [&](int row) -> const float* { return row == 0 ? zt + (size_t)j * V : zd + (size_t)j * V; };
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_barrier_init();
@@ -235,159 +238,129 @@ vocab_verify_kernel(VerifyArgs A, int nbuf) {
   pdl_trigger();
   pdl_wait();   // the logits are written by the previous kernels
   Stager sg{rows_s, &bar, 0u, slice, v0, n, (V % 4 == 0) && (n % 4 == 0)};
-  float* keys_s = rows_s + (size_t)nbuf * slice;
+  float* keys_s = rows_s + (size_t)2 * slice;
+  sg.stage(0, nrows, rowptr);
 
-  // ---- phase 1: per-row statistics over the slice (rows 0..g target, g+1..2g draft), two passes
-  // per staged group of rows: (a) the fp32 maximum and its first index, merged over the cluster in
-  // rank order; (b) S' = sum over v != argmax of exp(a_v - m), fp32 terms summed in fp64 (R13, R21)
-  // in a fixed thread / warp / rank order -- no rescaling, so no fp64 exponentials.
-  int resident0 = -1, resident_k = 0;
-  for (int r0 = 0; r0 < R; r0 += nbuf) {
-    const int k = min(nbuf, R - r0);
-    if (r0 > 0) __syncthreads();
-    sg.stage(r0, k, rowptr);
-    resident0 = r0;
-    resident_k = k;
-    for (int i = 0; i < k; ++i) {
-      const float* zs = rows_s + (size_t)i * slice;
-      MaxI mi{-INFINITY, -1};
-      for (int l = threadIdx.x; l < n; l += VT) {
-        const float xf = scaled_v(zs[l], A.T);
-        if (mi.i < 0 || xf > mi.m) mi = MaxI{xf, v0 + l};
-      }
-      mi = block_maxi(mi, red_m);
-      if (threadIdx.x == 0) cta_max[r0 + i] = mi;
+  // ---- statistics, two passes per row: (a) fp32 maximum and its first index, merged over the
+  // cluster in rank order; (b) S' = sum over v != argmax of exp(a_v - m), fp32 terms summed in
+  // fp64 in a fixed thread / warp / rank order (R13, R21) -- no rescaling, no fp64 exponentials
+  for (int i = 0; i < nrows; ++i) {
+    const float* zs = rows_s + (size_t)i * slice;
+    MaxI mi{-INFINITY, -1};
+    for (int l = threadIdx.x; l < n; l += VT) {
+      const float xf = scaled_v(zs[l], A.T);
+      if (mi.i < 0 || xf > mi.m) mi = MaxI{xf, v0 + l};
     }
-    cluster.sync();
-    for (int row = r0 + (int)threadIdx.x; row < r0 + k; row += VT) {
-      MaxI acc = *cluster.map_shared_rank(&cta_max[row], 0);
-      for (int c = 1; c < CS; ++c) acc = maxi_merge(acc, *cluster.map_shared_rank(&cta_max[row], c));
-      glob[row] = Stat{(double)acc.m, 0.0, acc.i};
-    }
-    __syncthreads();
-    for (int i = 0; i < k; ++i) {
-      const float* zs = rows_s + (size_t)i * slice;
-      const float m = (float)glob[r0 + i].m;
-      const int im = glob[r0 + i].i;
-      double S = 0.0;
-      if (im >= 0)
-        for (int l = threadIdx.x; l < n; l += VT)
-          if (v0 + l != im) S += (double)expf(scaled_v(zs[l], A.T) - m);
-      S = block_sum(S, red_d);
-      if (threadIdx.x == 0) cta_sum[r0 + i] = S;
-    }
-    cluster.sync();
-    for (int row = r0 + (int)threadIdx.x; row < r0 + k; row += VT) {
-      double acc = *cluster.map_shared_rank(&cta_sum[row], 0);
-      for (int c = 1; c < CS; ++c) acc += *cluster.map_shared_rank(&cta_sum[row], c);
-      glob[row].S = acc;
-    }
-    __syncthreads();
+    mi = block_maxi(mi, red_m);
+    if (threadIdx.x == 0) cta_max[i] = mi;
   }
-  cluster.sync();   // peers may still read cta_max / cta_sum of this CTA
-
-  // ---- phase 2: accept / reject chain
-  if (threadIdx.x == 0) {
-    int a = 0;
-    bool alive = true;
-    for (int j = 1; j <= g; ++j) {
-      const int x = A.xs[(size_t)b * g + (j - 1)];
-      const Stat st = glob[j - 1], sq = glob[g + j];
-      const double lp = ((double)scaled_v(__ldg(zt + (size_t)(j - 1) * V + x), A.T) - st.m) - log1p(st.S);
-      const double lq = ((double)scaled_v(__ldg(zd + (size_t)(j - 1) * V + x), A.T) - sq.m) - log1p(sq.S);
-      const double rho = exp(fmin(0.0, lp - lq));
-      const Philox4 ph = philox4x32_10(0u, (kTagAccept << 24) | (uint32_t)j, rr, sid, A.k0, A.k1);
-      const double u = philox_uniform(ph.x);
-      if (alive && u < rho) ++a;
-      else alive = false;
-      if (A.dbg && rank == 0) {
-        float* d = A.dbg + ((size_t)b * g + (j - 1)) * 4;
-        d[0] = (float)lp;
-        d[1] = (float)lq;
-        d[2] = (float)u;
-        d[3] = (float)rho;
-      }
-    }
-    s_a = a;
+  cluster.sync();
+  if (threadIdx.x < nrows) {
+    MaxI acc = *cluster.map_shared_rank(&cta_max[threadIdx.x], 0);
+    for (int c = 1; c < CS; ++c) acc = maxi_merge(acc, *cluster.map_shared_rank(&cta_max[threadIdx.x], c));
+    glob[threadIdx.x] = Stat{(double)acc.m, 0.0, acc.i};
   }
   __syncthreads();
-  const int a = s_a;
+  for (int i = 0; i < nrows; ++i) {
+    const float* zs = rows_s + (size_t)i * slice;
+    const float m = (float)glob[i].m;
+    const int im = glob[i].i;
+    double S = 0.0;
+    if (im >= 0)
+      for (int l = threadIdx.x; l < n; l += VT)
+        if (v0 + l != im) S += (double)expf(scaled_v(zs[l], A.T) - m);
+    S = block_sum(S, red_d);
+    if (threadIdx.x == 0) cta_sum[i] = S;
+  }
+  cluster.sync();
+  if (threadIdx.x < nrows) {
+    double acc = *cluster.map_shared_rank(&cta_sum[threadIdx.x], 0);
+    for (int c = 1; c < CS; ++c) acc += *cluster.map_shared_rank(&cta_sum[threadIdx.x], c);
+    glob[threadIdx.x].S = acc;
+  }
+  cluster.sync();   // peers have read cta_max / cta_sum; glob visible to the CTA
+  const Stat st = glob[0];
+  const double l1t = log1p(st.S);
 
-  // ---- phase 3: residual race on row a (0-based) or bonus race on row g, from shared memory
-  auto resident = [&](int row) -> const float* {
-    return (row >= resident0 && row < resident0 + resident_k) ? rows_s + (size_t)(row - resident0) * slice : nullptr;
-  };
-  const uint32_t c1 = (kTagResample << 24) | (uint32_t)(a + 1);
-  int y = -1;
-  if (a < g || A.bonus) {
-    const int rt = a < g ? a : g;           // target row of the race
-    const int rd = g + 1 + a;               // draft row (residual only)
-    const float* zt_s = resident(rt);
-    const float* zd_s = a < g ? resident(rd) : nullptr;
-    if (!zt_s || (a < g && !zd_s)) {        // not resident: stage the rows into buffers 0 / 1
-      __syncthreads();
-      sg.stage(rt, 1, rowptr);
-      resident0 = rt;
-      resident_k = 1;
-      zt_s = rows_s;
-      if (a < g) {
-        if (threadIdx.x == 0 && sg.bulk && n > 0) {
-          mbar_arrive_expect_tx(&bar, (uint32_t)(n * 4));
-          bulk_g2s(rows_s + slice, rowptr(rd) + v0, (uint32_t)(n * 4), &bar);
-        }
-        if (sg.bulk && n > 0) {
-          mbar_wait(&bar, sg.phase);
-          sg.phase ^= 1;
-        } else {
-          for (int l = threadIdx.x; l < n; l += VT) rows_s[slice + l] = __ldg(rowptr(rd) + v0 + l);
-          __syncthreads();
-        }
-        zd_s = rows_s + slice;
-      }
+  // ---- accept decision for x_{j+1}: u < min(1, p / q) in log space (R2, R13)
+  int accept = 0;
+  if (has_d && rank == 0 && threadIdx.x == 0) {
+    const Stat sq = glob[1];
+    const int x = A.xs[(size_t)b * g + j];
+    const double lp = ((double)scaled_v(__ldg(zt + (size_t)j * V + x), A.T) - st.m) - l1t;
+    const double lq = ((double)scaled_v(__ldg(zd + (size_t)j * V + x), A.T) - sq.m) - log1p(sq.S);
+    const double rho = exp(fmin(0.0, lp - lq));
+    const Philox4 ph = philox4x32_10(0u, (kTagAccept << 24) | (uint32_t)(j + 1), rr, sid, A.k0, A.k1);
+    const double u = philox_uniform(ph.x);
+    accept = u < rho ? 1 : 0;
+    if (A.dbg) {
+      float* d = A.dbg + ((size_t)b * g + j) * 4;
+      d[0] = (float)lp;
+      d[1] = (float)lq;
+      d[2] = (float)u;
+      d[3] = (float)rho;
     }
-    const Stat st = glob[rt];
-    const double l1t = log1p(st.S);
-    const float mt = (float)st.m, l1tf = (float)l1t;
-    auto bonus32 = [&](int l) -> float { return scaled_v(zt_s[l], A.T); };
-    auto bonus64 = [&](int l) -> double { return (double)scaled_v(zt_s[l], A.T); };
-    if (a < g) {
-      const Stat sq = glob[g + 1 + a];
-      const double l1q = log1p(sq.S);
-      const float mq = (float)sq.m, l1qf = (float)l1q;
-      auto res32 = [&](int l) -> float {
-        const float lp = (scaled_v(zt_s[l], A.T) - mt) - l1tf;
-        const float lq = (scaled_v(zd_s[l], A.T) - mq) - l1qf;
-        const float dlt = lq - lp;
-        if (dlt > -0.05f) return dlt >= 0.05f ? -INFINITY : NAN;  // near-equal p, q: fp64
-        return lp + logf(-expm1f(dlt));
-      };
-      auto res64 = [&](int l) -> double {
-        const double lp = ((double)scaled_v(zt_s[l], A.T) - st.m) - l1t;
-        const double lq = ((double)scaled_v(zd_s[l], A.T) - sq.m) - l1q;
-        return lq < lp ? lp + log(-expm1(lq - lp)) : -INFINITY;
-      };
-      y = race_exact(cluster, v0, n, c1, rr, sid, A.k0, A.k1, keys_s, red_f, &cta_f, red_b, &cta_best, res32, res64).v;
-      if (y < 0)  // empty residual (rounding only): bonus rule on the same row, same uniforms
-        y = race_exact(cluster, v0, n, c1, rr, sid, A.k0, A.k1, keys_s, red_f, &cta_f, red_b, &cta_best, bonus32,
-                       bonus64).v;
-    } else {
+  }
+
+  // ---- the token emitted if position j + 1 is the first rejection (residual race, slot j + 1),
+  // or the bonus token (j = gamma); ties to the smallest id (R14)
+  const uint32_t c1 = (kTagResample << 24) | (uint32_t)(j + 1);
+  const float* zt_s = rows_s;
+  const float* zd_s = rows_s + slice;
+  const float mt = (float)st.m, l1tf = (float)l1t;
+  auto bonus32 = [&](int l) -> float { return scaled_v(zt_s[l], A.T); };
+  auto bonus64 = [&](int l) -> double { return (double)scaled_v(zt_s[l], A.T); };
+  int y = -1;
+  if (has_d) {
+    const Stat sq = glob[1];
+    const double l1q = log1p(sq.S);
+    const float mq = (float)sq.m, l1qf = (float)l1q;
+    auto res32 = [&](int l) -> float {
+      const float lp = (scaled_v(zt_s[l], A.T) - mt) - l1tf;
+      const float lq = (scaled_v(zd_s[l], A.T) - mq) - l1qf;
+      const float dlt = lq - lp;
+      if (dlt > -0.05f) return dlt >= 0.05f ? -INFINITY : NAN;  // near-equal p, q: fp64
+      return lp + logf(-expm1f(dlt));
+    };
+    auto res64 = [&](int l) -> double {
+      const double lp = ((double)scaled_v(zt_s[l], A.T) - st.m) - l1t;
+      const double lq = ((double)scaled_v(zd_s[l], A.T) - sq.m) - l1q;
+      return lq < lp ? lp + log(-expm1(lq - lp)) : -INFINITY;
+    };
+    y = race_exact(cluster, v0, n, c1, rr, sid, A.k0, A.k1, keys_s, red_f, &cta_f, red_b, &cta_best, res32, res64).v;
+    if (y < 0)  // empty residual (rounding only): bonus rule on the same row, same uniforms
       y = race_exact(cluster, v0, n, c1, rr, sid, A.k0, A.k1, keys_s, red_f, &cta_f, red_b, &cta_best, bonus32,
                      bonus64).v;
-    }
+  } else if (A.bonus) {
+    y = race_exact(cluster, v0, n, c1, rr, sid, A.k0, A.k1, keys_s, red_f, &cta_f, red_b, &cta_best, bonus32, bonus64)
+            .v;
   }
+
+  if (A.stats && rank == 0 && threadIdx.x < nrows) {
+    const int row = threadIdx.x == 0 ? j : g + 1 + j;
+    A.stats[((size_t)b * (2 * g + 1) + row) * 2] = glob[threadIdx.x].m;
+    A.stats[((size_t)b * (2 * g + 1) + row) * 2 + 1] = log1p(glob[threadIdx.x].S);
+  }
+  // ---- publish (accept_j, y_j); the stream's last cluster emits x_1..x_a, y_a
   if (rank == 0 && threadIdx.x == 0) {
-    int32_t* ot = A.out_tok + (size_t)b * (g + 1);
-    for (int j = 0; j < a; ++j) ot[j] = A.xs[(size_t)b * g + j];
-    int cnt = a;
-    if (y >= 0) ot[cnt++] = y;
-    for (int j = cnt; j <= g; ++j) ot[j] = -1;
-    if (A.out_cnt) A.out_cnt[b] = cnt;
-    if (A.out_acc) A.out_acc[b] = a;
-  }
-  if (A.stats && rank == 0) {
-    for (int row = threadIdx.x; row < R; row += VT) {
-      A.stats[((size_t)b * R + row) * 2] = glob[row].m;
-      A.stats[((size_t)b * R + row) * 2 + 1] = log1p(glob[row].S);
+    int32_t* w = A.work + (size_t)b * (2 * (g + 1) + 1);
+    w[j] = accept;
+    w[g + 1 + j] = y;
+    fence_acq_rel_gpu();
+    if (atomicAdd(&w[2 * (g + 1)], 1) == g) {
+      fence_acq_rel_gpu();
+      volatile int32_t* vw = w;
+      int a = 0;
+      while (a < g && vw[a]) ++a;
+      const int ya = vw[g + 1 + a];
+      int32_t* ot = A.out_tok + (size_t)b * (g + 1);
+      for (int q = 0; q < a; ++q) ot[q] = A.xs[(size_t)b * g + q];
+      int cnt = a;
+      if (ya >= 0) ot[cnt++] = ya;
+      for (int q = cnt; q <= g; ++q) ot[q] = -1;
+      if (A.out_cnt) A.out_cnt[b] = cnt;
+      if (A.out_acc) A.out_acc[b] = a;
+      w[2 * (g + 1)] = 0;   // ready for the next launch (graph replay)
     }
   }
   cluster.sync();  // keep shared memory alive until every peer has read it
@@ -467,18 +440,16 @@ __global__ void rollback_commit_kernel(StreamState s, const int32_t* batch_slots
 }  // namespace
 
 cudaError_t vocab_verify(const VerifyArgs& a, cudaStream_t st) {
-  const int R = 2 * a.gamma + 1;
-  if (R > MAX_ROWS) return cudaErrorInvalidValue;
+  if (!a.work || a.gamma < 1) return cudaErrorInvalidValue;
   const int slice = ((a.V + CS - 1) / CS + 3) & ~3;
-  const int nbuf = std::max(2, std::min(R, SMEM_ROWS_BYTES / (slice * 4) - 1));
-  const size_t smem = (size_t)(nbuf + 1) * slice * 4;
+  const size_t smem = (size_t)3 * slice * 4;
   if (smem > 220 * 1024) return cudaErrorInvalidValue;
   static size_t attr = 0;
   if (smem > attr) {
     cudaFuncSetAttribute(vocab_verify_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = smem;
   }
-  return launch(vocab_verify_kernel, dim3(a.B * CS), dim3(VT), smem, st, a, nbuf);
+  return launch(vocab_verify_kernel, dim3(a.B * (a.gamma + 1) * CS), dim3(VT), smem, st, a);
 }
 
 cudaError_t draft_sample(const float* z, long ld, int B, int V, float T, uint32_t k0, uint32_t k1,
