@@ -113,17 +113,49 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
   // the descriptors were uploaded before the round's first kernel: safe before pdl_wait()
   const int q0 = seqs.q_start[seq], ql = seqs.q_len[seq], kvl = seqs.kv_len[seq];
   const int slot = seqs.slot[seq];
-  if (seqs.stable && threadIdx.x < 32) {
-    // keys below `stable` were written before this round: pull this chunk's cached K / V into
-    // L2 while our predecessor (the QKV GEMM) still runs
-    const int p0 = (split * CHUNK) / kv.P;
-    const int p1 = (min(seqs.stable[seq], split * CHUNK + CHUNK) + kv.P - 1) / kv.P;
-    const uint32_t blk = (uint32_t)kv.P * DH * 2;
-    for (int i = p0 + (int)threadIdx.x; i < p1; i += 32) {
-      const int page = __ldg(kv.page_table + (size_t)slot * kv.max_pages + i);
-      const __nv_bfloat16* kb0 = kv.pool + kv.offset(page, layer, 0, kvh, 0);
-      prefetch_l2(kb0, blk);
-      prefetch_l2(kb0 + kv.vofs(), blk);
+  const int r0 = qb * QB;
+  const bool active = r0 < ql;                     // this query block holds rows of the sequence
+  const int nr = min(QB, ql - r0);
+  const int new_first = kvl - ql;                  // position of the sequence's first new row
+  const int pos0 = new_first + r0;                 // position of the first row of this block
+  const int key_end = pos0 + nr;                   // keys [0, key_end) are visible to some row
+  const int c_begin = split * CHUNK;
+  const int c_end = min(c_begin + CHUNK, key_end);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;          // MMA fragment coordinates
+  const size_t ws_row = (size_t)(q0 + r0);
+  const int ldq = (H + 2 * Hk) * DH;               // row stride of the QKV GEMM output
+  const bool has_keys = active && c_begin < key_end;
+  // ---- cached keys of this warp's tile: one bulk copy (TMA) per K and V row into the padded
+  // tiles, completing on the warp's mbarrier; rows past the chunk are zero.  Rows below `stable`
+  // were written before this round, so they are copied while the predecessor (the QKV GEMM)
+  // still runs; the rest after the dependency wait.
+  const int kt = c_begin + warp * 32;
+  const int old_end = min(c_end, new_first);
+  const int stable = seqs.stable ? min(seqs.stable[seq], old_end) : 0;
+  __nv_bfloat16* kw = k_s + (size_t)warp * 32 * P;
+  __nv_bfloat16* vw = v_s + (size_t)warp * 32 * P;
+  auto copy_rows = [&](int k0, int k1) {   // cached rows with k0 <= key < k1 of this warp's tile
+    const int key = kt + lane;
+    if (key >= k0 && key < k1) {
+      const int page = __ldg(kv.page_table + (size_t)slot * kv.max_pages + key / kv.P);
+      const __nv_bfloat16* src = kv.pool + kv.offset(page, layer, 0, kvh, key % kv.P);
+      bulk_g2s(kw + lane * P, src, DH * 2, &bar_s[warp]);
+      bulk_g2s(vw + lane * P, src + kv.vofs(), DH * 2, &bar_s[warp]);
+    }
+  };
+  if (has_keys) {
+    const int n_old = max(0, min(32, old_end - kt));
+    if (lane == 0) mbar_arrive_expect_tx(&bar_s[warp], (uint32_t)n_old * DH * 2 * 2);
+    __syncwarp();
+    copy_rows(0, stable);
+    const int key = kt + lane;
+    if (key >= c_end) {
+#pragma unroll
+      for (int c16 = 0; c16 < VPR; ++c16) {
+        *reinterpret_cast<uint4*>(kw + lane * P + c16 * 8) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(vw + lane * P + c16 * 8) = make_uint4(0, 0, 0, 0);
+      }
     }
   }
   pdl_wait();
@@ -136,52 +168,18 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
       ws.timing[3] = 2;  // record kind: attention
     }
   };
-  const int r0 = qb * QB;
-  if (r0 >= ql) {
+  if (!active) {
     done();
     return;
   }
-  const int nr = min(QB, ql - r0);
-  const int new_first = kvl - ql;                  // position of the sequence's first new row
-  const int pos0 = new_first + r0;                 // position of the first row of this block
-  const int key_end = pos0 + nr;                   // keys [0, key_end) are visible to some row
-  const int c_begin = split * CHUNK;
-  const int c_end = min(c_begin + CHUNK, key_end);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, t4 = lane & 3;          // MMA fragment coordinates
-  const size_t ws_row = (size_t)(q0 + r0);
-  const int ldq = (H + 2 * Hk) * DH;               // row stride of the QKV GEMM output
 
   float o_acc[DT][4];
   float m_row[2] = {-INFINITY, -INFINITY}, l_row[2] = {0.f, 0.f};   // rows g, g + 8
 #pragma unroll
   for (int j = 0; j < DT; ++j) o_acc[j][0] = o_acc[j][1] = o_acc[j][2] = o_acc[j][3] = 0.f;
 
-  if (c_begin < key_end) {
-    // ---- cached keys of this warp's tile: one bulk copy (TMA) per K and V row into the padded
-    // tiles, completing on the warp's mbarrier; rows past the chunk are zero
-    const int kt = c_begin + warp * 32;
-    const int old_end = min(c_end, new_first);
-    __nv_bfloat16* kw = k_s + (size_t)warp * 32 * P;
-    __nv_bfloat16* vw = v_s + (size_t)warp * 32 * P;
-    {
-      const int key = kt + lane;
-      const int n_old = max(0, min(32, old_end - kt));
-      if (lane == 0) mbar_arrive_expect_tx(&bar_s[warp], (uint32_t)n_old * DH * 2 * 2);
-      __syncwarp();
-      if (lane < n_old) {
-        const int page = __ldg(kv.page_table + (size_t)slot * kv.max_pages + key / kv.P);
-        const __nv_bfloat16* src = kv.pool + kv.offset(page, layer, 0, kvh, key % kv.P);
-        bulk_g2s(kw + lane * P, src, DH * 2, &bar_s[warp]);
-        bulk_g2s(vw + lane * P, src + kv.vofs(), DH * 2, &bar_s[warp]);
-      } else if (key >= c_end || key >= key_end) {
-#pragma unroll
-        for (int c16 = 0; c16 < VPR; ++c16) {
-          *reinterpret_cast<uint4*>(kw + lane * P + c16 * 8) = make_uint4(0, 0, 0, 0);
-          *reinterpret_cast<uint4*>(vw + lane * P + c16 * 8) = make_uint4(0, 0, 0, 0);
-        }
-      }
-    }
+  if (has_keys) {
+    copy_rows(stable, old_end);
     // ---- Q of this block's rows and head: RoPE, bf16 rounding (B2); padding rows are zero.
     // Items of 4 rotation pairs; every load of the loop is issued before the first use.
     {
