@@ -87,7 +87,7 @@ if os.environ.get("SEED_CTA_TRACE") == "1":
     # per-CTA phases of the layer-1 verify GEMMs and the LM head, relative to the launch release
     ph = ["release", "prod_done", "first_full", "mma_done", "acc0_ready", "epi_done", "end", "part_stored",
           "ticket", "reduced", "finished", "ring_used", "first_refill"]
-    for want in ["t.L1.qkv", "t.L1.o", "t.L1.gu", "t.L1.down", "t.lm", "d1.L0.gu"]:
+    for want in ["t.L1.qkv", "t.L1.o", "t.L1.gu", "t.L1.down", "t.lm", "d1.L0.gu", "d1.L0.down", "d1.L0.o"]:
         i = names.index(want)
         ct = eng.gemm_cta_trace(i)[:148 * 16].reshape(148, 16)
         rel = tr[i, 1]
