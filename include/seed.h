@@ -164,6 +164,10 @@ SEED_API seed_status seed_last_round_buffers(seed_ctx ctx, const float** tgt_log
 SEED_API seed_status seed_get_profile(seed_ctx ctx, double* gemm_ms, int64_t* gemm_launches,
                              double* gemm_bytes, int64_t* kernel_launches, double* gemm_span_ms);
 SEED_API seed_status seed_reset_profile(seed_ctx ctx);
+/* Switch the device timing records on or off between rounds (the context must have been created
+ * with SEED_FLAG_PROFILE; the timing atomics cost ~2% of a round, so a benchmark times its
+ * rounds with profiling off).  SEED_ESTATE between seed_draft_round and seed_verify. */
+SEED_API seed_status seed_set_profile(seed_ctx ctx, int32_t on);
 /* GEMM trace of the most recent round (SEED_FLAG_PROFILE): out[4*i..4*i+3] = globaltimer ns of
  * launch i: first CTA start, dependency release (PDL wait returned), last CTA end, 0.
  * out: host buffer of 4*cap uint64; *n = launches written (in round launch order). */

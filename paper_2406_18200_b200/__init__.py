@@ -175,6 +175,10 @@ class SeedEngine:
                                                  C.byref(n)), "seed_gemm_cta_trace")
         return buf[:n.value].astype(np.int64)
 
+    def set_profile(self, on):
+        """Timing records on / off between rounds (the engine must be created with profile=True)."""
+        self._check(self.lib.seed_set_profile(self.ctx, int(bool(on))), "seed_set_profile")
+
     def reset_profile(self):
         self._check(self.lib.seed_reset_profile(self.ctx), "reset_profile")
 

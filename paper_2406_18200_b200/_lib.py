@@ -57,6 +57,7 @@ _SIGS = {
     "seed_get_profile": [_P, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_double),
                          C.POINTER(C.c_int64), C.POINTER(C.c_double)],
     "seed_reset_profile": [_P],
+    "seed_set_profile": [_P, C.c_int32],
     "seed_gemm_trace": [_P, C.POINTER(C.c_uint64), C.c_int32, _I32P],
     "seed_gemm_cta_trace": [_P, C.c_int32, C.POINTER(C.c_uint64), _I32P],
     "seed_last_error": [_P],

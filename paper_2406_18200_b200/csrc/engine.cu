@@ -889,7 +889,9 @@ seed_status run_phase(seed_ctx ctx, int n, bool draft, cudaStream_t st) {
     }
     return SEED_OK;
   }
-  auto& G = draft ? ctx->draft_graphs[ctx->plan.key_draft] : ctx->verify_graphs[ctx->plan.key_verify];
+  // profiled launches carry timing pointers: a separate graph per profiling state
+  const int64_t pbit = ctx->profile ? (int64_t)1 << 62 : 0;
+  auto& G = draft ? ctx->draft_graphs[ctx->plan.key_draft | pbit] : ctx->verify_graphs[ctx->plan.key_verify | pbit];
   cudaGraphExec_t& ex = G.exec;
   if (!ex) {
     cudaGraph_t graph;
@@ -1328,6 +1330,14 @@ seed_status seed_gemm_cta_trace(seed_ctx ctx, int32_t launch, uint64_t* out, int
       cudaMemcpy(out, ctx->cta_rec + idx * kCtaRec, kCtaRec * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
     return fail(ctx, SEED_ECUDA, "seed_gemm_cta_trace", "");
   *n_cta = (int32_t)kCtaRec;
+  return SEED_OK;
+}
+
+seed_status seed_set_profile(seed_ctx ctx, int32_t on) {
+  if (!ctx) return SEED_EINVAL;
+  if (on && !ctx->timing_rec) return fail(ctx, SEED_ESTATE, "seed_set_profile", "created without SEED_FLAG_PROFILE");
+  if (!ctx->drafted.empty()) return fail(ctx, SEED_ESTATE, "seed_set_profile", "a drafted batch is not verified");
+  ctx->profile = on != 0;
   return SEED_OK;
 }
 
