@@ -212,15 +212,14 @@ struct seed_ctx_s {
     double gemm_bytes = 0;
     int64_t gemms = 0, kernels = 0;
   };
-  std::map<int64_t, PhaseGraph> draft_graphs, verify_graphs;
+  std::map<int64_t, PhaseGraph> round_graphs;   // draft + verify of a round, one graph (R23)
+  bool draft_deferred = false;                   // seed_draft_round planned a round, not launched
   // profiling: per-GEMM globaltimer records accumulated on the device
   bool profile = false, in_round = false;
   unsigned long long *timing_rec = nullptr, *timing_acc = nullptr, *timing_last = nullptr;
   unsigned long long* cta_rec = nullptr;  // SEED_CTA_TRACE=1: [rec_cap][kCtaRec] per-CTA phases
   int last_draft_recs = 0, last_verify_recs = 0;
   std::map<int, int> draft_recs;  // records of the draft phase per batch size
-  double draft_gemm_bytes = 0;
-  int64_t draft_gemms = 0;
   int rec_cap = 0, rec_used = 0;
   double round_gemm_bytes = 0, gemm_bytes = 0;
   int64_t round_gemms = 0, gemm_launches = 0, kernel_launches = 0;
@@ -889,14 +888,33 @@ seed_status run_phase(seed_ctx ctx, int n, bool draft, cudaStream_t st) {
     }
     return SEED_OK;
   }
-  // profiled launches carry timing pointers: a separate graph per profiling state
+  // With graphs the draft phase is not launched on its own: seed_verify launches one graph holding
+  // the draft and verify phases of the round, so PDL overlaps their boundary too (R23: keyed by
+  // batch size, both phases' attention chunk counts and the profiling state).
+  if (draft) {
+    ctx->draft_deferred = true;
+    ctx->in_round = false;
+    return SEED_OK;
+  }
+  if (!ctx->draft_deferred) return fail(ctx, SEED_ESTATE, "seed_verify", "batch was not drafted");
+  ctx->draft_deferred = false;
   const int64_t pbit = ctx->profile ? (int64_t)1 << 62 : 0;
-  auto& G = draft ? ctx->draft_graphs[ctx->plan.key_draft | pbit] : ctx->verify_graphs[ctx->plan.key_verify | pbit];
+  const int64_t key = ((int64_t)n << 40) | ((ctx->plan.key_draft & 0xFFFFF) << 20) | (ctx->plan.key_verify & 0xFFFFF) | pbit;
+  auto& G = ctx->round_graphs[key];
   cudaGraphExec_t& ex = G.exec;
   if (!ex) {
     cudaGraph_t graph;
     CK(cudaStreamBeginCapture(ctx->gstream, cudaStreamCaptureModeThreadLocal));
-    s = draft ? enqueue_draft(ctx, ctx->gstream) : enqueue_verify(ctx, ctx->gstream);
+    ctx->in_round = true;
+    ctx->rec_used = 0;
+    ctx->round_gemm_bytes = 0;
+    ctx->round_gemms = 0;
+    s = enqueue_draft(ctx, ctx->gstream);
+    if (s == SEED_OK) {
+      ctx->draft_recs[n] = ctx->rec_used;
+      ctx->rec_used = ctx->rec_cap / 2;
+      s = enqueue_verify(ctx, ctx->gstream);
+    }
     cudaError_t e = cudaStreamEndCapture(ctx->gstream, &graph);
     if (s != SEED_OK) return s;
     CK(e);
@@ -905,21 +923,15 @@ seed_status run_phase(seed_ctx ctx, int n, bool draft, cudaStream_t st) {
     G.kernels = ctx->kernel_launches - k0;
     G.gemm_bytes = ctx->round_gemm_bytes;
     G.gemms = ctx->round_gemms;
-    if (draft) ctx->draft_recs[n] = ctx->rec_used;
   }
   CK(cudaEventRecord(ctx->ev_in, st));
   CK(cudaStreamWaitEvent(ctx->gstream, ctx->ev_in, 0));
   CK(cudaGraphLaunch(ex, ctx->gstream));
   ctx->kernel_launches = k0 + G.kernels;
-  if (draft) {
-    ctx->draft_gemm_bytes = G.gemm_bytes;
-    ctx->draft_gemms = G.gemms;
-  } else {
-    CK(cudaEventRecord(ctx->round_done, ctx->gstream));
-    ctx->gemm_bytes += ctx->draft_gemm_bytes + G.gemm_bytes;
-    ctx->gemm_launches += ctx->draft_gemms + G.gemms;
-    ctx->in_round = false;
-  }
+  CK(cudaEventRecord(ctx->round_done, ctx->gstream));
+  ctx->gemm_bytes += G.gemm_bytes;
+  ctx->gemm_launches += G.gemms;
+  ctx->in_round = false;
   CK(cudaEventRecord(ctx->ev_out, ctx->gstream));
   CK(cudaStreamWaitEvent(st, ctx->ev_out, 0));
   return SEED_OK;
@@ -1076,7 +1088,7 @@ void seed_destroy(seed_ctx ctx) {
   if (ctx->tok_host) cudaFreeHost(ctx->tok_host);
   ctx->arena.destroy();
   if (ctx->round_done) cudaEventDestroy(ctx->round_done);
-  for (auto* gm : {&ctx->draft_graphs, &ctx->verify_graphs})
+  for (auto* gm : {&ctx->round_graphs})
     for (auto& kv : *gm)
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
