@@ -336,6 +336,17 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
       const bool whole = (u == t * a.KB) && (seg_end == (t + 1) * a.KB);
       const int acc = seg % nacc;
       const uint32_t use = (uint32_t)(seg / nacc);
+      // a whole tile's residual rows and norm weight (ymode 1) do not depend on the accumulator:
+      // load them while it is computed
+      float xw[16];
+      float ww = 0.f;
+      const bool pre_whole = whole && a.ymode == 1 && a.m_pad == 16;
+      if (pre_whole) {
+        const int n = (int)t * BLOCK_N + nl;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) xw[i] = (i < a.M && n < a.N) ? a.Y[(size_t)i * a.ldY + n] : 0.f;
+        ww = n < a.N ? bf2f(a.nw[n]) : 0.f;
+      }
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
       if (ct && et == 0 && seg == 0) ct[5] = globaltimer();
@@ -348,7 +359,7 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
         for (int col = 0; col < a.m_pad; col += 16) {
           float v[16];
           tmem_ld16(row_addr + col, v);
-          finish16(a, col, (int)t, nl, v, ew, lane, inv_s, red_s, xch_s);
+          finish16(a, col, (int)t, nl, v, ew, lane, inv_s, red_s, xch_s, pre_whole ? xw : nullptr, ww);
         }
       } else if (!reducer) {
         float4* out = reinterpret_cast<float4*>(
