@@ -182,3 +182,37 @@ def test_toy_rounds_vs_oracle(pkg, T, bonus):
             pos += len(rec.emitted)
     assert exact >= 1
     eng.close()
+
+
+_MERGE_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, '.')
+import seedgen, paper_2406_18200_b200 as pkg
+ds = seedgen.SHAPES['llama_68m']
+ts = dict(seedgen.SHAPES['llama2_7b'], n_layers=1)
+dW, tW = seedgen.model_weights(ds, seedgen.DRAFT_SEED), seedgen.model_weights(ts, seedgen.TARGET_SEED)
+cu = lambda W: {'embed': W['embed'].cuda(), 'final_norm': W['final_norm'].cuda(), 'lm_head': W['lm_head'].cuda(),
+                'layers': [{k: v.cuda() for k, v in L.items()} for L in W['layers']]}
+eng = pkg.SeedEngine(ds, cu(dW), ts, cu(tW), gamma=4, temperature=1.0, seed=seedgen.PHILOX_SEED, max_new=8,
+                     max_streams=1, max_batch=1, max_ctx=1200)
+toks = np.random.default_rng(11).integers(3, ts['vocab'], size=700).tolist()   # 6 chunks of 128 keys
+np.save(sys.argv[1], eng.forward_logits(1, toks)[-64:].cpu().numpy())
+"""
+
+
+def test_attention_merge_paths_identical(pkg, tmp_path):
+    """R19: the chunk merge through distributed shared memory (thread-block cluster, <= 8 chunks)
+    and through global memory (SEED_ATTN_CLUSTER=0) sum the same values in the same chunk order,
+    so the logits are bit-identical."""
+    import os
+    import subprocess
+    import sys
+    out = {}
+    for flag in ("1", "0"):
+        f = tmp_path / f"z{flag}.npy"
+        env = dict(os.environ, SEED_ATTN_CLUSTER=flag)
+        r = subprocess.run([sys.executable, "-c", _MERGE_SCRIPT, str(f)], env=env, capture_output=True, text=True,
+                           cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[flag] = np.load(f)
+    assert np.array_equal(out["1"], out["0"])
