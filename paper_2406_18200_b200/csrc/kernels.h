@@ -27,6 +27,7 @@ struct KVLayout {
 struct GemmPlan {
   int N, K, KB, tiles, U, G, S;  // S = max segments per CTA
   int maxseg;                    // max partial segments per tile
+  int smem_kb;                   // dynamic shared memory per CTA (ring depth); 0: the default budget
   int* seg;                      // device [tiles][maxseg + 1]: count, then segment ids in CTA order
   int* counters;                 // device [tiles]: split-K tickets (zero between launches)
   CUtensorMap tmW;
