@@ -502,17 +502,17 @@ void gemm_plan(GemmPlan* p, const void* W, int N, int K, int min_units) {
   p->G = std::max(1, std::min(kNumSMs, p->U / std::max(1, min_units)));
   p->smem_kb = 0;
   {
-    // Target-size GEMMs (min_units <= 4) pick a grid by tile count (measured at 7B, GSM8K round;
-    // env SEED_GRID_POLICY=0 keeps plain stream-K on one CTA per SM):
-    //  * more tiles than SMs (gate/up, LM head): one CTA per whole tile, two CTAs per SM with
-    //    half the ring each -- no split-K reduction tail (gate/up 33.3 -> 32.2 us, LM head
-    //    42.6 -> 40.6 us);
-    //  * 64..148 tiles (QKV): stream-K over two CTAs per SM -- the QKV CTAs leave room for the
-    //    attention CTAs to become resident early (round -36 us);
+    // Grid by tile count (measured at 7B / 68M, GSM8K round; env SEED_GRID_POLICY=0 keeps plain
+    // stream-K on one CTA per SM):
+    //  * more tiles than SMs (gate/up, both LM heads): one CTA per whole tile, two CTAs per SM
+    //    with half the ring each -- no split-K reduction tail (gate/up 33.3 -> 32.2 us, LM head
+    //    42.6 -> 40.6 us, draft LM head 12 -> 8 us);
+    //  * target-size GEMMs with 64..148 tiles (QKV): stream-K over two CTAs per SM -- the QKV
+    //    CTAs leave room for the attention CTAs to become resident early (round -36 us);
     //  * fewer (O, down): stream-K on one CTA per SM with the deep ring (two per SM was slower).
     const char* e = getenv("SEED_GRID_POLICY");
     const bool on = !(e && e[0] == '0');
-    if (on && min_units <= 4 && p->tiles > kNumSMs && p->tiles <= 2 * kNumSMs) {
+    if (on && p->tiles > kNumSMs && p->tiles <= 2 * kNumSMs) {
       p->G = p->tiles;
       p->smem_kb = 112;   // two CTAs + 1 KB reserved each within 228 KB
     } else if (on && min_units <= 4 && p->tiles >= 64 && p->tiles <= kNumSMs) {
