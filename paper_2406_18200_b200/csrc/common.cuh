@@ -180,6 +180,24 @@ SEED_DEV bool elect_one() {
   return pred != 0;
 }
 
+// ---------------------------------------------------------------- thread-block clusters (raw PTX)
+// every thread of every CTA of the cluster must execute each cluster_sync (aligned form)
+SEED_DEV void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of `p` (this CTA's shared memory) in the CTA of cluster rank `rank`
+SEED_DEV uint32_t dsmem_addr(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+SEED_DEV float4 ld_dsmem_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr) : "memory");
+  return v;
+}
+
 // ---------------------------------------------------------------- host: launches with PDL
 bool pdl_enabled();
 

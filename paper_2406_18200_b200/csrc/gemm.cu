@@ -39,6 +39,7 @@ struct GemmArgs {
   int KB, U, G, S, M, m_pad, stages, N, K, ldY, maxseg;
   int ymode;                   // 0 store Y (x row scale, row map); 1 residual; 2 SwiGLU (see GemmIO)
   int ssq_in_ld;               // row stride of ssq_in
+  int dbg;                     // SEED_EPI_DEBUG experiments (timing only, wrong results): 1 no Y/h stores, 2 no finish, 4 no partial adds
   float eps;
   float* partial;              // split-K partials of tiles shared by several CTAs
   float* Y;                    // fp32 output [M][ldY]; ymode 1: the residual stream (in place)
@@ -90,7 +91,7 @@ __device__ __forceinline__ void finish16(const GemmArgs& a, int m0, int t, int n
       for (int i = 0; i < 16; ++i) row[i] = m0 + i >= a.M ? -1 : (a.yrow ? __ldg(a.yrow + m0 + i) : m0 + i);
 #pragma unroll
       for (int i = 0; i < 16; ++i)
-        if (row[i] >= 0) a.Y[(size_t)row[i] * a.ldY + n] = a.ssq_in ? v[i] * inv_s[m0 + i] : v[i];
+        if (row[i] >= 0 && !(a.dbg & 1)) a.Y[(size_t)row[i] * a.ldY + n] = a.ssq_in ? v[i] * inv_s[m0 + i] : v[i];
     }
     return;
   }
@@ -134,7 +135,8 @@ __device__ __forceinline__ void finish16(const GemmArgs& a, int m0, int t, int n
       for (int i = 0; i < 16; ++i) {
         if (m0 + i >= a.M) break;
         const float g = xch_s[i * 128 + nl], u = xch_s[i * 128 + 64 + nl];
-        a.hout[(size_t)(m0 + i) * (a.N / 2) + j] = f2bf(g / (1.0f + expf(-g)) * u);
+        const __nv_bfloat16 hv = f2bf(g / (1.0f + expf(-g)) * u);
+        if (!(a.dbg & 1)) a.hout[(size_t)(m0 + i) * (a.N / 2) + j] = hv;
       }
     }
   }
@@ -359,6 +361,7 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
         for (int col = 0; col < a.m_pad; col += 16) {
           float v[16];
           tmem_ld16(row_addr + col, v);
+          if (a.dbg & 2) continue;
           finish16(a, col, (int)t, nl, v, ew, lane, inv_s, red_s, xch_s, pre_whole ? xw : nullptr, ww);
         }
       } else if (!reducer) {
@@ -404,7 +407,7 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
         for (int m0 = 0; m0 < a.m_pad; m0 += 16) {
           float v[16];
           tmem_ld16(row_addr + m0, v);
-          add_partials16(a.partial, sl, cnt, a.m_pad, m0, nl, v, id0);
+          if (!(a.dbg & 4)) add_partials16(a.partial, sl, cnt, a.m_pad, m0, nl, v, id0);
           if (ct && et == 0) ct[10] = globaltimer() + (v[0] == 1.2345e-30f ? 1 : 0);   // waits for the loads
           finish16(a, m0, (int)t, nl, v, ew, lane, inv_s, red_s, xch_s, (a.ymode == 1 && m0 == 0) ? xo : nullptr, wn);
           if (ct && et == 0) ct[11] = globaltimer();
@@ -433,6 +436,324 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
   if (a.timing && threadIdx.x == 0) {
     atomicMax(&a.timing[2], globaltimer());
     a.timing[3] = 1;  // record kind: GEMM
+  }
+}
+
+// ============================================================================================
+// K2, cluster split-K form (the default): one thread-block cluster of c CTAs per 128-row weight
+// tile.  CTA rank r streams k-blocks [r KB / c, (r + 1) KB / c) of the tile into its TMEM
+// accumulator; the c partials meet in distributed shared memory, where CTA r sums them in rank
+// order 0 .. c-1 -- c is a function of (N, K) only, so every output element is reduced in the same
+// order whatever the batch (R19) -- and finishes the tile's tokens [r per, (r + 1) per).  c = 1:
+// whole tiles straight from TMEM.  Compared with the stream-K form this replaces the tail (one
+// reducer CTA per tile reading every partial back from L2, then the whole tile's epilogue) by a
+// c-way parallel reduction and epilogue that never leaves the cluster.
+struct SplitArgs {
+  int KB, c, per, M, m_pad, stages, N, K, ldY, ymode, ssq_in_ld, pc, pitch, dbg;
+  float eps;
+  float* Y;
+  const float* ssq_in;
+  const int32_t* yrow;
+  float* ssq_out;
+  const __nv_bfloat16* nw;
+  __nv_bfloat16* hout;
+  unsigned long long* timing;
+  unsigned long long* cta;
+};
+
+// rows m0 .. m0 + 15 below mlim of tile column nl (weight row n = 128 t + nl), v = the reduced
+// accumulator.  ymode 0: store (x 1/rms, row map); 1: residual add, x^2 row sums per warp, bf16
+// operand of the next RMSNorm; 2: SwiGLU -- gate (nl < 64) and up (nl >= 64) meet in shared memory
+// and all 128 threads form 8 rows each of silu(g) * u                                        (B4)
+__device__ __forceinline__ void split_finish16(const SplitArgs& a, int t, int nl, int et, int lane, int m0, int mlim,
+                                               const float* v, const float* inv_s, const int* rowmap_s, float* red_s,
+                                               const float* xo, float w) {
+  const int n = t * BLOCK_N + nl;
+  if (a.ymode == 0) {
+    if (n < a.N && !(a.dbg & 1)) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int m = m0 + i;
+        if (m < mlim) {
+          const int row = a.yrow ? rowmap_s[m] : m;
+          if (row >= 0) a.Y[(size_t)row * a.ldY + n] = a.ssq_in ? v[i] * inv_s[m] : v[i];
+        }
+      }
+    }
+    return;
+  }
+  if (a.ymode == 1) {
+    float sq[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int m = m0 + i;
+      sq[i] = 0.f;
+      if (m < mlim && n < a.N) {
+        const float xn = xo[i] + v[i];
+        a.Y[(size_t)m * a.ldY + n] = xn;
+        sq[i] = xn * xn;
+        a.hout[(size_t)m * a.N + n] = f2bf(xn * w);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) sq[i] = warp_sum(sq[i]);
+    if (lane == 0) {
+      const int ew = et >> 5;
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (m0 + i < mlim) red_s[ew * 256 + m0 + i] = sq[i];
+    }
+    return;
+  }
+  float* xch = red_s;   // [16][128]
+#pragma unroll
+  for (int i = 0; i < 16; ++i) xch[i * 128 + nl] = (m0 + i < mlim) ? v[i] * inv_s[m0 + i] : 0.f;
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  const int j = et & 63, i0 = (et >> 6) * 8;
+  float h[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float g = xch[(i0 + q) * 128 + j], u = xch[(i0 + q) * 128 + 64 + j];
+    h[q] = g * __frcp_rn(1.0f + __expf(-g)) * u;
+  }
+  if (!(a.dbg & 1)) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (m0 + i0 + q < mlim) a.hout[(size_t)(m0 + i0 + q) * (a.N / 2) + t * 64 + j] = f2bf(h[q]);
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(192, 2)
+gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, SplitArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int S = a.stages;
+  const int x_bytes = a.m_pad * BLOCK_K * 2;
+  uint8_t* sW = smem;
+  uint8_t* sX = smem + S * W_TILE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sX + S * x_bytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 2);
+  float* inv_s = reinterpret_cast<float*>(tmem_slot + 4);   // [256] 1/rms per X row (ssq_in)
+  int* rowmap_s = reinterpret_cast<int*>(inv_s + 256);      // [256] output row map (yrow)
+  float* red_s = reinterpret_cast<float*>(rowmap_s + 256);  // [4][256] x^2 row sums | [16][128] gate/up
+  float* part_s = reinterpret_cast<float*>(smem);           // [128][pitch] accumulator dump (aliases the ring)
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x, t = blockIdx.y, c = a.c;
+  const int kb0 = (int)((long)r * a.KB / c), kb1 = (int)((long)(r + 1) * a.KB / c);
+  const int nk = kb1 - kb0;
+  pdl_trigger();
+  if (a.timing && threadIdx.x == 0) atomicMin(&a.timing[0], globaltimer());
+  unsigned long long* ct = a.cta ? a.cta + (size_t)(t * c + r) * 16 : nullptr;
+  if (ct && threadIdx.x == 0) ct[0] = globaltimer();
+
+  uint32_t cols = 32;
+  while (cols < (uint32_t)a.m_pad) cols <<= 1;
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmW);
+    prefetch_tmap(&tmX);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(&tfull[0], 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int mcols = (a.M + 15) / 16 * 16;               // accumulator columns holding real rows
+  const int npass = c > 1 ? (mcols + a.pc - 1) / a.pc : 0;
+
+  if (warp == 0) {
+    // ---------------- producer (one lane): weight + X k-blocks by TMA; the weights of the first
+    // ring fill are requested before the PDL wait (they do not depend on the predecessor)
+    if (lane == 0) {
+      const uint64_t pol_w = l2_policy_evict_first();
+      const uint64_t pol_x = l2_policy_evict_last();
+      const uint32_t tx = W_TILE_BYTES + x_bytes;
+      const int n_pre = min(S, nk);
+      for (int i = 0; i < n_pre; ++i) {
+        mbar_arrive_expect_tx(&full[i], tx);
+        tma_load_2d(sW + i * W_TILE_BYTES, &tmW, &full[i], (kb0 + i) * BLOCK_K, t * BLOCK_N, pol_w);
+      }
+      pdl_wait();
+      if (a.timing) atomicMin(&a.timing[1], globaltimer());
+      if (ct) ct[1] = globaltimer();
+      for (int i = 0; i < n_pre; ++i)
+        tma_load_2d(sX + i * x_bytes, &tmX, &full[i], (kb0 + i) * BLOCK_K, 0, pol_x);
+      int stage = n_pre % S;
+      uint32_t phase = n_pre == S ? 1u : 0u;
+      for (int k = n_pre; k < nk; ++k) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&full[stage], tx);
+        tma_load_2d(sW + stage * W_TILE_BYTES, &tmW, &full[stage], (kb0 + k) * BLOCK_K, t * BLOCK_N, pol_w);
+        tma_load_2d(sX + stage * x_bytes, &tmX, &full[stage], (kb0 + k) * BLOCK_K, 0, pol_x);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (ct) ct[2] = globaltimer();
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one elected lane)
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(a.m_pad >> 3) << 17) |
+                           ((uint32_t)(BLOCK_N >> 4) << 24);
+    const uint32_t sW0 = smem_u32(sW), sX0 = smem_u32(sX);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int k = 0; k < nk; ++k) {
+      mbar_wait(&full[stage], phase);
+      tc_fence_after();
+      if (ct && k == 0 && lane == 0) ct[3] = globaltimer();
+      if (elect_one()) {
+        const uint32_t wa = sW0 + stage * W_TILE_BYTES, xa = sX0 + stage * x_bytes;
+#pragma unroll
+        for (int kk = 0; kk < BLOCK_K / 16; ++kk)
+          umma_bf16(tmem_base, sw128_desc(wa + kk * 32), sw128_desc(xa + kk * 32), idesc,
+                    (k > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&empty[stage]);
+        if (k == nk - 1) umma_commit(&tfull[0]);
+      }
+      __syncwarp();
+      if (++stage == S) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    if (ct && lane == 0) ct[4] = globaltimer();
+  } else {
+    // ---------------- epilogue warps 2..5: thread = weight row nl of the tile (TMEM lane)
+    const int lane_grp = warp & 3;
+    const int nl = lane_grp * 32 + lane;
+    const int n = t * BLOCK_N + nl;
+    const int et = threadIdx.x - 64;
+    const int m_lo = c > 1 ? min(a.M, r * a.per) : 0;
+    const int m_hi = c > 1 ? min(a.M, (r + 1) * a.per) : a.M;
+    pdl_wait();   // ssq_in, the residual and the row map are written by predecessors
+    // what does not depend on the accumulator is loaded while it is computed
+    if (a.ssq_in) {
+      const int kt = (a.K + 127) / 128;
+      for (int m = m_lo + et; m < m_hi; m += 128) {
+        float ss = 0.f;
+        for (int i = 0; i < kt; ++i) ss += __ldcg(a.ssq_in + (size_t)i * a.ssq_in_ld + m);
+        inv_s[m] = 1.0f / sqrtf(ss / (float)a.K + a.eps);
+      }
+    }
+    if (a.yrow)
+      for (int m = m_lo + et; m < m_hi; m += 128) rowmap_s[m] = __ldg(a.yrow + m);
+    const bool res = a.ymode == 1;
+    const float w = (res && n < a.N) ? bf2f(a.nw[n]) : 0.f;
+    float xo[16], xn[16];
+    auto load_res = [&](int m0, float* dst) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        dst[i] = (m0 + i < m_hi && n < a.N) ? a.Y[(size_t)(m0 + i) * a.ldY + n] : 0.f;
+    };
+    if (res) load_res(m_lo, xo);
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    mbar_wait(&tfull[0], 0);
+    tc_fence_after();
+    if (ct && et == 0) ct[5] = globaltimer();
+    const uint32_t row_addr = tmem_base + ((uint32_t)(lane_grp * 32) << 16);
+    if (c == 1) {
+      for (int m0 = 0; m0 < a.M; m0 += 16) {
+        float v[16];
+        tmem_ld16(row_addr + m0, v);
+        if (a.dbg & 2) continue;
+        if (res && m0 + 16 < a.M) load_res(m0 + 16, xn);
+        split_finish16(a, t, nl, et, lane, m0, min(m0 + 16, a.M), v, inv_s, rowmap_s, red_s, xo, w);
+        if (res) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) xo[i] = xn[i];
+        }
+      }
+    } else {
+      for (int pass = 0; pass < npass; ++pass) {
+        const int pb = pass * a.pc, pe = min(pb + a.pc, mcols);
+        // this CTA's partial -> its shared memory [nl][col - pb] (row pitch = pc + 4 floats:
+        // 16-byte accesses of 8 consecutive threads hit distinct banks)
+        for (int col = pb; col < pe; col += 16) {
+          float v[16];
+          tmem_ld16(row_addr + col, v);
+          float4* dst = reinterpret_cast<float4*>(part_s + (size_t)nl * a.pitch + (col - pb));
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        }
+        if (ct && et == 0) ct[8] = globaltimer();
+        cluster_sync();   // every rank's partial is visible cluster-wide
+        if (ct && et == 0) ct[9] = globaltimer();
+        const int lo = max(m_lo, pb), hi = min(m_hi, pe);
+        if (res && lo != m_lo && lo < hi) load_res(lo, xo);
+        for (int m0 = lo; m0 < hi; m0 += 16) {
+          const int nq = (min(16, hi - m0) + 3) / 4;
+          float v[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+          const float* src = part_s + (size_t)nl * a.pitch + (m0 - pb);
+          // ranks in order 0 .. c-1 (R19); the loads of four ranks in flight at a time
+          for (int s0 = 0; s0 < c; s0 += 4) {
+            float4 q[4][4];
+#pragma unroll
+            for (int ss = 0; ss < 4; ++ss)
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                q[ss][j] = (s0 + ss < c && j < nq) ? ld_dsmem_f4(dsmem_addr(src + 4 * j, (uint32_t)(s0 + ss)))
+                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (!(a.dbg & 4) || s0 == 0) {
+#pragma unroll
+              for (int ss = 0; ss < 4; ++ss) {
+                if (s0 + ss >= c) break;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  v[4 * j] += q[ss][j].x;
+                  v[4 * j + 1] += q[ss][j].y;
+                  v[4 * j + 2] += q[ss][j].z;
+                  v[4 * j + 3] += q[ss][j].w;
+                }
+              }
+            }
+          }
+          if (ct && et == 0) ct[10] = globaltimer() + (v[0] == 1.2345e-30f ? 1 : 0);
+          if (a.dbg & 2) continue;
+          if (res && m0 + 16 < hi) load_res(m0 + 16, xn);
+          split_finish16(a, t, nl, et, lane, m0, min(m0 + 16, hi), v, inv_s, rowmap_s, red_s, xo, w);
+          if (res) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) xo[i] = xn[i];
+          }
+        }
+        cluster_sync();   // peers finished reading this CTA's partial
+      }
+    }
+    if (res) {
+      // per-tile sums of squares of the updated residual rows, warps in a fixed order
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      for (int m = m_lo + et; m < m_hi; m += 128)
+        a.ssq_out[(size_t)t * a.M + m] = ((red_s[m] + red_s[256 + m]) + red_s[512 + m]) + red_s[768 + m];
+    }
+    if (ct && et == 0) ct[6] = globaltimer();
+  }
+  if (warp < 2)
+    for (int p = 0; p < npass; ++p) {
+      cluster_sync();
+      cluster_sync();
+    }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem_base, cols);
+  if (ct && threadIdx.x == 0) ct[7] = globaltimer();
+  if (a.timing && threadIdx.x == 0) {
+    atomicMax(&a.timing[2], globaltimer());
+    a.timing[3] = 1;
   }
 }
 
@@ -519,6 +840,20 @@ void gemm_plan(GemmPlan* p, const void* W, int N, int K, int min_units) {
       p->G = std::min(2 * kNumSMs, p->U / min_units);
       p->smem_kb = 112;
     }
+  }
+  // cluster split-K form: c CTAs per tile, c a function of (N, K) only (R19).  Enough clusters to
+  // fill two CTAs per SM, at most 8 (portable cluster), at least min_units k-blocks per CTA; more
+  // tiles than SMs: whole tiles.  Env SEED_SPLIT_C caps c (experiments).
+  {
+    int c = 1;
+    if (p->tiles < kNumSMs) c = std::min(8, (2 * kNumSMs) / p->tiles);
+    c = std::min(c, std::max(1, p->KB / std::max(1, min_units)));
+    const char* e = getenv("SEED_SPLIT_C");
+    if (e && atoi(e) > 0) c = std::min(c, atoi(e));
+    p->c = std::max(1, c);
+    p->split_smem_kb = p->tiles * p->c <= kNumSMs ? 180 : 112;
+    const char* k = getenv("SEED_GEMM_SPLIT");
+    p->split = !(k && k[0] == '0');
   }
   // segments per CTA: ceil(range / KB) + 1 bound
   const int range = (p->U + p->G - 1) / p->G;
@@ -622,10 +957,62 @@ cudaError_t gemm_run(const GemmPlan& p, int M, const GemmIO& io, float* partial,
   a.hout = io.hout;
   a.timing = timing;
   a.cta = cta;
+  static int dbg = -1;
+  if (dbg < 0) {
+    const char* e = getenv("SEED_EPI_DEBUG");
+    dbg = e ? atoi(e) : 0;
+  }
+  a.dbg = dbg;
   if (!io.tmX) return cudaErrorInvalidValue;
   if (io.ymode == 1 && (!io.Y || !io.ssq_out || !io.nw || !io.hout)) return cudaErrorInvalidValue;
   if (io.ymode == 2 && (!io.ssq_in || !io.hout || p.N % BLOCK_N)) return cudaErrorInvalidValue;
   if (io.ymode == 0 && !io.Y) return cudaErrorInvalidValue;
+  if (p.split) {
+    SplitArgs b{};
+    b.KB = p.KB;
+    b.c = p.c;
+    b.M = M;
+    b.m_pad = a.m_pad;
+    b.per = (a.m_pad / 4 + p.c - 1) / p.c * 4;
+    b.N = p.N;
+    b.K = p.K;
+    b.ldY = io.ldY;
+    b.ymode = io.ymode;
+    b.ssq_in_ld = io.ssq_in_ld;
+    b.pc = std::min(a.m_pad, 128);
+    b.pitch = b.pc + 4;
+    b.dbg = a.dbg;
+    b.eps = io.eps;
+    b.Y = io.Y;
+    b.ssq_in = io.ssq_in;
+    b.yrow = io.yrow;
+    b.ssq_out = io.ssq_out;
+    b.nw = io.nw;
+    b.hout = io.hout;
+    b.timing = timing;
+    b.cta = cta;
+    const int stage_bytes = W_TILE_BYTES + a.m_pad * BLOCK_K * 2;
+    const int extra = (256 + 256 + 2048) * 4 + 64;   // inv_s, rowmap_s, red_s | xch, barriers
+    const char* e = getenv("SEED_SPLIT_SMEM_KB");
+    const int budget = (e ? atoi(e) : p.split_smem_kb) * 1024;
+    int stages = (budget - 1024 - extra - 16 * 16) / stage_bytes;
+    if (stages > MAX_STAGES) stages = MAX_STAGES;
+    // the accumulator dump (c > 1) aliases the ring
+    while (p.c > 1 && stages * stage_bytes < 128 * b.pitch * 4) ++stages;
+    if (stages < 2) stages = 2;
+    b.stages = stages;
+    const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 2) * 8 + 16 + extra;
+    static bool sattr = false;
+    if (!sattr) {
+      cudaFuncSetAttribute(gemm_splitk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      if (cudaFuncSetAttribute(gemm_splitk_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+        cudaGetLastError();
+      sattr = true;
+    }
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    return launch_clustered(gemm_splitk_kernel, dim3(p.c, p.tiles), dim3(192), smem, st, dim3(p.c, 1, 1), p.tmW,
+                            *io.tmX, b);
+  }
   const int stage_bytes = W_TILE_BYTES + a.m_pad * BLOCK_K * 2;
   const int extra = (256 + 2048 + 8) * 4;   // inv_s, red_s | xch_s, flags
   int stages = ((p.smem_kb > 0 ? p.smem_kb * 1024 : smem_budget()) - 1024 - 256 - extra) / stage_bytes;

@@ -28,6 +28,9 @@ struct GemmPlan {
   int N, K, KB, tiles, U, G, S;  // S = max segments per CTA
   int maxseg;                    // max partial segments per tile
   int smem_kb;                   // dynamic shared memory per CTA (ring depth); 0: the default budget
+  int c;                         // cluster split-K: CTAs (k-ranges) per tile, a function of (N, K)
+  int split_smem_kb;             // cluster split-K: dynamic shared memory per CTA
+  bool split;                    // launch the cluster split-K form (env SEED_GEMM_SPLIT=0: stream-K)
   int* seg;                      // device [tiles][maxseg + 1]: count, then segment ids in CTA order
   int* counters;                 // device [tiles]: split-K tickets (zero between launches)
   CUtensorMap tmW;

@@ -89,7 +89,7 @@ if os.environ.get("SEED_CTA_TRACE") == "1":
           "ticket", "reduced", "finished", "ring_used", "first_refill"]
     for want in ["t.L1.qkv", "t.L1.o", "t.L1.gu", "t.L1.down", "t.lm", "d1.L0.gu", "d1.L0.down", "d1.L0.o"]:
         i = names.index(want)
-        ct = eng.gemm_cta_trace(i)[:148 * 16].reshape(148, 16)
+        ct = eng.gemm_cta_trace(i)[:512 * 16].reshape(512, 16)
         rel = tr[i, 1]
         used = ct[:, 7] >= tr[i, 0]
         ct = ct[used]
