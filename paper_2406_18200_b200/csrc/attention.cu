@@ -439,20 +439,32 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
     stamp(4);
     for (int e = tid + split * NT; e < nr * (DH / 4); e += NT * nsplit) {
       const int r = e / (DH / 4), d = (e % (DH / 4)) * 4;
+      // every rank's (max, sum, o) loaded at once (one DSMEM round trip), then merged in rank order
+      float msv[8], lsv[8];
+      float4 ov[8];
+#pragma unroll
+      for (int sp = 0; sp < 8; ++sp) {
+        if (sp < nsplit) {
+          msv[sp] = *cluster.map_shared_rank(cm + r, sp);
+          lsv[sp] = *cluster.map_shared_rank(cl + r, sp);
+          ov[sp] = *reinterpret_cast<const float4*>(cluster.map_shared_rank(own + r * DH + d, sp));
+        }
+      }
       float mx = -INFINITY;
-      for (int sp = 0; sp < nsplit; ++sp) mx = fmaxf(mx, *cluster.map_shared_rank(cm + r, sp));
+#pragma unroll
+      for (int sp = 0; sp < 8; ++sp)
+        if (sp < nsplit) mx = fmaxf(mx, msv[sp]);
       float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
       float l = 0.f;
-      for (int sp = 0; sp < nsplit; ++sp) {
-        const float ms = *cluster.map_shared_rank(cm + r, sp);
-        if (ms == -INFINITY) continue;
-        const float f = exp2_approx(ms - mx);
-        const float4 v = *reinterpret_cast<const float4*>(cluster.map_shared_rank(own + r * DH + d, sp));
-        o.x += v.x * f;
-        o.y += v.y * f;
-        o.z += v.z * f;
-        o.w += v.w * f;
-        l += *cluster.map_shared_rank(cl + r, sp) * f;
+#pragma unroll
+      for (int sp = 0; sp < 8; ++sp) {
+        if (sp >= nsplit || msv[sp] == -INFINITY) continue;
+        const float f = exp2_approx(msv[sp] - mx);
+        o.x += ov[sp].x * f;
+        o.y += ov[sp].y * f;
+        o.z += ov[sp].z * f;
+        o.w += ov[sp].w * f;
+        l += lsv[sp] * f;
       }
       const size_t row = ws_row + r;
       *reinterpret_cast<uint2*>(out + (row * H + head) * DH + d) =

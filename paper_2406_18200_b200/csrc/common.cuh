@@ -180,16 +180,37 @@ SEED_DEV bool elect_one() {
   return pred != 0;
 }
 
+// 1D bulk async copy shared -> global (TMA non-tensor), tracked by this thread's bulk groups;
+// bytes % 16 == 0, both addresses 16-byte aligned
+SEED_DEV void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+SEED_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// at most one committed group of this thread may still be reading shared memory
+SEED_DEV void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+// every committed group of this thread has completed (its global writes performed)
+SEED_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // ---------------------------------------------------------------- thread-block clusters (raw PTX)
 // every thread of every CTA of the cluster must execute each cluster_sync (aligned form)
 SEED_DEV void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// execution-only cluster barrier (no memory ordering beyond the wait's acquire)
+SEED_DEV void cluster_sync_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
 }
 // shared::cluster address of `p` (this CTA's shared memory) in the CTA of cluster rank `rank`
 SEED_DEV uint32_t dsmem_addr(const void* p, uint32_t rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
+}
+SEED_DEV void st_dsmem_f4(uint32_t addr, float4 v) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
 }
 SEED_DEV float4 ld_dsmem_f4(uint32_t addr) {
   float4 v;

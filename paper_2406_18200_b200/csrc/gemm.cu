@@ -462,38 +462,41 @@ struct SplitArgs {
 };
 
 // rows m0 .. m0 + 15 below mlim of tile column nl (weight row n = 128 t + nl), v = the reduced
-// accumulator.  ymode 0: store (x 1/rms, row map); 1: residual add, x^2 row sums per warp, bf16
-// operand of the next RMSNorm; 2: SwiGLU -- gate (nl < 64) and up (nl >= 64) meet in shared memory
-// and all 128 threads form 8 rows each of silu(g) * u                                        (B4)
+// accumulator.  The finished rows are staged in shared memory (`stg`, one of two 12 KB buffers
+// used alternately, so one barrier per chunk suffices) and leave as coalesced 16-byte stores, a
+// warp per 512-byte row segment.  ymode 0: store (x 1/rms, row map); 1: residual add, x^2 row
+// sums per warp, bf16 operand of the next RMSNorm; 2: SwiGLU -- gate (nl < 64) and up (nl >= 64)
+// meet in shared memory and all 128 threads form 8 rows each of silu(g) * u               (B4)
+__host__ __device__ __forceinline__ int c_dump_bytes(const SplitArgs& a) { return a.c > 1 ? a.c * 128 * a.pitch * 4 : 0; }
+
+SEED_DEV float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ void split_finish16(const SplitArgs& a, int t, int nl, int et, int lane, int m0, int mlim,
                                                const float* v, const float* inv_s, const int* rowmap_s, float* red_s,
-                                               const float* xo, float w) {
+                                               const float* xo, float w, uint8_t* stg,
+                                               unsigned long long* pr = nullptr) {
   const int n = t * BLOCK_N + nl;
+  const long long c0 = clock64();
+  float* sf = reinterpret_cast<float*>(stg);                       // [16][128] fp32 rows
+  __nv_bfloat16* sh = reinterpret_cast<__nv_bfloat16*>(stg + 8192); // [16][128] | [16][64] bf16 rows
   if (a.ymode == 0) {
-    if (n < a.N && !(a.dbg & 1)) {
+    float sc[16];   // every load before the first store (no load-after-store chains)
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int m = m0 + i;
-        if (m < mlim) {
-          const int row = a.yrow ? rowmap_s[m] : m;
-          if (row >= 0) a.Y[(size_t)row * a.ldY + n] = a.ssq_in ? v[i] * inv_s[m] : v[i];
-        }
-      }
-    }
-    return;
-  }
-  if (a.ymode == 1) {
+    for (int i = 0; i < 16; ++i) sc[i] = a.ssq_in ? inv_s[min(m0 + i, 255)] : 1.0f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) sf[i * 128 + nl] = a.ssq_in ? v[i] * sc[i] : v[i];
+  } else if (a.ymode == 1) {
     float sq[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const int m = m0 + i;
-      sq[i] = 0.f;
-      if (m < mlim && n < a.N) {
-        const float xn = xo[i] + v[i];
-        a.Y[(size_t)m * a.ldY + n] = xn;
-        sq[i] = xn * xn;
-        a.hout[(size_t)m * a.N + n] = f2bf(xn * w);
-      }
+      const float xn = xo[i] + v[i];
+      sf[i * 128 + nl] = xn;
+      sh[i * 128 + nl] = f2bf(xn * w);
+      sq[i] = (m0 + i < mlim && n < a.N) ? xn * xn : 0.f;
     }
 #pragma unroll
     for (int i = 0; i < 16; ++i) sq[i] = warp_sum(sq[i]);
@@ -503,31 +506,76 @@ __device__ __forceinline__ void split_finish16(const SplitArgs& a, int t, int nl
       for (int i = 0; i < 16; ++i)
         if (m0 + i < mlim) red_s[ew * 256 + m0 + i] = sq[i];
     }
-    return;
-  }
-  float* xch = red_s;   // [16][128]
+  } else {
+    float* xch = red_s;   // [16][128]
+    float sc[16];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) xch[i * 128 + nl] = (m0 + i < mlim) ? v[i] * inv_s[m0 + i] : 0.f;
+    for (int i = 0; i < 16; ++i) sc[i] = inv_s[min(m0 + i, 255)];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) xch[i * 128 + nl] = v[i] * sc[i];
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    const int j = et & 63, i0 = (et >> 6) * 8;
+    float g[8], u[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      g[q] = xch[(i0 + q) * 128 + j];
+      u[q] = xch[(i0 + q) * 128 + 64 + j];
+    }
+    // silu(g) u = g u / (1 + e^-g) on the SFU (ex2 / rcp approx; the product is rounded to bf16, B4)
+    __nv_bfloat16 hb[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) hb[q] = f2bf(g[q] * rcp_approx(1.0f + __expf(-g[q])) * u[q]);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) sh[(i0 + q) * 64 + j] = hb[q];
+  }
+  const long long c1 = clock64();
   asm volatile("bar.sync 1, 128;" ::: "memory");
-  const int j = et & 63, i0 = (et >> 6) * 8;
-  float h[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const float g = xch[(i0 + q) * 128 + j], u = xch[(i0 + q) * 128 + 64 + j];
-    h[q] = g * __frcp_rn(1.0f + __expf(-g)) * u;
-  }
+  const long long c2 = clock64();
   if (!(a.dbg & 1)) {
+    const int ncols = min(BLOCK_N, a.N - t * BLOCK_N);
+    if (a.ymode != 2) {
+      // fp32 rows: 16 x 32 float4, a warp per row
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
-      if (m0 + i0 + q < mlim) a.hout[(size_t)(m0 + i0 + q) * (a.N / 2) + t * 64 + j] = f2bf(h[q]);
+      for (int k = 0; k < 4; ++k) {
+        const int q = et + 128 * k, i = q >> 5, c4 = (q & 31) * 4, m = m0 + i;
+        if (m < mlim && c4 < ncols) {
+          const int row = a.ymode == 0 && a.yrow ? rowmap_s[m] : m;
+          if (row >= 0)
+            *reinterpret_cast<float4*>(a.Y + (size_t)row * a.ldY + t * BLOCK_N + c4) =
+                *reinterpret_cast<const float4*>(sf + i * 128 + c4);
+        }
+      }
+    }
+    if (a.ymode == 1) {
+      // bf16 rows: 16 x 16 uint4
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int q = et + 128 * k, i = q >> 4, c8 = (q & 15) * 8, m = m0 + i;
+        if (m < mlim && c8 < ncols)
+          *reinterpret_cast<uint4*>(a.hout + (size_t)m * a.N + t * BLOCK_N + c8) =
+              *reinterpret_cast<const uint4*>(sh + i * 128 + c8);
+      }
+    } else if (a.ymode == 2) {
+      const int i = et >> 3, c8 = (et & 7) * 8, m = m0 + i;
+      if (m < mlim)
+        *reinterpret_cast<uint4*>(a.hout + (size_t)m * (a.N / 2) + t * 64 + c8) =
+            *reinterpret_cast<const uint4*>(sh + i * 64 + c8);
+    }
   }
-  asm volatile("bar.sync 1, 128;" ::: "memory");
+  const long long c3 = clock64();
+  if (pr) {
+    pr[4] = (unsigned long long)(c1 - c0);
+    pr[5] = (unsigned long long)(c2 - c1);
+    pr[6] = (unsigned long long)(c3 - c2);
+  }
 }
 
 __global__ void __launch_bounds__(192, 2)
 gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, SplitArgs a) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte aligned by pointer arithmetic on the shared array (the compiler keeps the shared
+  // state space: ld/st.shared instead of generic accesses)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int S = a.stages;
   const int x_bytes = a.m_pad * BLOCK_K * 2;
   uint8_t* sW = smem;
@@ -540,6 +588,8 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
   int* rowmap_s = reinterpret_cast<int*>(inv_s + 256);      // [256] output row map (yrow)
   float* red_s = reinterpret_cast<float*>(rowmap_s + 256);  // [4][256] x^2 row sums | [16][128] gate/up
   float* part_s = reinterpret_cast<float*>(smem);           // [128][pitch] accumulator dump (aliases the ring)
+  // two 12 KB output staging buffers after the dump (the ring is idle once the accumulator is ready)
+  uint8_t* stg0 = smem + (c_dump_bytes(a) + 1023) / 1024 * 1024;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.x, t = blockIdx.y, c = a.c;
@@ -635,27 +685,29 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
     const int nl = lane_grp * 32 + lane;
     const int n = t * BLOCK_N + nl;
     const int et = threadIdx.x - 64;
-    const int m_lo = c > 1 ? min(a.M, r * a.per) : 0;
-    const int m_hi = c > 1 ? min(a.M, (r + 1) * a.per) : a.M;
+    // rows this CTA finishes first (pass 0 for c > 1); 1/rms and the row map cover every row
+    const int perp0 = c > 1 ? ((min(a.pc, mcols) / 4) + c - 1) / c * 4 : a.M;
+    const int m_lo = c > 1 ? min(a.M, r * perp0) : 0;
+    const int m_hi = c > 1 ? min(a.M, min(min(a.pc, mcols), (r + 1) * perp0)) : a.M;
     pdl_wait();   // ssq_in, the residual and the row map are written by predecessors
     // what does not depend on the accumulator is loaded while it is computed
     if (a.ssq_in) {
       const int kt = (a.K + 127) / 128;
-      for (int m = m_lo + et; m < m_hi; m += 128) {
+      for (int m = et; m < a.M; m += 128) {
         float ss = 0.f;
         for (int i = 0; i < kt; ++i) ss += __ldcg(a.ssq_in + (size_t)i * a.ssq_in_ld + m);
         inv_s[m] = 1.0f / sqrtf(ss / (float)a.K + a.eps);
       }
     }
     if (a.yrow)
-      for (int m = m_lo + et; m < m_hi; m += 128) rowmap_s[m] = __ldg(a.yrow + m);
+      for (int m = et; m < a.M; m += 128) rowmap_s[m] = __ldg(a.yrow + m);
     const bool res = a.ymode == 1;
     const float w = (res && n < a.N) ? bf2f(a.nw[n]) : 0.f;
     float xo[16], xn[16];
     auto load_res = [&](int m0, float* dst) {
 #pragma unroll
       for (int i = 0; i < 16; ++i)
-        dst[i] = (m0 + i < m_hi && n < a.N) ? a.Y[(size_t)(m0 + i) * a.ldY + n] : 0.f;
+        dst[i] = (m0 + i < a.M && n < a.N) ? a.Y[(size_t)(m0 + i) * a.ldY + n] : 0.f;
     };
     if (res) load_res(m_lo, xo);
     asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -663,13 +715,16 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
     tc_fence_after();
     if (ct && et == 0) ct[5] = globaltimer();
     const uint32_t row_addr = tmem_base + ((uint32_t)(lane_grp * 32) << 16);
+    int chunk = 0;
     if (c == 1) {
       for (int m0 = 0; m0 < a.M; m0 += 16) {
         float v[16];
         tmem_ld16(row_addr + m0, v);
         if (a.dbg & 2) continue;
         if (res && m0 + 16 < a.M) load_res(m0 + 16, xn);
-        split_finish16(a, t, nl, et, lane, m0, min(m0 + 16, a.M), v, inv_s, rowmap_s, red_s, xo, w);
+        split_finish16(a, t, nl, et, lane, m0, min(m0 + 16, a.M), v, inv_s, rowmap_s, red_s, xo, w,
+                       stg0 + (chunk++ & 1) * 12288, (ct && et == 0 && m0 == 16) ? ct + 8 : nullptr);
+        if (ct && et == 0 && m0 == 0) ct[11] = globaltimer();
         if (res) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) xo[i] = xn[i];
@@ -678,62 +733,74 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
     } else {
       for (int pass = 0; pass < npass; ++pass) {
         const int pb = pass * a.pc, pe = min(pb + a.pc, mcols);
-        // this CTA's partial -> its shared memory [nl][col - pb] (row pitch = pc + 4 floats:
-        // 16-byte accesses of 8 consecutive threads hit distinct banks)
+        const int perp = ((pe - pb) / 4 + c - 1) / c * 4;   // tokens each rank reduces in this pass
+        // the slots alias the peers' rings: every rank's MMAs have finished reading its ring
+        if (pass == 0) cluster_sync_relaxed();
+        // push: every 4-token group of this CTA's partial goes straight into the shared memory of
+        // the rank that reduces it, slot [my rank][nl] (posted DSMEM stores, no round trips)
         for (int col = pb; col < pe; col += 16) {
           float v[16];
           tmem_ld16(row_addr + col, v);
-          float4* dst = reinterpret_cast<float4*>(part_s + (size_t)nl * a.pitch + (col - pb));
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          for (int j = 0; j < 4; ++j) {
+            const int cc = col + 4 * j - pb, owner = cc / perp;
+            st_dsmem_f4(dsmem_addr(part_s + ((size_t)r * 128 + nl) * a.pitch + (cc - owner * perp), (uint32_t)owner),
+                        make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+          }
         }
         if (ct && et == 0) ct[8] = globaltimer();
-        cluster_sync();   // every rank's partial is visible cluster-wide
+        cluster_sync();   // every rank's slices have landed
         if (ct && et == 0) ct[9] = globaltimer();
-        const int lo = max(m_lo, pb), hi = min(m_hi, pe);
-        if (res && lo != m_lo && lo < hi) load_res(lo, xo);
+        const int lo = min(a.M, pb + r * perp), hi = min(a.M, min(pe, pb + (r + 1) * perp));
+        if (res && pass > 0 && lo < hi) load_res(lo, xo);
         for (int m0 = lo; m0 < hi; m0 += 16) {
-          const int nq = (min(16, hi - m0) + 3) / 4;
           float v[16];
+          const float* src = part_s + (size_t)nl * a.pitch + (m0 - lo);
+          // ranks in order 0 .. c-1 (R19); all loads of the chunk first
+          const int nq = (min(16, hi - m0) + 3) / 4;
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] = 0.f;
-          const float* src = part_s + (size_t)nl * a.pitch + (m0 - pb);
-          // ranks in order 0 .. c-1 (R19); the loads of four ranks in flight at a time
           for (int s0 = 0; s0 < c; s0 += 4) {
             float4 q[4][4];
 #pragma unroll
             for (int ss = 0; ss < 4; ++ss)
 #pragma unroll
               for (int j = 0; j < 4; ++j)
-                q[ss][j] = (s0 + ss < c && j < nq) ? ld_dsmem_f4(dsmem_addr(src + 4 * j, (uint32_t)(s0 + ss)))
-                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-            if (!(a.dbg & 4) || s0 == 0) {
+                q[ss][j] = (s0 + ss < c && j < nq)
+                               ? *reinterpret_cast<const float4*>(src + (size_t)(s0 + ss) * 128 * a.pitch + 4 * j)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-              for (int ss = 0; ss < 4; ++ss) {
-                if (s0 + ss >= c) break;
+            for (int ss = 0; ss < 4; ++ss) {
+              if (s0 + ss >= c) break;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                  v[4 * j] += q[ss][j].x;
-                  v[4 * j + 1] += q[ss][j].y;
-                  v[4 * j + 2] += q[ss][j].z;
-                  v[4 * j + 3] += q[ss][j].w;
-                }
+              for (int j = 0; j < 4; ++j) {
+                v[4 * j] += q[ss][j].x;
+                v[4 * j + 1] += q[ss][j].y;
+                v[4 * j + 2] += q[ss][j].z;
+                v[4 * j + 3] += q[ss][j].w;
               }
             }
           }
           if (ct && et == 0) ct[10] = globaltimer() + (v[0] == 1.2345e-30f ? 1 : 0);
           if (a.dbg & 2) continue;
           if (res && m0 + 16 < hi) load_res(m0 + 16, xn);
-          split_finish16(a, t, nl, et, lane, m0, min(m0 + 16, hi), v, inv_s, rowmap_s, red_s, xo, w);
+          split_finish16(a, t, nl, et, lane, m0, min(m0 + 16, hi), v, inv_s, rowmap_s, red_s, xo, w,
+                         stg0 + (chunk++ & 1) * 12288);
           if (res) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) xo[i] = xn[i];
           }
         }
-        cluster_sync();   // peers finished reading this CTA's partial
+        if (res) {
+          // per-tile sums of squares of this rank's rows, warps in a fixed order
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          for (int m = lo + et; m < hi; m += 128)
+            a.ssq_out[(size_t)t * a.M + m] = ((red_s[m] + red_s[256 + m]) + red_s[512 + m]) + red_s[768 + m];
+        }
+        if (pass + 1 < npass) cluster_sync();   // slots are rewritten by the next pass
       }
     }
-    if (res) {
+    if (res && c == 1) {
       // per-tile sums of squares of the updated residual rows, warps in a fixed order
       asm volatile("bar.sync 1, 128;" ::: "memory");
       for (int m = m_lo + et; m < m_hi; m += 128)
@@ -741,11 +808,10 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
     }
     if (ct && et == 0) ct[6] = globaltimer();
   }
-  if (warp < 2)
-    for (int p = 0; p < npass; ++p) {
-      cluster_sync();
-      cluster_sync();
-    }
+  if (warp < 2 && npass > 0) {
+    cluster_sync_relaxed();
+    for (int p = 0; p < 2 * npass - 1; ++p) cluster_sync();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -813,6 +879,32 @@ bool encode_tmap_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t 
   return r == CUDA_SUCCESS;
 }
 
+// clusters of c gemm_splitk_kernel CTAs (smem_kb each) the device can hold at once
+int split_cluster_capacity(int c, int smem_kb) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_splitk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(c, 1024);
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = (size_t)smem_kb * 1024;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = c;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, gemm_splitk_kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
 void gemm_plan(GemmPlan* p, const void* W, int N, int K, int min_units) {
   p->N = N;
   p->K = K;
@@ -850,10 +942,22 @@ void gemm_plan(GemmPlan* p, const void* W, int N, int K, int min_units) {
     c = std::min(c, std::max(1, p->KB / std::max(1, min_units)));
     const char* e = getenv("SEED_SPLIT_C");
     if (e && atoi(e) > 0) c = std::min(c, atoi(e));
-    p->c = std::max(1, c);
+    c = std::max(1, c);
+    // every cluster of the grid must be resident at once (one wave): a cluster is placed inside
+    // one GPC, so fewer c-CTA clusters fit than SMs / c (measured: 15 clusters of 8 at 2 CTAs per
+    // SM); shrink c until the device reports room for all tiles
+    int smem_kb = 112;
+    for (; c > 1; --c) {
+      smem_kb = p->tiles * c <= kNumSMs ? 180 : 112;
+      if (split_cluster_capacity(c, smem_kb) >= p->tiles) break;
+    }
+    p->c = c;
     p->split_smem_kb = p->tiles * p->c <= kNumSMs ? 180 : 112;
+    if (getenv("SEED_GEMM_VERBOSE"))
+      fprintf(stderr, "[seed] gemm N=%d K=%d tiles=%d c=%d smem=%dKB cluster capacity=%d\n", N, K, p->tiles, p->c,
+              p->split_smem_kb, p->c > 1 ? split_cluster_capacity(p->c, p->split_smem_kb) : -1);
     const char* k = getenv("SEED_GEMM_SPLIT");
-    p->split = !(k && k[0] == '0');
+    p->split = !(k && k[0] == '0') && N % 4 == 0;   // fp32 rows leave by 16-byte stores
   }
   // segments per CTA: ceil(range / KB) + 1 bound
   const int range = (p->U + p->G - 1) / p->G;
@@ -968,6 +1072,8 @@ cudaError_t gemm_run(const GemmPlan& p, int M, const GemmIO& io, float* partial,
   if (io.ymode == 2 && (!io.ssq_in || !io.hout || p.N % BLOCK_N)) return cudaErrorInvalidValue;
   if (io.ymode == 0 && !io.Y) return cudaErrorInvalidValue;
   if (p.split) {
+    // rows leave by 16-byte stores
+    if ((io.ymode == 1 && p.N % 8) || (io.ymode != 2 && io.ldY % 4)) return cudaErrorInvalidValue;
     SplitArgs b{};
     b.KB = p.KB;
     b.c = p.c;
@@ -980,7 +1086,7 @@ cudaError_t gemm_run(const GemmPlan& p, int M, const GemmIO& io, float* partial,
     b.ymode = io.ymode;
     b.ssq_in_ld = io.ssq_in_ld;
     b.pc = std::min(a.m_pad, 128);
-    b.pitch = b.pc + 4;
+    b.pitch = (b.pc / 4 + p.c - 1) / p.c * 4 + 4;   // [rank][128][tokens per rank + 4] slots
     b.dbg = a.dbg;
     b.eps = io.eps;
     b.Y = io.Y;
@@ -997,8 +1103,8 @@ cudaError_t gemm_run(const GemmPlan& p, int M, const GemmIO& io, float* partial,
     const int budget = (e ? atoi(e) : p.split_smem_kb) * 1024;
     int stages = (budget - 1024 - extra - 16 * 16) / stage_bytes;
     if (stages > MAX_STAGES) stages = MAX_STAGES;
-    // the accumulator dump (c > 1) aliases the ring
-    while (p.c > 1 && stages * stage_bytes < 128 * b.pitch * 4) ++stages;
+    // the accumulator dump (c > 1) and the two output staging buffers alias the ring
+    while (stages * stage_bytes < (c_dump_bytes(b) + 1023) / 1024 * 1024 + 2 * 12288) ++stages;
     if (stages < 2) stages = 2;
     b.stages = stages;
     const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 2) * 8 + 16 + extra;

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_ops.py -x -q -m gpu > gpurun_out/gputests.log 2>&1; echo tests=$?
+tail -3 gpurun_out/gputests.log
+export CFG=sweep SEED_CTA_TRACE=1
+timeout 300 python scripts/trace_round.py > gpurun_out/t9_sw.log 2>&1; echo trace=$?
