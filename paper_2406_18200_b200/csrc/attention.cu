@@ -33,17 +33,32 @@ constexpr int QB = 16;                   // query rows per CTA (one m16 MMA tile
 
 template <int DH>
 struct Smem {
-  static constexpr int PITCH = DH + 8;   // bf16 row pitch (16-byte pad: conflict-free ldmatrix)
-  static constexpr size_t Q = 0;                                     // bf16 [16][PITCH]
-  static constexpr size_t K = Q + (size_t)QB * PITCH * 2;            // bf16 [WARPS][32][PITCH]
-  static constexpr size_t V = K + (size_t)WARPS * 32 * PITCH * 2;    // bf16 [WARPS][32][PITCH]
-  static constexpr size_t ML = V + (size_t)WARPS * 32 * PITCH * 2;   // fp32 m, l [2][WARPS][QB], merge
+  static constexpr int PITCH = DH + 8;   // bf16 row pitch of Q (16-byte pad: conflict-free ldmatrix)
+  static constexpr int RB = (DH >= 64 ? 64 : DH) * 2;   // bytes per swizzled K/V row segment (<= 128)
+  static constexpr int OP = DH + 4;      // fp32 row pitch of the warp-merge scratch (conflict-free float2)
+  static constexpr size_t TILE = (size_t)32 * DH * 2;                 // one warp's 32 K (or V) rows
+  static constexpr size_t K = 0;                                      // bf16 [WARPS] tiles, 128B swizzle
+  static constexpr size_t V = K + WARPS * TILE;
+  static constexpr size_t Q = V + WARPS * TILE;                       // bf16 [16][PITCH]
+  static constexpr size_t ML = Q + (size_t)QB * PITCH * 2;           // fp32 m, l [2][WARPS][QB], merge
                                                                      // factors [WARPS][QB], row m, l [2][QB]
   static constexpr size_t TK = ML + (size_t)(3 * WARPS + 2) * QB * 4; // ticket
   static constexpr size_t BAR = TK + 16;                             // mbarrier per warp (K / V tile)
-  static constexpr size_t BYTES = BAR + WARPS * 8;
-  // o merge scratch fp32 [WARPS][QB][DH] aliases K|V after the MMAs
+  static constexpr size_t BYTES = BAR + WARPS * 8 + 1024;            // + alignment of the tiles
+  // o merge scratch fp32 [WARPS][QB][OP] aliases K|V after the MMAs
 };
+
+// K / V tiles hold 32 rows per warp in the TMA swizzle of their row size (RB = 128 B: 16-byte chunk
+// bits [4:6] of the shared address XOR bits [7:9]; RB = 64 B: bits [4:5] XOR bits [7:8]), so page
+// blocks land by one tensor copy each and ldmatrix stays conflict-free.  Byte address of element e
+// of tile row `row` (tile 1024-aligned):
+template <int DH>
+SEED_DEV uint32_t tile_addr(uint32_t tile, int row, int e) {
+  constexpr int RB = Smem<DH>::RB, EH = RB / 2;
+  constexpr uint32_t MASK = RB == 128 ? 0x70u : 0x30u;
+  const uint32_t a = tile + (uint32_t)((e / EH) * 32 * RB + row * RB + (e % EH) * 2);
+  return a ^ ((a >> 3) & MASK);
+}
 
 SEED_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -71,18 +86,106 @@ SEED_DEV uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<const uint32_t*>(&v);
 }
 
+// ---- one warp's 32-key tile (keys kt .. kt + 31 of a chunk ending at c_end): S = Q K^T (two
+// accumulator chains), mask, base-2 softmax -> P in s (rows g, g + 8; lane holds keys 8 nt + 2 t4, +1),
+// the tile's row max and sum.  Shared by the chunk-parallel and the sequential kernel, so a chunk's
+// result is bit-identical in both (R19).
+template <int DH>
+SEED_DEV void warp_scores(const __nv_bfloat16* q_s, uint32_t kb, int kt, int c_end, int nr, int pos0,
+                          float scale, int lane, float (&s)[4][4], float* m_row, float* l_row) {
+  constexpr int P = DH + 8;
+  const int g = lane >> 2, t4 = lane & 3;
+  float s2[4][4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    s[j][0] = s[j][1] = s[j][2] = s[j][3] = s2[j][0] = s2[j][1] = s2[j][2] = s2[j][3] = 0.f;
+  const uint32_t qa = smem_u32(q_s);
+#pragma unroll
+  for (int ks = 0; ks < DH / 16; ++ks) {
+    uint32_t a0, a1, a2, a3;
+    ldsm_x4(qa + ((lane & 15) * P + ks * 16 + (lane >> 4) * 8) * 2, a0, a1, a2, a3);
+    float (*acc)[4] = (ks & 1) ? s2 : s;
+#pragma unroll
+    for (int nt = 0; nt < 4; nt += 2) {
+      uint32_t b0, b1, b2, b3;
+      const int key = nt * 8 + (lane >> 4) * 8 + (lane & 7);
+      ldsm_x4(tile_addr<DH>(kb, key, ks * 16 + ((lane >> 3) & 1) * 8), b0, b1, b2, b3);
+      mma_bf16(acc[nt], a0, a1, a2, a3, b0, b1);
+      mma_bf16(acc[nt + 1], a0, a1, a2, a3, b2, b3);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) s[j][c] += s2[j][c];
+#pragma unroll
+  for (int h2 = 0; h2 < 2; ++h2) {
+    const int r = g + 8 * h2;
+    float mx = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int key = kt + nt * 8 + 2 * t4 + c;
+        const bool ok = r < nr && key < c_end && key <= pos0 + r;
+        float& v = s[nt][2 * h2 + c];
+        v = ok ? v * scale : -INFINITY;
+        mx = fmaxf(mx, v);
+      }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    float sum = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        float& v = s[nt][2 * h2 + c];
+        v = (mx == -INFINITY) ? 0.f : exp2_approx(v - mx);
+        sum += v;
+      }
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+    m_row[h2] = mx;
+    l_row[h2] = sum;
+  }
+}
+
+// ---- O += P V for the tile: P (bf16, B5) re-packed from the score accumulators; V via ldmatrix.trans
+template <int DH>
+SEED_DEV void warp_pv(uint32_t vb, int lane, const float (&s)[4][4], float (*o_acc)[4]) {
+  constexpr int DT = DH / 8;
+#pragma unroll
+  for (int kc = 0; kc < 2; ++kc) {   // keys 16 kc .. 16 kc + 15
+    const uint32_t pa0 = pack_bf16(s[2 * kc][0], s[2 * kc][1]);
+    const uint32_t pa1 = pack_bf16(s[2 * kc][2], s[2 * kc][3]);
+    const uint32_t pa2 = pack_bf16(s[2 * kc + 1][0], s[2 * kc + 1][1]);
+    const uint32_t pa3 = pack_bf16(s[2 * kc + 1][2], s[2 * kc + 1][3]);
+#pragma unroll
+    for (int dt = 0; dt < DT; dt += 2) {
+      uint32_t b0, b1, b2, b3;
+      const int key = kc * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+      const int dim = dt * 8 + (lane >> 4) * 8;
+      ldsm_x4_t(tile_addr<DH>(vb, key, dim), b0, b1, b2, b3);
+      mma_bf16(o_acc[dt], pa0, pa1, pa2, pa3, b0, b1);
+      mma_bf16(o_acc[dt + 1], pa0, pa1, pa2, pa3, b2, b3);
+    }
+  }
+}
+
 template <int DH>
 __global__ void __launch_bounds__(WARPS * 32)
-attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, const float2* __restrict__ rope,
-                  KVLayout kv, int layer, int n_qblk, float scale, AttnWorkspace ws, int M,
-                  __nv_bfloat16* __restrict__ out, int clustered) {
+attn_fused_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __restrict__ qkv, int H, int Hk,
+                  SeqInfo seqs, const float2* __restrict__ rope, KVLayout kv, int layer, int n_qblk, float scale,
+                  AttnWorkspace ws, int M, __nv_bfloat16* __restrict__ out, int clustered) {
   using L = Smem<DH>;
   constexpr int P = L::PITCH;
+  constexpr int OP = L::OP;
   constexpr int HALF = DH / 2;
-  constexpr int VPR = DH / 8;            // 16-byte pieces per row
   constexpr int NT = WARPS * 32;
   constexpr int DT = DH / 8;             // 8-dim n-tiles of the output
-  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int EH = L::RB / 2;          // elements per swizzled row segment (TMA box width)
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __nv_bfloat16* q_s = reinterpret_cast<__nv_bfloat16*>(smem + L::Q);
   __nv_bfloat16* k_s = reinterpret_cast<__nv_bfloat16*>(smem + L::K);
   __nv_bfloat16* v_s = reinterpret_cast<__nv_bfloat16*>(smem + L::V);
@@ -95,6 +198,7 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
   uint64_t* bar_s = reinterpret_cast<uint64_t*>(smem + L::BAR);
 
   if (threadIdx.x == 0) {
+    prefetch_tmap(&tmKV);
     for (int w = 0; w < WARPS; ++w) mbar_init(&bar_s[w], 1);
     fence_barrier_init();
   }
@@ -126,37 +230,34 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
   const size_t ws_row = (size_t)(q0 + r0);
   const int ldq = (H + 2 * Hk) * DH;               // row stride of the QKV GEMM output
   const bool has_keys = active && c_begin < key_end;
-  // ---- cached keys of this warp's tile: one bulk copy (TMA) per K and V row into the padded
-  // tiles, completing on the warp's mbarrier; rows past the chunk are zero.  Rows below `stable`
-  // were written before this round, so they are copied while the predecessor (the QKV GEMM)
-  // still runs; the rest after the dependency wait.
+  // ---- cached keys of this warp's 32-key tile: one 2D tensor copy (TMA) per page block of BR
+  // rows, K and V, each 64-dim half, completing on the warp's mbarrier.  Blocks whose rows were all
+  // written before this round (< `stable`) are requested while the predecessor (the QKV GEMM)
+  // still runs; the rest after the dependency wait.  Rows of a block past the cached keys are
+  // rewritten below (new keys, or zero past the chunk) once the copies landed.
   const int kt = c_begin + warp * 32;
   const int old_end = min(c_end, new_first);
   const int stable = seqs.stable ? min(seqs.stable[seq], old_end) : 0;
-  __nv_bfloat16* kw = k_s + (size_t)warp * 32 * P;
-  __nv_bfloat16* vw = v_s + (size_t)warp * 32 * P;
-  auto copy_rows = [&](int k0, int k1) {   // cached rows with k0 <= key < k1 of this warp's tile
-    const int key = kt + lane;
-    if (key >= k0 && key < k1) {
-      const int page = __ldg(kv.page_table + (size_t)slot * kv.max_pages + key / kv.P);
-      const __nv_bfloat16* src = kv.pool + kv.offset(page, layer, 0, kvh, key % kv.P);
-      bulk_g2s(kw + lane * P, src, DH * 2, &bar_s[warp]);
-      bulk_g2s(vw + lane * P, src + kv.vofs(), DH * 2, &bar_s[warp]);
-    }
-  };
-  if (has_keys) {
-    const int n_old = max(0, min(32, old_end - kt));
-    if (lane == 0) mbar_arrive_expect_tx(&bar_s[warp], (uint32_t)n_old * DH * 2 * 2);
-    __syncwarp();
-    copy_rows(0, stable);
-    const int key = kt + lane;
-    if (key >= c_end) {
+  const int BR = min(kv.P, 32);                    // rows per tensor copy (a page, or 32 of it)
+  const uint32_t kw = smem_u32(k_s) + (uint32_t)(warp * L::TILE);
+  const uint32_t vw = smem_u32(v_s) + (uint32_t)(warp * L::TILE);
+  auto copy_blocks = [&](bool pre) {               // lane 0 of the warp
+    for (int k0 = kt; k0 < kt + 32 && k0 < old_end; k0 += BR) {
+      if ((k0 + BR <= stable) != pre) continue;
+      const int page = __ldg(kv.page_table + (size_t)slot * kv.max_pages + k0 / kv.P);
+      const int row = (((page * kv.n_layers + layer) * 2) * kv.Hk + kvh) * kv.P + (k0 % kv.P);
 #pragma unroll
-      for (int c16 = 0; c16 < VPR; ++c16) {
-        *reinterpret_cast<uint4*>(kw + lane * P + c16 * 8) = make_uint4(0, 0, 0, 0);
-        *reinterpret_cast<uint4*>(vw + lane * P + c16 * 8) = make_uint4(0, 0, 0, 0);
+      for (int h = 0; h < DH / EH; ++h) {
+        const uint32_t o = (uint32_t)(h * 32 * L::RB + (k0 - kt) * L::RB);
+        tma_load_2d_u32(kw + o, &tmKV, &bar_s[warp], h * EH, row);
+        tma_load_2d_u32(vw + o, &tmKV, &bar_s[warp], h * EH, row + kv.Hk * kv.P);
       }
     }
+  };
+  if (has_keys && lane == 0) {
+    const int nblk = old_end > kt ? (min(kt + 32, old_end) - kt + BR - 1) / BR : 0;
+    mbar_arrive_expect_tx(&bar_s[warp], (uint32_t)nblk * BR * DH * 2 * 2);
+    copy_blocks(true);
   }
   pdl_wait();
   if (ws.timing && threadIdx.x == 0) atomicMin(&ws.timing[1], globaltimer_ns());
@@ -179,7 +280,7 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
   for (int j = 0; j < DT; ++j) o_acc[j][0] = o_acc[j][1] = o_acc[j][2] = o_acc[j][3] = 0.f;
 
   if (has_keys) {
-    copy_rows(stable, old_end);
+    if (lane == 0) copy_blocks(false);
     // ---- Q of this block's rows and head: RoPE, bf16 rounding (B2); padding rows are zero.
     // Items of 4 rotation pairs; every load of the loop is issued before the first use.
     {
@@ -210,6 +311,16 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
           *reinterpret_cast<uint2*>(q_s + r * P + i) = make_uint2(pack_bf16(a0, a1), pack_bf16(a2, a3));
           *reinterpret_cast<uint2*>(q_s + r * P + i + HALF) = make_uint2(pack_bf16(b0, b1), pack_bf16(b2, b3));
         }
+      }
+    }
+    // every warp's tensor copies have landed before any thread rewrites rows of the tiles
+    for (int w = 0; w < WARPS; ++w) mbar_wait(&bar_s[w], 0);
+    // ---- rows past the chunk: zero (each lane its own row of its warp's tiles)
+    if (kt + lane >= c_end) {
+#pragma unroll
+      for (int e = 0; e < DH; e += 8) {
+        st_shared_v4(tile_addr<DH>(kw, lane, e), make_uint4(0, 0, 0, 0));
+        st_shared_v4(tile_addr<DH>(vw, lane, e), make_uint4(0, 0, 0, 0));
       }
     }
     // ---- new rows of the sequence inside this chunk: K (RoPE) and V from the QKV output into
@@ -251,12 +362,11 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
           const uint2 vlo = make_uint2(pack_bf16(va[k].x, va[k].y), pack_bf16(va[k].z, va[k].w));
           const uint2 vhi = make_uint2(pack_bf16(vb[k].x, vb[k].y), pack_bf16(vb[k].z, vb[k].w));
           const int w = (key - c_begin) >> 5, kk = (key - c_begin) & 31;
-          __nv_bfloat16* kr = k_s + ((size_t)w * 32 + kk) * P;
-          __nv_bfloat16* vr = v_s + ((size_t)w * 32 + kk) * P;
-          *reinterpret_cast<uint2*>(kr + i) = klo;
-          *reinterpret_cast<uint2*>(kr + i + HALF) = khi;
-          *reinterpret_cast<uint2*>(vr + i) = vlo;
-          *reinterpret_cast<uint2*>(vr + i + HALF) = vhi;
+          const uint32_t kt_w = smem_u32(k_s) + (uint32_t)(w * L::TILE), vt_w = smem_u32(v_s) + (uint32_t)(w * L::TILE);
+          st_shared_v2(tile_addr<DH>(kt_w, kk, i), klo);
+          st_shared_v2(tile_addr<DH>(kt_w, kk, i + HALF), khi);
+          st_shared_v2(tile_addr<DH>(vt_w, kk, i), vlo);
+          st_shared_v2(tile_addr<DH>(vt_w, kk, i + HALF), vhi);
           if (head % (H / Hk) == 0 && qb == (key - new_first) / QB) {
             const int page = __ldg(kv.page_table + (size_t)slot * kv.max_pages + key / kv.P);
             __nv_bfloat16* kdst = kv.pool + kv.offset(page, layer, 0, kvh, key % kv.P);
@@ -268,85 +378,13 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
         }
       }
     }
-    mbar_wait(&bar_s[warp], 0);
     __syncthreads();
     stamp(2);
 
     if (kt < c_end) {
-      // ---- S = Q K^T for this warp's 32 keys: 4 n-tiles of 8 keys, DH/16 k-steps
-      // two accumulator sets (even / odd k-steps) halve the dependent mma chain
-      float s[4][4], s2[4][4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        s[j][0] = s[j][1] = s[j][2] = s[j][3] = s2[j][0] = s2[j][1] = s2[j][2] = s2[j][3] = 0.f;
-      const uint32_t qa = smem_u32(q_s), kb = smem_u32(kw);
-#pragma unroll
-      for (int ks = 0; ks < DH / 16; ++ks) {
-        uint32_t a0, a1, a2, a3;
-        ldsm_x4(qa + ((lane & 15) * P + ks * 16 + (lane >> 4) * 8) * 2, a0, a1, a2, a3);
-        float (*acc)[4] = (ks & 1) ? s2 : s;
-#pragma unroll
-        for (int nt = 0; nt < 4; nt += 2) {
-          uint32_t b0, b1, b2, b3;
-          const int key = nt * 8 + (lane >> 4) * 8 + (lane & 7);
-          ldsm_x4(kb + (key * P + ks * 16 + ((lane >> 3) & 1) * 8) * 2, b0, b1, b2, b3);
-          mma_bf16(acc[nt], a0, a1, a2, a3, b0, b1);
-          mma_bf16(acc[nt + 1], a0, a1, a2, a3, b2, b3);
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) s[j][c] += s2[j][c];
-      // ---- mask + softmax over the tile (rows g, g + 8; lane holds keys 8 nt + 2 t4, +1)
-#pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        const int r = g + 8 * h2;
-        float mx = -INFINITY;
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const int key = kt + nt * 8 + 2 * t4 + c;
-            const bool ok = r < nr && key < c_end && key <= pos0 + r;
-            float& v = s[nt][2 * h2 + c];
-            v = ok ? v * scale : -INFINITY;
-            mx = fmaxf(mx, v);
-          }
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        float sum = 0.f;
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            float& v = s[nt][2 * h2 + c];
-            v = (mx == -INFINITY) ? 0.f : exp2_approx(v - mx);
-            sum += v;
-          }
-        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-        m_row[h2] = mx;
-        l_row[h2] = sum;
-      }
-      // ---- O = P V: P (bf16, B5) re-packed from the S accumulators; V via ldmatrix.trans
-      const uint32_t vb = smem_u32(vw);
-#pragma unroll
-      for (int kc = 0; kc < 2; ++kc) {   // keys 16 kc .. 16 kc + 15
-        const uint32_t pa0 = pack_bf16(s[2 * kc][0], s[2 * kc][1]);
-        const uint32_t pa1 = pack_bf16(s[2 * kc][2], s[2 * kc][3]);
-        const uint32_t pa2 = pack_bf16(s[2 * kc + 1][0], s[2 * kc + 1][1]);
-        const uint32_t pa3 = pack_bf16(s[2 * kc + 1][2], s[2 * kc + 1][3]);
-#pragma unroll
-        for (int dt = 0; dt < DT; dt += 2) {
-          uint32_t b0, b1, b2, b3;
-          const int key = kc * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-          const int dim = dt * 8 + (lane >> 4) * 8;
-          ldsm_x4_t(vb + (key * P + dim) * 2, b0, b1, b2, b3);
-          mma_bf16(o_acc[dt], pa0, pa1, pa2, pa3, b0, b1);
-          mma_bf16(o_acc[dt + 1], pa0, pa1, pa2, pa3, b2, b3);
-        }
-      }
+      float sc[4][4];
+      warp_scores<DH>(q_s, kw, kt, c_end, nr, pos0, scale, lane, sc, m_row, l_row);
+      warp_pv<DH>(vw, lane, sc, o_acc);
     }
   }
 
@@ -358,14 +396,18 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
     l_s[warp * QB + g] = l_row[0];
     l_s[warp * QB + g + 8] = l_row[1];
   }
+  // rows g, g + 8 of the fragments (only the block's real rows), row pitch OP: conflict-free float2
+  if (g < nr) {
 #pragma unroll
-  for (int dt = 0; dt < DT; ++dt) {
-    float* o0 = o_s + ((size_t)warp * QB + g) * DH + dt * 8 + 2 * t4;
-    float* o1 = o_s + ((size_t)warp * QB + g + 8) * DH + dt * 8 + 2 * t4;
-    o0[0] = o_acc[dt][0];
-    o0[1] = o_acc[dt][1];
-    o1[0] = o_acc[dt][2];
-    o1[1] = o_acc[dt][3];
+    for (int dt = 0; dt < DT; ++dt)
+      *reinterpret_cast<float2*>(o_s + ((size_t)warp * QB + g) * OP + dt * 8 + 2 * t4) =
+          make_float2(o_acc[dt][0], o_acc[dt][1]);
+  }
+  if (g + 8 < nr) {
+#pragma unroll
+    for (int dt = 0; dt < DT; ++dt)
+      *reinterpret_cast<float2*>(o_s + ((size_t)warp * QB + g + 8) * OP + dt * 8 + 2 * t4) =
+          make_float2(o_acc[dt][2], o_acc[dt][3]);
   }
   __syncthreads();
   const bool single = nsplit == 1;
@@ -374,7 +416,7 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
   // merges through distributed shared memory; otherwise the last chunk (it holds the new keys)
   // merges from global memory after the others published theirs.
   const bool reducer = clustered || split == nsplit - 1;
-  float* own = o_s + (size_t)WARPS * QB * DH;      // [QB][DH] after the warp scratch, inside K|V
+  float* own = o_s + (size_t)WARPS * QB * OP;      // [QB][DH] after the warp scratch, inside K|V
   float* cm = own + QB * DH;                        // [QB] own chunk max and sum
   float* cl = cm + QB;
   float* oml = cl + QB;                             // [nsplit - 1][QB][2] other chunks' (max, sum)
@@ -410,7 +452,7 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
 #pragma unroll
     for (int w = 0; w < WARPS; ++w) {
       const float f = fw_s[w * QB + r];
-      const float4 v = *reinterpret_cast<const float4*>(o_s + ((size_t)w * QB + r) * DH + d);
+      const float4 v = *reinterpret_cast<const float4*>(o_s + ((size_t)w * QB + r) * OP + d);
       o.x += v.x * f;
       o.y += v.y * f;
       o.z += v.z * f;
@@ -545,28 +587,33 @@ attn_fused_kernel(const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, co
   done();
 }
 
-// env SEED_ATTN_CLUSTER=0 forces the global-memory merge (both give identical results)
-bool attn_cluster_merge() {
-  static int on = -1;
-  if (on < 0) {
+// env SEED_ATTN_CLUSTER: 0 global-memory merge, 1 DSMEM merge (<= 8 chunks), default: DSMEM merge
+// while the grid fits one wave of three CTAs per SM -- thread-block clusters must be co-scheduled
+// inside a GPC, which costs occupancy once the grid is larger (measured at N = 24 streams: 96 us
+// per layer clustered vs 74 us global).  Both give identical results (R19).
+int attn_cluster_mode() {
+  static int mode = -2;
+  if (mode == -2) {
     const char* e = getenv("SEED_ATTN_CLUSTER");
-    on = (e && e[0] == '0') ? 0 : 1;
+    mode = e ? atoi(e) : -1;
   }
-  return on == 1;
+  return mode;
 }
 
 template <int DH>
-cudaError_t launch_dh(int M, int n_seq, int max_q_len, int max_kv, int H, int Hk, const float* qkv,
-                      const SeqInfo& seqs, const float2* rope, const KVLayout& kv, int layer, const AttnWorkspace& ws,
-                      __nv_bfloat16* out, cudaStream_t st) {
+cudaError_t launch_dh(int M, int n_seq, int max_q_len, int max_kv, int H, int Hk, const CUtensorMap& tmkv,
+                      const float* qkv, const SeqInfo& seqs, const float2* rope, const KVLayout& kv, int layer,
+                      const AttnWorkspace& ws, __nv_bfloat16* out, cudaStream_t st) {
+  using L = Smem<DH>;
   const int n_qblk = (max_q_len + QB - 1) / QB;
   const int splits = (max_kv + CHUNK - 1) / CHUNK;
-  const size_t smem = Smem<DH>::BYTES;
-  static_assert((size_t)WARPS * QB * DH * 4 <= 2 * (size_t)WARPS * 32 * (DH + 8) * 2, "o merge scratch fits");
-  // reducer scratch after the warp scratch: own [QB][DH] + (max, sum) of every chunk
-  const size_t kv_bytes = 2 * (size_t)WARPS * 32 * (DH + 8) * 2;
-  if (((size_t)WARPS * QB * DH + (size_t)QB * DH + 2 * QB + (size_t)2 * QB * splits) * 4 > kv_bytes)
+  const size_t smem = L::BYTES;
+  // warp-merge scratch, the reducer's own result and every chunk's (max, sum) alias the K|V tiles
+  const size_t kv_bytes = 2 * WARPS * L::TILE;
+  if (((size_t)WARPS * QB * L::OP + (size_t)QB * DH + 2 * QB + (size_t)2 * QB * splits) * 4 > kv_bytes)
     return cudaErrorInvalidValue;
+  // tensor copies of whole page blocks into the swizzled tiles: blocks of >= 16 rows (1 KB atoms)
+  if (kv.P < 16 || (kv.P & (kv.P - 1))) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn_fused_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -574,26 +621,34 @@ cudaError_t launch_dh(int M, int n_seq, int max_q_len, int max_kv, int H, int Hk
   }
   // scores are kept in the base-2 domain: s = q.k / sqrt(Dh) * log2(e), p = 2^(s - max)
   const float scale = 1.0f / sqrtf((float)DH) * 1.4426950408889634f;
-  // <= 8 chunks: one cluster per (sequence block, head) along z, merged through DSMEM
-  const int clustered = (splits > 1 && splits <= 8 && attn_cluster_merge()) ? 1 : 0;
+  const int cm = attn_cluster_mode();
+  const long ctas = (long)n_seq * n_qblk * H * splits;
+  const int clustered = (splits > 1 && splits <= 8 && (cm == 1 || (cm < 0 && ctas <= 3 * kNumSMs))) ? 1 : 0;
   return launch_clustered(attn_fused_kernel<DH>, dim3(n_seq * n_qblk, H, splits), dim3(WARPS * 32), smem, st,
-                          dim3(1, 1, clustered ? splits : 1), qkv, H, Hk, seqs, rope, kv, layer, n_qblk, scale, ws, M,
-                          out, clustered);
+                          dim3(1, 1, clustered ? splits : 1), tmkv, qkv, H, Hk, seqs, rope, kv, layer, n_qblk, scale,
+                          ws, M, out, clustered);
 }
 }  // namespace
 
 int attn_chunk_tokens() { return CHUNK; }
 int attn_query_block() { return QB; }
 
+bool attn_kv_tmap(CUtensorMap* map, const KVLayout& kv, size_t n_pages) {
+  const uint64_t rows = (uint64_t)n_pages * kv.n_layers * 2 * kv.Hk * kv.P;
+  // rows of 128 B (Dh >= 64: 64-dim halves) in the 128-byte swizzle, 64-byte rows (Dh = 32) in the 64-byte one
+  return encode_tmap_2d(map, kv.pool, (uint64_t)kv.Dh, rows, (uint32_t)(kv.Dh >= 64 ? 64 : kv.Dh),
+                        (uint32_t)(kv.P < 32 ? kv.P : 32), kv.Dh >= 64 ? 128 : 64);
+}
+
 cudaError_t attention(const float* qkv, int M, int n_seq, int max_q_len, int max_kv, int H, int Hk, int Dh,
-                      const SeqInfo& seqs, const float2* rope, const KVLayout& kv, int layer,
+                      const SeqInfo& seqs, const float2* rope, const KVLayout& kv, const CUtensorMap& tmkv, int layer,
                       const AttnWorkspace& ws, __nv_bfloat16* out, cudaStream_t st) {
   const int splits = (max_kv + CHUNK - 1) / CHUNK;
   if (splits > ws.max_splits) return cudaErrorInvalidValue;
   if ((size_t)n_seq * ((max_q_len + QB - 1) / QB) * H > (size_t)ws.max_counters) return cudaErrorInvalidValue;
-  if (Dh == 128) return launch_dh<128>(M, n_seq, max_q_len, max_kv, H, Hk, qkv, seqs, rope, kv, layer, ws, out, st);
-  if (Dh == 64) return launch_dh<64>(M, n_seq, max_q_len, max_kv, H, Hk, qkv, seqs, rope, kv, layer, ws, out, st);
-  if (Dh == 32) return launch_dh<32>(M, n_seq, max_q_len, max_kv, H, Hk, qkv, seqs, rope, kv, layer, ws, out, st);
+  if (Dh == 128) return launch_dh<128>(M, n_seq, max_q_len, max_kv, H, Hk, tmkv, qkv, seqs, rope, kv, layer, ws, out, st);
+  if (Dh == 64) return launch_dh<64>(M, n_seq, max_q_len, max_kv, H, Hk, tmkv, qkv, seqs, rope, kv, layer, ws, out, st);
+  if (Dh == 32) return launch_dh<32>(M, n_seq, max_q_len, max_kv, H, Hk, tmkv, qkv, seqs, rope, kv, layer, ws, out, st);
   return cudaErrorInvalidValue;
 }
 

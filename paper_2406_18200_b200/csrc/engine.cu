@@ -120,6 +120,7 @@ struct Model {
   GemmPlan plm{};
   // paged KV
   KVLayout kv{};
+  CUtensorMap tmkv;                 // 2D tensor map of the KV pool (attention's page-block copies)
   int32_t* page_table_dev = nullptr;
   int32_t* page_table = nullptr;          // pinned host mirror [slots][max_pages]
   std::vector<int32_t> free_pages;
@@ -389,6 +390,7 @@ seed_status build_model(seed_ctx ctx, Model& m, const seed_model_shape& sh, cons
   std::memset(m.page_table, 0, (size_t)slots * max_pages * 4);
   CK(cudaMemset(m.page_table_dev, 0, (size_t)slots * max_pages * 4));
   m.kv.page_table = m.page_table_dev;
+  if (!seed::attn_kv_tmap(&m.tmkv, m.kv, pool_pages)) return fail(ctx, SEED_ECUDA, "seed_init", "KV tensor map");
   m.held.assign(slots, 0);
   for (size_t i = pool_pages; i-- > 0;) m.free_pages.push_back((int32_t)i);
   CK(cudaMalloc(&m.rope, (size_t)max_pos * (m.Dh / 2) * sizeof(float2)));
@@ -512,7 +514,7 @@ seed_status forward_chunk(seed_ctx ctx, Model& m, const ChunkDesc& c, cudaStream
         if (ctx->cta_rec) aws.cta = ctx->cta_rec + (size_t)ctx->rec_used * kCtaRec;
         aws.timing = ctx->timing_rec + 4 * ctx->rec_used++;
       }
-      CK(seed::attention(m.y, M, c.n_seq, c.max_q_len, c.max_kv, m.H, m.Hk, m.Dh, seqs, m.rope, m.kv, l, aws,
+      CK(seed::attention(m.y, M, c.n_seq, c.max_q_len, c.max_kv, m.H, m.Hk, m.Dh, seqs, m.rope, m.kv, m.tmkv, l, aws,
                          m.attn, st));
     }
     // O: x += attn Wo^T; sums of squares -> ssq_a; h = bf16(x * mlp_norm)

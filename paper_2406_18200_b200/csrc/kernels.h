@@ -36,8 +36,9 @@ struct GemmPlan {
   CUtensorMap tmW;
 };
 
+// bf16 2D tensor map, swizzle 128 B (default) or 64 B
 bool encode_tmap_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
-                    uint32_t box_outer);
+                    uint32_t box_outer, int swizzle_bytes = 128);
 void gemm_plan(GemmPlan* plan, const void* W, int N, int K, int min_units = 4);
 void gemm_plan_free(GemmPlan* plan);
 size_t gemm_partial_floats(const GemmPlan& plan, int M);
@@ -105,8 +106,11 @@ struct AttnWorkspace {
 int attn_chunk_tokens();
 int attn_query_block();
 // fused: QKV epilogue (RoPE, bf16, KV append) + paged attention + split-KV merge; qkv = Y [M][(H+2Hk)Dh]
+// tmkv: 2D tensor map of the KV pool (attn_kv_tmap): rows of Dh elements, boxes of min(Dh, 64) x
+// min(P, 32) with the 128-byte swizzle
+bool attn_kv_tmap(CUtensorMap* map, const KVLayout& kv, size_t n_pages);
 cudaError_t attention(const float* qkv, int M, int n_seq, int max_q_len, int max_kv, int H, int Hk, int Dh,
-                      const SeqInfo& seqs, const float2* rope, const KVLayout& kv, int layer,
+                      const SeqInfo& seqs, const float2* rope, const KVLayout& kv, const CUtensorMap& tmkv, int layer,
                       const AttnWorkspace& ws, __nv_bfloat16* out, cudaStream_t st);
 
 // ------------------------------------------------------------------ K4 / K1 sampler / K5

@@ -200,19 +200,50 @@ np.save(sys.argv[1], eng.forward_logits(1, toks)[-64:].cpu().numpy())
 """
 
 
-def test_attention_merge_paths_identical(pkg, tmp_path):
-    """R19: the chunk merge through distributed shared memory (thread-block cluster, <= 8 chunks)
-    and through global memory (SEED_ATTN_CLUSTER=0) sum the same values in the same chunk order,
-    so the logits are bit-identical."""
+_ROUNDS_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, '.')
+import seedgen, paper_2406_18200_b200 as pkg
+ds = seedgen.SHAPES['llama_68m']
+ts = dict(seedgen.SHAPES['llama2_7b'], n_layers=1)
+dW, tW = seedgen.model_weights(ds, seedgen.DRAFT_SEED), seedgen.model_weights(ts, seedgen.TARGET_SEED)
+cu = lambda W: {'embed': W['embed'].cuda(), 'final_norm': W['final_norm'].cuda(), 'lm_head': W['lm_head'].cuda(),
+                'layers': [{k: v.cuda() for k, v in L.items()} for L in W['layers']]}
+n = 32
+eng = pkg.SeedEngine(ds, cu(dW), ts, cu(tW), gamma=4, temperature=1.0, seed=seedgen.PHILOX_SEED, max_new=64,
+                     max_streams=n, max_batch=n, max_ctx=1024)
+rng = np.random.default_rng(5)
+for i in range(n):
+    eng.add_stream(i, rng.integers(3, ts['vocab'], size=int(rng.integers(60, 700))).tolist())
+toks = []
+for _ in range(3):
+    b = eng.schedule()
+    tok, cnt = eng.round_host(b)
+    toks.append(np.asarray(tok))
+zt, zd, xs = eng.last_round(n)
+np.save(sys.argv[1], np.concatenate([np.concatenate(toks).ravel().astype(np.float32), zt.cpu().numpy().ravel()]))
+"""
+
+# attention chunk merges: through distributed shared memory (thread-block cluster) or global memory
+_ATTN_VARIANTS = {"cluster": {"SEED_ATTN_CLUSTER": "1"}, "global": {"SEED_ATTN_CLUSTER": "0"}}
+
+
+@pytest.mark.parametrize("script", ["prefill", "rounds"])
+def test_attention_merge_paths_identical(pkg, tmp_path, script):
+    """R19: the chunk merge through distributed shared memory (thread-block cluster, <= 8 chunks) and
+    through global memory reduce the same values in the same chunk order, so the logits (one
+    700-token prefill; three verify rounds of 32 streams with 60..700-token prompts) and the emitted
+    tokens are bit-identical (the engine picks one by grid size)."""
     import os
     import subprocess
     import sys
+    src = _MERGE_SCRIPT if script == "prefill" else _ROUNDS_SCRIPT
     out = {}
-    for flag in ("1", "0"):
-        f = tmp_path / f"z{flag}.npy"
-        env = dict(os.environ, SEED_ATTN_CLUSTER=flag)
-        r = subprocess.run([sys.executable, "-c", _MERGE_SCRIPT, str(f)], env=env, capture_output=True, text=True,
-                           cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=600)
+    for name, flags in _ATTN_VARIANTS.items():
+        f = tmp_path / f"z_{name}.npy"
+        env = dict(os.environ, **flags)
+        r = subprocess.run([sys.executable, "-c", src, str(f)], env=env, capture_output=True, text=True,
+                           cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=900)
         assert r.returncode == 0, r.stderr[-2000:]
-        out[flag] = np.load(f)
-    assert np.array_equal(out["1"], out["0"])
+        out[name] = np.load(f)
+    assert np.array_equal(out["cluster"], out["global"])
