@@ -31,21 +31,28 @@ constexpr int WARPS = 4;
 constexpr int CHUNK = WARPS * 32;        // keys per CTA
 constexpr int QB = 16;                   // query rows per CTA (one m16 MMA tile)
 
-template <int DH>
+// KV1 = false: K and V tiles resident together (64 KB at Dh = 128, three CTAs per SM).
+// KV1 = true (blocks of <= 8 query rows): one tile buffer, K first, then V into the same buffer
+// after the scores -- half the shared memory, five CTAs per SM; the arithmetic is identical.
+template <int DH, bool KV1 = false>
 struct Smem {
   static constexpr int PITCH = DH + 8;   // bf16 row pitch of Q (16-byte pad: conflict-free ldmatrix)
   static constexpr int RB = (DH >= 64 ? 64 : DH) * 2;   // bytes per swizzled K/V row segment (<= 128)
   static constexpr int OP = DH + 4;      // fp32 row pitch of the warp-merge scratch (conflict-free float2)
+  static constexpr int QR = KV1 ? 8 : QB;  // query rows a block may hold
   static constexpr size_t TILE = (size_t)32 * DH * 2;                 // one warp's 32 K (or V) rows
   static constexpr size_t K = 0;                                      // bf16 [WARPS] tiles, 128B swizzle
-  static constexpr size_t V = K + WARPS * TILE;
+  static constexpr size_t V = KV1 ? K : K + WARPS * TILE;
   static constexpr size_t Q = V + WARPS * TILE;                       // bf16 [16][PITCH]
-  static constexpr size_t ML = Q + (size_t)QB * PITCH * 2;           // fp32 m, l [2][WARPS][QB], merge
-                                                                     // factors [WARPS][QB], row m, l [2][QB]
+  static constexpr size_t OWN = Q + (size_t)QB * PITCH * 2;          // KV1: fp32 [QR][DH] reducer's own o,
+                                                                     // own max / sum [2][QB], others [splits][QB][2]
+  static constexpr size_t ML = KV1 ? OWN + (size_t)QR * DH * 4 + 2 * QB * 4 : OWN;
   static constexpr size_t TK = ML + (size_t)(3 * WARPS + 2) * QB * 4; // ticket
   static constexpr size_t BAR = TK + 16;                             // mbarrier per warp (K / V tile)
-  static constexpr size_t BYTES = BAR + WARPS * 8 + 1024;            // + alignment of the tiles
-  // o merge scratch fp32 [WARPS][QB][OP] aliases K|V after the MMAs
+  static constexpr size_t OML = BAR + WARPS * 8;                      // KV1: other chunks' (max, sum)
+  static size_t bytes(int splits) { return OML + (KV1 ? (size_t)splits * QB * 2 * 4 : 0) + 1024; }
+  // KV1 = false: o merge scratch fp32 [WARPS][QB][OP], own, max / sum and others alias K|V after
+  // the MMAs; KV1: only the scratch [WARPS][QR][OP] aliases the tile buffer
 };
 
 // K / V tiles hold 32 rows per warp in the TMA swizzle of their row size (RB = 128 B: 16-byte chunk
@@ -54,7 +61,7 @@ struct Smem {
 // of tile row `row` (tile 1024-aligned):
 template <int DH>
 SEED_DEV uint32_t tile_addr(uint32_t tile, int row, int e) {
-  constexpr int RB = Smem<DH>::RB, EH = RB / 2;
+  constexpr int RB = Smem<DH, false>::RB, EH = RB / 2;
   constexpr uint32_t MASK = RB == 128 ? 0x70u : 0x30u;
   const uint32_t a = tile + (uint32_t)((e / EH) * 32 * RB + row * RB + (e % EH) * 2);
   return a ^ ((a >> 3) & MASK);
@@ -172,12 +179,14 @@ SEED_DEV void warp_pv(uint32_t vb, int lane, const float (&s)[4][4], float (*o_a
   }
 }
 
-template <int DH>
-__global__ void __launch_bounds__(WARPS * 32)
+template <int DH, bool KV1>
+// minimum CTAs per SM = what shared memory allows (caps the registers accordingly)
+__global__ void __launch_bounds__(WARPS * 32, KV1 ? (DH >= 128 ? 4 : 5) : (DH >= 128 ? 3 : 4))
 attn_fused_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __restrict__ qkv, int H, int Hk,
                   SeqInfo seqs, const float2* __restrict__ rope, KVLayout kv, int layer, int n_qblk, float scale,
                   AttnWorkspace ws, int M, __nv_bfloat16* __restrict__ out, int clustered) {
-  using L = Smem<DH>;
+  using L = Smem<DH, KV1>;
+  constexpr int QR = L::QR;
   constexpr int P = L::PITCH;
   constexpr int OP = L::OP;
   constexpr int HALF = DH / 2;
@@ -241,23 +250,30 @@ attn_fused_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __restr
   const int BR = min(kv.P, 32);                    // rows per tensor copy (a page, or 32 of it)
   const uint32_t kw = smem_u32(k_s) + (uint32_t)(warp * L::TILE);
   const uint32_t vw = smem_u32(v_s) + (uint32_t)(warp * L::TILE);
-  auto copy_blocks = [&](bool pre) {               // lane 0 of the warp
-    for (int k0 = kt; k0 < kt + 32 && k0 < old_end; k0 += BR) {
-      if ((k0 + BR <= stable) != pre) continue;
-      const int page = __ldg(kv.page_table + (size_t)slot * kv.max_pages + k0 / kv.P);
+  // page of block b in lane b (page-table rows are uploaded before the round: safe before the
+  // PDL wait), all blocks' loads in flight together
+  int pg = 0;
+  if (has_keys && lane < 32 / BR && kt + lane * BR < old_end)
+    pg = __ldg(kv.page_table + (size_t)slot * kv.max_pages + (kt + lane * BR) / kv.P);
+  // pre: blocks written before the round (-1: every block); which: 1 K, 2 V, 3 both
+  auto copy_blocks = [&](int pre, int which) {     // whole warp; lane 0 issues
+    for (int b = 0; b < 32 / BR; ++b) {
+      const int k0 = kt + b * BR;
+      const int page = __shfl_sync(0xffffffffu, pg, b);
+      if (k0 >= old_end || (pre >= 0 && (k0 + BR <= stable) != (pre == 1)) || lane != 0) continue;
       const int row = (((page * kv.n_layers + layer) * 2) * kv.Hk + kvh) * kv.P + (k0 % kv.P);
 #pragma unroll
       for (int h = 0; h < DH / EH; ++h) {
-        const uint32_t o = (uint32_t)(h * 32 * L::RB + (k0 - kt) * L::RB);
-        tma_load_2d_u32(kw + o, &tmKV, &bar_s[warp], h * EH, row);
-        tma_load_2d_u32(vw + o, &tmKV, &bar_s[warp], h * EH, row + kv.Hk * kv.P);
+        const uint32_t o = (uint32_t)(h * 32 * L::RB + b * BR * L::RB);
+        if (which & 1) tma_load_2d_u32(kw + o, &tmKV, &bar_s[warp], h * EH, row);
+        if (which & 2) tma_load_2d_u32(vw + o, &tmKV, &bar_s[warp], h * EH, row + kv.Hk * kv.P);
       }
     }
   };
-  if (has_keys && lane == 0) {
-    const int nblk = old_end > kt ? (min(kt + 32, old_end) - kt + BR - 1) / BR : 0;
-    mbar_arrive_expect_tx(&bar_s[warp], (uint32_t)nblk * BR * DH * 2 * 2);
-    copy_blocks(true);
+  const int nblk = old_end > kt ? (min(kt + 32, old_end) - kt + BR - 1) / BR : 0;
+  if (has_keys) {
+    if (lane == 0) mbar_arrive_expect_tx(&bar_s[warp], (uint32_t)nblk * BR * DH * 2 * (KV1 ? 1 : 2));
+    copy_blocks(1, KV1 ? 1 : 3);
   }
   pdl_wait();
   if (ws.timing && threadIdx.x == 0) atomicMin(&ws.timing[1], globaltimer_ns());
@@ -269,7 +285,11 @@ attn_fused_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __restr
       ws.timing[3] = 2;  // record kind: attention
     }
   };
-  if (!active) {
+  // chunks holding keys of this block: 0 .. n_ne - 1.  Outside a cluster an empty chunk has nothing
+  // to publish (the merge would skip its -inf maximum anyway): it leaves at once, unless it is the
+  // reducer (the last chunk of the grid)
+  const int n_ne = (key_end + CHUNK - 1) / CHUNK;
+  if (!active || (!clustered && !has_keys && split != nsplit - 1)) {
     done();
     return;
   }
@@ -280,7 +300,7 @@ attn_fused_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __restr
   for (int j = 0; j < DT; ++j) o_acc[j][0] = o_acc[j][1] = o_acc[j][2] = o_acc[j][3] = 0.f;
 
   if (has_keys) {
-    if (lane == 0) copy_blocks(false);
+    copy_blocks(0, KV1 ? 1 : 3);
     // ---- Q of this block's rows and head: RoPE, bf16 rounding (B2); padding rows are zero.
     // Items of 4 rotation pairs; every load of the loop is issued before the first use.
     {
@@ -314,19 +334,19 @@ attn_fused_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __restr
       }
     }
     // every warp's tensor copies have landed before any thread rewrites rows of the tiles
-    for (int w = 0; w < WARPS; ++w) mbar_wait(&bar_s[w], 0);
-    // ---- rows past the chunk: zero (each lane its own row of its warp's tiles)
-    if (kt + lane >= c_end) {
+    auto rewrite_rows = [&](bool do_k, bool do_v, uint32_t parity) {
+      for (int w = 0; w < WARPS; ++w) mbar_wait(&bar_s[w], parity);
+      // ---- rows past the chunk: zero (each lane its own row of its warp's tiles)
+      if (kt + lane >= c_end) {
 #pragma unroll
-      for (int e = 0; e < DH; e += 8) {
-        st_shared_v4(tile_addr<DH>(kw, lane, e), make_uint4(0, 0, 0, 0));
-        st_shared_v4(tile_addr<DH>(vw, lane, e), make_uint4(0, 0, 0, 0));
+        for (int e = 0; e < DH; e += 8) {
+          if (do_k) st_shared_v4(tile_addr<DH>(kw, lane, e), make_uint4(0, 0, 0, 0));
+          if (do_v) st_shared_v4(tile_addr<DH>(vw, lane, e), make_uint4(0, 0, 0, 0));
+        }
       }
-    }
-    // ---- new rows of the sequence inside this chunk: K (RoPE) and V from the QKV output into
-    // the tiles; the owning query block appends them to the cache (one writer per kv head and
-    // position).  Same 4-pair items, loads first.
-    {
+      // ---- new rows of the sequence inside this chunk: K (RoPE) and V from the QKV output into
+      // the tiles; the owning query block appends them to the cache (one writer per kv head and
+      // position).  Same 4-pair items, loads first.
       const int nk0 = max(c_begin, new_first), nk1 = c_end;
       const int NI = (nk1 - nk0) * (HALF / 4);
       for (int base = 0; base < NI; base += 2 * NT) {
@@ -340,13 +360,17 @@ attn_fused_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __restr
             const int m = q0 + (key - new_first);
             const float* yk = qkv + (size_t)m * ldq + (H + kvh) * DH;
             const float* yv = qkv + (size_t)m * ldq + (H + Hk + kvh) * DH;
-            const float4* cs = reinterpret_cast<const float4*>(rope + (size_t)key * HALF + i);
-            ka[k] = *reinterpret_cast<const float4*>(yk + i);
-            kb[k] = *reinterpret_cast<const float4*>(yk + i + HALF);
-            va[k] = *reinterpret_cast<const float4*>(yv + i);
-            vb[k] = *reinterpret_cast<const float4*>(yv + i + HALF);
-            c0[k] = __ldg(cs);
-            c1[k] = __ldg(cs + 1);
+            if (do_k) {
+              const float4* cs = reinterpret_cast<const float4*>(rope + (size_t)key * HALF + i);
+              ka[k] = *reinterpret_cast<const float4*>(yk + i);
+              kb[k] = *reinterpret_cast<const float4*>(yk + i + HALF);
+              c0[k] = __ldg(cs);
+              c1[k] = __ldg(cs + 1);
+            }
+            if (do_v) {
+              va[k] = *reinterpret_cast<const float4*>(yv + i);
+              vb[k] = *reinterpret_cast<const float4*>(yv + i + HALF);
+            }
           }
         }
 #pragma unroll
@@ -354,38 +378,56 @@ attn_fused_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __restr
           const int it = base + tid + k * NT;
           if (it >= NI) continue;
           const int key = nk0 + it / (HALF / 4), i = (it % (HALF / 4)) * 4;
-          const float4 x0 = ka[k], x1 = kb[k];
-          const uint2 klo = make_uint2(pack_bf16(x0.x * c0[k].x - x1.x * c0[k].y, x0.y * c0[k].z - x1.y * c0[k].w),
-                                       pack_bf16(x0.z * c1[k].x - x1.z * c1[k].y, x0.w * c1[k].z - x1.w * c1[k].w));
-          const uint2 khi = make_uint2(pack_bf16(x1.x * c0[k].x + x0.x * c0[k].y, x1.y * c0[k].z + x0.y * c0[k].w),
-                                       pack_bf16(x1.z * c1[k].x + x0.z * c1[k].y, x1.w * c1[k].z + x0.w * c1[k].w));
-          const uint2 vlo = make_uint2(pack_bf16(va[k].x, va[k].y), pack_bf16(va[k].z, va[k].w));
-          const uint2 vhi = make_uint2(pack_bf16(vb[k].x, vb[k].y), pack_bf16(vb[k].z, vb[k].w));
           const int w = (key - c_begin) >> 5, kk = (key - c_begin) & 31;
-          const uint32_t kt_w = smem_u32(k_s) + (uint32_t)(w * L::TILE), vt_w = smem_u32(v_s) + (uint32_t)(w * L::TILE);
-          st_shared_v2(tile_addr<DH>(kt_w, kk, i), klo);
-          st_shared_v2(tile_addr<DH>(kt_w, kk, i + HALF), khi);
-          st_shared_v2(tile_addr<DH>(vt_w, kk, i), vlo);
-          st_shared_v2(tile_addr<DH>(vt_w, kk, i + HALF), vhi);
-          if (head % (H / Hk) == 0 && qb == (key - new_first) / QB) {
+          const bool own_row = head % (H / Hk) == 0 && qb == (key - new_first) / QB;
+          __nv_bfloat16* kdst = nullptr;
+          if (own_row) {
             const int page = __ldg(kv.page_table + (size_t)slot * kv.max_pages + key / kv.P);
-            __nv_bfloat16* kdst = kv.pool + kv.offset(page, layer, 0, kvh, key % kv.P);
-            *reinterpret_cast<uint2*>(kdst + i) = klo;
-            *reinterpret_cast<uint2*>(kdst + i + HALF) = khi;
-            *reinterpret_cast<uint2*>(kdst + kv.vofs() + i) = vlo;
-            *reinterpret_cast<uint2*>(kdst + kv.vofs() + i + HALF) = vhi;
+            kdst = kv.pool + kv.offset(page, layer, 0, kvh, key % kv.P);
+          }
+          if (do_k) {
+            const float4 x0 = ka[k], x1 = kb[k];
+            const uint2 klo = make_uint2(pack_bf16(x0.x * c0[k].x - x1.x * c0[k].y, x0.y * c0[k].z - x1.y * c0[k].w),
+                                         pack_bf16(x0.z * c1[k].x - x1.z * c1[k].y, x0.w * c1[k].z - x1.w * c1[k].w));
+            const uint2 khi = make_uint2(pack_bf16(x1.x * c0[k].x + x0.x * c0[k].y, x1.y * c0[k].z + x0.y * c0[k].w),
+                                         pack_bf16(x1.z * c1[k].x + x0.z * c1[k].y, x1.w * c1[k].z + x0.w * c1[k].w));
+            const uint32_t kt_w = smem_u32(k_s) + (uint32_t)(w * L::TILE);
+            st_shared_v2(tile_addr<DH>(kt_w, kk, i), klo);
+            st_shared_v2(tile_addr<DH>(kt_w, kk, i + HALF), khi);
+            if (own_row) {
+              *reinterpret_cast<uint2*>(kdst + i) = klo;
+              *reinterpret_cast<uint2*>(kdst + i + HALF) = khi;
+            }
+          }
+          if (do_v) {
+            const uint2 vlo = make_uint2(pack_bf16(va[k].x, va[k].y), pack_bf16(va[k].z, va[k].w));
+            const uint2 vhi = make_uint2(pack_bf16(vb[k].x, vb[k].y), pack_bf16(vb[k].z, vb[k].w));
+            const uint32_t vt_w = smem_u32(v_s) + (uint32_t)(w * L::TILE);
+            st_shared_v2(tile_addr<DH>(vt_w, kk, i), vlo);
+            st_shared_v2(tile_addr<DH>(vt_w, kk, i + HALF), vhi);
+            if (own_row) {
+              *reinterpret_cast<uint2*>(kdst + kv.vofs() + i) = vlo;
+              *reinterpret_cast<uint2*>(kdst + kv.vofs() + i + HALF) = vhi;
+            }
           }
         }
       }
-    }
-    __syncthreads();
+      __syncthreads();
+    };
+    rewrite_rows(true, !KV1, 0);
     stamp(2);
 
-    if (kt < c_end) {
-      float sc[4][4];
-      warp_scores<DH>(q_s, kw, kt, c_end, nr, pos0, scale, lane, sc, m_row, l_row);
-      warp_pv<DH>(vw, lane, sc, o_acc);
+    float sc[4][4];
+    if (kt < c_end) warp_scores<DH>(q_s, kw, kt, c_end, nr, pos0, scale, lane, sc, m_row, l_row);
+    if (KV1) {
+      // V into the buffer the scores were read from: every warp is done with K first
+      __syncthreads();
+      fence_proxy_async();
+      if (lane == 0) mbar_arrive_expect_tx(&bar_s[warp], (uint32_t)nblk * BR * DH * 2);
+      copy_blocks(-1, 2);
+      rewrite_rows(false, true, 1);
     }
+    if (kt < c_end) warp_pv<DH>(vw, lane, sc, o_acc);
   }
 
   // ---- merge the 4 warps (fixed order) into this chunk's result
@@ -400,13 +442,13 @@ attn_fused_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __restr
   if (g < nr) {
 #pragma unroll
     for (int dt = 0; dt < DT; ++dt)
-      *reinterpret_cast<float2*>(o_s + ((size_t)warp * QB + g) * OP + dt * 8 + 2 * t4) =
+      *reinterpret_cast<float2*>(o_s + ((size_t)warp * QR + g) * OP + dt * 8 + 2 * t4) =
           make_float2(o_acc[dt][0], o_acc[dt][1]);
   }
-  if (g + 8 < nr) {
+  if (!KV1 && g + 8 < nr) {
 #pragma unroll
     for (int dt = 0; dt < DT; ++dt)
-      *reinterpret_cast<float2*>(o_s + ((size_t)warp * QB + g + 8) * OP + dt * 8 + 2 * t4) =
+      *reinterpret_cast<float2*>(o_s + ((size_t)warp * QR + g + 8) * OP + dt * 8 + 2 * t4) =
           make_float2(o_acc[dt][2], o_acc[dt][3]);
   }
   __syncthreads();
@@ -416,10 +458,11 @@ attn_fused_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __restr
   // merges through distributed shared memory; otherwise the last chunk (it holds the new keys)
   // merges from global memory after the others published theirs.
   const bool reducer = clustered || split == nsplit - 1;
-  float* own = o_s + (size_t)WARPS * QB * OP;      // [QB][DH] after the warp scratch, inside K|V
-  float* cm = own + QB * DH;                        // [QB] own chunk max and sum
+  // [QR][DH] own result, [QB] own chunk max and sum, [nsplit - 1][QB][2] other chunks' (max, sum)
+  float* own = KV1 ? reinterpret_cast<float*>(smem + L::OWN) : o_s + (size_t)WARPS * QB * OP;
+  float* cm = own + QR * DH;
   float* cl = cm + QB;
-  float* oml = cl + QB;                             // [nsplit - 1][QB][2] other chunks' (max, sum)
+  float* oml = KV1 ? reinterpret_cast<float*>(smem + L::OML) : cl + QB;
   // per row: the 4 warps' merge factors exp(m_w - m) and the row sum, warps in a fixed order
   if (tid < nr) {
     const int r = tid;
@@ -452,7 +495,7 @@ attn_fused_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __restr
 #pragma unroll
     for (int w = 0; w < WARPS; ++w) {
       const float f = fw_s[w * QB + r];
-      const float4 v = *reinterpret_cast<const float4*>(o_s + ((size_t)w * QB + r) * OP + d);
+      const float4 v = *reinterpret_cast<const float4*>(o_s + ((size_t)w * QR + r) * OP + d);
       o.x += v.x * f;
       o.y += v.y * f;
       o.z += v.z * f;
@@ -528,14 +571,15 @@ attn_fused_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __restr
   }
   if (tid == 0) {
     volatile int* vc = ctr;
-    while (*vc < nsplit - 1) {
+    while (*vc < min(nsplit - 1, n_ne)) {
     }
     fence_acq_rel_gpu();     // acquire the other chunks' partials
     *vc = 0;                 // ready for the next launch (graph replay)
   }
   __syncthreads();
   stamp(4);
-  for (int e = tid; e < (nsplit - 1) * nr; e += NT) {
+  const int n_oth = min(nsplit - 1, n_ne);   // published chunks (the reducer's own excluded)
+  for (int e = tid; e < n_oth * nr; e += NT) {
     const int sp = e / nr, r = e % nr;
     const float2 v = __ldcg(reinterpret_cast<const float2*>(ws.ml_part + (((size_t)sp * M + ws_row + r) * H + head) * 2));
     oml[(sp * QB + r) * 2] = v.x;
@@ -549,20 +593,20 @@ attn_fused_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __restr
     const int it = tid + k * NT, r = it / (DH / 4), d = (it % (DH / 4)) * 4;
     if (it >= MI || r >= nr) continue;
     float mx = cm[r];
-    for (int sp = 0; sp < nsplit - 1; ++sp) mx = fmaxf(mx, oml[(sp * QB + r) * 2]);
+    for (int sp = 0; sp < n_oth; ++sp) mx = fmaxf(mx, oml[(sp * QB + r) * 2]);
     float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
     float l = 0.f;
     const size_t row = ws_row + r;
-    for (int s0 = 0; s0 < nsplit - 1; s0 += 4) {
+    for (int s0 = 0; s0 < n_oth; s0 += 4) {
       float4 v[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q)
-        v[q] = s0 + q < nsplit - 1
+        v[q] = s0 + q < n_oth
                    ? __ldcg(reinterpret_cast<const float4*>(ws.o_part + (((size_t)(s0 + q) * M + row) * H + head) * DH + d))
                    : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        if (s0 + q >= nsplit - 1) break;
+        if (s0 + q >= n_oth) break;
         const float ms = oml[((s0 + q) * QB + r) * 2];
         if (ms == -INFINITY) continue;
         const float f = exp2_approx(ms - mx);
@@ -600,33 +644,57 @@ int attn_cluster_mode() {
   return mode;
 }
 
+template <int DH, bool KV1>
+cudaError_t launch_form(int M, int n_seq, int n_qblk, int splits, int H, int Hk, const CUtensorMap& tmkv,
+                        const float* qkv, const SeqInfo& seqs, const float2* rope, const KVLayout& kv, int layer,
+                        const AttnWorkspace& ws, __nv_bfloat16* out, cudaStream_t st, int clustered) {
+  using L = Smem<DH, KV1>;
+  const size_t smem = L::bytes(splits);
+  // warp-merge scratch (and, two-tile form, the reducer's own result and every chunk's (max, sum))
+  // alias the tiles
+  const size_t kv_bytes = (KV1 ? 1 : 2) * WARPS * L::TILE;
+  const size_t alias = KV1 ? (size_t)WARPS * L::QR * L::OP * 4
+                           : ((size_t)WARPS * QB * L::OP + (size_t)QB * DH + 2 * QB + (size_t)2 * QB * splits) * 4;
+  if (alias > kv_bytes || smem > 227 * 1024) return cudaErrorInvalidValue;
+  static int attr = 0;
+  if (attr < (int)smem) {
+    cudaFuncSetAttribute(attn_fused_kernel<DH, KV1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = (int)smem;
+  }
+  // scores are kept in the base-2 domain: s = q.k / sqrt(Dh) * log2(e), p = 2^(s - max)
+  const float scale = 1.0f / sqrtf((float)DH) * 1.4426950408889634f;
+  return launch_clustered(attn_fused_kernel<DH, KV1>, dim3(n_seq * n_qblk, H, splits), dim3(WARPS * 32), smem, st,
+                          dim3(1, 1, clustered ? splits : 1), tmkv, qkv, H, Hk, seqs, rope, kv, layer, n_qblk, scale,
+                          ws, M, out, clustered);
+}
+
+// env SEED_ATTN_KV1: 0 never, 1 whenever possible, default: blocks of <= 8 rows and a grid beyond one
+// wave of the two-tile form (results identical, R19)
+int attn_kv1_mode() {
+  static int mode = -2;
+  if (mode == -2) {
+    const char* e = getenv("SEED_ATTN_KV1");
+    mode = e ? atoi(e) : -1;
+  }
+  return mode;
+}
+
 template <int DH>
 cudaError_t launch_dh(int M, int n_seq, int max_q_len, int max_kv, int H, int Hk, const CUtensorMap& tmkv,
                       const float* qkv, const SeqInfo& seqs, const float2* rope, const KVLayout& kv, int layer,
                       const AttnWorkspace& ws, __nv_bfloat16* out, cudaStream_t st) {
-  using L = Smem<DH>;
   const int n_qblk = (max_q_len + QB - 1) / QB;
   const int splits = (max_kv + CHUNK - 1) / CHUNK;
-  const size_t smem = L::BYTES;
-  // warp-merge scratch, the reducer's own result and every chunk's (max, sum) alias the K|V tiles
-  const size_t kv_bytes = 2 * WARPS * L::TILE;
-  if (((size_t)WARPS * QB * L::OP + (size_t)QB * DH + 2 * QB + (size_t)2 * QB * splits) * 4 > kv_bytes)
-    return cudaErrorInvalidValue;
   // tensor copies of whole page blocks into the swizzled tiles: blocks of >= 16 rows (1 KB atoms)
   if (kv.P < 16 || (kv.P & (kv.P - 1))) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attn_fused_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  // scores are kept in the base-2 domain: s = q.k / sqrt(Dh) * log2(e), p = 2^(s - max)
-  const float scale = 1.0f / sqrtf((float)DH) * 1.4426950408889634f;
   const int cm = attn_cluster_mode();
   const long ctas = (long)n_seq * n_qblk * H * splits;
   const int clustered = (splits > 1 && splits <= 8 && (cm == 1 || (cm < 0 && ctas <= 3 * kNumSMs))) ? 1 : 0;
-  return launch_clustered(attn_fused_kernel<DH>, dim3(n_seq * n_qblk, H, splits), dim3(WARPS * 32), smem, st,
-                          dim3(1, 1, clustered ? splits : 1), tmkv, qkv, H, Hk, seqs, rope, kv, layer, n_qblk, scale,
-                          ws, M, out, clustered);
+  const int k1 = attn_kv1_mode();
+  if (max_q_len <= 8 && !clustered && (k1 == 1 || (k1 < 0 && ctas > 3 * kNumSMs)))
+    return launch_form<DH, true>(M, n_seq, n_qblk, splits, H, Hk, tmkv, qkv, seqs, rope, kv, layer, ws, out, st, 0);
+  return launch_form<DH, false>(M, n_seq, n_qblk, splits, H, Hk, tmkv, qkv, seqs, rope, kv, layer, ws, out, st,
+                                clustered);
 }
 }  // namespace
 

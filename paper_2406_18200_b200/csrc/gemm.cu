@@ -948,7 +948,8 @@ void gemm_plan(GemmPlan* p, const void* W, int N, int K, int min_units) {
     // one GPC, so fewer c-CTA clusters fit than SMs / c (measured: 15 clusters of 8 at 2 CTAs per
     // SM); shrink c until the device reports room for all tiles
     int smem_kb = 112;
-    for (; c > 1; --c) {
+    const char* force = getenv("SEED_SPLIT_FORCE");   // experiments: skip the capacity check
+    for (; c > 1 && !(force && force[0] == '1'); --c) {
       smem_kb = p->tiles * c <= kNumSMs ? 180 : 112;
       if (split_cluster_capacity(c, smem_kb) >= p->tiles) break;
     }
