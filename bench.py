@@ -98,7 +98,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def traffic_from_profiles(kernel="gemm_streamk"):
+def traffic_from_profiles(kernel="k2_gemm"):
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
         d = json.load(open(p))
@@ -300,7 +300,7 @@ def run_ours(args):
                    "l2": "inputs larger than L2: all target weights (13.2 GB at 7B) streamed every round"},
         "emitted_per_stream_round": alpha_rounds,
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "kernel": "gemm_streamk_kernel (K2)", "achieved": achieved, "peak": hbm,
+        "roofline": {"bound": "hbm", "kernel": "gemm_splitk_kernel (K2)", "achieved": achieved, "peak": hbm,
                      "unit": "GB/s", "frac": achieved / hbm, "peak_source": peak_src,
                      "traffic": traffic_from_profiles(), "launches": prof["gemm_launches"],
                      "gemm_share_of_step": (prof["gemm_ms"] / prof_rounds) / (ms / steps) if world == 1 else None,

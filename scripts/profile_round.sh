@@ -12,8 +12,14 @@ timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --l
 timeout 900 ncu --profile-from-start off --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
   --clock-control none --csv --log-file $OUT/round_dram.csv python scripts/ncu_round.py > $OUT/ncu_dram.log 2>&1; echo dram=$?
 # GEMM launches of a round: draft 4 steps x (2 layers x 4 + LM) = 36, then verify L0 (36-39), L1 QKV 40, O 41, GU 42
-timeout 600 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:gemm_streamk \
+timeout 600 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:gemm_splitk \
   -s 42 -c 1 -o $OUT/gemm_gu_l1 python scripts/ncu_round.py > $OUT/ncu_gemm.log 2>&1; echo gemm=$?
 # attention launches: draft 4 x 2 = 8, verify L0 = 8, L1 = 9
 timeout 600 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:attn_fused \
   -s 9 -c 1 -o $OUT/attn_l1 python scripts/ncu_round.py > $OUT/ncu_attn.log 2>&1; echo attn=$?
+# the same captures at N = 24 streams (sweep shape): the O projection (split-K over a 4-CTA cluster)
+# and attention (single-buffer form)
+CFG=sweep timeout 600 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:gemm_splitk \
+  -s 41 -c 1 -o $OUT/gemm_o_l1_sweep python scripts/ncu_round.py > $OUT/ncu_gemm_sw.log 2>&1; echo gemm_sw=$?
+CFG=sweep timeout 600 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:attn_fused \
+  -s 9 -c 1 -o $OUT/attn_l1_sweep python scripts/ncu_round.py > $OUT/ncu_attn_sw.log 2>&1; echo attn_sw=$?

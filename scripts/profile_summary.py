@@ -71,7 +71,7 @@ for r in rs:
         continue
     d = per.setdefault(r[idi], {"name": r[ki]})
     d[r[mi]] = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
-gem = [d for d in per.values() if "gemm_streamk" in d["name"]]
+gem = [d for d in per.values() if "gemm_splitk" in d["name"]]
 tr = [d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0) for d in gem]
 avg_tr = sum(tr) / max(len(tr), 1)
 lines.append("## DRAM traffic per launch (one round, `dram__bytes_read.sum + dram__bytes_write.sum`)\n")
@@ -86,14 +86,16 @@ for k, (c, by, t) in kinds.items():
     lines.append(f"| {k} | {c} | {by/c/1e6:.2f} | {t/c:.2f} |")
 if bench:
     alg = bench["roofline"]["bytes_per_launch"]
-    lines.append(f"\nK2 (gemm_streamk) over the round's {len(gem)} launches: DRAM {avg_tr/1e6:.2f} MB per launch vs "
+    lines.append(f"\nK2 (gemm_splitk) over the round's {len(gem)} launches: DRAM {avg_tr/1e6:.2f} MB per launch vs "
                  f"{alg/1e6:.2f} MB algorithmic (ratio {avg_tr/alg:.3f}).\n")
-json.dump({"gemm_streamk": avg_tr, "source": f"{dst}/summary.md: ncu dram__bytes_read.sum + dram__bytes_write.sum, "
+json.dump({"k2_gemm": avg_tr, "source": f"{dst}/summary.md: ncu dram__bytes_read.sum + dram__bytes_write.sum, "
            f"mean over the {len(gem)} GEMM launches of one GSM8K round"},
           open(os.path.join(os.path.dirname(dst.rstrip('/')), "ncu_traffic.json"), "w"), indent=1)
 
 # ---- full captures
-for rep, what in (("gemm_gu_l1", "verify gate/up GEMM, layer 1"), ("attn_l1", "verify attention, layer 1")):
+for rep, what in (("gemm_gu_l1", "verify gate/up GEMM, layer 1"), ("attn_l1", "verify attention, layer 1"),
+                  ("gemm_o_l1_sweep", "verify O GEMM, layer 1, N = 24 streams (M = 120)"),
+                  ("attn_l1_sweep", "verify attention, layer 1, N = 24 streams")):
     p = os.path.join(src, rep + ".ncu-rep")
     if not os.path.exists(p):
         continue
@@ -103,7 +105,9 @@ for rep, what in (("gemm_gu_l1", "verify gate/up GEMM, layer 1"), ("attn_l1", "v
     want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
             "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
             "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
-            "launch__shared_mem_per_block_dynamic", "smsp__inst_executed.sum", "lts__t_sector_hit_rate.pct"]
+            "launch__shared_mem_per_block_dynamic", "smsp__inst_executed.sum", "lts__t_sector_hit_rate.pct",
+            "launch__cluster_size", "launch__occupancy_limit_shared_mem", "launch__occupancy_limit_registers",
+            "sm__warps_active.avg.pct_of_peak_sustained_active"]
     lines.append(f"## Full capture: {what} (`--set full --clock-control none`)\n")
     lines.append("| metric | value |\n|---|---|")
     for w in want:
