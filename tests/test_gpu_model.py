@@ -225,15 +225,18 @@ np.save(sys.argv[1], np.concatenate([np.concatenate(toks).ravel().astype(np.floa
 """
 
 # attention chunk merges: through distributed shared memory (thread-block cluster) or global memory
-_ATTN_VARIANTS = {"cluster": {"SEED_ATTN_CLUSTER": "1"}, "global": {"SEED_ATTN_CLUSTER": "0"}}
+_ATTN_VARIANTS = {"cluster": {"SEED_ATTN_CLUSTER": "1", "SEED_ATTN_KV1": "0"},
+                  "global": {"SEED_ATTN_CLUSTER": "0", "SEED_ATTN_KV1": "0"},
+                  "kv1": {"SEED_ATTN_CLUSTER": "0", "SEED_ATTN_KV1": "1"}}
 
 
 @pytest.mark.parametrize("script", ["prefill", "rounds"])
 def test_attention_merge_paths_identical(pkg, tmp_path, script):
-    """R19: the chunk merge through distributed shared memory (thread-block cluster, <= 8 chunks) and
-    through global memory reduce the same values in the same chunk order, so the logits (one
-    700-token prefill; three verify rounds of 32 streams with 60..700-token prompts) and the emitted
-    tokens are bit-identical (the engine picks one by grid size)."""
+    """R19: every attention form -- the two-tile form with the chunk merge through distributed
+    shared memory (thread-block cluster, <= 8 chunks) or global memory, and the single-buffer form
+    (K, then V into the same tiles; blocks of <= 8 rows) -- reduces the same values in the same
+    order, so the logits (one 700-token prefill; three verify rounds of 32 streams with
+    60..700-token prompts) and the emitted tokens are bit-identical (the engine picks by grid size)."""
     import os
     import subprocess
     import sys
@@ -246,4 +249,5 @@ def test_attention_merge_paths_identical(pkg, tmp_path, script):
                            cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=900)
         assert r.returncode == 0, r.stderr[-2000:]
         out[name] = np.load(f)
-    assert np.array_equal(out["cluster"], out["global"])
+    for name in ("global", "kv1"):
+        assert np.array_equal(out["cluster"], out[name]), name
