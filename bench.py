@@ -146,6 +146,13 @@ def oracle_round_sample(cfg_name, temperature, n_streams, target_layers=2, rank_
     return est, emitted, desc, torch.get_num_threads()
 
 
+def config_of(args, cfg, n_local, world):
+    """The workload description shared by both arms' JSON lines."""
+    return {"workload": args.config, "streams_per_gpu": n_local, "gamma": cfg["gamma"], "draft": cfg["draft"],
+            "target": cfg["target"], "temperature": args.temperature, "parallelism": f"replicas x{world}",
+            "l2": "inputs larger than L2: all target weights (13.2 GB at 7B) streamed every round"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -164,8 +171,7 @@ def run_reference(args):
     line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config, "streams": n, "gamma": cfg["gamma"], "draft": cfg["draft"],
-                       "target": cfg["target"]},
+            "config": config_of(args, cfg, n, int(os.environ.get("WORLD_SIZE", "1"))),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -295,9 +301,7 @@ def run_ours(args):
         "metric": METRIC, "value": emitted / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": steps,
         "warmup": warm, "ms_per_step": ms / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init weights, seedgen prompts)",
-        "config": {"workload": args.config, "streams_per_gpu": n_local, "gamma": g, "draft": cfg["draft"],
-                   "target": cfg["target"], "temperature": args.temperature, "parallelism": f"replicas x{world}",
-                   "l2": "inputs larger than L2: all target weights (13.2 GB at 7B) streamed every round"},
+        "config": config_of(args, cfg, n_local, world),
         "emitted_per_stream_round": alpha_rounds,
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "kernel": "gemm_splitk_kernel (K2)", "achieved": achieved, "peak": hbm,
