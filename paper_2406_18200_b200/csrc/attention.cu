@@ -180,8 +180,10 @@ SEED_DEV void warp_pv(uint32_t vb, int lane, const float (&s)[4][4], float (*o_a
 }
 
 template <int DH, bool KV1>
-// minimum CTAs per SM = what shared memory allows (caps the registers accordingly)
-__global__ void __launch_bounds__(WARPS * 32, KV1 ? (DH >= 128 ? 4 : 5) : (DH >= 128 ? 3 : 4))
+// minimum CTAs per SM = what shared memory allows (caps the registers accordingly; the
+// single-buffer form at Dh = 128 spills ~140 bytes at five per SM and is still faster: 55 vs 59 us
+// per layer at N = 24)
+__global__ void __launch_bounds__(WARPS * 32, KV1 ? 5 : (DH >= 128 ? 3 : 4))
 attn_fused_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __restrict__ qkv, int H, int Hk,
                   SeqInfo seqs, const float2* __restrict__ rope, KVLayout kv, int layer, int n_qblk, float scale,
                   AttnWorkspace ws, int M, __nv_bfloat16* __restrict__ out, int clustered) {
