@@ -323,7 +323,9 @@ seed_status build_model(seed_ctx ctx, Model& m, const seed_model_shape& sh, cons
   int min_units = 4;
   if (m.d < 2048) {
     const char* e = getenv("SEED_MIN_UNITS_SMALL");
-    min_units = e ? atoi(e) : 12;   // measured: 12 (whole 768-wide k-rows) beats 4 and 24
+    // measured (GSM8K round, 68M draft): stream-K GEMM 12 best; cluster split-K 6 (two CTAs per
+    // 768-wide k-row: draft phase 311 -> 287 us; 3 and 4 within noise of 6)
+    min_units = e ? atoi(e) : 6;
   }
   const size_t d = m.d, ff = m.ff, V = m.V, dkv = (size_t)m.Hk * m.Dh, dq = (size_t)m.H * m.Dh;
   auto alloc = [&](size_t elems) -> bf16* {
