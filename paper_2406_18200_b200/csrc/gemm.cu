@@ -709,7 +709,9 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
       for (int i = 0; i < 16; ++i)
         dst[i] = (m0 + i < a.M && n < a.N) ? a.Y[(size_t)(m0 + i) * a.ldY + n] : 0.f;
     };
+    // the first two chunks' residual rows (c > 1: the rest stays one chunk ahead in the loop)
     if (res) load_res(m_lo, xo);
+    if (res && c > 1 && m_lo + 16 < m_hi) load_res(m_lo + 16, xn);
     asm volatile("bar.sync 1, 128;" ::: "memory");
     mbar_wait(&tfull[0], 0);
     tc_fence_after();
@@ -737,14 +739,17 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
         // the slots alias the peers' rings: every rank's MMAs have finished reading its ring
         if (pass == 0) cluster_sync_relaxed();
         // push: every 4-token group of this CTA's partial goes straight into the shared memory of
-        // the rank that reduces it, slot [my rank][nl] (posted DSMEM stores, no round trips)
+        // the rank that reduces it (posted DSMEM stores, no round trips), slot [my rank][group][nl]
+        // of float4: a warp's store covers 512 contiguous bytes, and the owner's 16-byte reads of
+        // consecutive lanes are conflict-free
+        const int ng = perp / 4;   // token groups per rank
         for (int col = pb; col < pe; col += 16) {
           float v[16];
           tmem_ld16(row_addr + col, v);
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            const int cc = col + 4 * j - pb, owner = cc / perp;
-            st_dsmem_f4(dsmem_addr(part_s + ((size_t)r * 128 + nl) * a.pitch + (cc - owner * perp), (uint32_t)owner),
+            const int cc = col + 4 * j - pb, owner = cc / perp, grp = (cc - owner * perp) / 4;
+            st_dsmem_f4(dsmem_addr(part_s + (((size_t)r * ng + grp) * 128 + nl) * 4, (uint32_t)owner),
                         make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
           }
         }
@@ -752,10 +757,13 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
         cluster_sync();   // every rank's slices have landed
         if (ct && et == 0) ct[9] = globaltimer();
         const int lo = min(a.M, pb + r * perp), hi = min(a.M, min(pe, pb + (r + 1) * perp));
-        if (res && pass > 0 && lo < hi) load_res(lo, xo);
+        if (res && pass > 0 && lo < hi) {
+          load_res(lo, xo);
+          if (lo + 16 < hi) load_res(lo + 16, xn);
+        }
         for (int m0 = lo; m0 < hi; m0 += 16) {
           float v[16];
-          const float* src = part_s + (size_t)nl * a.pitch + (m0 - lo);
+          const float* src = part_s + ((size_t)((m0 - lo) / 4) * 128 + nl) * 4;   // [rank][group][nl][4]
           // ranks in order 0 .. c-1 (R19); all loads of the chunk first
           const int nq = (min(16, hi - m0) + 3) / 4;
 #pragma unroll
@@ -767,7 +775,7 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
 #pragma unroll
               for (int j = 0; j < 4; ++j)
                 q[ss][j] = (s0 + ss < c && j < nq)
-                               ? *reinterpret_cast<const float4*>(src + (size_t)(s0 + ss) * 128 * a.pitch + 4 * j)
+                               ? *reinterpret_cast<const float4*>(src + ((size_t)(s0 + ss) * ng + j) * 128 * 4)
                                : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
             for (int ss = 0; ss < 4; ++ss) {
@@ -783,12 +791,13 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
           }
           if (ct && et == 0) ct[10] = globaltimer() + (v[0] == 1.2345e-30f ? 1 : 0);
           if (a.dbg & 2) continue;
-          if (res && m0 + 16 < hi) load_res(m0 + 16, xn);
+          // (the next chunk's residual rows are already in flight)
           split_finish16(a, t, nl, et, lane, m0, min(m0 + 16, hi), v, inv_s, rowmap_s, red_s, xo, w,
                          stg0 + (chunk++ & 1) * 12288);
           if (res) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) xo[i] = xn[i];
+            if (m0 + 32 < hi) load_res(m0 + 32, xn);   // two chunks ahead of its use
           }
         }
         if (res) {
