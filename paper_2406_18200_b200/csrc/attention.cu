@@ -422,12 +422,24 @@ attn_fused_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __restr
     float sc[4][4];
     if (kt < c_end) warp_scores<DH>(q_s, kw, kt, c_end, nr, pos0, scale, lane, sc, m_row, l_row);
     if (KV1) {
-      // V into the buffer the scores were read from: every warp is done with K first
-      __syncthreads();
-      fence_proxy_async();
-      if (lane == 0) mbar_arrive_expect_tx(&bar_s[warp], (uint32_t)nblk * BR * DH * 2);
-      copy_blocks(-1, 2);
-      rewrite_rows(false, true, 1);
+      // V into the buffer the scores were read from
+      if (max(c_begin, new_first) < c_end) {
+        // the chunk holds new keys, whose V rows every thread helps to form: every warp is done
+        // with K first
+        __syncthreads();
+        fence_proxy_async();
+        if (lane == 0) mbar_arrive_expect_tx(&bar_s[warp], (uint32_t)nblk * BR * DH * 2);
+        copy_blocks(-1, 2);
+        rewrite_rows(false, true, 1);
+      } else {
+        // only cached keys (and no rows past the chunk): a warp's K rows are read by that warp
+        // alone, so each warp requests its V rows as soon as its scores are done
+        __syncwarp();
+        fence_proxy_async();
+        if (lane == 0) mbar_arrive_expect_tx(&bar_s[warp], (uint32_t)nblk * BR * DH * 2);
+        copy_blocks(-1, 2);
+        mbar_wait(&bar_s[warp], 1);
+      }
     }
     if (kt < c_end) warp_pv<DH>(vw, lane, sc, o_acc);
   }
