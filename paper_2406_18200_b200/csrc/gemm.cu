@@ -477,10 +477,8 @@ SEED_DEV float rcp_approx(float x) {
 
 __device__ __forceinline__ void split_finish16(const SplitArgs& a, int t, int nl, int et, int lane, int m0, int mlim,
                                                const float* v, const float* inv_s, const int* rowmap_s, float* red_s,
-                                               const float* xo, float w, uint8_t* stg,
-                                               unsigned long long* pr = nullptr) {
+                                               const float* xo, float w, uint8_t* stg) {
   const int n = t * BLOCK_N + nl;
-  const long long c0 = clock64();
   float* sf = reinterpret_cast<float*>(stg);                       // [16][128] fp32 rows
   __nv_bfloat16* sh = reinterpret_cast<__nv_bfloat16*>(stg + 8192); // [16][128] | [16][64] bf16 rows
   if (a.ymode == 0) {
@@ -528,9 +526,7 @@ __device__ __forceinline__ void split_finish16(const SplitArgs& a, int t, int nl
 #pragma unroll
     for (int q = 0; q < 8; ++q) sh[(i0 + q) * 64 + j] = hb[q];
   }
-  const long long c1 = clock64();
   asm volatile("bar.sync 1, 128;" ::: "memory");
-  const long long c2 = clock64();
   if (!(a.dbg & 1)) {
     const int ncols = min(BLOCK_N, a.N - t * BLOCK_N);
     if (a.ymode != 2) {
@@ -561,12 +557,6 @@ __device__ __forceinline__ void split_finish16(const SplitArgs& a, int t, int nl
         *reinterpret_cast<uint4*>(a.hout + (size_t)m * (a.N / 2) + t * 64 + c8) =
             *reinterpret_cast<const uint4*>(sh + i * 64 + c8);
     }
-  }
-  const long long c3 = clock64();
-  if (pr) {
-    pr[4] = (unsigned long long)(c1 - c0);
-    pr[5] = (unsigned long long)(c2 - c1);
-    pr[6] = (unsigned long long)(c3 - c2);
   }
 }
 
@@ -725,7 +715,7 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
         if (a.dbg & 2) continue;
         if (res && m0 + 16 < a.M) load_res(m0 + 16, xn);
         split_finish16(a, t, nl, et, lane, m0, min(m0 + 16, a.M), v, inv_s, rowmap_s, red_s, xo, w,
-                       stg0 + (chunk++ & 1) * 12288, (ct && et == 0 && m0 == 16) ? ct + 8 : nullptr);
+                       stg0 + (chunk++ & 1) * 12288);
         if (ct && et == 0 && m0 == 0) ct[11] = globaltimer();
         if (res) {
 #pragma unroll

@@ -86,7 +86,7 @@ for r in rows[nd:nd + 15]:
 if os.environ.get("SEED_CTA_TRACE") == "1":
     # per-CTA phases of the layer-1 verify GEMMs and the LM head, relative to the launch release
     ph = ["release", "prod_done", "first_full", "mma_done", "acc0_ready", "epi_done", "end", "part_stored",
-          "ticket", "reduced", "chunk0", "chunk1", "first_refill", "c1_ld0", "c1_ld1"]
+          "ticket", "reduced", "chunk0", "chunk1", "first_refill"]
     for want in ["t.L1.qkv", "t.L1.o", "t.L1.gu", "t.L1.down", "t.lm", "d1.L0.gu", "d1.L0.down", "d1.L0.o"]:
         i = names.index(want)
         ct = eng.gemm_cta_trace(i)[:512 * 16].reshape(512, 16)
@@ -100,12 +100,6 @@ if os.environ.get("SEED_CTA_TRACE") == "1":
             if len(v) == 0:
                 continue
             print(f"    {name:11s} {v.min():8.2f} {np.median(v):8.2f} {v.max():8.2f}")
-        if want in ("t.L1.gu", "t.lm", "d1.L0.gu"):
-            cy = ct[:, 12:15]
-            cy = cy[(cy > 0).all(axis=1) & (cy < 10**7).all(axis=1)]
-            if len(cy):
-                print("    chunk-1 phase cycles (compute, bar, stores): median", np.median(cy, axis=0),
-                      "max", cy.max(axis=0))
         last = np.argmax(ct[:, 7])
         print("    last CTA:", " ".join(f"{(ct[last, k + 1] - rel)/1e3:.2f}" for k in range(len(ph))))
     # attention CTA phases (layer 1): start, release, tiles ready, chunk stored, ticket, end
