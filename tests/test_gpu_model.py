@@ -39,7 +39,7 @@ def _rel_rows(a, b):
 
 @pytest.mark.parametrize("name,M,ctx", [("toy_target", 5, 0), ("toy_target", 9, 37), ("toy_draft", 2, 130),
                                         ("llama_68m", 3, 0), ("llama_68m", 5, 300), ("llama2_7b", 15, 0),
-                                        ("llama2_7b", 5, 290), ("llama2_7b", 1, 129)])
+                                        ("llama2_7b", 5, 290), ("llama2_7b", 1, 129), ("llama2_13b", 12, 300)])
 def test_decoder_layer_vs_oracle(pkg, name, M, ctx):
     shape = seedgen.SHAPES[name]
     sh = ll.LlamaShape(**shape)

@@ -44,7 +44,7 @@ def test_philox_kat_and_oracle(ops):
 
 @pytest.mark.parametrize("N,K,M", [(128, 64, 1), (192, 128, 15), (32, 128, 3), (300, 256, 37), (4096, 4096, 15),
                                    (12288, 4096, 120), (4096, 11008, 5), (2304, 768, 48), (1000, 512, 256),
-                                   (640, 1024, 300), (32000, 768, 3)])
+                                   (640, 1024, 300), (32000, 768, 3), (5120, 5120, 72), (5120, 13824, 15)])
 def test_gemm_vs_fp64(ops, N, K, M):
     W = seedgen.bf16_matrix(N, K, seed=N * 7 + K).cuda()
     X = seedgen.bf16_matrix(M, K, seed=M * 13 + K + 1).cuda()
@@ -56,7 +56,7 @@ def test_gemm_vs_fp64(ops, N, K, M):
     assert err < 1e-5, err
 
 
-@pytest.mark.parametrize("N,K", [(4096, 4096), (4096, 11008), (12288, 4096), (768, 3072)])
+@pytest.mark.parametrize("N,K", [(4096, 4096), (4096, 11008), (12288, 4096), (768, 3072), (5120, 13824)])
 def test_gemm_batch_invariance(ops, N, K):
     """R19: a row's result does not depend on how many other rows share the launch (the cluster
     split-K reduction order is a function of (N, K) only); repeated launches are bit-identical."""
