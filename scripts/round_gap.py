@@ -9,10 +9,11 @@ import torch
 import seedgen
 import paper_2406_18200_b200 as pkg
 
-cfg = seedgen.CONFIGS["gsm8k"]
+CFG = os.environ.get("CFG", "gsm8k")
+cfg = seedgen.CONFIGS[CFG]
 ds, ts = seedgen.SHAPES[cfg["draft"]], seedgen.SHAPES[cfg["target"]]
-n, g = cfg["n_streams"], cfg["gamma"]
-prompts = seedgen.prompts("gsm8k", n_streams=n)
+n, g = int(os.environ.get("STREAMS", cfg["n_streams"])), cfg["gamma"]
+prompts = seedgen.prompts(CFG, n_streams=n)
 dW = seedgen.model_weights(ds, seedgen.DRAFT_SEED, device="cuda")
 tW = seedgen.model_weights(ts, seedgen.TARGET_SEED, device="cuda")
 eng = pkg.SeedEngine(ds, dW, ts, tW, gamma=g, temperature=1.0, seed=seedgen.PHILOX_SEED, max_new=400,
