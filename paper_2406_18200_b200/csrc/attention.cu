@@ -569,7 +569,8 @@ attn_fused_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __restr
       *reinterpret_cast<uint2*>(out + (row * H + head) * DH + d) =
           make_uint2(pack_bf16(o.x / l, o.y / l), pack_bf16(o.z / l, o.w / l));
     }
-    cluster.sync();   // peers finished reading this CTA's shared memory
+    cluster_sync_relaxed();   // peers finished reading this CTA's shared memory (execution order only:
+                              // the reads completed when their values were used)
     done();
     return;
   }
