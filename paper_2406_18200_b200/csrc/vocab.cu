@@ -131,7 +131,9 @@ __device__ __forceinline__ Best cluster_best(cg::cluster_group& cluster, Best* c
   cluster.sync();
   Best acc = *cluster.map_shared_rank(cta_best, 0);
   for (int c = 1; c < CS; ++c) acc = best_merge(acc, *cluster.map_shared_rank(cta_best, c));
-  cluster.sync();  // every peer has read cta_best before it may change
+  // every peer has read cta_best (the values are consumed above) before it may change:
+  // execution order only, no GPU-scope fence
+  cluster_sync_relaxed();
   return acc;
 }
 
@@ -363,7 +365,7 @@ vocab_verify_kernel(VerifyArgs A) {
       w[2 * (g + 1)] = 0;   // ready for the next launch (graph replay)
     }
   }
-  cluster.sync();  // keep shared memory alive until every peer has read it
+  cluster_sync_relaxed();  // keep shared memory alive until every peer has read it (execution order)
 }
 
 // K1 sampler: one cluster per row
