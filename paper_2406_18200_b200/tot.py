@@ -76,8 +76,8 @@ class EngineGenerator:
             eng.verify(batch)
             self.rounds += 1
         outs = []
-        for g, p in zip(gids, prefixes):
-            outs.append(eng.tokens(g)[len(p):])
+        for g in gids:
+            outs.append(eng.tokens(g))          # seed_get_tokens: the new tokens only
             eng.remove_stream(g)
         return outs
 
