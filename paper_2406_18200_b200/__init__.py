@@ -96,6 +96,9 @@ class SeedEngine:
         a, p = _i32(prompt)
         self._check(self.lib.seed_add_stream(self.ctx, int(gid), p, len(a), _stream(stream)), "seed_add_stream")
 
+    def fork_stream(self, src_gid, gid, stream=None):
+        self._check(self.lib.seed_fork_stream(self.ctx, int(src_gid), int(gid), _stream(stream)), "seed_fork_stream")
+
     def schedule(self, cap=None):
         cap = self.max_batch if cap is None else int(cap)
         buf = np.zeros(max(cap, 1), dtype=np.int32)

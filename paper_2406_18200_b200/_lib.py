@@ -52,6 +52,7 @@ _SIGS = {
     "seed_get_tokens": [_P, C.c_uint32, _I32P, C.c_int32, _I32P],
     "seed_stream_info": [_P, C.c_uint32, _I32P],
     "seed_remove_stream": [_P, C.c_uint32],
+    "seed_fork_stream": [_P, C.c_uint32, C.c_uint32, _P],
     "seed_forward_logits": [_P, C.c_int32, _I32P, C.c_int32, _P, _P],
     "seed_last_round_buffers": [_P, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)],
     "seed_get_profile": [_P, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_double),

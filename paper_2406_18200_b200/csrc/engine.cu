@@ -1108,6 +1108,26 @@ void seed_destroy(seed_ctx ctx) {
   delete ctx;
 }
 
+seed_status install_slot(seed_ctx ctx, int slot, uint32_t gid, const int32_t* prefix, int len, cudaStream_t st) {
+  SlotState& ss = ctx->slots[slot];
+  ss = SlotState();
+  ss.used = true;
+  ss.gid = gid;
+  ss.T.assign(prefix, prefix + len);
+  ss.prompt_len = len;
+  ss.len_t = ss.len_d = len - 1;
+  // device state (K5 reads/writes it)
+  int32_t vals[6] = {len, len - 1, len - 1, 0, 0, 0};
+  int32_t* dst[6] = {ctx->ds.tlen, ctx->ds.len_t, ctx->ds.len_d, ctx->ds.L, ctx->ds.r, ctx->ds.done};
+  for (int i = 0; i < 6; ++i) CK(cudaMemcpyAsync(dst[i] + slot, &vals[i], 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ctx->ds.hist + (size_t)slot * ctx->ds.max_ctx, prefix, (size_t)len * 4, cudaMemcpyHostToDevice,
+                     st));
+  CK(cudaStreamSynchronize(st));
+  ctx->gid2slot[gid] = slot;
+  seed_sched_add(ctx->sched, (int32_t)gid);
+  return SEED_OK;
+}
+
 seed_status seed_add_stream(seed_ctx ctx, uint32_t gid, const int32_t* prefix, int32_t len, void* stream) {
   seed_status s = check_ctx(ctx);
   if (s != SEED_OK) return s;
@@ -1133,23 +1153,44 @@ seed_status seed_add_stream(seed_ctx ctx, uint32_t gid, const int32_t* prefix, i
   // Alg. 1 Initialize: prefill both models with the prefix (all but the last token, R6)
   if ((s = prefill(ctx, ctx->tm, slot, prefix, len - 1, 0, nullptr, st)) != SEED_OK) return s;
   if ((s = prefill(ctx, ctx->dm, slot, prefix, len - 1, 0, nullptr, st)) != SEED_OK) return s;
-  SlotState& ss = ctx->slots[slot];
-  ss = SlotState();
-  ss.used = true;
-  ss.gid = gid;
-  ss.T.assign(prefix, prefix + len);
-  ss.prompt_len = len;
-  ss.len_t = ss.len_d = len - 1;
-  // device state (K5 reads/writes it)
-  int32_t vals[6] = {len, len - 1, len - 1, 0, 0, 0};
-  int32_t* dst[6] = {ctx->ds.tlen, ctx->ds.len_t, ctx->ds.len_d, ctx->ds.L, ctx->ds.r, ctx->ds.done};
-  for (int i = 0; i < 6; ++i) CK(cudaMemcpyAsync(dst[i] + slot, &vals[i], 4, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(ctx->ds.hist + (size_t)slot * ctx->ds.max_ctx, prefix, (size_t)len * 4, cudaMemcpyHostToDevice,
-                     st));
-  CK(cudaStreamSynchronize(st));
-  ctx->gid2slot[gid] = slot;
-  seed_sched_add(ctx->sched, (int32_t)gid);
-  return SEED_OK;
+  return install_slot(ctx, slot, gid, prefix, len, st);
+}
+
+seed_status seed_fork_stream(seed_ctx ctx, uint32_t src_gid, uint32_t gid, void* stream) {
+  seed_status s = check_ctx(ctx);
+  if (s != SEED_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  if ((s = quiesce(ctx)) != SEED_OK) return s;
+  auto it = ctx->gid2slot.find(src_gid);
+  if (it == ctx->gid2slot.end()) return fail(ctx, SEED_EINVAL, "seed_fork_stream", "unknown source id");
+  if (ctx->gid2slot.count(gid)) return fail(ctx, SEED_EINVAL, "seed_fork_stream", "duplicate global id");
+  const int src = it->second;
+  const SlotState& from = ctx->slots[src];
+  if (from.r != 0 || from.L != 0)  // only a freshly prefilled stream (no round yet)
+    return fail(ctx, SEED_ESTATE, "seed_fork_stream", "source stream has already run a round");
+  int slot = -1;
+  for (int i = 0; i < ctx->cfg.max_streams; ++i)
+    if (!ctx->slots[i].used) {
+      slot = i;
+      break;
+    }
+  if (slot < 0) return fail(ctx, SEED_ECAPACITY, "seed_fork_stream", "max_streams reached");
+  const std::vector<int32_t> prefix = from.T;
+  const int len = (int)prefix.size(), g = ctx->cfg.gamma;
+  // the prefilled K/V of the first len - 1 positions: page-granular device copies of both models'
+  // pages (a page holds every layer's K and V of P positions), bit-identical to a fresh prefill
+  for (Model* m : {&ctx->tm, &ctx->dm}) {
+    if ((s = ensure_pages(ctx, *m, slot, len + g + 1, st)) != SEED_OK) return s;
+    const int n_pages = (len - 1 + ctx->P - 1) / ctx->P;
+    const size_t bytes = m->kv.page_elems() * sizeof(bf16);
+    for (int i = 0; i < n_pages; ++i) {
+      const int a = m->page_table[(size_t)src * ctx->max_pages + i];
+      const int b = m->page_table[(size_t)slot * ctx->max_pages + i];
+      CK(cudaMemcpyAsync(m->kv.pool + (size_t)b * m->kv.page_elems(), m->kv.pool + (size_t)a * m->kv.page_elems(),
+                         bytes, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  return install_slot(ctx, slot, gid, prefix.data(), len, st);
 }
 
 seed_status seed_schedule_round(seed_ctx ctx, int32_t* batch_ids, int32_t cap, int32_t* n) {

@@ -58,16 +58,29 @@ def top_b(scores, b):
 
 
 class EngineGenerator:
-    """G(p_theta, prefixes): run SeedEngine rounds until every stream of the call is done."""
+    """G(p_theta, prefixes): run SeedEngine rounds until every stream of the call is done.
 
-    def __init__(self, engine):
+    share_prefix: a prefix repeated inside one call (the n thoughts of a state) is prefilled once;
+    its siblings get a device copy of those K/V pages (seed_fork_stream) -- same tokens.
+    """
+
+    def __init__(self, engine, share_prefix=True):
         self.eng = engine
+        self.share_prefix = share_prefix
         self.rounds = 0
+        self.prefills = 0
 
     def __call__(self, prefixes, gids):
         eng = self.eng
+        first = {}
         for g, p in zip(gids, prefixes):
+            key = tuple(p)
+            if self.share_prefix and key in first:
+                eng.fork_stream(first[key], g)
+                continue
             eng.add_stream(g, p)
+            first[key] = g
+            self.prefills += 1
         while True:
             batch = eng.schedule()
             if not batch:

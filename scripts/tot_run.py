@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--n", type=int, default=3)
     ap.add_argument("--b", type=int, default=1)
     ap.add_argument("--l", type=int, default=64)
+    ap.add_argument("--no-share", action="store_true", help="prefill every sibling (no seed_fork_stream)")
     a = ap.parse_args()
     cfg = seedgen.CONFIGS[a.config]
     depth = a.depth or DEPTH[a.config]
@@ -47,7 +48,7 @@ def main():
     V = ts["vocab"]
     tcfg = tot.ToTConfig(depth=depth, n=a.n, b=a.b, eval_prefix=(1, 29871), eval_suffix=(29901,),
                          digit_base=29896 if V > 29906 else 3)
-    gen = tot.EngineGenerator(eng)
+    gen = tot.EngineGenerator(eng, share_prefix=not a.no_share)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     res = tot.ToTBFS(gen, tcfg).build(prompt)
@@ -56,6 +57,7 @@ def main():
     streams = sum(c[1] for c in res.calls)
     print(json.dumps({"workload": a.config, "depth": depth, "n": a.n, "b": a.b, "l": a.l,
                       "scheduler_calls": len(res.calls), "streams": streams, "rounds": gen.rounds,
+                      "prefills": gen.prefills, "share_prefix": gen.share_prefix,
                       "tokens": streams * a.l, "wall_s": dt, "tokens_per_s_wall": streams * a.l / dt,
                       "ms_per_round_wall": 1e3 * dt / max(gen.rounds, 1),
                       "scores": [lv["scores"] for lv in res.levels], "answer_len": len(res.answer)}))

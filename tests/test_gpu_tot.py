@@ -103,3 +103,57 @@ def test_tot_bfs_vs_oracle(pkg, depth, n, b):
     assert res.calls == calls and res.answer == ans
     for a, o in zip(res.levels, levels):
         assert a["states"] == o["states"] and a["scores"] == o["scores"] and a["keep"] == o["keep"]
+
+
+@pytest.mark.parametrize("dname,tname,plen", [("toy_draft", "toy_target", 8), ("toy_draft", "toy_target", 77),
+                                              ("llama_68m", "llama_68m", 150)])
+def test_fork_stream_equals_add_stream(pkg, dname, tname, plen):
+    """seed_fork_stream (device copy of the prefilled pages) == seed_add_stream of the same prefix."""
+    ds, ts = seedgen.SHAPES[dname], seedgen.SHAPES[tname]
+    dW = _cuda(seedgen.model_weights(ds, seedgen.DRAFT_SEED))
+    tW = _cuda(seedgen.model_weights(ts, seedgen.TARGET_SEED))
+    prompt = np.random.default_rng(plen).integers(3, ts["vocab"], size=plen).tolist()
+    outs = []
+    for fork in (False, True):
+        eng = pkg.SeedEngine(ds, dW, ts, tW, gamma=4, temperature=1.0, seed=SEED, max_new=24, max_streams=4,
+                             max_batch=4, max_ctx=512)
+        eng.add_stream(10, prompt)
+        for g in (11, 12, 13):
+            eng.fork_stream(10, g) if fork else eng.add_stream(g, prompt)
+        if fork:
+            with pytest.raises(pkg.SeedError):
+                eng.fork_stream(99, 14)                      # unknown source
+        while True:
+            b = eng.schedule()
+            if not b:
+                break
+            eng.draft(b)
+            eng.verify(b)
+        outs.append([eng.tokens(g) for g in (10, 11, 12, 13)])
+        if fork:
+            eng.remove_stream(11)
+            with pytest.raises(pkg.SeedError):
+                eng.fork_stream(10, 15)                      # source already ran rounds
+        eng.close()
+    assert outs[0] == outs[1]
+    assert all(len(t) == 24 for t in outs[1])
+    assert len({tuple(t) for t in outs[1]}) > 1              # distinct Philox streams per id
+
+
+def test_tot_shared_prefix_same_tree(pkg):
+    from paper_2406_18200_b200 import tot as ptot
+    cfg = seedgen.CONFIGS["toy"]
+    ds, ts = seedgen.SHAPES[cfg["draft"]], seedgen.SHAPES[cfg["target"]]
+    dW = _cuda(seedgen.model_weights(ds, seedgen.DRAFT_SEED))
+    tW = _cuda(seedgen.model_weights(ts, seedgen.TARGET_SEED))
+    trees = []
+    for share in (False, True):
+        eng = pkg.SeedEngine(ds, dW, ts, tW, gamma=cfg["gamma"], temperature=1.0, seed=SEED, max_new=8,
+                             max_streams=6, max_batch=6, max_ctx=256)
+        gen = ptot.EngineGenerator(eng, share_prefix=share)
+        tcfg = ptot.ToTConfig(depth=3, n=3, b=2, eval_prefix=(1, 2), eval_suffix=(31,), digit_base=3)
+        res = ptot.ToTBFS(gen, tcfg).build(seedgen.prompts("toy")[0])
+        trees.append((res.answer, [(lv["states"], lv["scores"], lv["keep"]) for lv in res.levels], gen.prefills))
+        eng.close()
+    assert trees[0][:2] == trees[1][:2]
+    assert trees[1][2] < trees[0][2]
