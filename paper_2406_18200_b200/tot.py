@@ -18,6 +18,7 @@ seed_draft_round -> seed_verify) through `EngineGenerator`.  Per tree level:
 Global stream ids come from one counter in call order (R27); finished streams are removed
 (seed_remove_stream frees their KV pages) so max_streams bounds one call, not the tree.
 """
+import time
 from dataclasses import dataclass, field
 
 
@@ -69,9 +70,11 @@ class EngineGenerator:
         self.share_prefix = share_prefix
         self.rounds = 0
         self.prefills = 0
+        self.t_add = self.t_rounds = 0.0      # host wall seconds (admission incl. prefill / round loop)
 
     def __call__(self, prefixes, gids):
         eng = self.eng
+        t0 = time.perf_counter()
         first = {}
         for g, p in zip(gids, prefixes):
             key = tuple(p)
@@ -81,6 +84,7 @@ class EngineGenerator:
             eng.add_stream(g, p)
             first[key] = g
             self.prefills += 1
+        t1 = time.perf_counter()
         while True:
             batch = eng.schedule()
             if not batch:
@@ -88,6 +92,8 @@ class EngineGenerator:
             eng.draft(batch)
             eng.verify(batch)
             self.rounds += 1
+        self.t_add += t1 - t0
+        self.t_rounds += time.perf_counter() - t1
         outs = []
         for g in gids:
             outs.append(eng.tokens(g))          # seed_get_tokens: the new tokens only

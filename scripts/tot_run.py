@@ -57,7 +57,7 @@ def main():
     streams = sum(c[1] for c in res.calls)
     print(json.dumps({"workload": a.config, "depth": depth, "n": a.n, "b": a.b, "l": a.l,
                       "scheduler_calls": len(res.calls), "streams": streams, "rounds": gen.rounds,
-                      "prefills": gen.prefills, "share_prefix": gen.share_prefix,
+                      "prefills": gen.prefills, "t_admit_s": gen.t_add, "t_rounds_s": gen.t_rounds, "share_prefix": gen.share_prefix,
                       "tokens": streams * a.l, "wall_s": dt, "tokens_per_s_wall": streams * a.l / dt,
                       "ms_per_round_wall": 1e3 * dt / max(gen.rounds, 1),
                       "scores": [lv["scores"] for lv in res.levels], "answer_len": len(res.answer)}))
