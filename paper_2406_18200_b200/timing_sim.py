@@ -18,6 +18,9 @@ every strategy sees the same draws (common random numbers).
                (ties -> lowest stream id, R10), one verification at a time
   batched-sd   this build's lock-step form (R9): all undone streams draft together, then ONE
                batched verification whose time is t_verify_batch(m) for m streams
+  pipelined-sd §8(f) rank 2 / Fig. 1(c) overlap: the streams split into two lock-step groups
+               (even / odd ids); group A's batched verification runs while group B drafts and
+               vice versa, each phase lasting max(verify, draft)
   parallel     n independent target AR sequences fully overlapped (n target instances)
 """
 import heapq
@@ -132,10 +135,30 @@ def simulate(strategy, p, t_verify_batch=None):
             for s in live:
                 nxt[s] += 1
         return StrategyResult(strategy, T, busy, toks, 1)
+    if strategy == "pipelined-sd":
+        tvb = t_verify_batch or (lambda m: p.t_verify)
+        nxt = [0] * p.n
+        groups = [list(range(0, p.n, 2)), list(range(1, p.n, 2))]
+        live = lambda g: [s for s in groups[g] if nxt[s] < len(rounds[s])]     # noqa: E731
+        T = p.k * p.t_draft if live(0) else 0            # group A drafts alone first
+        busy, g = 0, 0
+        while live(0) or live(1):
+            lv = live(g)
+            v = 0
+            if lv:
+                rej = any(rounds[s][nxt[s]][1] for s in lv)
+                v = tvb(len(lv)) + (p.t_resample if rej else 0)
+                for s in lv:
+                    nxt[s] += 1
+            d = p.k * p.t_draft if live(1 - g) else 0    # the other group drafts meanwhile
+            T += max(v, d)
+            busy += v
+            g = 1 - g
+        return StrategyResult(strategy, T, busy, toks, 1)
     raise ValueError(f"unknown strategy {strategy}")
 
 
-STRATEGIES = ("serial", "serial-sd", "scheduled-sd", "batched-sd", "parallel")
+STRATEGIES = ("serial", "serial-sd", "scheduled-sd", "batched-sd", "pipelined-sd", "parallel")
 
 
 def sweep(params_list, strategies=STRATEGIES, t_verify_batch=None):

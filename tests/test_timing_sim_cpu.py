@@ -66,3 +66,15 @@ def test_batched_sd_with_batch_cost_and_sweep():
     assert rows[0].startswith("strategy,") and len(rows) == 1 + 2 * len(STRATEGIES)
     with pytest.raises(ValueError):
         simulate("serial", TimingParams(alpha=2.0))
+
+
+def test_pipelined_hand_trace():
+    # n = 2, alpha = 1, k = 1, l = 2: one round per stream.  A drafts [0, 2); then verify A (3)
+    # || draft B (2) -> 3; then verify B (3) -> 3; makespan 2 + 3 + 3 = 8.
+    p = TimingParams(t_draft=2, t_verify=3, n=2, k=1, l=2, alpha=1.0)
+    r = simulate("pipelined-sd", p)
+    assert r.makespan == 8 and r.target_busy == 6
+    # when drafting dominates, the overlap hides verification: draft 10, verify 1, two rounds each
+    p = TimingParams(t_draft=10, t_verify=1, n=2, k=1, l=4, alpha=1.0)
+    assert simulate("pipelined-sd", p).makespan == 10 + 10 + 10 + 10 + 1
+    assert simulate("batched-sd", p).makespan == 2 * (10 + 1)
