@@ -112,10 +112,12 @@ SEED_API seed_status seed_add_stream(seed_ctx ctx, uint32_t global_id, const int
 
 /* ToT siblings (Alg. 2 line P:738: the n thoughts of a state share its prefix; §4.1 "the input
  * instructions are the same"): adds stream `global_id` with the same prefix as `src_global_id`
- * by copying src's prefilled K/V pages of both models on the device (page-granular
- * cudaMemcpyAsync on `stream`) instead of recomputing the prefill.  The new stream is
- * bit-identical to seed_add_stream(global_id, same prefix).  Its own pages are allocated (no
- * sharing), so both streams can run and be removed independently.  Errors: unknown src or
+ * from src's prefilled K/V instead of recomputing the prefill: pages holding only prefix
+ * positions (index < (len-1)/page_tokens) are SHARED (refcounted; rounds never write below
+ * position len-1), the page holding position len-1 is copied on the device (cudaMemcpyAsync on
+ * `stream`).  The new stream is bit-identical to seed_add_stream(global_id, same prefix); both
+ * streams run and are removed independently (a page returns to the pool with its last
+ * reference).  Errors: unknown src or
  * duplicate id -> EINVAL; src has already run a round -> ESTATE (not poisoning); no free slot ->
  * ECAPACITY; no free pages -> ENOMEM.  Synchronous with respect to `stream`. */
 SEED_API seed_status seed_fork_stream(seed_ctx ctx, uint32_t src_global_id, uint32_t global_id, void* stream);

@@ -124,6 +124,7 @@ struct Model {
   int32_t* page_table_dev = nullptr;
   int32_t* page_table = nullptr;          // pinned host mirror [slots][max_pages]
   std::vector<int32_t> free_pages;
+  std::vector<int32_t> refs;              // slots referencing each page (ToT siblings share full prefix pages)
   std::vector<int32_t> held;              // pages held per slot
   size_t n_pages = 0;
   float2* rope = nullptr;
@@ -395,6 +396,7 @@ seed_status build_model(seed_ctx ctx, Model& m, const seed_model_shape& sh, cons
   if (!seed::attn_kv_tmap(&m.tmkv, m.kv, pool_pages)) return fail(ctx, SEED_ECUDA, "seed_init", "KV tensor map");
   m.held.assign(slots, 0);
   for (size_t i = pool_pages; i-- > 0;) m.free_pages.push_back((int32_t)i);
+  m.refs.assign(pool_pages, 0);
   CK(cudaMalloc(&m.rope, (size_t)max_pos * (m.Dh / 2) * sizeof(float2)));
   CK(seed::rope_table_init(m.rope, max_pos, m.Dh, sh.rope_theta > 0 ? sh.rope_theta : 10000.0, 0));
   // activations (rows rounded to >= 256 so every TMA box fits)
@@ -458,6 +460,7 @@ seed_status ensure_pages(seed_ctx ctx, Model& m, int slot, int n_tokens, cudaStr
   while (held < need) {
     if (m.free_pages.empty()) return fail(ctx, SEED_ENOMEM, "KV", "page pool exhausted");
     m.page_table[(size_t)slot * ctx->max_pages + held] = m.free_pages.back();
+    m.refs[m.free_pages.back()] = 1;
     m.free_pages.pop_back();
     ++held;
   }
@@ -469,7 +472,10 @@ seed_status ensure_pages(seed_ctx ctx, Model& m, int slot, int n_tokens, cudaStr
 }
 
 void release_pages(Model& m, int slot, int max_pages) {
-  for (int i = 0; i < m.held[slot]; ++i) m.free_pages.push_back(m.page_table[(size_t)slot * max_pages + i]);
+  for (int i = 0; i < m.held[slot]; ++i) {
+    const int32_t pg = m.page_table[(size_t)slot * max_pages + i];
+    if (--m.refs[pg] == 0) m.free_pages.push_back(pg);
+  }
   m.held[slot] = 0;
 }
 
@@ -1177,17 +1183,31 @@ seed_status seed_fork_stream(seed_ctx ctx, uint32_t src_gid, uint32_t gid, void*
   if (slot < 0) return fail(ctx, SEED_ECAPACITY, "seed_fork_stream", "max_streams reached");
   const std::vector<int32_t> prefix = from.T;
   const int len = (int)prefix.size(), g = ctx->cfg.gamma;
-  // the prefilled K/V of the first len - 1 positions: page-granular device copies of both models'
-  // pages (a page holds every layer's K and V of P positions), bit-identical to a fresh prefill
+  // the prefilled K/V of the first len - 1 positions: pages holding only prefix positions
+  // (index < (len - 1) / P) are never written again -- rounds write positions >= len - 1 -- so
+  // the new slot shares them (refcounted); the page holding position len - 1, if it also holds
+  // prefix positions, is copied on the device.  Bit-identical to a fresh prefill.
+  const int shared = (len - 1) / ctx->P;
   for (Model* m : {&ctx->tm, &ctx->dm}) {
-    if ((s = ensure_pages(ctx, *m, slot, len + g + 1, st)) != SEED_OK) return s;
-    const int n_pages = (len - 1 + ctx->P - 1) / ctx->P;
-    const size_t bytes = m->kv.page_elems() * sizeof(bf16);
-    for (int i = 0; i < n_pages; ++i) {
-      const int a = m->page_table[(size_t)src * ctx->max_pages + i];
-      const int b = m->page_table[(size_t)slot * ctx->max_pages + i];
-      CK(cudaMemcpyAsync(m->kv.pool + (size_t)b * m->kv.page_elems(), m->kv.pool + (size_t)a * m->kv.page_elems(),
-                         bytes, cudaMemcpyDeviceToDevice, st));
+    int32_t* pt_src = m->page_table + (size_t)src * ctx->max_pages;
+    int32_t* pt_new = m->page_table + (size_t)slot * ctx->max_pages;
+    for (int i = 0; i < shared; ++i) {
+      pt_new[i] = pt_src[i];
+      ++m->refs[pt_new[i]];
+    }
+    m->held[slot] = shared;
+    if (shared > 0)
+      CK(cudaMemcpyAsync(m->page_table_dev + (size_t)slot * ctx->max_pages, pt_new, (size_t)shared * 4,
+                         cudaMemcpyHostToDevice, st));
+    if ((s = ensure_pages(ctx, *m, slot, len + g + 1, st)) != SEED_OK) {
+      release_pages(ctx->tm, slot, ctx->max_pages);  // the slot was never installed: drop its references
+      release_pages(ctx->dm, slot, ctx->max_pages);
+      return s;
+    }
+    if ((len - 1) % ctx->P != 0) {
+      const size_t elems = m->kv.page_elems();
+      CK(cudaMemcpyAsync(m->kv.pool + (size_t)pt_new[shared] * elems, m->kv.pool + (size_t)pt_src[shared] * elems,
+                         elems * sizeof(bf16), cudaMemcpyDeviceToDevice, st));
     }
   }
   return install_slot(ctx, slot, gid, prefix.data(), len, st);

@@ -108,7 +108,7 @@ def test_tot_bfs_vs_oracle(pkg, depth, n, b):
 @pytest.mark.parametrize("dname,tname,plen", [("toy_draft", "toy_target", 8), ("toy_draft", "toy_target", 77),
                                               ("llama_68m", "llama_68m", 150)])
 def test_fork_stream_equals_add_stream(pkg, dname, tname, plen):
-    """seed_fork_stream (device copy of the prefilled pages) == seed_add_stream of the same prefix."""
+    """seed_fork_stream (shared full prefix pages + a copied partial page) == seed_add_stream."""
     ds, ts = seedgen.SHAPES[dname], seedgen.SHAPES[tname]
     dW = _cuda(seedgen.model_weights(ds, seedgen.DRAFT_SEED))
     tW = _cuda(seedgen.model_weights(ts, seedgen.TARGET_SEED))
@@ -121,19 +121,21 @@ def test_fork_stream_equals_add_stream(pkg, dname, tname, plen):
         for g in (11, 12, 13):
             eng.fork_stream(10, g) if fork else eng.add_stream(g, prompt)
         if fork:
+            assert eng.stream_info(11)["pages"] == eng.stream_info(10)["pages"]
             with pytest.raises(pkg.SeedError):
                 eng.fork_stream(99, 14)                      # unknown source
+        eng.remove_stream(10)                                # shared prefix pages must outlive the source
+        eng.add_stream(20, prompt[::-1])                     # reuses freed pages; must not clobber shared ones
         while True:
             b = eng.schedule()
             if not b:
                 break
             eng.draft(b)
             eng.verify(b)
-        outs.append([eng.tokens(g) for g in (10, 11, 12, 13)])
+        outs.append([eng.tokens(g) for g in (11, 12, 13, 20)])
         if fork:
-            eng.remove_stream(11)
             with pytest.raises(pkg.SeedError):
-                eng.fork_stream(10, 15)                      # source already ran rounds
+                eng.fork_stream(12, 15)                      # source already ran rounds
         eng.close()
     assert outs[0] == outs[1]
     assert all(len(t) == 24 for t in outs[1])
