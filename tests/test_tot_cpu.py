@@ -116,3 +116,56 @@ def test_oracle_invariants_and_product_parity(T, n, b):
 def test_driver_rejects_bad_config():
     with pytest.raises(ValueError):
         ptot.ToTBFS(fake_generate, ptot.ToTConfig(depth=0))
+
+
+class _FakeEngine:
+    """Records the C-ABI calls EngineGenerator makes (host logic only)."""
+
+    def __init__(self):
+        self.calls, self.live, self.prefix = [], set(), {}
+
+    def add_stream(self, g, p):
+        self.calls.append(("add", g))
+        self.live.add(g)
+        self.prefix[g] = list(p)
+
+    def fork_stream(self, src, g):
+        assert src in self.live
+        self.calls.append(("fork", src, g))
+        self.live.add(g)
+        self.prefix[g] = list(self.prefix[src])
+
+    def schedule(self):
+        b = sorted(g for g in self.live if ("done", g) not in self.calls)
+        return b
+
+    def draft(self, b):
+        self.calls.append(("draft", tuple(b)))
+
+    def verify(self, b):
+        self.calls += [("done", g) for g in b]
+
+    def tokens(self, g):
+        return fake_generate([self.prefix[g]], [g])[0]
+
+    def remove_stream(self, g):
+        self.live.remove(g)
+        self.calls.append(("remove", g))
+
+
+@pytest.mark.parametrize("share", [True, False])
+def test_engine_generator_forks_repeated_prefixes(share):
+    eng = _FakeEngine()
+    gen = ptot.EngineGenerator(eng, share_prefix=share)
+    prefixes = [[5, 6], [5, 6], [7, 8], [5, 6], [7, 8]]
+    outs = gen(prefixes, [10, 11, 12, 13, 14])
+    adds = [c for c in eng.calls if c[0] == "add"]
+    forks = [c for c in eng.calls if c[0] == "fork"]
+    if share:
+        assert adds == [("add", 10), ("add", 12)]
+        assert forks == [("fork", 10, 11), ("fork", 10, 13), ("fork", 12, 14)]     # call order
+        assert gen.prefills == 2
+    else:
+        assert len(adds) == 5 and not forks and gen.prefills == 5
+    assert outs == fake_generate(prefixes, [10, 11, 12, 13, 14])
+    assert not eng.live and gen.rounds == 1                  # every stream removed after the call
