@@ -1,14 +1,16 @@
 #!/usr/bin/env python
 """Benchmark of the SeeD draft-then-verify round (BASELINE.json metric) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config gsm8k] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config sweep] [--impl ours|reference]
 
 One step = one whole round of the hot path: FCFS admission, gamma
 batched draft steps, the batched target verify forward, the fused vocabulary kernel, KV
-rollback and (N > 1) the all-gather of emitted tokens.  Workload (N = 1): BASELINE configs[1],
-the GSM8K shape -- 3 streams, 68M-shape draft, Llama-2-7B-shape target, gamma = 4, random-init
-weights, synthetic prompts (seedgen).  With N GPUs each rank runs a full replica with its own
-streams (weak scaling; the rank's streams have global ids rank, rank + N, ...).
+rollback and (N > 1) the all-gather of the exchange blocks.  Workload (default): BASELINE
+configs[4], the scaling sweep the metric is quoted on -- 24 streams per GPU, 68M-shape draft,
+Llama-2-7B-shape target, gamma = 4, prompts of 300-500 tokens, random-init weights, synthetic
+prompts (seedgen).  With N GPUs each rank runs a full replica with its own 24 streams (weak
+scaling; the rank's streams have global ids rank, rank + N, ...).  --config gsm8k / cw / bw
+select the other BASELINE shapes.
 
 Prints one JSON line (rank 0).  --impl reference times the CPU oracle (oracle/) on the same
 config as a bounded sample per step.
@@ -16,6 +18,7 @@ config as a bounded sample per step.
 import argparse
 import json
 import os
+import statistics
 import subprocess
 import sys
 import time
@@ -36,7 +39,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="gsm8k", choices=["gsm8k", "cw", "bw", "sweep", "toy"])
+    ap.add_argument("--config", default="sweep", choices=["gsm8k", "cw", "bw", "sweep", "toy"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--temperature", type=float, default=1.0)
     ap.add_argument("--streams", type=int, default=0, help="streams per GPU (default: the config's)")
@@ -50,6 +53,17 @@ def measured_peaks():
         d = json.load(open(p))
         return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops_sustained", 1400.0), "measured"
     return 6650.0, 1590.0, "fallback"
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -98,86 +112,148 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def traffic_from_profiles(kernel="k2_gemm"):
+def traffic_from_profiles(config):
+    """DRAM bytes per K2 launch from the committed ncu capture of this config (profiles/)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return d.get(kernel)
+        v = d.get(config, {})
+        return v.get("k2_gemm") if isinstance(v, dict) else None
     return None
 
 
 # ------------------------------------------------------------------ CPU oracle timing
-def oracle_round_sample(cfg_name, temperature, n_streams, target_layers=2, rank_seed=0):
-    """Time one oracle round on a bounded sample: the full draft, the target forward on
-    `target_layers` of its layers (scaled to full depth), the full verification.
-    Returns (estimated seconds per round, emitted tokens, description)."""
+def _synthetic_cache(shape, n, rng):
+    """An oracle KV cache holding n positions of bf16-valued synthetic keys / values (timing only:
+    the bounded CPU sample skips the prefill, which is not part of a round)."""
     import torch
 
     from oracle import llama as ll
-    from oracle.seed_round import SeedOracle
-    cfg = seedgen.CONFIGS[cfg_name]
-    ds, ts = seedgen.SHAPES[cfg["draft"]], seedgen.SHAPES[cfg["target"]]
-    tl = min(target_layers, ts["n_layers"])
-    ts_s = dict(ts, n_layers=tl)
-    dW = seedgen.model_weights(ds, seedgen.DRAFT_SEED)
-    tW = seedgen.model_weights(ts_s, seedgen.TARGET_SEED)
-    orc = SeedOracle(ll.LlamaShape(**ts_s), tW, ll.LlamaShape(**ds), dW, gamma=cfg["gamma"],
-                     temperature=temperature, seed=seedgen.PHILOX_SEED, max_new=10 ** 6)
-    prompts = seedgen.prompts(cfg_name, n_streams=n_streams)
-    for i, p in enumerate(prompts):
-        orc.add_stream(i, p)
-    batch = list(range(n_streams))
-    t0 = time.perf_counter()
-    xs, zds, gaps = orc.draft(batch)
-    t1 = time.perf_counter()
-    zts = orc.verify(batch, xs)
-    t2 = time.perf_counter()
-    from oracle import sampling as sp
-    emitted = 0
-    for s in batch:
-        st = orc.streams[s]
-        r = sp.verify_stream(zts[s], np.stack(zds[s]), xs[s], temperature, seedgen.PHILOX_SEED, s, st.r)
-        emitted += len(r.emitted)
-    t3 = time.perf_counter()
-    scale = ts["n_layers"] / tl
-    est = (t1 - t0) + (t2 - t1) * scale + (t3 - t2)
-    desc = (f"one {cfg_name} round, {n_streams} streams: full draft, target forward on {tl} of "
-            f"{ts['n_layers']} layers scaled x{scale:g}, full verification; prefill excluded")
-    return est, emitted, desc, torch.get_num_threads()
+    c = ll.KVCache(shape)
+    for layer in range(shape.n_layers):
+        for lst in (c.k, c.v):
+            t = torch.from_numpy(rng.standard_normal((n, shape.kv_heads, shape.head_dim)).astype(np.float32))
+            lst[layer] = t.to(torch.bfloat16).to(torch.float64).numpy()
+    return c
+
+
+class OracleSampler:
+    """Times oracle rounds of a config's batch on a bounded sample: the full draft (every layer of
+    the draft model, gamma steps), the target verify forward on `target_layers` of its layers
+    (scaled to full depth: the per-layer time only), the final norm + LM head once, and the full
+    verification (oracle.sampling.verify_stream).  The prefill is replaced by synthetic caches of
+    the prompts' lengths (built once, rolled back after every sample)."""
+
+    def __init__(self, cfg_name, temperature, n_streams, target_layers=1):
+        from oracle import llama as ll
+        from oracle.seed_round import SeedOracle, StreamState
+        self.cfg = seedgen.CONFIGS[cfg_name]
+        self.name, self.T, self.n = cfg_name, temperature, n_streams
+        ds, ts = seedgen.SHAPES[self.cfg["draft"]], seedgen.SHAPES[self.cfg["target"]]
+        self.L_full = ts["n_layers"]
+        self.tl = min(target_layers, ts["n_layers"])
+        self.dW = seedgen.model_weights(ds, seedgen.DRAFT_SEED)
+        self.tW = seedgen.model_weights(dict(ts, n_layers=self.tl), seedgen.TARGET_SEED)
+        self.dsh, self.tsh = ll.LlamaShape(**ds), ll.LlamaShape(**dict(ts, n_layers=self.tl))
+        self.orc = SeedOracle(self.tsh, self.tW, self.dsh, self.dW, gamma=self.cfg["gamma"], temperature=temperature,
+                              seed=seedgen.PHILOX_SEED, max_new=10 ** 6)
+        rng = np.random.default_rng(0)
+        for i, p in enumerate(seedgen.prompts(cfg_name, n_streams=n_streams)):
+            self.orc.streams[i] = StreamState(sid=i, T=list(p), prompt_len=len(p),
+                                              tcache=_synthetic_cache(self.tsh, len(p) - 1, rng),
+                                              dcache=_synthetic_cache(self.dsh, len(p) - 1, rng))
+
+    def sample(self, r=0):
+        """One round (stream-local round r); returns (estimated s per full round, measured s, emitted)."""
+        from oracle import llama as ll
+        from oracle import sampling as sp
+        orc, g = self.orc, self.cfg["gamma"]
+        batch = list(range(self.n))
+        for s in batch:
+            orc.streams[s].r = r
+        t0 = time.perf_counter()
+        xs, zds, _ = orc.draft(batch)
+        t1 = time.perf_counter()
+        # the target layers (the LM head is timed once below, not scaled)
+        seqs = [([orc.streams[s].T[-1]] + xs[s], orc.streams[s].tcache) for s in batch]
+        ll.forward_batch(self.tsh, self.tW, seqs, mode="bf16", logits_rows=[[]] * len(seqs))
+        t2 = time.perf_counter()
+        xh = np.zeros((self.n * (g + 1), self.tsh.d_model))
+        zt_all = ll.f32_round(ll.norm_matmul(xh, ll._w(self.tW["final_norm"]), [ll._w(self.tW["lm_head"])],
+                                             self.tsh.rms_eps, True)[0])
+        t3 = time.perf_counter()
+        emitted = 0
+        for k, s in enumerate(batch):
+            zt = zt_all[k * (g + 1):(k + 1) * (g + 1)] + 0.1 * np.stack(zds[s] + [zds[s][-1]])   # synthetic rows
+            res = sp.verify_stream(zt, np.stack(zds[s]), xs[s], self.T, seedgen.PHILOX_SEED, s, r)
+            emitted += len(res.emitted)
+        t4 = time.perf_counter()
+        for s in batch:                      # roll the caches back to the prompt
+            st = orc.streams[s]
+            st.tcache.truncate(st.prompt_len - 1)
+            st.dcache.truncate(st.prompt_len - 1)
+        est = (t1 - t0) + (t2 - t1) * (self.L_full / self.tl) + (t3 - t2) + (t4 - t3)
+        return est, t4 - t0, emitted
+
+    def describe(self):
+        return (f"one {self.name} round, {self.n} streams (prefill replaced by synthetic caches of the prompts' "
+                f"lengths): full draft, target forward on {self.tl} of {self.L_full} layers (layer time "
+                f"x{self.L_full / self.tl:g}), final norm + LM head once, full verification on the draft rows + "
+                f"the head output")
 
 
 def config_of(args, cfg, n_local, world):
     """The workload description shared by both arms' JSON lines."""
     return {"workload": args.config, "streams_per_gpu": n_local, "gamma": cfg["gamma"], "draft": cfg["draft"],
-            "target": cfg["target"], "temperature": args.temperature, "parallelism": f"replicas x{world}",
+            "target": cfg["target"], "prompt_len": list(cfg["prompt_len"]), "temperature": args.temperature,
+            "parallelism": f"replicas x{world}",
             "l2": "inputs larger than L2: all target weights (13.2 GB at 7B) streamed every round"}
 
 
 def run_reference(args):
+    import torch
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     cfg = seedgen.CONFIGS[args.config]
     n = args.streams or cfg["n_streams"]
-    for _ in range(args.warmup):
-        oracle_round_sample(args.config, args.temperature, n, target_layers=1)
-    tot_t, tot_e = 0.0, 0
-    desc, cores = "", os.cpu_count()
-    for _ in range(args.steps):
-        t, e, desc, cores = oracle_round_sample(args.config, args.temperature, n, target_layers=1)
-        tot_t += t
-        tot_e += e
-    v = tot_e / tot_t
+    smp = OracleSampler(args.config, args.temperature, n)
+    for w in range(args.warmup):
+        smp.sample(r=w)
+    est, meas, emitted = [], [], 0
+    for k in range(args.steps):
+        t, m, e = smp.sample(r=args.warmup + k)
+        est.append(t)
+        meas.append(m)
+        emitted += e
+    v = emitted / sum(est)
     line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(meas) / args.steps,
+            "ms_per_round_estimate": 1e3 * sum(est) / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_of(args, cfg, n, int(os.environ.get("WORLD_SIZE", "1"))),
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": torch.get_num_threads(), "kind": "oracle",
+                             "cpu": cpu_model(),
+                             "sample": smp.describe() + "; ms_per_step is the measured time of one sample, value = "
+                                                        "emitted tokens / estimated full-round time"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ GPU arm
+def exposed_by_kind(tr):
+    """Critical-path time per launch kind from one round's device trace: launch i owns
+    [max(release_i, end_{i-1}), end_i] -- a partition of the round's traced timeline (PDL overlaps
+    each kernel's prologue and prefetch with its predecessor; that time is the predecessor's)."""
+    out = {1: 0.0, 2: 0.0}
+    prev = None
+    for s, r, e, k in tr:
+        beg = max(r, prev) if prev is not None else r
+        out[int(k)] = out.get(int(k), 0.0) + max(0, e - beg)
+        prev = e if prev is None else max(prev, e)
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -228,7 +304,7 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     def one_round():
-        b = eng.schedule()
+        b = eng.schedule()     # every rank runs every round (an empty batch still joins the exchange)
         eng.draft(b)
         eng.verify(b)
         return len(b)
@@ -251,38 +327,46 @@ def run_ours(args):
     launches = eng.profile()["kernel_launches"]
     ms = e0.elapsed_time(e1)
     emitted = sum(eng.stream_info(gid)["L"] - t_before[gid] for gid in my_ids)
-    alpha_rounds = emitted / (steps * len(my_ids))
+    per_stream_round = emitted / (steps * len(my_ids))
 
-    # e2e: the same rounds through seed_round_host (host in, host out)
+    # e2e: the same rounds through the public host-buffer call seed_round_host (batch ids in,
+    # emitted tokens + counts out, every round), wall clock around the K rounds
     for _ in range(warm):
         eng.round_host(eng.schedule())
     eng.schedule(0)
     t2 = {gid: eng.stream_info(gid)["L"] for gid in my_ids}
     barrier()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
     h2d = d2h = 0
+    w0 = time.perf_counter()
     for _ in range(steps):
         b = eng.schedule()
         eng.round_host(b)
         h2d += 4 * len(b)
         d2h += 4 * len(b) * (g + 2)
-    f1.record(stream)
+    eng.schedule(0)
+    w1 = time.perf_counter()
     barrier()
-    ms_e2e = f0.elapsed_time(f1)
+    ms_e2e = (w1 - w0) * 1e3
     emitted_e2e = sum(eng.stream_info(gid)["L"] - t2[gid] for gid in my_ids)
 
-    # roofline of K2 from separate, profiled rounds (device %globaltimer records per launch)
-    eng.schedule(0)
+    # roofline of K2 from separate, profiled rounds: device %globaltimer records of every GEMM and
+    # attention launch; each launch owns its critical-path interval (exposed_by_kind)
     eng.set_profile(True)
     one_round()
     eng.schedule(0)
     eng.reset_profile()
+    k2_ns, k3_ns, round_ns = [], [], []
     for _ in range(prof_rounds):
         one_round()
-    eng.schedule(0)
+        eng.schedule(0)
+        tr = eng.launch_trace()
+        ex = exposed_by_kind(tr)
+        k2_ns.append(ex.get(1, 0.0))
+        k3_ns.append(ex.get(2, 0.0))
+        round_ns.append(float(tr[:, 2].max() - tr[:, 0].min()))
     torch.cuda.synchronize()
     prof = eng.profile()
+    eng.set_profile(False)
 
     # max over ranks of the device time, sum of the work
     vals = torch.tensor([ms, ms_e2e, float(emitted), float(emitted_e2e)], dtype=torch.float64, device="cuda")
@@ -294,32 +378,45 @@ def run_ours(args):
         vals = torch.cat([mx, sm])
     ms, ms_e2e, emitted, emitted_e2e = vals.tolist()
     hbm, tf, peak_src = measured_peaks()
-    gemm_avg_ms = prof["gemm_ms"] / max(prof["gemm_launches"], 1)
-    gemm_bytes = prof["gemm_bytes"] / max(prof["gemm_launches"], 1)
-    achieved = gemm_bytes / (gemm_avg_ms * 1e-3) / 1e9
+    n_gemm = max(prof["gemm_launches"], 1)
+    bytes_per_launch = prof["gemm_bytes"] / n_gemm
+    launches_per_round = n_gemm / prof_rounds
+    k2_us = statistics.median(k2_ns) * 1e-3 / launches_per_round        # exposed time per K2 launch
+    achieved = bytes_per_launch / (k2_us * 1e-6) / 1e9
+    rel_us = prof["gemm_ms"] / n_gemm * 1e3                              # release -> end per launch
+    step_ms = ms / steps
     line = {
         "metric": METRIC, "value": emitted / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": steps,
-        "warmup": warm, "ms_per_step": ms / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "warmup": warm, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init weights, seedgen prompts)",
         "config": config_of(args, cfg, n_local, world),
-        "emitted_per_stream_round": alpha_rounds,
+        "emitted_per_stream_round": per_stream_round,
+        "verified_positions_per_s": world * n_local * (g + 1) / (step_ms * 1e-3),
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "kernel": "gemm_splitk_kernel (K2)", "achieved": achieved, "peak": hbm,
                      "unit": "GB/s", "frac": achieved / hbm, "peak_source": peak_src,
-                     "traffic": traffic_from_profiles(), "launches": prof["gemm_launches"],
-                     "gemm_share_of_step": (prof["gemm_ms"] / prof_rounds) / (ms / steps) if world == 1 else None,
-                     "bytes_per_launch": gemm_bytes, "avg_launch_us": gemm_avg_ms * 1e3,
-                     "timing": "device %globaltimer per launch: dependency release -> last CTA end "
-                               "(the weight prefetch overlapped with the predecessor under PDL is not counted), "
-                               f"over {prof_rounds} profiled rounds run after the timed ones",
-                     "avg_span_us": prof["gemm_span_ms"] / max(prof["gemm_launches"], 1) * 1e3},
-        "e2e": {"value": emitted_e2e / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d // steps,
-                "d2h_bytes_per_step": d2h // steps},
+                     "traffic": traffic_from_profiles(args.config), "bytes_per_launch": bytes_per_launch,
+                     "launches_per_round": launches_per_round, "exposed_us_per_launch": k2_us,
+                     "timing": ("device %globaltimer over " + str(prof_rounds) + " profiled rounds after the timed "
+                                "ones: each GEMM launch is charged its critical-path interval [max(its release, "
+                                "the previous launch's end), its end], so the weight prefetch it overlaps with its "
+                                "predecessor is the predecessor's time; share = K2 time / traced round span"),
+                     "k2_share_of_round": statistics.median(k2_ns) / statistics.median(round_ns),
+                     "k3_share_of_round": statistics.median(k3_ns) / statistics.median(round_ns),
+                     "frac_release_to_end": bytes_per_launch / (rel_us * 1e-6) / 1e9 / hbm,
+                     "frac_round_level": (launches_per_round * bytes_per_launch) / (step_ms * 1e-3) / 1e9 / hbm},
+        "e2e": {"value": emitted_e2e / (ms_e2e * 1e-3), "unit": UNIT, "ms_per_step": ms_e2e / steps,
+                "h2d_bytes_per_step": h2d // steps, "d2h_bytes_per_step": d2h // steps,
+                "timing": "wall clock (perf_counter) around the K seed_round_host rounds, host-synchronised"},
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        t, e, desc, cores = oracle_round_sample(args.config, args.temperature, n_local)
-        line["cpu_baseline"] = {"value": e / t, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+        import torch as _t
+        smp = OracleSampler(args.config, args.temperature, n_local)
+        runs = [smp.sample(r=k) for k in range(3)]
+        est = statistics.median(x[0] for x in runs)
+        line["cpu_baseline"] = {"value": runs[0][2] / est, "unit": UNIT, "cores": _t.get_num_threads(),
+                                "kind": "oracle", "cpu": cpu_model(), "sample": smp.describe() + "; median of 3"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     eng.close()

@@ -93,7 +93,8 @@ typedef struct {
   int32_t max_streams;                   /* resident streams (stream slots) */
   int32_t max_batch;                     /* capacity C per round (R11) */
   int32_t max_ctx;                       /* longest |T_s| + gamma + 1 supported */
-  int32_t page_tokens;                   /* KV page size in tokens (16 if 0) */
+  int32_t page_tokens;                   /* KV page size in tokens: 16 (if 0), 32, 64, 128 or 256 -- a page
+                                            holds whole 16-key attention tiles; anything else: EINVAL */
   int64_t kv_pool_bytes;                 /* KV pool size; 0 = enough for max_streams x max_ctx */
   int32_t rank, world;                   /* data-parallel replica index / count (replicas, R20) */
   const void* nccl_id;                   /* 128-byte ncclUniqueId (same on all ranks) or NULL if world == 1 */
@@ -105,17 +106,18 @@ typedef struct {
 SEED_API seed_status seed_init(const seed_config* cfg, seed_ctx* out);
 
 /* Alg. 1 "Initialize": prefill both models with the prefix and enqueue the stream
- * FCFS with ready = 1.  prefix_host: host int32 token ids, len >= 2, ids < vocab.
- * Synchronous with respect to `stream` (returns after the prefill is enqueued). */
+ * FCFS with ready = 1.  prefix_host: host int32 token ids, len >= 2 (R30), ids < vocab;
+ * global_id < 2^31, not already present on this rank (a removed id may be added again).
+ * Synchronous with respect to `stream`.  ESTATE between seed_draft_round and seed_verify. */
 SEED_API seed_status seed_add_stream(seed_ctx ctx, uint32_t global_id, const int32_t* prefix_host,
                             int32_t len, void* stream);
 
 /* ToT siblings (Alg. 2 line P:738: the n thoughts of a state share its prefix; §4.1 "the input
  * instructions are the same"): adds stream `global_id` with the same prefix as `src_global_id`
- * from src's prefilled K/V instead of recomputing the prefill: pages holding only prefix
- * positions (index < (len-1)/page_tokens) are SHARED (refcounted; rounds never write below
- * position len-1), the page holding position len-1 is copied on the device (cudaMemcpyAsync on
- * `stream`).  The new stream is bit-identical to seed_add_stream(global_id, same prefix); both
+ * from src's prefilled K/V instead of recomputing the prefill: pages holding only positions
+ * < len-2 (index < (len-2)/page_tokens) are SHARED (refcounted; rounds write positions >= len-2:
+ * the draft's first step rewrites len-2, R22), the page holding position len-2 is copied on the
+ * device (cudaMemcpyAsync on `stream`).  The new stream is bit-identical to seed_add_stream(global_id, same prefix); both
  * streams run and are removed independently (a page returns to the pool with its last
  * reference).  Errors: unknown src or
  * duplicate id -> EINVAL; src has already run a round -> ESTATE (not poisoning); no free slot ->
@@ -125,14 +127,20 @@ SEED_API seed_status seed_fork_stream(seed_ctx ctx, uint32_t src_global_id, uint
 /* a1: completes the previous round on the host (waits for its counts), re-enqueues undone
  * streams at the tail in batch order, then pops up to min(cap, max_batch)
  * ready, undone streams FCFS (ties -> lowest global id, R10).
- * batch_ids: host buffer of `cap` int32 (global ids).  *n = 0 when every stream is done. */
+ * batch_ids: host buffer of `cap` int32 (global ids).  *n = 0 when every own stream is done.
+ * Returns SEED_EDEVICE (after scheduling normally) when the completed round raised the device
+ * error word (seed_device_status). */
 SEED_API seed_status seed_schedule_round(seed_ctx ctx, int32_t* batch_ids, int32_t cap, int32_t* n);
 
 /* a2: gamma draft steps for the batch (K1: batched draft forward + Philox race sampler).
- * batch_ids: host array of n global ids returned by seed_schedule_round. */
+ * batch_ids: host array of n global ids returned by seed_schedule_round; n = 0 is allowed (a
+ * rank whose streams are done still takes part in the round's exchange, world > 1). */
 SEED_API seed_status seed_draft_round(seed_ctx ctx, const int32_t* batch_ids, int32_t n, void* stream);
 
 /* a3-a6: target verify forward, fused vocabulary kernel, rollback, all-gather.
+ * World > 1: EVERY rank calls seed_draft_round + seed_verify EVERY round (n = 0 once its own
+ * streams are done: it then contributes an empty exchange block) until seed_global_pending
+ * reports 0 -- the all-gather is collective.
  * out_tok: device int32 [n][gamma+1]: x_1..x_a, y, then -1 padding (R1; Alg. 1 emits
  *          x_1..x_gamma only when bonus = 0 and a = gamma).
  * out_cnt: device int32 [n]: tokens emitted this round (before truncation to l).
@@ -154,10 +162,25 @@ SEED_API seed_status seed_get_tokens(seed_ctx ctx, uint32_t global_id, int32_t* 
  * pages held, slot. */
 SEED_API seed_status seed_stream_info(seed_ctx ctx, uint32_t global_id, int32_t* info);
 
-/* Frees the stream's pages and slot (pruned ToT node). */
+/* Frees the stream's pages and slot (pruned ToT node) and forgets the id (scheduler entry and
+ * tokens: read them with seed_get_tokens first).  ESTATE between seed_draft_round and seed_verify. */
 SEED_API seed_status seed_remove_stream(seed_ctx ctx, uint32_t global_id);
 
-/* Forward of one model over `tokens` from an empty cache (debug / parity):
+/* Streams not yet done on ALL ranks after the last completed round (the sum of the undone counts
+ * every rank posted in its exchange block); world == 1 before any round: this rank's count.
+ * Completes the pending round first.  The loop of a multi-GPU run:
+ *   do { n = schedule(); draft(n); verify(n); } while (global_pending() > 0)
+ * stops on the same round on every rank. */
+SEED_API seed_status seed_global_pending(seed_ctx ctx, int64_t* n);
+
+/* Device error word (SEED_EDEVICE, cumulative since seed_init): bit 0 (1) a token id outside
+ * [0, vocab) reached an embedding gather (the row read id 0 instead); bit 1 (2) a sampling race
+ * found no finite key (non-finite logits).  fallbacks: K4 empty-residual fallbacks (R3: p <= q
+ * everywhere after rounding; the bonus rule on the same row is used, as in the oracle). */
+SEED_API seed_status seed_device_status(seed_ctx ctx, uint32_t* bits, int64_t* fallbacks);
+
+/* Forward of one model over `tokens` from an empty cache (debug / parity; ESTATE between
+ * seed_draft_round and seed_verify):
  * which = 0 draft, 1 target; logits_dev: device fp32 [n][vocab]. Synchronous w.r.t. stream. */
 SEED_API seed_status seed_forward_logits(seed_ctx ctx, int32_t which, const int32_t* tokens_host, int32_t n,
                                 float* logits_dev, void* stream);
@@ -211,6 +234,8 @@ SEED_API seed_status seed_sched_pop(seed_sched s, int32_t* out, int32_t cap, int
 /* after verification: ready = 1; undone ids re-enter at the tail in batch order */
 SEED_API seed_status seed_sched_complete(seed_sched s, const int32_t* batch, const int32_t* done, int32_t n);
 SEED_API int32_t seed_sched_all_done(seed_sched s);
+/* forget an id entirely (queue entry, ready / done flags): a removed stream's id may be re-added */
+SEED_API seed_status seed_sched_remove(seed_sched s, int32_t id);
 SEED_API void seed_sched_destroy(seed_sched s);
 
 /* Token table merged from per-rank round records (a6).  Record layout (int32):
@@ -219,7 +244,44 @@ typedef struct seed_table_s* seed_table;
 SEED_API seed_status seed_table_create(int32_t record_stride, seed_table* out);
 SEED_API seed_status seed_table_merge(seed_table t, const int32_t* records, int32_t n_records);
 SEED_API seed_status seed_table_get(seed_table t, uint32_t global_id, int32_t* dst, int32_t cap, int32_t* len);
+SEED_API seed_status seed_table_erase(seed_table t, uint32_t global_id);
 SEED_API void seed_table_destroy(seed_table t);
+
+/* Round book of one rank (H1 + a5 + a6): the host state seed_schedule_round /
+ * seed_verify drive inside a context, exported so the multi-rank protocol runs on CPU too.
+ *   own streams: validated tokens T, L (new tokens, done at l = max_new, R7), r (stream-local
+ *   round, R5); the FCFS scheduler; the token table of other ranks' streams.
+ * Exchange block (int32, seed_book_block_ints() = cap * (gamma + 3) + 1 words): cap records
+ *   [gid, c, tok_0 .. tok_gamma] (c tokens committed this round after truncation to l; padding
+ *   records have gid = -1), then one word: this rank's streams still undone after the round.
+ * Protocol (every rank, every round, in lock step): schedule (a batch, possibly empty) ->
+ *   the round -> pack (device: K5) -> all-gather of the blocks in rank order -> complete.
+ *   Stop when seed_book_global_pending() == 0: the same value on every rank (it sums the gathered
+ *   tails), so no rank leaves a collective the others still enter. */
+typedef struct seed_book_s* seed_book;
+SEED_API seed_status seed_book_create(int32_t gamma, int32_t max_new, int32_t cap, int32_t world, int32_t rank,
+                                      seed_book* out);
+/* register one of this rank's streams (prefix host int32, len >= 1; duplicate id -> EINVAL) */
+SEED_API seed_status seed_book_add(seed_book b, uint32_t global_id, const int32_t* prefix, int32_t len);
+SEED_API seed_status seed_book_remove(seed_book b, uint32_t global_id);
+/* a1: FCFS pop of <= min(cap, book cap) ready, undone own streams; *n = 0 once all are done */
+SEED_API seed_status seed_book_schedule(seed_book b, int32_t* ids, int32_t cap, int32_t* n);
+/* a5 record formation on the host (the device path's K5 writes the same block): out_tok
+ * [n][gamma+1], out_cnt [n] as seed_verify returns them; block: seed_book_block_ints() words.
+ * Does not change the book (seed_book_complete applies the round). */
+SEED_API seed_status seed_book_pack(seed_book b, const int32_t* ids, int32_t n, const int32_t* out_tok,
+                                    const int32_t* out_cnt, int32_t* block);
+/* a6: apply the gathered blocks (world blocks, rank order): own records update T / L / r / done
+ * and requeue undone streams at the tail in batch order; other ranks' records go
+ * to the token table; the tails give the global pending count.  EINVAL on a malformed block. */
+SEED_API seed_status seed_book_complete(seed_book b, const int32_t* blocks, int32_t n_blocks);
+/* streams undone on all ranks after the last completed exchange; -1 before the first */
+SEED_API seed_status seed_book_global_pending(seed_book b, int64_t* n);
+SEED_API seed_status seed_book_tokens(seed_book b, uint32_t global_id, int32_t* dst, int32_t cap, int32_t* len);
+/* info[0..4] = |T|, L, r, done, prompt length (own streams; ENOTFOUND otherwise) */
+SEED_API seed_status seed_book_info(seed_book b, uint32_t global_id, int32_t* info);
+SEED_API int32_t seed_book_block_ints(seed_book b);
+SEED_API void seed_book_destroy(seed_book b);
 
 #ifdef __cplusplus
 }

@@ -140,6 +140,18 @@ class SeedEngine:
     def remove_stream(self, gid):
         self._check(self.lib.seed_remove_stream(self.ctx, int(gid)), "seed_remove_stream")
 
+    def global_pending(self):
+        """Streams undone on all ranks after the last completed round (seed_global_pending)."""
+        n = C.c_int64(0)
+        self._check(self.lib.seed_global_pending(self.ctx, C.byref(n)), "seed_global_pending")
+        return n.value
+
+    def device_status(self):
+        """(error bits seen since init, K4 empty-residual fallbacks) -- seed_device_status."""
+        bits, fb = C.c_uint32(0), C.c_int64(0)
+        self._check(self.lib.seed_device_status(self.ctx, C.byref(bits), C.byref(fb)), "seed_device_status")
+        return bits.value, fb.value
+
     def forward_logits(self, which, tokens, stream=None):
         a, p = _i32(tokens)
         out = torch.empty((len(a), self.vocab), dtype=torch.float32, device="cuda")
@@ -169,6 +181,15 @@ class SeedEngine:
         self._check(self.lib.seed_gemm_trace(self.ctx, buf.ctypes.data_as(C.POINTER(C.c_uint64)), cap, C.byref(n)),
                     "seed_gemm_trace")
         return buf[:4 * n.value].reshape(-1, 4)[:, :3].astype(np.int64)
+
+    def launch_trace(self, cap=8192):
+        """[(start, release, end, kind)] globaltimer ns of every traced launch of the last round
+        (profile=True): kind 1 = K2 GEMM, 2 = K3 attention; rows in launch order."""
+        buf = np.zeros(4 * cap, dtype=np.uint64)
+        n = C.c_int32(0)
+        self._check(self.lib.seed_gemm_trace(self.ctx, buf.ctypes.data_as(C.POINTER(C.c_uint64)), cap, C.byref(n)),
+                    "seed_gemm_trace")
+        return buf[:4 * n.value].reshape(-1, 4).astype(np.int64)
 
     def gemm_cta_trace(self, launch):
         """Raw per-CTA phase words (8192) of one launch (profile=True, SEED_CTA_TRACE=1); see seed.h."""
@@ -268,6 +289,70 @@ class TokenTable:
             self.h = None
 
 
+class RoundBook:
+    """One rank's host round bookkeeping (seed_book_*): scheduler, own streams' tokens, the exchange
+    block of the per-round all-gather and its merge.  Usable without a GPU (multi-rank CPU tests)."""
+
+    def __init__(self, gamma, max_new, cap, world=1, rank=0):
+        self.lib = _lib.load()
+        self.gamma = int(gamma)
+        h = C.c_void_p()
+        check(self.lib.seed_book_create(int(gamma), int(max_new), int(cap), int(world), int(rank), C.byref(h)), None,
+              "seed_book_create")
+        self.h = h
+        self.block_ints = int(self.lib.seed_book_block_ints(h))
+
+    def add(self, gid, prefix):
+        a, p = _i32(prefix)
+        check(self.lib.seed_book_add(self.h, int(gid), p, len(a)), None, "seed_book_add")
+
+    def remove(self, gid):
+        check(self.lib.seed_book_remove(self.h, int(gid)), None, "seed_book_remove")
+
+    def schedule(self, cap):
+        buf = np.zeros(max(int(cap), 1), dtype=np.int32)
+        n = C.c_int32(0)
+        check(self.lib.seed_book_schedule(self.h, buf.ctypes.data_as(_lib._I32P), int(cap), C.byref(n)), None,
+              "seed_book_schedule")
+        return buf[:n.value].tolist()
+
+    def pack(self, ids, out_tok, out_cnt):
+        a, p = _i32(ids)
+        t, tp = _i32(np.asarray(out_tok, dtype=np.int32).reshape(-1) if len(a) else np.zeros(1, np.int32))
+        c, cp = _i32(out_cnt if len(a) else [0])
+        blk = np.zeros(self.block_ints, dtype=np.int32)
+        check(self.lib.seed_book_pack(self.h, p, len(a), tp, cp, blk.ctypes.data_as(_lib._I32P)), None,
+              "seed_book_pack")
+        return blk
+
+    def complete(self, blocks):
+        b = np.ascontiguousarray(blocks, dtype=np.int32).reshape(-1)
+        check(self.lib.seed_book_complete(self.h, b.ctypes.data_as(_lib._I32P), b.size // self.block_ints), None,
+              "seed_book_complete")
+
+    def global_pending(self):
+        n = C.c_int64(0)
+        check(self.lib.seed_book_global_pending(self.h, C.byref(n)), None, "seed_book_global_pending")
+        return n.value
+
+    def tokens(self, gid, cap=1 << 16):
+        buf = np.zeros(cap, dtype=np.int32)
+        n = C.c_int32(0)
+        check(self.lib.seed_book_tokens(self.h, int(gid), buf.ctypes.data_as(_lib._I32P), cap, C.byref(n)), None,
+              "seed_book_tokens")
+        return buf[:n.value].tolist()
+
+    def info(self, gid):
+        info = np.zeros(5, dtype=np.int32)
+        check(self.lib.seed_book_info(self.h, int(gid), info.ctypes.data_as(_lib._I32P)), None, "seed_book_info")
+        return dict(zip(("T_len", "L", "r", "done", "prompt_len"), info.tolist()))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.seed_book_destroy(self.h)
+            self.h = None
+
+
 from . import ops  # noqa: E402
 
-__all__ = ["SeedEngine", "Scheduler", "TokenTable", "ops", "SeedError", "nccl_unique_id", "LAYER_KEYS"]
+__all__ = ["SeedEngine", "Scheduler", "TokenTable", "RoundBook", "ops", "SeedError", "nccl_unique_id", "LAYER_KEYS"]

@@ -52,6 +52,8 @@ _SIGS = {
     "seed_get_tokens": [_P, C.c_uint32, _I32P, C.c_int32, _I32P],
     "seed_stream_info": [_P, C.c_uint32, _I32P],
     "seed_remove_stream": [_P, C.c_uint32],
+    "seed_global_pending": [_P, C.POINTER(C.c_int64)],
+    "seed_device_status": [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_int64)],
     "seed_fork_stream": [_P, C.c_uint32, C.c_uint32, _P],
     "seed_forward_logits": [_P, C.c_int32, _I32P, C.c_int32, _P, _P],
     "seed_last_round_buffers": [_P, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)],
@@ -70,6 +72,19 @@ _SIGS = {
     "seed_sched_complete": [_P, _I32P, _I32P, C.c_int32],
     "seed_sched_all_done": [_P],
     "seed_sched_destroy": [_P],
+    "seed_sched_remove": [_P, C.c_int32],
+    "seed_table_erase": [_P, C.c_uint32],
+    "seed_book_create": [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)],
+    "seed_book_add": [_P, C.c_uint32, _I32P, C.c_int32],
+    "seed_book_remove": [_P, C.c_uint32],
+    "seed_book_schedule": [_P, _I32P, C.c_int32, _I32P],
+    "seed_book_pack": [_P, _I32P, C.c_int32, _I32P, _I32P, _I32P],
+    "seed_book_complete": [_P, _I32P, C.c_int32],
+    "seed_book_global_pending": [_P, C.POINTER(C.c_int64)],
+    "seed_book_tokens": [_P, C.c_uint32, _I32P, C.c_int32, _I32P],
+    "seed_book_info": [_P, C.c_uint32, _I32P],
+    "seed_book_block_ints": [_P],
+    "seed_book_destroy": [_P],
     "seed_table_create": [C.c_int32, C.POINTER(C.c_void_p)],
     "seed_table_merge": [_P, _I32P, C.c_int32],
     "seed_table_get": [_P, C.c_uint32, _I32P, C.c_int32, _I32P],
@@ -85,7 +100,8 @@ _SIGS = {
                               _P, _P, _P],
 }
 _RESTYPE = {"seed_last_error": C.c_char_p, "seed_destroy": None, "seed_sched_destroy": None,
-            "seed_table_destroy": None, "seed_sched_all_done": C.c_int32}
+            "seed_table_destroy": None, "seed_sched_all_done": C.c_int32, "seed_book_destroy": None,
+            "seed_book_block_ints": C.c_int32}
 
 _lib = None
 

@@ -21,6 +21,7 @@
 
 #include "../../include/seed.h"
 #include "../../include/seed_ops.h"
+#include "host_book.h"
 #include "kernels.h"
 
 using seed::GemmPlan;
@@ -140,11 +141,10 @@ struct Model {
   std::vector<bf16*> owned;
 };
 
-struct SlotState {  // host mirror of one stream slot
+struct SlotState {  // one stream slot; the validated tokens live in the round book (host_book.h)
   uint32_t gid = 0;
   bool used = false;
-  std::vector<int32_t> T;  // validated tokens
-  int prompt_len = 0, L = 0, r = 0, done = 0, len_t = 0, len_d = 0;
+  int len_t = 0, len_d = 0;   // KV entries of the target / draft cache (R6)
 };
 
 struct ChunkDesc {
@@ -160,7 +160,7 @@ struct ChunkDesc {
 struct RoundPlan {  // descriptors of one round at batch-size-determined arena offsets
   int n = 0;
   int64_t key_draft = 0, key_verify = 0;  // graph keys: batch size and attention chunk counts
-  size_t o_sid = 0, o_r = 0, o_sl = 0, o_last = 0;
+  size_t o_sid = 0, o_r = 0, o_sl = 0, o_last = 0, o_out = 0;  // o_out: undone own streams outside the batch
   std::vector<ChunkDesc> draft, verify;
   std::vector<int> verify_b0;
 };
@@ -177,15 +177,12 @@ struct seed_ctx_s {
   int dev = 0;
   Model dm, tm;                   // draft, target
   int P = 16, max_pages = 0, n_slots = 0;
-  float* partial = nullptr;
-  size_t partial_floats = 0;
   std::map<std::tuple<const void*, int, int>, CUtensorMap> xmaps;
   Arena arena;
   // stream registry
   std::vector<SlotState> slots;
   std::unordered_map<uint32_t, int> gid2slot;
-  seed_sched sched = nullptr;
-  seed_table table = nullptr;
+  seed_book book = nullptr;       // FCFS scheduler, own streams' tokens, other ranks' tokens (a1, a5, a6)
   // device state (K5)
   seed::StreamState ds{};
   // per-round buffers (capacity C = max_batch)
@@ -193,14 +190,20 @@ struct seed_ctx_s {
   float *tgt_logits = nullptr, *drf_logits = nullptr;
   int32_t *xs = nullptr, *vtok = nullptr, *out_tok = nullptr, *out_cnt = nullptr, *out_acc = nullptr;
   int32_t* verify_work = nullptr;  // K4 scratch [C][2 (gamma + 1) + 1] (tickets zero between launches)
-  int32_t *records = nullptr, *records_all = nullptr, *records_host = nullptr, *cnt_host = nullptr,
-          *tok_host = nullptr;
+  int32_t *records = nullptr, *records_all = nullptr, *records_host = nullptr;   // exchange blocks (a6)
+  int block_ints = 0;             // words per rank's block: C records of gamma + 3, then the undone count
+  // device error word (SEED_EDEVICE): [0] contract-violation bits, [1] empty-residual fallbacks (K4)
+  int32_t* dev_err = nullptr;
+  int32_t* err_host = nullptr;    // pinned copy, refreshed at the end of every verify
+  uint32_t err_bits_seen = 0;
+  int64_t fallbacks = 0;
   uint32_t* sids_dev = nullptr;
   int32_t* rs_dev = nullptr;
   int32_t* slots_dev = nullptr;
   cudaEvent_t round_done = nullptr;
   std::vector<int32_t> last_batch;  // global ids of the batch in flight
   std::vector<int32_t> drafted;     // batch drafted and not yet verified
+  bool draft_called = false;        // seed_draft_round called for `drafted` (n may be 0 when world > 1)
   RoundPlan plan;
   bool round_pending = false;
   // NCCL
@@ -266,7 +269,7 @@ seed_status run_gemm(seed_ctx ctx, const GemmPlan& p, int M, const seed::GemmIO&
     if (ctx->cta_rec) cta = ctx->cta_rec + (size_t)ctx->rec_used * kCtaRec;
     rec = ctx->timing_rec + 4 * ctx->rec_used++;
   }
-  CK(seed::gemm_run(p, M, io, ctx->partial, st, rec, cta));
+  CK(seed::gemm_run(p, M, io, st, rec, cta));
   if (ctx->in_round) {
     // algorithmic bytes: weights + bf16 X + output (fp32 Y; residual: read + write x, write bf16 h;
     // SwiGLU: bf16 act of half the width)
@@ -439,17 +442,6 @@ void free_model(Model& m) {
   if (m.aws.counters) cudaFree(m.aws.counters);
 }
 
-size_t max_partial(const Model& m, int M) {
-  size_t mx = seed::gemm_partial_floats(m.plm, M);
-  for (int l = 0; l < m.L; ++l) {
-    mx = std::max(mx, seed::gemm_partial_floats(m.pq[l], M));
-    mx = std::max(mx, seed::gemm_partial_floats(m.po[l], M));
-    mx = std::max(mx, seed::gemm_partial_floats(m.pgu[l], M));
-    mx = std::max(mx, seed::gemm_partial_floats(m.pd[l], M));
-  }
-  return mx;
-}
-
 // make sure `slot` holds pages for positions [0, n_tokens)
 seed_status ensure_pages(seed_ctx ctx, Model& m, int slot, int n_tokens, cudaStream_t st) {
   const int need = (n_tokens + ctx->P - 1) / ctx->P;
@@ -490,8 +482,8 @@ seed_status forward_chunk(seed_ctx ctx, Model& m, const ChunkDesc& c, cudaStream
   // the RMSNorm weight applied to the residual after layer l (B1, R24)
   auto next_norm = [&](int l) { return l + 1 < m.L ? m.an[l + 1] : m.final_norm; };
   // embedding (or the given residual), its per-tile sums of squares and h = bf16(x * attn_norm)
-  CK(seed::embed_stats(embed ? m.embed : nullptr, c.tok.dev, c.tok.stride, M, m.d, m.x, m.ssq_b,
-                       first_layer < m.L ? m.an[first_layer] : m.final_norm, m.h, st));
+  CK(seed::embed_stats(embed ? m.embed : nullptr, c.tok.dev, c.tok.stride, M, m.d, m.V, m.x, m.ssq_b,
+                       first_layer < m.L ? m.an[first_layer] : m.final_norm, m.h, ctx->dev_err, st));
   ctx->kernel_launches++;
   seed::SeqInfo seqs{c.q_start, c.q_len, c.kv_len, c.seq_slot, c.seq_stable};
   const CUtensorMap* tm_h = xmap(ctx, m.h, m.d, m.m_cap, M);
@@ -651,65 +643,69 @@ seed_status check_ctx(seed_ctx ctx) {
   return SEED_OK;
 }
 
-// host mirror of K5 (same formula, DESIGN R6/R7)
-void commit_host(seed_ctx ctx, SlotState& s, const int32_t* toks, int cnt) {
-  const int g = ctx->cfg.gamma;
-  const int t_before = (int)s.T.size();
-  const int c = std::min(cnt, std::max(ctx->cfg.max_new_tokens - s.L, 0));
-  s.T.insert(s.T.end(), toks, toks + c);
-  s.L += c;
-  s.r += 1;
-  s.len_t = (int)s.T.size() - 1;
-  s.len_d = std::min((int)s.T.size() - 1, t_before + g - 1);
-  s.done = s.L >= ctx->cfg.max_new_tokens;
-}
+seed::BookStream& stream_of(seed_ctx ctx, uint32_t gid) { return ctx->book->own.at(gid); }
 
+// a5 / a6 on the host, once round r's work completed on the device: the gathered exchange
+// blocks (K5 wrote this rank's, the all-gather the others') go to the round book -- own streams
+// commit their tokens and are requeued FCFS, other ranks' tokens go to the token
+// table, the undone counts give the global pending count -- and the KV lengths follow (R6).
+// A device contract violation (error word) is reported here as SEED_EDEVICE, without poisoning.
 seed_status complete_round(seed_ctx ctx) {
   if (!ctx->round_pending) return SEED_OK;
   CK(cudaEventSynchronize(ctx->round_done));
   ctx->round_pending = false;
-  const int g = ctx->cfg.gamma, stride = g + 3;
+  const int g = ctx->cfg.gamma;
   const int world = std::max(ctx->cfg.world, 1);
-  const int32_t* recs = ctx->records_host;
-  // own streams: update mirrors from our records (first C records of our rank)
-  const int B = (int)ctx->last_batch.size();
-  std::vector<int32_t> done(B);
-  for (int b = 0; b < B; ++b) {
-    const int32_t* rec = recs + ((size_t)ctx->cfg.rank * ctx->C + b) * stride;
-    SlotState& s = ctx->slots[ctx->gid2slot[(uint32_t)ctx->last_batch[b]]];
-    // rec[1] is already truncated; commit the untruncated count semantics via tokens
-    const int t_before = (int)s.T.size();
-    s.T.insert(s.T.end(), rec + 2, rec + 2 + rec[1]);
-    s.L += rec[1];
-    s.r += 1;
-    s.len_t = (int)s.T.size() - 1;
-    s.len_d = std::min((int)s.T.size() - 1, t_before + g - 1);
-    s.done = s.L >= ctx->cfg.max_new_tokens;
-    done[b] = s.done;
+  std::vector<int> t_before;
+  t_before.reserve(ctx->last_batch.size());
+  for (int32_t gid : ctx->last_batch) t_before.push_back((int)stream_of(ctx, (uint32_t)gid).T.size());
+  seed_status st = seed_book_complete(ctx->book, ctx->records_host, world);
+  if (st != SEED_OK) return fail(ctx, SEED_ESTATE, "seed_book_complete", "malformed exchange block");
+  for (size_t b = 0; b < ctx->last_batch.size(); ++b) {
+    const uint32_t gid = (uint32_t)ctx->last_batch[b];
+    const int T = (int)stream_of(ctx, gid).T.size();
+    SlotState& ss = ctx->slots[ctx->gid2slot[gid]];
+    ss.len_t = T - 1;                                  // keep T'[:-1]
+    ss.len_d = std::min(T - 1, t_before[b] + g - 1);   // the draft wrote up to |T| + gamma - 2
   }
-  seed_status st = seed_table_merge(ctx->table, recs, world * ctx->C);
-  if (st != SEED_OK) return fail(ctx, st, "seed_table_merge", "bad record");
-  st = seed_sched_complete(ctx->sched, ctx->last_batch.data(), done.data(), B);
-  if (st != SEED_OK) return fail(ctx, st, "seed_sched_complete", "");
   ctx->last_batch.clear();
+  const uint32_t bits = (uint32_t)ctx->err_host[0];
+  ctx->fallbacks = ctx->err_host[1];
+  if (bits) {
+    ctx->err_bits_seen |= bits;
+    CK(cudaMemset(ctx->dev_err, 0, sizeof(int32_t)));
+    ctx->err_host[0] = 0;
+    char msg[256];
+    snprintf(msg, sizeof(msg),
+             "device contract violation (error word 0x%x): 1 = token id out of range at an embedding gather (read "
+             "as id 0), 2 = a race over no finite key (non-finite logits)", bits);
+    ctx->err = msg;
+    return SEED_EDEVICE;
+  }
   return SEED_OK;
 }
 
 // finish any round work in flight before the descriptor arena is reused outside a round
+// (a device error word found here stays visible through seed_device_status)
 seed_status quiesce(seed_ctx ctx) {
   if (ctx->gstream) CK(cudaStreamSynchronize(ctx->gstream));
-  if (ctx->round_pending) return complete_round(ctx);
+  if (ctx->round_pending) {
+    const seed_status s = complete_round(ctx);
+    return s == SEED_EDEVICE ? SEED_OK : s;
+  }
   return SEED_OK;
 }
 
 seed_status map_batch(seed_ctx ctx, const int32_t* ids, int n, std::vector<int>& slots) {
-  if (n < 1 || n > ctx->C || !ids) return fail(ctx, n > ctx->C ? SEED_ECAPACITY : SEED_EINVAL, "batch", "size");
+  if (n < 0 || n > ctx->C || (n > 0 && !ids)) return fail(ctx, n > ctx->C ? SEED_ECAPACITY : SEED_EINVAL, "batch", "size");
   slots.resize(n);
   for (int i = 0; i < n; ++i) {
     auto it = ctx->gid2slot.find((uint32_t)ids[i]);
     if (it == ctx->gid2slot.end()) return fail(ctx, SEED_ENOTFOUND, "batch", "unknown stream id");
     slots[i] = it->second;
-    if (ctx->slots[slots[i]].done) return fail(ctx, SEED_EINVAL, "batch", "stream already done");
+    if (stream_of(ctx, (uint32_t)ids[i]).done) return fail(ctx, SEED_EINVAL, "batch", "stream already done");
+    for (int k = 0; k < i; ++k)
+      if (ids[k] == ids[i]) return fail(ctx, SEED_EINVAL, "batch", "duplicate stream id");
   }
   return SEED_OK;
 }
@@ -718,8 +714,9 @@ seed_status map_batch(seed_ctx ctx, const int32_t* ids, int n, std::vector<int>&
 // All descriptors of a round (draft steps and verify chunks) are packed into the arena at
 // offsets that depend on the batch size only, so the captured graph of a batch size can be
 // replayed with fresh descriptor contents (R23).
-seed_status build_round_plan(seed_ctx ctx, const std::vector<int>& slots, int n, RoundPlan& P) {
-  const int g = ctx->cfg.gamma;
+seed_status build_round_plan(seed_ctx ctx, const std::vector<int32_t>& ids, const std::vector<int>& slots,
+                             RoundPlan& P) {
+  const int g = ctx->cfg.gamma, n = (int)ids.size();
   Arena& A = ctx->arena;
   A.begin();
   P.n = n;
@@ -727,26 +724,33 @@ seed_status build_round_plan(seed_ctx ctx, const std::vector<int>& slots, int n,
   P.o_r = A.alloc(n);
   P.o_sl = A.alloc(n);
   P.o_last = A.alloc(n);
-  if (P.o_last == (size_t)-1) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
+  P.o_out = A.alloc(1);
+  if (P.o_out == (size_t)-1) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
+  std::vector<const seed::BookStream*> bs(n);
   for (int b = 0; b < n; ++b) {
-    const SlotState& ss = ctx->slots[slots[b]];
-    A.host[P.o_sid + b] = (int32_t)ss.gid;
-    A.host[P.o_r + b] = ss.r;
+    bs[b] = &stream_of(ctx, (uint32_t)ids[b]);
+    A.host[P.o_sid + b] = ids[b];
+    A.host[P.o_r + b] = bs[b]->r;
     A.host[P.o_sl + b] = slots[b];
-    A.host[P.o_last + b] = ss.T.back();
+    A.host[P.o_last + b] = bs[b]->T.back();
   }
+  A.host[P.o_out] = (int32_t)(ctx->book->undone - n);   // K5 adds the batch's undone streams
+  P.draft.clear();
+  P.verify.clear();
+  P.verify_b0.clear();
+  P.key_draft = P.key_verify = 0;
+  if (n == 0) return SEED_OK;   // a rank with nothing to run still joins the exchange (world > 1)
   const int max_pos = ctx->cfg.max_ctx + g + 2;
   // draft step 1 feeds (T[-2], T[-1]); when one token is pending the first row rewrites an
   // existing entry with identical values (R22), so M = 2n every round
   P.draft.assign(g, ChunkDesc{});
   std::vector<Segment> segs(n);
   for (int b = 0; b < n; ++b) {
-    const SlotState& ss = ctx->slots[slots[b]];
-    const int T = (int)ss.T.size();
+    const int T = (int)bs[b]->T.size();
     const size_t to = A.alloc(2);
     if (to == (size_t)-1) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
-    A.host[to] = ss.T[T - 2];
-    A.host[to + 1] = ss.T[T - 1];
+    A.host[to] = bs[b]->T[T - 2];
+    A.host[to + 1] = bs[b]->T[T - 1];
     segs[b] = Segment{slots[b], T - 2, 2, (int)to, T - 2};
   }
   size_t tok_off;
@@ -754,21 +758,19 @@ seed_status build_round_plan(seed_ctx ctx, const std::vector<int>& slots, int n,
     return fail(ctx, SEED_ECAPACITY, "seed_draft_round", "batch too large");
   for (int j = 2; j <= g; ++j) {
     for (int b = 0; b < n; ++b) {
-      const int T = (int)ctx->slots[slots[b]].T.size();
+      const int T = (int)bs[b]->T.size();
       segs[b] = Segment{slots[b], T + j - 2, 1, -1, T - 2};
     }
     if (!pack_chunk(ctx, segs, 2, &P.draft[j - 1], &tok_off)) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
     P.draft[j - 1].tok = TokSrc{ctx->xs + (j - 2), g};  // x_{j-1} of every stream ([B][g] layout)
   }
   // verify chunks of whole streams
-  P.verify.clear();
-  P.verify_b0.clear();
   const int per_chunk = std::max(1, kMaxChunkRows / (g + 1));
   for (int b0 = 0; b0 < n; b0 += per_chunk) {
     const int nb = std::min(per_chunk, n - b0);
     std::vector<Segment> vs(nb);
     for (int b = 0; b < nb; ++b) {
-      const int T = (int)ctx->slots[slots[b0 + b]].T.size();
+      const int T = (int)bs[b0 + b]->T.size();
       vs[b] = Segment{slots[b0 + b], T - 1, g + 1, -1, T - 1};
     }
     ChunkDesc c;
@@ -779,9 +781,9 @@ seed_status build_round_plan(seed_ctx ctx, const std::vector<int>& slots, int n,
     P.verify.push_back(c);
     P.verify_b0.push_back(b0);
   }
-  // attention grids sized by the round's longest context, rounded up to whole chunks; the
-  // graphs are keyed by (batch size, chunk counts), so a graph is re-captured only when a
-  // context crosses a chunk boundary (R23)
+  // attention grids sized by the round's longest context, rounded up to whole splits; the
+  // graphs are keyed by (batch size, split counts), so a graph is re-captured only when a
+  // context crosses a split boundary (R23)
   const int ch = seed::attn_chunk_tokens();
   int dk = 0, vk = 0;
   for (auto& c : P.draft) dk = std::max(dk, c.max_kv);
@@ -801,6 +803,7 @@ seed_status enqueue_draft(seed_ctx ctx, cudaStream_t st) {
   Arena& A = ctx->arena;
   seed_status s;
   CK(cudaMemcpyAsync(A.dev, A.host, A.used * 4, cudaMemcpyHostToDevice, st));
+  if (n == 0) return SEED_OK;
   CK(cudaMemcpyAsync(ctx->sids_dev, A.dev + P.o_sid, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(ctx->rs_dev, A.dev + P.o_r, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(ctx->slots_dev, A.dev + P.o_sl, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
@@ -814,7 +817,7 @@ seed_status enqueue_draft(seed_ctx ctx, cudaStream_t st) {
     if ((s = forward_chunk(ctx, ctx->dm, c, st)) != SEED_OK) return s;
     // K1 sampler: x_j -> xs[b][j-1] and the verify input vtok[b][j]
     CK(seed::draft_sample(c.Y, (long)g * V, n, V, ctx->cfg.temperature, k0, k1, ctx->sids_dev, ctx->rs_dev, j,
-                          ctx->xs + (j - 1), g, ctx->vtok + j, g + 1, st));
+                          ctx->xs + (j - 1), g, ctx->vtok + j, g + 1, ctx->dev_err, st));
     ctx->kernel_launches++;
   }
   return SEED_OK;
@@ -826,34 +829,38 @@ seed_status enqueue_verify(seed_ctx ctx, cudaStream_t st) {
   seed_status s;
   for (auto& c : P.verify)
     if ((s = forward_chunk(ctx, ctx->tm, c, st)) != SEED_OK) return s;
-  // a4: K4 fused vocabulary kernel
-  seed::VerifyArgs a{};
-  a.zt = ctx->tgt_logits;
-  a.zd = ctx->drf_logits;
-  a.xs = ctx->xs;
-  a.zt_stride_b = (long)(g + 1) * V;
-  a.zd_stride_b = (long)g * V;
-  a.B = n;
-  a.gamma = g;
-  a.V = V;
-  a.T = ctx->cfg.temperature;
-  a.k0 = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu);
-  a.k1 = (uint32_t)(ctx->cfg.seed >> 32);
-  a.sids = ctx->sids_dev;
-  a.rs = ctx->rs_dev;
-  a.bonus = ctx->cfg.bonus;
-  a.out_tok = ctx->out_tok;
-  a.out_cnt = ctx->out_cnt;
-  a.out_acc = ctx->out_acc;
-  a.work = ctx->verify_work;
-  CK(seed::vocab_verify(a, st));
-  // a5: K5 commit + rollback, emit the exchange records
+  if (n > 0) {
+    // a4: K4 fused vocabulary kernel
+    seed::VerifyArgs a{};
+    a.zt = ctx->tgt_logits;
+    a.zd = ctx->drf_logits;
+    a.xs = ctx->xs;
+    a.zt_stride_b = (long)(g + 1) * V;
+    a.zd_stride_b = (long)g * V;
+    a.B = n;
+    a.gamma = g;
+    a.V = V;
+    a.T = ctx->cfg.temperature;
+    a.k0 = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu);
+    a.k1 = (uint32_t)(ctx->cfg.seed >> 32);
+    a.sids = ctx->sids_dev;
+    a.rs = ctx->rs_dev;
+    a.bonus = ctx->cfg.bonus;
+    a.out_tok = ctx->out_tok;
+    a.out_cnt = ctx->out_cnt;
+    a.out_acc = ctx->out_acc;
+    a.work = ctx->verify_work;
+    a.err = ctx->dev_err;
+    CK(seed::vocab_verify(a, st));
+    ctx->kernel_launches++;
+  }
+  // a5: K5 commit + rollback and this rank's exchange block (records, then the undone count)
   const int world = std::max(ctx->cfg.world, 1);
-  const size_t rec_bytes = (size_t)ctx->C * (g + 3) * 4;
-  CK(cudaMemsetAsync(ctx->records, 0xFF, rec_bytes, st));
+  const size_t blk_bytes = (size_t)ctx->block_ints * 4;
+  CK(cudaMemsetAsync(ctx->records, 0xFF, blk_bytes, st));
   CK(seed::rollback_commit(ctx->ds, ctx->slots_dev, n, g, ctx->out_tok, ctx->out_cnt, ctx->cfg.max_new_tokens,
-                           ctx->records, ctx->sids_dev, st));
-  ctx->kernel_launches += 2;
+                           ctx->records, ctx->C, ctx->sids_dev, ctx->arena.dev + P.o_out, st));
+  ctx->kernel_launches++;
   if (ctx->profile) {
     // draft records live in [0, half), verify records in [half, ...)
     const int half = ctx->rec_cap / 2;
@@ -865,13 +872,15 @@ seed_status enqueue_verify(seed_ctx ctx, cudaStream_t st) {
                                ctx->timing_last + 4 * (size_t)half, st));
     ctx->kernel_launches += 2;
   }
-  // a6: all-gather of the per-rank records over NVLink (world > 1)
+  // the device error word travels with the round's results
+  CK(cudaMemcpyAsync(ctx->err_host, ctx->dev_err, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  // a6: all-gather of the per-rank exchange blocks over NVLink (world > 1)
   if (world > 1) {
-    if (g_nccl.allgather(ctx->records, ctx->records_all, (size_t)ctx->C * (g + 3), kNcclInt32, ctx->comm, st) != 0)
-      return fail(ctx, SEED_ENCCL, "ncclAllGather", "records");
-    CK(cudaMemcpyAsync(ctx->records_host, ctx->records_all, rec_bytes * world, cudaMemcpyDeviceToHost, st));
+    if (g_nccl.allgather(ctx->records, ctx->records_all, (size_t)ctx->block_ints, kNcclInt32, ctx->comm, st) != 0)
+      return fail(ctx, SEED_ENCCL, "ncclAllGather", "exchange blocks");
+    CK(cudaMemcpyAsync(ctx->records_host, ctx->records_all, blk_bytes * world, cudaMemcpyDeviceToHost, st));
   } else {
-    CK(cudaMemcpyAsync(ctx->records_host, ctx->records, rec_bytes, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(ctx->records_host, ctx->records, blk_bytes, cudaMemcpyDeviceToHost, st));
   }
   return SEED_OK;
 }
@@ -947,6 +956,38 @@ seed_status run_phase(seed_ctx ctx, int n, bool draft, cudaStream_t st) {
   return SEED_OK;
 }
 
+seed_status install_slot(seed_ctx ctx, int slot, uint32_t gid, const int32_t* prefix, int len, cudaStream_t st) {
+  SlotState& ss = ctx->slots[slot];
+  ss = SlotState();
+  ss.used = true;
+  ss.gid = gid;
+  ss.len_t = ss.len_d = len - 1;
+  // device state (K5 reads/writes it)
+  int32_t vals[6] = {len, len - 1, len - 1, 0, 0, 0};
+  int32_t* dst[6] = {ctx->ds.tlen, ctx->ds.len_t, ctx->ds.len_d, ctx->ds.L, ctx->ds.r, ctx->ds.done};
+  for (int i = 0; i < 6; ++i) CK(cudaMemcpyAsync(dst[i] + slot, &vals[i], 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ctx->ds.hist + (size_t)slot * ctx->ds.max_ctx, prefix, (size_t)len * 4, cudaMemcpyHostToDevice,
+                     st));
+  CK(cudaStreamSynchronize(st));
+  seed_status s = seed_book_add(ctx->book, gid, prefix, len);
+  if (s != SEED_OK) return fail(ctx, s, "seed_book_add", "");
+  ctx->gid2slot[gid] = slot;
+  return SEED_OK;
+}
+
+// calls that change streams or reuse the descriptor arena must not fall between seed_draft_round
+// and seed_verify (the planned round's descriptors and pages are in flight)
+seed_status check_between(seed_ctx ctx, const char* what) {
+  if (ctx->draft_called) return fail(ctx, SEED_ESTATE, what, "a drafted batch is not verified");
+  return SEED_OK;
+}
+
+int free_slot(seed_ctx ctx) {
+  for (int i = 0; i < ctx->cfg.max_streams; ++i)
+    if (!ctx->slots[i].used) return i;
+  return -1;
+}
+
 }  // namespace
 
 // ====================================================================== C ABI
@@ -970,6 +1011,10 @@ seed_status seed_init(const seed_config* cfg, seed_ctx* out) {
   if (cfg->gamma < 1 || cfg->gamma > 16 || !(cfg->temperature > 0.f) || cfg->max_new_tokens < 1 ||
       cfg->max_streams < 1 || cfg->max_batch < 1 || cfg->max_ctx < 8)
     return SEED_EINVAL;
+  // KV pages hold whole 16-key attention tiles (one tensor copy each): 16, 32, ..., 256 tokens
+  const int P = cfg->page_tokens > 0 ? cfg->page_tokens : 16;
+  if (P < 16 || P > 256 || (P & (P - 1))) return SEED_EINVAL;
+  if (cfg->world < 0 || (cfg->world > 1 && (cfg->rank < 0 || cfg->rank >= cfg->world))) return SEED_EINVAL;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return SEED_ECUDA;
   int dev = 0;
@@ -980,7 +1025,7 @@ seed_status seed_init(const seed_config* cfg, seed_ctx* out) {
   seed_ctx ctx = new seed_ctx_s;
   ctx->cfg = *cfg;
   ctx->dev = dev;
-  ctx->P = cfg->page_tokens > 0 ? cfg->page_tokens : 16;
+  ctx->P = P;
   ctx->C = std::min(cfg->max_batch, cfg->max_streams);
   ctx->profile = (cfg->flags & SEED_FLAG_PROFILE) != 0;
   const int g = cfg->gamma;
@@ -1009,8 +1054,6 @@ seed_status seed_init(const seed_config* cfg, seed_ctx* out) {
     seed_destroy(ctx);
     return st;
   };
-  ctx->partial_floats = std::max(max_partial(ctx->tm, 256), max_partial(ctx->dm, 256));
-  if (cudaMalloc(&ctx->partial, ctx->partial_floats * 4) != cudaSuccess) return fail_init(SEED_ENOMEM);
   if (ctx->arena.init(1 << 20) != cudaSuccess) return fail_init(SEED_ENOMEM);
   const int V = cfg->target.vocab, C = ctx->C, S = ctx->n_slots;
   ctx->slots.resize(S);
@@ -1025,11 +1068,14 @@ seed_status seed_init(const seed_config* cfg, seed_ctx* out) {
   ok &= cudaMalloc(&ctx->verify_work, (size_t)C * (2 * (g + 1) + 1) * 4) == cudaSuccess;
   if (ok) ok &= cudaMemset(ctx->verify_work, 0, (size_t)C * (2 * (g + 1) + 1) * 4) == cudaSuccess;
   const int world = std::max(cfg->world, 1);
-  ok &= cudaMalloc(&ctx->records, (size_t)C * (g + 3) * 4) == cudaSuccess;
-  ok &= cudaMalloc(&ctx->records_all, (size_t)world * C * (g + 3) * 4) == cudaSuccess;
-  ok &= cudaMallocHost(&ctx->records_host, (size_t)world * C * (g + 3) * 4) == cudaSuccess;
-  ok &= cudaMallocHost(&ctx->cnt_host, (size_t)C * 4) == cudaSuccess;
-  ok &= cudaMallocHost(&ctx->tok_host, (size_t)C * (g + 1) * 4) == cudaSuccess;
+  ctx->block_ints = C * (g + 3) + 1;
+  ok &= cudaMalloc(&ctx->records, (size_t)ctx->block_ints * 4) == cudaSuccess;
+  ok &= cudaMalloc(&ctx->records_all, (size_t)world * ctx->block_ints * 4) == cudaSuccess;
+  ok &= cudaMallocHost(&ctx->records_host, (size_t)world * ctx->block_ints * 4) == cudaSuccess;
+  ok &= cudaMalloc(&ctx->dev_err, 2 * sizeof(int32_t)) == cudaSuccess;
+  if (ok) ok &= cudaMemset(ctx->dev_err, 0, 2 * sizeof(int32_t)) == cudaSuccess;
+  ok &= cudaMallocHost(&ctx->err_host, 2 * sizeof(int32_t)) == cudaSuccess;
+  if (ok) ctx->err_host[0] = ctx->err_host[1] = 0;
   ok &= cudaMalloc(&ctx->sids_dev, (size_t)C * 4) == cudaSuccess;
   ok &= cudaMalloc(&ctx->rs_dev, (size_t)C * 4) == cudaSuccess;
   ok &= cudaMalloc(&ctx->slots_dev, (size_t)C * 4) == cudaSuccess;
@@ -1069,8 +1115,8 @@ seed_status seed_init(const seed_config* cfg, seed_ctx* out) {
     }
   }
   if (!ok) return fail_init(SEED_ENOMEM);
-  if (seed_sched_create(nullptr, 0, &ctx->sched) != SEED_OK) return fail_init(SEED_ENOMEM);
-  if (seed_table_create(g + 3, &ctx->table) != SEED_OK) return fail_init(SEED_ENOMEM);
+  if (seed_book_create(g, cfg->max_new_tokens, C, world, world > 1 ? cfg->rank : 0, &ctx->book) != SEED_OK)
+    return fail_init(SEED_ENOMEM);
   if (world > 1) {
     if (!cfg->nccl_id || !g_nccl.load()) return fail_init(SEED_ENCCL);
     Id128 id;
@@ -1087,15 +1133,14 @@ void seed_destroy(seed_ctx ctx) {
   cudaDeviceSynchronize();
   free_model(ctx->tm);
   free_model(ctx->dm);
-  void* bufs[] = {ctx->partial, ctx->tgt_logits, ctx->drf_logits, ctx->xs, ctx->vtok, ctx->out_tok,
+  void* bufs[] = {ctx->dev_err, ctx->tgt_logits, ctx->drf_logits, ctx->xs, ctx->vtok, ctx->out_tok,
                   ctx->out_cnt, ctx->out_acc, ctx->verify_work, ctx->records, ctx->records_all, ctx->sids_dev, ctx->rs_dev,
                   ctx->slots_dev, ctx->ds.tlen, ctx->ds.len_t, ctx->ds.len_d, ctx->ds.L, ctx->ds.r,
                   ctx->ds.done, ctx->ds.hist};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (ctx->records_host) cudaFreeHost(ctx->records_host);
-  if (ctx->cnt_host) cudaFreeHost(ctx->cnt_host);
-  if (ctx->tok_host) cudaFreeHost(ctx->tok_host);
+  if (ctx->err_host) cudaFreeHost(ctx->err_host);
   ctx->arena.destroy();
   if (ctx->round_done) cudaEventDestroy(ctx->round_done);
   for (auto* gm : {&ctx->round_graphs})
@@ -1108,50 +1153,26 @@ void seed_destroy(seed_ctx ctx) {
   if (ctx->timing_acc) cudaFree(ctx->timing_acc);
   if (ctx->timing_last) cudaFree(ctx->timing_last);
   if (ctx->cta_rec) cudaFree(ctx->cta_rec);
-  if (ctx->sched) seed_sched_destroy(ctx->sched);
-  if (ctx->table) seed_table_destroy(ctx->table);
+  if (ctx->book) seed_book_destroy(ctx->book);
   if (ctx->comm && g_nccl.destroy) g_nccl.destroy(ctx->comm);
   delete ctx;
-}
-
-seed_status install_slot(seed_ctx ctx, int slot, uint32_t gid, const int32_t* prefix, int len, cudaStream_t st) {
-  SlotState& ss = ctx->slots[slot];
-  ss = SlotState();
-  ss.used = true;
-  ss.gid = gid;
-  ss.T.assign(prefix, prefix + len);
-  ss.prompt_len = len;
-  ss.len_t = ss.len_d = len - 1;
-  // device state (K5 reads/writes it)
-  int32_t vals[6] = {len, len - 1, len - 1, 0, 0, 0};
-  int32_t* dst[6] = {ctx->ds.tlen, ctx->ds.len_t, ctx->ds.len_d, ctx->ds.L, ctx->ds.r, ctx->ds.done};
-  for (int i = 0; i < 6; ++i) CK(cudaMemcpyAsync(dst[i] + slot, &vals[i], 4, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(ctx->ds.hist + (size_t)slot * ctx->ds.max_ctx, prefix, (size_t)len * 4, cudaMemcpyHostToDevice,
-                     st));
-  CK(cudaStreamSynchronize(st));
-  ctx->gid2slot[gid] = slot;
-  seed_sched_add(ctx->sched, (int32_t)gid);
-  return SEED_OK;
 }
 
 seed_status seed_add_stream(seed_ctx ctx, uint32_t gid, const int32_t* prefix, int32_t len, void* stream) {
   seed_status s = check_ctx(ctx);
   if (s != SEED_OK) return s;
+  if ((s = check_between(ctx, "seed_add_stream")) != SEED_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
   if (!prefix || len < 2) return fail(ctx, SEED_EINVAL, "seed_add_stream", "prefix must hold >= 2 tokens");
+  if ((int32_t)gid < 0) return fail(ctx, SEED_EINVAL, "seed_add_stream", "global id must be < 2^31");
   if ((s = quiesce(ctx)) != SEED_OK) return s;
-  if (len + ctx->cfg.max_new_tokens + ctx->cfg.gamma + 2 > ctx->cfg.max_ctx + ctx->cfg.gamma + 2)
+  if (len + ctx->cfg.max_new_tokens > ctx->cfg.max_ctx)
     return fail(ctx, SEED_ECAPACITY, "seed_add_stream", "prefix + l exceeds max_ctx");
   for (int i = 0; i < len; ++i)
     if (prefix[i] < 0 || prefix[i] >= ctx->cfg.target.vocab)
       return fail(ctx, SEED_EINVAL, "seed_add_stream", "token id out of range");
   if (ctx->gid2slot.count(gid)) return fail(ctx, SEED_EINVAL, "seed_add_stream", "duplicate global id");
-  int slot = -1;
-  for (int i = 0; i < ctx->cfg.max_streams; ++i)
-    if (!ctx->slots[i].used) {
-      slot = i;
-      break;
-    }
+  const int slot = free_slot(ctx);
   if (slot < 0) return fail(ctx, SEED_ECAPACITY, "seed_add_stream", "max_streams reached");
   const int g = ctx->cfg.gamma;
   if ((s = ensure_pages(ctx, ctx->tm, slot, len + g + 1, st)) != SEED_OK) return s;
@@ -1165,29 +1186,27 @@ seed_status seed_add_stream(seed_ctx ctx, uint32_t gid, const int32_t* prefix, i
 seed_status seed_fork_stream(seed_ctx ctx, uint32_t src_gid, uint32_t gid, void* stream) {
   seed_status s = check_ctx(ctx);
   if (s != SEED_OK) return s;
+  if ((s = check_between(ctx, "seed_fork_stream")) != SEED_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
   if ((s = quiesce(ctx)) != SEED_OK) return s;
   auto it = ctx->gid2slot.find(src_gid);
   if (it == ctx->gid2slot.end()) return fail(ctx, SEED_EINVAL, "seed_fork_stream", "unknown source id");
-  if (ctx->gid2slot.count(gid)) return fail(ctx, SEED_EINVAL, "seed_fork_stream", "duplicate global id");
+  if (ctx->gid2slot.count(gid) || (int32_t)gid < 0)
+    return fail(ctx, SEED_EINVAL, "seed_fork_stream", "duplicate or invalid global id");
   const int src = it->second;
-  const SlotState& from = ctx->slots[src];
+  const seed::BookStream& from = stream_of(ctx, src_gid);
   if (from.r != 0 || from.L != 0)  // only a freshly prefilled stream (no round yet)
     return fail(ctx, SEED_ESTATE, "seed_fork_stream", "source stream has already run a round");
-  int slot = -1;
-  for (int i = 0; i < ctx->cfg.max_streams; ++i)
-    if (!ctx->slots[i].used) {
-      slot = i;
-      break;
-    }
+  const int slot = free_slot(ctx);
   if (slot < 0) return fail(ctx, SEED_ECAPACITY, "seed_fork_stream", "max_streams reached");
   const std::vector<int32_t> prefix = from.T;
   const int len = (int)prefix.size(), g = ctx->cfg.gamma;
-  // the prefilled K/V of the first len - 1 positions: pages holding only prefix positions
-  // (index < (len - 1) / P) are never written again -- rounds write positions >= len - 1 -- so
-  // the new slot shares them (refcounted); the page holding position len - 1, if it also holds
-  // prefix positions, is copied on the device.  Bit-identical to a fresh prefill.
-  const int shared = (len - 1) / ctx->P;
+  // The prefilled K/V of positions 0 .. len - 2.  Rounds write positions >= len - 2 (the draft's
+  // first step rewrites len - 2, R22; the target writes from len - 1), so pages holding only
+  // positions < len - 2 are never written again: the new slot shares them (refcounted).  The page
+  // holding position len - 2 is copied on the device; later pages are fresh.  Bit-identical to a
+  // fresh prefill (test_fork_stream_equals_add_stream).
+  const int shared = (len - 2) / ctx->P;
   for (Model* m : {&ctx->tm, &ctx->dm}) {
     int32_t* pt_src = m->page_table + (size_t)src * ctx->max_pages;
     int32_t* pt_new = m->page_table + (size_t)slot * ctx->max_pages;
@@ -1204,11 +1223,9 @@ seed_status seed_fork_stream(seed_ctx ctx, uint32_t src_gid, uint32_t gid, void*
       release_pages(ctx->dm, slot, ctx->max_pages);
       return s;
     }
-    if ((len - 1) % ctx->P != 0) {
-      const size_t elems = m->kv.page_elems();
-      CK(cudaMemcpyAsync(m->kv.pool + (size_t)pt_new[shared] * elems, m->kv.pool + (size_t)pt_src[shared] * elems,
-                         elems * sizeof(bf16), cudaMemcpyDeviceToDevice, st));
-    }
+    const size_t elems = m->kv.page_elems();
+    CK(cudaMemcpyAsync(m->kv.pool + (size_t)pt_new[shared] * elems, m->kv.pool + (size_t)pt_src[shared] * elems,
+                       elems * sizeof(bf16), cudaMemcpyDeviceToDevice, st));
   }
   return install_slot(ctx, slot, gid, prefix.data(), len, st);
 }
@@ -1216,32 +1233,49 @@ seed_status seed_fork_stream(seed_ctx ctx, uint32_t src_gid, uint32_t gid, void*
 seed_status seed_schedule_round(seed_ctx ctx, int32_t* batch_ids, int32_t cap, int32_t* n) {
   seed_status s = check_ctx(ctx);
   if (s != SEED_OK) return s;
-  if (!n || (cap > 0 && !batch_ids)) return fail(ctx, SEED_EINVAL, "seed_schedule_round", "args");
-  if ((s = complete_round(ctx)) != SEED_OK) return s;
+  if (!n || cap < 0 || (cap > 0 && !batch_ids)) return fail(ctx, SEED_EINVAL, "seed_schedule_round", "args");
   *n = 0;
-  if (seed_sched_all_done(ctx->sched)) return SEED_OK;
-  s = seed_sched_pop(ctx->sched, batch_ids, std::min(cap, ctx->C), n);
+  if ((s = check_between(ctx, "seed_schedule_round")) != SEED_OK) return s;
+  const seed_status done_st = complete_round(ctx);   // SEED_EDEVICE still schedules the next round
+  if (done_st != SEED_OK && done_st != SEED_EDEVICE) return done_st;
+  s = seed_book_schedule(ctx->book, batch_ids, cap, n);
   if (s != SEED_OK) return fail(ctx, s, "seed_schedule_round", "no ready stream (liveness)");
-  return SEED_OK;
+  return done_st;
+}
+
+seed_status seed_global_pending(seed_ctx ctx, int64_t* n) {
+  if (!ctx || !n) return SEED_EINVAL;
+  seed_status s = complete_round(ctx);
+  if (s != SEED_OK && s != SEED_EDEVICE) return s;
+  seed_book_global_pending(ctx->book, n);
+  if (*n < 0 && std::max(ctx->cfg.world, 1) == 1) *n = ctx->book->undone;   // no exchange yet: own count
+  return s;
 }
 
 seed_status seed_draft_round(seed_ctx ctx, const int32_t* ids, int32_t n, void* stream) {
   seed_status s = check_ctx(ctx);
   if (s != SEED_OK) return s;
+  if ((s = check_between(ctx, "seed_draft_round")) != SEED_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
   std::vector<int> slots;
   if ((s = map_batch(ctx, ids, n, slots)) != SEED_OK) return s;
-  if (ctx->round_pending && (s = complete_round(ctx)) != SEED_OK) return s;
+  if (ctx->round_pending) {
+    s = complete_round(ctx);
+    if (s != SEED_OK && s != SEED_EDEVICE) return s;
+    if ((s = map_batch(ctx, ids, n, slots)) != SEED_OK) return s;   // the previous round may have finished some
+  }
   const int g = ctx->cfg.gamma;
+  std::vector<int32_t> batch(ids, ids + n);
   for (int b = 0; b < n; ++b) {
-    const int T = (int)ctx->slots[slots[b]].T.size();
+    const int T = (int)stream_of(ctx, (uint32_t)ids[b]).T.size();
     if ((s = ensure_pages(ctx, ctx->tm, slots[b], T + g + 1, st)) != SEED_OK) return s;
     if ((s = ensure_pages(ctx, ctx->dm, slots[b], T + g + 1, st)) != SEED_OK) return s;
   }
   RoundPlan& P = ctx->plan;
-  if ((s = build_round_plan(ctx, slots, n, P)) != SEED_OK) return s;
+  if ((s = build_round_plan(ctx, batch, slots, P)) != SEED_OK) return s;
   if ((s = run_phase(ctx, n, true, st)) != SEED_OK) return s;
-  ctx->drafted.assign(ids, ids + n);
+  ctx->drafted = batch;
+  ctx->draft_called = true;
   return SEED_OK;
 }
 
@@ -1250,16 +1284,17 @@ seed_status seed_verify(seed_ctx ctx, const int32_t* ids, int32_t n, int32_t* ou
   seed_status s = check_ctx(ctx);
   if (s != SEED_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
-  if ((int)ctx->drafted.size() != n || !std::equal(ids, ids + n, ctx->drafted.begin()))
+  if (!ctx->draft_called || (int)ctx->drafted.size() != n || (n > 0 && !std::equal(ids, ids + n, ctx->drafted.begin())))
     return fail(ctx, SEED_ESTATE, "seed_verify", "batch was not drafted");
   if ((s = run_phase(ctx, n, false, st)) != SEED_OK) return s;
   const int g = ctx->cfg.gamma;
-  if (out_tok)
+  if (out_tok && n > 0)
     CK(cudaMemcpyAsync(out_tok, ctx->out_tok, (size_t)n * (g + 1) * 4, cudaMemcpyDeviceToDevice, st));
-  if (out_cnt) CK(cudaMemcpyAsync(out_cnt, ctx->out_cnt, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+  if (out_cnt && n > 0) CK(cudaMemcpyAsync(out_cnt, ctx->out_cnt, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
   ctx->round_pending = true;
-  ctx->last_batch.assign(ids, ids + n);
+  ctx->last_batch = ctx->drafted;
   ctx->drafted.clear();
+  ctx->draft_called = false;
   return SEED_OK;
 }
 
@@ -1270,69 +1305,67 @@ seed_status seed_round_host(seed_ctx ctx, const int32_t* ids, int32_t n, int32_t
   if ((s = seed_verify(ctx, ids, n, nullptr, nullptr, stream)) != SEED_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
   const int g = ctx->cfg.gamma;
-  if (out_tok_host)
+  if (out_tok_host && n > 0)
     CK(cudaMemcpyAsync(out_tok_host, ctx->out_tok, (size_t)n * (g + 1) * 4, cudaMemcpyDeviceToHost, st));
-  if (out_cnt_host) CK(cudaMemcpyAsync(out_cnt_host, ctx->out_cnt, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+  if (out_cnt_host && n > 0) CK(cudaMemcpyAsync(out_cnt_host, ctx->out_cnt, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return SEED_OK;
 }
 
 seed_status seed_get_tokens(seed_ctx ctx, uint32_t gid, int32_t* dst, int32_t cap, int32_t* len) {
-  if (!ctx || !len) return SEED_EINVAL;
-  if (ctx->round_pending) {
-    seed_status s = complete_round(ctx);
-    if (s != SEED_OK) return s;
-  }
-  auto it = ctx->gid2slot.find(gid);
-  if (it != ctx->gid2slot.end()) {
-    const SlotState& ss = ctx->slots[it->second];
-    *len = (int32_t)ss.T.size() - ss.prompt_len;
-    if (dst) std::copy(ss.T.begin() + ss.prompt_len, ss.T.begin() + ss.prompt_len + std::min(cap, *len), dst);
-    return SEED_OK;
-  }
-  return seed_table_get(ctx->table, gid, dst, cap, len);
+  if (!ctx || !len || cap < 0) return SEED_EINVAL;
+  seed_status s = complete_round(ctx);
+  if (s != SEED_OK && s != SEED_EDEVICE) return s;
+  const seed_status t = seed_book_tokens(ctx->book, gid, dst, cap, len);
+  return t != SEED_OK ? t : s;
 }
 
 seed_status seed_stream_info(seed_ctx ctx, uint32_t gid, int32_t* info) {
   if (!ctx || !info) return SEED_EINVAL;
-  if (ctx->round_pending) {
-    seed_status s = complete_round(ctx);
-    if (s != SEED_OK) return s;
-  }
+  seed_status s = complete_round(ctx);
+  if (s != SEED_OK && s != SEED_EDEVICE) return s;
   auto it = ctx->gid2slot.find(gid);
   if (it == ctx->gid2slot.end()) return SEED_ENOTFOUND;
-  const SlotState& s = ctx->slots[it->second];
-  info[0] = (int32_t)s.T.size();
-  info[1] = s.L;
-  info[2] = s.r;
-  info[3] = s.done;
-  info[4] = s.len_t;
-  info[5] = s.len_d;
+  const seed::BookStream& b = stream_of(ctx, gid);
+  const SlotState& ss = ctx->slots[it->second];
+  info[0] = (int32_t)b.T.size();
+  info[1] = b.L;
+  info[2] = b.r;
+  info[3] = b.done ? 1 : 0;
+  info[4] = ss.len_t;
+  info[5] = ss.len_d;
   info[6] = ctx->tm.held[it->second];
   info[7] = it->second;
-  return SEED_OK;
+  return s;
 }
 
 seed_status seed_remove_stream(seed_ctx ctx, uint32_t gid) {
   seed_status s = check_ctx(ctx);
   if (s != SEED_OK) return s;
-  if (ctx->round_pending && (s = complete_round(ctx)) != SEED_OK) return s;
+  if ((s = check_between(ctx, "seed_remove_stream")) != SEED_OK) return s;
+  if (ctx->round_pending) {
+    s = complete_round(ctx);
+    if (s != SEED_OK && s != SEED_EDEVICE) return s;
+  }
   auto it = ctx->gid2slot.find(gid);
   if (it == ctx->gid2slot.end()) return SEED_ENOTFOUND;
   const int slot = it->second;
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(ctx, SEED_ECUDA, "seed_remove_stream", "sync");
   release_pages(ctx->tm, slot, ctx->max_pages);
   release_pages(ctx->dm, slot, ctx->max_pages);
-  // keep the emitted tokens reachable through the table
-  const SlotState& ss = ctx->slots[slot];
-  std::vector<int32_t> rec(ctx->cfg.gamma + 3, -1);
-  (void)rec;
   ctx->slots[slot] = SlotState();
   ctx->gid2slot.erase(it);
-  // mark done in the scheduler so it is dropped from the queue
-  int32_t one = 1, id = (int32_t)gid;
-  (void)ss;
-  seed_sched_complete(ctx->sched, &id, &one, 1);
+  // forget the id: scheduler entry, tokens (a removed id may be added again)
+  seed_book_remove(ctx->book, gid);
+  return s;
+}
+
+seed_status seed_device_status(seed_ctx ctx, uint32_t* bits, int64_t* fallbacks) {
+  if (!ctx) return SEED_EINVAL;
+  seed_status s = complete_round(ctx);
+  if (s != SEED_OK && s != SEED_EDEVICE) return s;
+  if (bits) *bits = ctx->err_bits_seen;
+  if (fallbacks) *fallbacks = ctx->fallbacks;
   return SEED_OK;
 }
 
@@ -1340,6 +1373,7 @@ seed_status seed_forward_logits(seed_ctx ctx, int32_t which, const int32_t* toke
                                 void* stream) {
   seed_status s = check_ctx(ctx);
   if (s != SEED_OK) return s;
+  if ((s = check_between(ctx, "seed_forward_logits")) != SEED_OK) return s;
   if (!tokens || n < 1 || !logits) return fail(ctx, SEED_EINVAL, "seed_forward_logits", "args");
   cudaStream_t st = (cudaStream_t)stream;
   if ((s = quiesce(ctx)) != SEED_OK) return s;
@@ -1413,7 +1447,7 @@ seed_status seed_gemm_cta_trace(seed_ctx ctx, int32_t launch, uint64_t* out, int
 seed_status seed_set_profile(seed_ctx ctx, int32_t on) {
   if (!ctx) return SEED_EINVAL;
   if (on && !ctx->timing_rec) return fail(ctx, SEED_ESTATE, "seed_set_profile", "created without SEED_FLAG_PROFILE");
-  if (!ctx->drafted.empty()) return fail(ctx, SEED_ESTATE, "seed_set_profile", "a drafted batch is not verified");
+  if (ctx->draft_called) return fail(ctx, SEED_ESTATE, "seed_set_profile", "a drafted batch is not verified");
   ctx->profile = on != 0;
   return SEED_OK;
 }
@@ -1437,16 +1471,13 @@ seed_status seed_op_philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, u
 }
 
 seed_status seed_op_gemm(const void* W, int32_t N, int32_t K, const void* X, int32_t M, float* Y, void* stream) {
-  if (!W || !X || !Y || N < 1 || K < 64 || K % 64 || M < 1) return SEED_EINVAL;
+  if (!W || !X || !Y || N < 4 || N % 4 || K < 64 || K % 64 || M < 1) return SEED_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   GemmPlan p;
   seed::gemm_plan(&p, W, N, K);
-  float* part = nullptr;
   int done = 0;
   bf16* xpad = nullptr;
-  if (cudaMallocAsync(&part, seed::gemm_partial_floats(p, std::min(M, 256)) * 4, st) != cudaSuccess ||
-      cudaMallocAsync(&xpad, (size_t)256 * K * 2, st) != cudaSuccess)
-    return SEED_ENOMEM;
+  if (cudaMallocAsync(&xpad, (size_t)256 * K * 2, st) != cudaSuccess) return SEED_ENOMEM;
   cudaMemsetAsync(xpad, 0, (size_t)256 * K * 2, st);
   seed_status s = SEED_OK;
   while (done < M && s == SEED_OK) {
@@ -1467,10 +1498,9 @@ seed_status seed_op_gemm(const void* W, int32_t N, int32_t K, const void* X, int
     io.tmX = &tm;
     io.Y = Y + (size_t)done * N;
     io.ldY = N;
-    if (seed::gemm_run(p, m, io, part, st) != cudaSuccess) s = SEED_ECUDA;
+    if (seed::gemm_run(p, m, io, st) != cudaSuccess) s = SEED_ECUDA;
     done += m;
   }
-  cudaFreeAsync(part, st);
   cudaFreeAsync(xpad, st);
   cudaStreamSynchronize(st);
   seed::gemm_plan_free(&p);
@@ -1516,7 +1546,7 @@ seed_status seed_op_draft_sample(const float* z, int32_t ld, int32_t B, int32_t 
                                  const uint32_t* sids, const int32_t* rs, int32_t j, int32_t* out, void* stream) {
   if (!z || B < 1 || V < 1 || !sids || !rs || !out || !(temperature > 0.f)) return SEED_EINVAL;
   return seed::draft_sample(z, ld, B, V, temperature, (uint32_t)(seed & 0xFFFFFFFFu), (uint32_t)(seed >> 32), sids,
-                            rs, j, out, 1, nullptr, 0, (cudaStream_t)stream) == cudaSuccess
+                            rs, j, out, 1, nullptr, 0, nullptr, (cudaStream_t)stream) == cudaSuccess
              ? SEED_OK
              : SEED_ECUDA;
 }
@@ -1547,10 +1577,6 @@ seed_status seed_op_decoder_layer(const seed_model_shape* shape, const void* con
   seed_model_weights mw{dummy, w, w[7], dummy};
   s = build_model(ctx, ctx->tm, sh, mw, M, 1, ctx->max_pages, ctx->max_pages, max_pos);
   Model& m = ctx->tm;
-  if (s == SEED_OK) {
-    ctx->partial_floats = max_partial(m, std::max(M, 1));
-    if (cudaMalloc(&ctx->partial, ctx->partial_floats * 4) != cudaSuccess) s = SEED_ENOMEM;
-  }
   if (s == SEED_OK && ctx->arena.init(1 << 16) != cudaSuccess) s = SEED_ENOMEM;
   if (s == SEED_OK) s = ensure_pages(ctx, m, 0, ctx_len + M, st);
   if (s == SEED_OK && ctx_len > 0 &&
@@ -1593,7 +1619,6 @@ seed_status seed_op_decoder_layer(const seed_model_shape* shape, const void* con
   cudaStreamSynchronize(st);
   if (s == SEED_OK && cudaGetLastError() != cudaSuccess) s = SEED_ECUDA;
   free_model(ctx->tm);
-  if (ctx->partial) cudaFree(ctx->partial);
   ctx->arena.destroy();
   cudaFree(dummy);
   delete ctx;

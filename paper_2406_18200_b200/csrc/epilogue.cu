@@ -29,8 +29,8 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 // in its epilogue, R24).  grid (ceil(d/128), M), block 128.
 __global__ void __launch_bounds__(128)
 embed_stats_kernel(const __nv_bfloat16* __restrict__ embed, const int32_t* __restrict__ tok, int tok_stride, int d,
-                   float* __restrict__ x, float* __restrict__ ssq, const __nv_bfloat16* __restrict__ nw,
-                   __nv_bfloat16* __restrict__ h, int M) {
+                   int V, float* __restrict__ x, float* __restrict__ ssq, const __nv_bfloat16* __restrict__ nw,
+                   __nv_bfloat16* __restrict__ h, int32_t* err, int M) {
   __shared__ float red[4];
   pdl_trigger();
   pdl_wait();
@@ -38,7 +38,12 @@ embed_stats_kernel(const __nv_bfloat16* __restrict__ embed, const int32_t* __res
   float v = 0.f;
   if (n < d) {
     if (embed) {
-      v = bf2f(embed[(size_t)tok[(size_t)m * tok_stride] * d + n]);
+      int id = tok[(size_t)m * tok_stride];
+      if (id < 0 || id >= V) {   // contract violation (SEED_EDEVICE): never read outside the table
+        if (err && threadIdx.x == 0 && t == 0) atomicOr(err, 1);
+        id = 0;
+      }
+      v = bf2f(embed[(size_t)id * d + n]);
       x[(size_t)m * d + n] = v;
     } else {
       v = x[(size_t)m * d + n];
@@ -80,10 +85,10 @@ __global__ void kv_write_dense_kernel(KVLayout kv, int layer, int slot, int n, c
 
 }  // namespace
 
-cudaError_t embed_stats(const __nv_bfloat16* embed, const int32_t* tok, int tok_stride, int M, int d, float* x,
-                        float* ssq, const __nv_bfloat16* nw, __nv_bfloat16* h, cudaStream_t st) {
-  return launch(embed_stats_kernel, dim3((d + 127) / 128, M), dim3(128), 0, st, embed, tok, tok_stride, d, x, ssq,
-                nw, h, M);
+cudaError_t embed_stats(const __nv_bfloat16* embed, const int32_t* tok, int tok_stride, int M, int d, int V, float* x,
+                        float* ssq, const __nv_bfloat16* nw, __nv_bfloat16* h, int32_t* err, cudaStream_t st) {
+  return launch(embed_stats_kernel, dim3((d + 127) / 128, M), dim3(128), 0, st, embed, tok, tok_stride, d, V, x, ssq,
+                nw, h, err, M);
 }
 
 cudaError_t kv_write_dense(const KVLayout& kv, int layer, int slot, int n, const __nv_bfloat16* k,

@@ -1,4 +1,4 @@
-// gemm.cu -- K2: the verify / draft projections as a persistent stream-K GEMM on tcgen05.
+// gemm.cu -- K2: every projection of both models (and the LM heads) on tcgen05.
 //
 // Y[m][n] = sum_k X[m][k] * W[n][k]  (nn.Linear, W row-major [N][K], bf16 in, fp32 accumulate).
 // The method streams every weight once per round with only M = B(gamma+1) tokens
@@ -6,15 +6,12 @@
 // HBM busy: swap-AB puts the weight rows on the UMMA M = 128 side and the tokens on
 // UMMA N = M_pad (16..256); TMA streams 128 x 64 weight tiles through a deep smem ring
 // (evict-first), the token tile rides along (evict-last, L2 resident); one elected
-// thread issues tcgen05.mma into a double-buffered TMEM accumulator; four epilogue
-// warps drain TMEM with tcgen05.ld while the next tile accumulates.
+// thread issues tcgen05.mma into a TMEM accumulator; four epilogue warps drain TMEM
+// with tcgen05.ld and apply the fused epilogue (store / residual + RMSNorm operand / SwiGLU).
 //
-// Work split: the (tile, k-block) units are cut into G = min(148, U / 4) contiguous ranges,
-// one persistent CTA per SM (stream-K).  A tile owned by one CTA goes straight from TMEM to Y;
-// a tile shared by several CTAs is written as fp32 partials and the last CTA to finish it
-// (atomic ticket) sums them in CTA order and writes Y.  G and the cut points depend on
-// (N, K) only, never on M, so every output column is computed in the same order whatever the
-// batch (batch invariance, DESIGN R19).
+// Work split (cluster split-K, below): c CTAs per 128-row weight tile, c a function of (N, K)
+// only, never of M, so every output element is reduced in the same order whatever the batch
+// (batch invariance, DESIGN R19).
 #include <cuda.h>
 #include <algorithm>
 #include <cstdio>
@@ -32,27 +29,6 @@ constexpr int BLOCK_N = 128;   // weight rows per tile (UMMA M)
 constexpr int BLOCK_K = 64;    // one 128-byte swizzle row of bf16
 constexpr int W_TILE_BYTES = BLOCK_N * BLOCK_K * 2;
 constexpr int MAX_STAGES = 16;
-// 8 weight stages (128 KB in flight per SM) saturate HBM; the smem cap leaves room for an
-// attention / epilogue CTA to co-reside, so the next GEMM's weight prefetch overlaps it (PDL)
-
-struct GemmArgs {
-  int KB, U, G, S, M, m_pad, stages, N, K, ldY, maxseg;
-  int ymode;                   // 0 store Y (x row scale, row map); 1 residual; 2 SwiGLU (see GemmIO)
-  int ssq_in_ld;               // row stride of ssq_in
-  int dbg;                     // SEED_EPI_DEBUG experiments (timing only, wrong results): 1 no Y/h stores, 2 no finish, 4 no partial adds
-  float eps;
-  float* partial;              // split-K partials of tiles shared by several CTAs
-  float* Y;                    // fp32 output [M][ldY]; ymode 1: the residual stream (in place)
-  const int* seg;              // per tile: count, partial-segment ids in CTA order
-  int* counters;               // per tile: finished segments (zero between launches)
-  const float* ssq_in;         // optional [ceil(K/128)][ssq_in_ld]: rows scaled by 1/rms (R24)
-  const int32_t* yrow;         // ymode 0: optional output row map (-1: row not stored)
-  float* ssq_out;              // ymode 1: [ceil(N/128)][M] sums of squares of the new residual
-  const __nv_bfloat16* nw;     // ymode 1: next RMSNorm weight [N]
-  __nv_bfloat16* hout;         // ymode 1: bf16(x_new * nw) [M][N]; ymode 2: bf16(silu(g) * u) [M][N/2]
-  unsigned long long* timing;  // optional [4]: min CTA start, min release (PDL), max CTA end (ns), kind
-  unsigned long long* cta;     // optional [G][8] per-CTA phase timestamps (diagnostics, see gemm_run)
-};
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -69,376 +45,6 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return d;
 }
 
-__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
-  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<const uint32_t*>(&v);
-}
-
-// Epilogue for 16 rows m0..m0+15 of output column n (tile t, weight row nl) held by this thread;
-// the 128 epilogue threads hold the 128 columns of the tile.
-//   ymode 0: Y[row(m)][n] = acc * inv[m]
-//   ymode 1: x[m][n] += acc; per-warp x^2 row sums (-> ssq_out); hout[m][n] = bf16(x * nw[n])
-//   ymode 2: gate (nl < 64) and up (nl >= 64) of output j = 64 t + nl % 64, scaled by inv[m],
-//            meet in shared memory; hout[m][j] = bf16(silu(g) * u)                   (B4)
-__device__ __forceinline__ void finish16(const GemmArgs& a, int m0, int t, int nl, const float* v, int ew, int lane,
-                                         const float* inv_s, float* red_s, float* xch_s,
-                                         const float* xpre = nullptr, float wpre = 0.f) {
-  const int n = t * BLOCK_N + nl;
-  if (a.ymode == 0) {
-    if (n < a.N) {
-      int row[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) row[i] = m0 + i >= a.M ? -1 : (a.yrow ? __ldg(a.yrow + m0 + i) : m0 + i);
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        if (row[i] >= 0 && !(a.dbg & 1)) a.Y[(size_t)row[i] * a.ldY + n] = a.ssq_in ? v[i] * inv_s[m0 + i] : v[i];
-    }
-    return;
-  }
-  if (a.ymode == 1) {
-    float sq[16], xo[16];
-    const float w = xpre ? wpre : (n < a.N ? bf2f(a.nw[n]) : 0.f);
-    // all residual loads first (one round trip), then the stores
-    if (xpre) {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) xo[i] = xpre[i];
-    } else {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) xo[i] = (m0 + i < a.M && n < a.N) ? a.Y[(size_t)(m0 + i) * a.ldY + n] : 0.f;
-    }
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      sq[i] = 0.f;
-      if (m0 + i < a.M && n < a.N) {
-        const float xn = xo[i] + v[i];
-        a.Y[(size_t)(m0 + i) * a.ldY + n] = xn;
-        sq[i] = xn * xn;
-        a.hout[(size_t)(m0 + i) * a.N + n] = f2bf(xn * w);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 16; ++i) sq[i] = warp_sum(sq[i]);
-    if (lane == 0) {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) red_s[ew * 256 + m0 + i] = sq[i];
-    }
-    return;
-  }
-  // ymode 2: SwiGLU across the tile's gate / up halves
-#pragma unroll
-  for (int i = 0; i < 16; ++i) xch_s[i * 128 + nl] = (m0 + i < a.M) ? v[i] * inv_s[m0 + i] : 0.f;
-  asm volatile("bar.sync 1, 128;" ::: "memory");
-  if (nl < 64) {
-    const int j = t * 64 + nl;
-    if (j < a.N / 2) {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        if (m0 + i >= a.M) break;
-        const float g = xch_s[i * 128 + nl], u = xch_s[i * 128 + 64 + nl];
-        const __nv_bfloat16 hv = f2bf(g / (1.0f + expf(-g)) * u);
-        if (!(a.dbg & 1)) a.hout[(size_t)(m0 + i) * (a.N / 2) + j] = hv;
-      }
-    }
-  }
-  asm volatile("bar.sync 1, 128;" ::: "memory");
-}
-
-// Add the other contributors' partials (segments 1..cnt-1 of the tile, in CTA order, R19) to the
-// reducer's own accumulator rows m0..m0+15 of tile column nl.  Partials are laid out
-// [segment][column][m_pad] so a thread's 16 rows are 64 contiguous bytes; loads go four segments
-// at a time.
-__device__ __forceinline__ void add_partials16(const float* __restrict__ P, const int* __restrict__ sl, int cnt,
-                                               int m_pad, int m0, int nl, float* acc, const int* id0) {
-  for (int k = 1; k < cnt; k += 4) {
-    int id[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) id[q] = k == 1 ? id0[q] : (k + q < cnt ? __ldg(sl + 1 + k + q) : -1);
-    float4 v[4][4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float4* src =
-          reinterpret_cast<const float4*>(P + ((size_t)(id[q] < 0 ? 0 : id[q]) * BLOCK_N + nl) * m_pad + m0);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) v[q][j] = id[q] >= 0 ? __ldcg(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (id[q] >= 0) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          acc[4 * j] += v[q][j].x;
-          acc[4 * j + 1] += v[q][j].y;
-          acc[4 * j + 2] += v[q][j].z;
-          acc[4 * j + 3] += v[q][j].w;
-        }
-      }
-  }
-}
-
-// __launch_bounds__(192, 2) keeps registers low enough for two CTAs per SM (SEED_GEMM_SMEM_KB <= 110)
-__global__ void __launch_bounds__(192, 2)
-gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GemmArgs a) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int S = a.stages;
-  const int x_bytes = a.m_pad * BLOCK_K * 2;
-  uint8_t* sW = smem;
-  uint8_t* sX = smem + S * W_TILE_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sX + S * x_bytes);
-  uint64_t* empty = full + S;
-  uint64_t* tfull = empty + S;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* inv_s = reinterpret_cast<float*>(tmem_slot + 4);   // [256] 1/rms per X row (ssq_in)
-  float* red_s = inv_s + 256;                               // [4][256] per-warp x^2 row sums (ymode 1)
-  float* xch_s = red_s;                                     // [16][128] gate/up exchange (ymode 2)
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.x;
-  const long u_begin = (long)c * a.U / a.G, u_end = (long)(c + 1) * a.U / a.G;
-  if (u_begin >= u_end) return;
-  pdl_trigger();
-  if (a.timing && threadIdx.x == 0) atomicMin(&a.timing[0], globaltimer());
-  unsigned long long* ct = a.cta ? a.cta + (size_t)c * 16 : nullptr;
-  if (ct && threadIdx.x == 0) ct[0] = globaltimer();
-
-  // TMEM: two accumulator buffers while they fit in 256 columns, else one -- at most 256 columns
-  // per CTA, so the two CTAs an SM can hold never wait on each other's allocation (a reducer
-  // waits on other CTAs of its grid, which may share its SM)
-  const int nacc = 2 * a.m_pad <= 256 ? 2 : 1;
-  uint32_t cols = 32;
-  while (cols < (uint32_t)(nacc * a.m_pad)) cols <<= 1;
-
-  if (warp == 0 && lane == 0) {
-    prefetch_tmap(&tmW);
-    prefetch_tmap(&tmX);
-    for (int i = 0; i < S; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc(tmem_slot, cols);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  const long t_begin = u_begin / a.KB;
-
-  if (warp == 0) {
-    // ---------------- producer warp (one lane): weights and X tiles by TMA
-    if (lane == 0) {
-      const uint64_t pol_w = l2_policy_evict_first();
-      const uint64_t pol_x = l2_policy_evict_last();
-      const uint32_t tx = W_TILE_BYTES + x_bytes;
-      // The weights do not depend on the previous kernel: fill the whole ring with weight tiles
-      // before waiting on it (PDL), so weight streaming overlaps the predecessor.
-      const long n_pre = min((long)S, u_end - u_begin);
-      for (long i = 0; i < n_pre; ++i) {
-        const long u = u_begin + i;
-        mbar_arrive_expect_tx(&full[i], tx);
-        tma_load_2d(sW + i * W_TILE_BYTES, &tmW, &full[i], (int)(u % a.KB) * BLOCK_K, (int)(u / a.KB) * BLOCK_N, pol_w);
-      }
-      pdl_wait();  // X depends on the previous kernel
-      if (a.timing) atomicMin(&a.timing[1], globaltimer());
-      if (ct) ct[1] = globaltimer();
-      for (long i = 0; i < n_pre; ++i)
-        tma_load_2d(sX + i * x_bytes, &tmX, &full[i], (int)((u_begin + i) % a.KB) * BLOCK_K, 0, pol_x);
-      int stage = (int)(n_pre % S);
-      uint32_t phase = n_pre == S ? 1u : 0u;
-      for (long u = u_begin + n_pre; u < u_end; ++u) {
-        const int t = (int)(u / a.KB), kb = (int)(u % a.KB);
-        mbar_wait(&empty[stage], phase ^ 1);
-        if (ct && u == u_begin + n_pre) ct[13] = globaltimer();
-        mbar_arrive_expect_tx(&full[stage], tx);
-        tma_load_2d(sW + stage * W_TILE_BYTES, &tmW, &full[stage], kb * BLOCK_K, t * BLOCK_N, pol_w);
-        tma_load_2d(sX + stage * x_bytes, &tmX, &full[stage], kb * BLOCK_K, 0, pol_x);
-        if (++stage == S) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-      if (ct) ct[2] = globaltimer();
-    }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer (one elected lane)
-    const uint32_t idesc = (1u << 4)                       // D = f32
-                           | (1u << 7) | (1u << 10)         // A = B = bf16
-                           | ((uint32_t)(a.m_pad >> 3) << 17)  // N = m_pad
-                           | ((uint32_t)(BLOCK_N >> 4) << 24); // M = 128
-    const uint32_t sW0 = smem_u32(sW), sX0 = smem_u32(sX);
-    int stage = 0;
-    uint32_t phase = 0;
-    int seg = 0;
-    long u = u_begin;
-    while (u < u_end) {
-      const long t = u / a.KB;
-      const long seg_end = min(u_end, (t + 1) * a.KB);
-      const int acc = seg % nacc;
-      const uint32_t use = (uint32_t)(seg / nacc);
-      mbar_wait(&tempty[acc], (use & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * a.m_pad);
-      const long seg_start = u;
-      for (; u < seg_end; ++u) {
-        mbar_wait(&full[stage], phase);
-        tc_fence_after();
-        if (ct && u == u_begin && lane == 0) ct[3] = globaltimer();
-        if (ct && u == u_begin + S - 1 && lane == 0) ct[12] = globaltimer();
-        if (elect_one()) {
-          const uint32_t wa = sW0 + stage * W_TILE_BYTES, xa = sX0 + stage * x_bytes;
-#pragma unroll
-          for (int k = 0; k < BLOCK_K / 16; ++k)
-            umma_bf16(d_tmem, sw128_desc(wa + k * 32), sw128_desc(xa + k * 32), idesc,
-                      (u != seg_start || k > 0) ? 1u : 0u);
-          umma_commit(&empty[stage]);
-          if (u == seg_end - 1) umma_commit(&tfull[acc]);
-        }
-        __syncwarp();
-        if (++stage == S) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-      ++seg;
-    }
-    if (ct && lane == 0) ct[4] = globaltimer();
-  } else {
-    // ---------------- epilogue warps 2..5: TMEM -> Y (whole tiles) or -> split-K partial; the
-    // last CTA to finish a shared tile sums its partials in CTA order (R19) and applies the
-    // epilogue (store, or residual add + per-tile sums of squares for the next RMSNorm)
-    const int lane_grp = warp & 3;               // TMEM lanes this warp may access
-    const int nl = lane_grp * 32 + lane;         // weight row within the tile
-    const int et = threadIdx.x - 64;             // 0..127 among the epilogue threads
-    const int ew = et >> 5;
-    pdl_wait();                                  // Y and the partials are read by the predecessor
-    if (a.ssq_in) {
-      // 1 / rms of each X row from the per-tile sums of squares, in tile order (R24)
-      const int kt = (a.K + 127) / 128;
-      for (int m = et; m < a.m_pad; m += 128) {
-        float inv = 0.f;
-        if (m < a.M) {
-          float ss = 0.f;
-          for (int i = 0; i < kt; ++i) ss += __ldcg(a.ssq_in + (size_t)i * a.ssq_in_ld + m);
-          inv = 1.0f / sqrtf(ss / (float)a.K + a.eps);
-        }
-        inv_s[m] = inv;
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-    }
-    int seg = 0;
-    long u = u_begin;
-    while (u < u_end) {
-      const long t = u / a.KB;
-      const long seg_end = min(u_end, (t + 1) * a.KB);
-      const bool whole = (u == t * a.KB) && (seg_end == (t + 1) * a.KB);
-      const int acc = seg % nacc;
-      const uint32_t use = (uint32_t)(seg / nacc);
-      // a whole tile's residual rows and norm weight (ymode 1) do not depend on the accumulator:
-      // load them while it is computed
-      float xw[16];
-      float ww = 0.f;
-      const bool pre_whole = whole && a.ymode == 1 && a.m_pad == 16;
-      if (pre_whole) {
-        const int n = (int)t * BLOCK_N + nl;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) xw[i] = (i < a.M && n < a.N) ? a.Y[(size_t)i * a.ldY + n] : 0.f;
-        ww = n < a.N ? bf2f(a.nw[n]) : 0.f;
-      }
-      mbar_wait(&tfull[acc], use & 1);
-      tc_fence_after();
-      if (ct && et == 0 && seg == 0) ct[5] = globaltimer();
-      const uint32_t row_addr = tmem_base + ((uint32_t)(lane_grp * 32) << 16) + (uint32_t)(acc * a.m_pad);
-      // Split tile: the CTA holding the tile's first k-blocks (its range's last segment, the first
-      // contributor in CTA order) reduces; the others publish their partials and move on.
-      const bool reducer = !whole && u == t * a.KB;
-      const bool do_finish = whole || reducer;
-      if (whole) {
-        for (int col = 0; col < a.m_pad; col += 16) {
-          float v[16];
-          tmem_ld16(row_addr + col, v);
-          if (a.dbg & 2) continue;
-          finish16(a, col, (int)t, nl, v, ew, lane, inv_s, red_s, xch_s, pre_whole ? xw : nullptr, ww);
-        }
-      } else if (!reducer) {
-        float4* out = reinterpret_cast<float4*>(
-            a.partial + ((size_t)((long)c * a.S + (t - t_begin)) * BLOCK_N + nl) * a.m_pad);
-        for (int col = 0; col < a.m_pad; col += 16) {
-          float v[16];
-          tmem_ld16(row_addr + col, v);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) out[col / 4 + j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-        }
-        if (ct && et == 0) ct[8] = globaltimer();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (et == 0) {
-          fence_acq_rel_gpu();                  // release the CTA's partial (bar.sync + cumulativity)
-          atomicAdd(&a.counters[t], 1);
-        }
-      } else {
-        const int* sl = a.seg + t * (a.maxseg + 1);
-        const int cnt = __ldg(sl);
-        // what does not depend on the other contributors is loaded before waiting: the residual
-        // rows and the next norm weight (ymode 1)
-        int id0[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) id0[q] = 1 + q < cnt ? __ldg(sl + 2 + q) : -1;
-        float xo[16];
-        float wn = 0.f;
-        if (a.ymode == 1) {
-          const int n = (int)t * BLOCK_N + nl;
-#pragma unroll
-          for (int i = 0; i < 16; ++i) xo[i] = (i < a.M && n < a.N) ? a.Y[(size_t)i * a.ldY + n] : 0.f;
-          wn = n < a.N ? bf2f(a.nw[n]) : 0.f;
-        }
-        if (et == 0) {
-          volatile int* ctr = a.counters + t;
-          while (*ctr < cnt - 1) {
-          }
-          fence_acq_rel_gpu();                  // acquire the other partials
-          *ctr = 0;                              // ready for the next launch (graph replay)
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (ct && et == 0) ct[9] = globaltimer() + (xo[0] == 1.2345e-30f ? 1 : 0);
-        for (int m0 = 0; m0 < a.m_pad; m0 += 16) {
-          float v[16];
-          tmem_ld16(row_addr + m0, v);
-          if (!(a.dbg & 4)) add_partials16(a.partial, sl, cnt, a.m_pad, m0, nl, v, id0);
-          if (ct && et == 0) ct[10] = globaltimer() + (v[0] == 1.2345e-30f ? 1 : 0);   // waits for the loads
-          finish16(a, m0, (int)t, nl, v, ew, lane, inv_s, red_s, xch_s, (a.ymode == 1 && m0 == 0) ? xo : nullptr, wn);
-          if (ct && et == 0) ct[11] = globaltimer();
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (do_finish && a.ymode == 1) {
-        // per-tile sums of squares of the updated residual rows, warps in a fixed order
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        for (int m = et; m < a.M; m += 128)
-          a.ssq_out[(size_t)t * a.M + m] = ((red_s[m] + red_s[256 + m]) + red_s[512 + m]) + red_s[768 + m];
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // red_s / xch_s are reused by the next segment
-      u = seg_end;
-      ++seg;
-    }
-    if (ct && et == 0) ct[6] = globaltimer();
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == 1) tmem_dealloc(tmem_base, cols);
-  if (ct && threadIdx.x == 0) ct[7] = globaltimer();
-  if (a.timing && threadIdx.x == 0) {
-    atomicMax(&a.timing[2], globaltimer());
-    a.timing[3] = 1;  // record kind: GEMM
-  }
-}
-
 // ============================================================================================
 // K2, cluster split-K form (the default): one thread-block cluster of c CTAs per 128-row weight
 // tile.  CTA rank r streams k-blocks [r KB / c, (r + 1) KB / c) of the tile into its TMEM
@@ -449,7 +55,7 @@ gemm_streamk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
 // reducer CTA per tile reading every partial back from L2, then the whole tile's epilogue) by a
 // c-way parallel reduction and epilogue that never leaves the cluster.
 struct SplitArgs {
-  int KB, c, per, M, m_pad, stages, N, K, ldY, ymode, ssq_in_ld, pc, pitch, dbg;
+  int KB, c, per, M, m_pad, stages, N, K, ldY, ymode, ssq_in_ld, pc, pitch;
   float eps;
   float* Y;
   const float* ssq_in;
@@ -527,7 +133,7 @@ __device__ __forceinline__ void split_finish16(const SplitArgs& a, int t, int nl
     for (int q = 0; q < 8; ++q) sh[(i0 + q) * 64 + j] = hb[q];
   }
   asm volatile("bar.sync 1, 128;" ::: "memory");
-  if (!(a.dbg & 1)) {
+  {
     const int ncols = min(BLOCK_N, a.N - t * BLOCK_N);
     if (a.ymode != 2) {
       // fp32 rows: 16 x 32 float4, a warp per row
@@ -712,7 +318,6 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
       for (int m0 = 0; m0 < a.M; m0 += 16) {
         float v[16];
         tmem_ld16(row_addr + m0, v);
-        if (a.dbg & 2) continue;
         if (res && m0 + 16 < a.M) load_res(m0 + 16, xn);
         split_finish16(a, t, nl, et, lane, m0, min(m0 + 16, a.M), v, inv_s, rowmap_s, red_s, xo, w,
                        stg0 + (chunk++ & 1) * 12288);
@@ -780,8 +385,7 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
             }
           }
           if (ct && et == 0) ct[10] = globaltimer() + (v[0] == 1.2345e-30f ? 1 : 0);
-          if (a.dbg & 2) continue;
-          // (the next chunk's residual rows are already in flight)
+            // (the next chunk's residual rows are already in flight)
           split_finish16(a, t, nl, et, lane, m0, min(m0 + 16, hi), v, inv_s, rowmap_s, red_s, xo, w,
                          stg0 + (chunk++ & 1) * 12288);
           if (res) {
@@ -910,90 +514,33 @@ void gemm_plan(GemmPlan* p, const void* W, int N, int K, int min_units) {
   p->K = K;
   p->KB = K / BLOCK_K;
   p->tiles = (N + BLOCK_N - 1) / BLOCK_N;
-  p->U = p->tiles * p->KB;
-  // at least min_units k-blocks per CTA, so a small GEMM's tiles meet few partial segments
-  p->G = std::max(1, std::min(kNumSMs, p->U / std::max(1, min_units)));
-  p->smem_kb = 0;
-  {
-    // Grid by tile count (measured at 7B / 68M, GSM8K round; env SEED_GRID_POLICY=0 keeps plain
-    // stream-K on one CTA per SM):
-    //  * more tiles than SMs (gate/up, both LM heads): one CTA per whole tile, two CTAs per SM
-    //    with half the ring each -- no split-K reduction tail (gate/up 33.3 -> 32.2 us, LM head
-    //    42.6 -> 40.6 us, draft LM head 12 -> 8 us);
-    //  * target-size GEMMs with 64..148 tiles (QKV): stream-K over two CTAs per SM -- the QKV
-    //    CTAs leave room for the attention CTAs to become resident early (round -36 us);
-    //  * fewer (O, down): stream-K on one CTA per SM with the deep ring (two per SM was slower).
-    const char* e = getenv("SEED_GRID_POLICY");
-    const bool on = !(e && e[0] == '0');
-    if (on && p->tiles > kNumSMs && p->tiles <= 2 * kNumSMs) {
-      p->G = p->tiles;
-      p->smem_kb = 112;   // two CTAs + 1 KB reserved each within 228 KB
-    } else if (on && min_units <= 4 && p->tiles >= 64 && p->tiles <= kNumSMs) {
-      p->G = std::min(2 * kNumSMs, p->U / min_units);
-      p->smem_kb = 112;
-    }
+  // c CTAs per tile, c a function of (N, K) only (R19).  Enough clusters to fill two CTAs per SM,
+  // at most 8 (portable cluster), at least min_units k-blocks per CTA; more tiles than SMs: whole
+  // tiles.  Env SEED_SPLIT_C caps c (experiments).
+  int c = 1;
+  if (p->tiles < kNumSMs) c = std::min(8, (2 * kNumSMs) / p->tiles);
+  c = std::min(c, std::max(1, p->KB / std::max(1, min_units)));
+  const char* e = getenv("SEED_SPLIT_C");
+  if (e && atoi(e) > 0) c = std::min(c, atoi(e));
+  c = std::max(1, c);
+  // every cluster of the grid must be resident at once (one wave): a cluster is placed inside
+  // one GPC, so fewer c-CTA clusters fit than SMs / c (measured: 15 clusters of 8 at 2 CTAs per
+  // SM); shrink c until the device reports room for all tiles
+  for (; c > 1; --c) {
+    const int smem_kb = p->tiles * c <= kNumSMs ? 180 : 112;
+    if (split_cluster_capacity(c, smem_kb) >= p->tiles) break;
   }
-  // cluster split-K form: c CTAs per tile, c a function of (N, K) only (R19).  Enough clusters to
-  // fill two CTAs per SM, at most 8 (portable cluster), at least min_units k-blocks per CTA; more
-  // tiles than SMs: whole tiles.  Env SEED_SPLIT_C caps c (experiments).
-  {
-    int c = 1;
-    if (p->tiles < kNumSMs) c = std::min(8, (2 * kNumSMs) / p->tiles);
-    c = std::min(c, std::max(1, p->KB / std::max(1, min_units)));
-    const char* e = getenv("SEED_SPLIT_C");
-    if (e && atoi(e) > 0) c = std::min(c, atoi(e));
-    c = std::max(1, c);
-    // every cluster of the grid must be resident at once (one wave): a cluster is placed inside
-    // one GPC, so fewer c-CTA clusters fit than SMs / c (measured: 15 clusters of 8 at 2 CTAs per
-    // SM); shrink c until the device reports room for all tiles
-    int smem_kb = 112;
-    const char* force = getenv("SEED_SPLIT_FORCE");   // experiments: skip the capacity check
-    for (; c > 1 && !(force && force[0] == '1'); --c) {
-      smem_kb = p->tiles * c <= kNumSMs ? 180 : 112;
-      if (split_cluster_capacity(c, smem_kb) >= p->tiles) break;
-    }
-    p->c = c;
-    p->split_smem_kb = p->tiles * p->c <= kNumSMs ? 180 : 112;
-    if (getenv("SEED_GEMM_VERBOSE"))
-      fprintf(stderr, "[seed] gemm N=%d K=%d tiles=%d c=%d smem=%dKB cluster capacity=%d\n", N, K, p->tiles, p->c,
-              p->split_smem_kb, p->c > 1 ? split_cluster_capacity(p->c, p->split_smem_kb) : -1);
-    const char* k = getenv("SEED_GEMM_SPLIT");
-    p->split = !(k && k[0] == '0') && N % 4 == 0;   // fp32 rows leave by 16-byte stores
-  }
-  // segments per CTA: ceil(range / KB) + 1 bound
-  const int range = (p->U + p->G - 1) / p->G;
-  p->S = (range + p->KB - 1) / p->KB + 1;
+  p->c = c;
+  // one CTA per SM with the deep ring while the grid fits the SMs, else two per SM (gate/up and
+  // the LM heads: 172 / 250 whole tiles)
+  p->split_smem_kb = p->tiles * p->c <= kNumSMs ? 180 : 112;
+  if (getenv("SEED_GEMM_VERBOSE"))
+    fprintf(stderr, "[seed] gemm N=%d K=%d tiles=%d c=%d smem=%dKB cluster capacity=%d\n", N, K, p->tiles, p->c,
+            p->split_smem_kb, p->c > 1 ? split_cluster_capacity(p->c, p->split_smem_kb) : -1);
   encode_tmap_2d(&p->tmW, W, (uint64_t)K, (uint64_t)N, BLOCK_K, BLOCK_N);
-  // per tile: the partial-segment indices (c * S + j) in CTA order -- the fixed, M-independent
-  // reduction order every consumer uses (R19)
-  std::vector<std::vector<int>> lists(p->tiles);
-  for (int c = 0; c < p->G; ++c) {
-    const long ub = (long)c * p->U / p->G, ue = (long)(c + 1) * p->U / p->G;
-    if (ub >= ue) continue;
-    const long tb = ub / p->KB;
-    for (long t = tb; t <= (ue - 1) / p->KB; ++t) lists[t].push_back(c * p->S + (int)(t - tb));
-  }
-  p->maxseg = 0;
-  for (auto& l : lists) p->maxseg = std::max<int>(p->maxseg, (int)l.size());
-  std::vector<int> flat((size_t)p->tiles * (p->maxseg + 1), -1);
-  for (int t = 0; t < p->tiles; ++t) {
-    flat[(size_t)t * (p->maxseg + 1)] = (int)lists[t].size();
-    for (size_t k = 0; k < lists[t].size(); ++k) flat[(size_t)t * (p->maxseg + 1) + 1 + k] = lists[t][k];
-  }
-  p->seg = nullptr;
-  if (cudaMalloc(&p->seg, flat.size() * sizeof(int)) == cudaSuccess)
-    cudaMemcpy(p->seg, flat.data(), flat.size() * sizeof(int), cudaMemcpyHostToDevice);
-  p->counters = nullptr;
-  if (cudaMalloc(&p->counters, (size_t)p->tiles * sizeof(int)) == cudaSuccess)
-    cudaMemset(p->counters, 0, (size_t)p->tiles * sizeof(int));
 }
 
-void gemm_plan_free(GemmPlan* p) {
-  if (p->seg) cudaFree(p->seg);
-  if (p->counters) cudaFree(p->counters);
-  p->seg = nullptr;
-  p->counters = nullptr;
-}
+void gemm_plan_free(GemmPlan*) {}
 
 void carveout_once(const void* kern) {
   static std::vector<const void*> done;
@@ -1014,19 +561,6 @@ bool pdl_enabled() {
   return on == 1;
 }
 
-// dynamic smem per GEMM CTA (env SEED_GEMM_SMEM_KB).  180 KB (one GEMM CTA per SM, 9 stages at M <= 16)
-// measured faster than 100 KB (two per SM, the next GEMM prefetching beside the running one).
-int smem_budget() {
-  static int b = -1;
-  if (b < 0) {
-    const char* e = getenv("SEED_GEMM_SMEM_KB");
-    b = (e ? atoi(e) : 180) * 1024;
-  }
-  return b;
-}
-
-size_t gemm_partial_floats(const GemmPlan& p, int M) { return (size_t)p.G * p.S * gemm_mpad(M) * BLOCK_N; }
-
 cudaError_t timing_accumulate(unsigned long long* rec, int n, unsigned long long* acc, unsigned long long* last,
                               cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
@@ -1034,105 +568,58 @@ cudaError_t timing_accumulate(unsigned long long* rec, int n, unsigned long long
   return cudaGetLastError();
 }
 
-cudaError_t gemm_run(const GemmPlan& p, int M, const GemmIO& io, float* partial, cudaStream_t st,
-                     unsigned long long* timing, unsigned long long* cta) {
-  GemmArgs a{};
-  a.KB = p.KB;
-  a.U = p.U;
-  a.G = p.G;
-  a.S = p.S;
-  a.M = M;
-  a.m_pad = gemm_mpad(M);
-  if (a.m_pad > 256) return cudaErrorInvalidValue;
-  a.N = p.N;
-  a.K = p.K;
-  a.maxseg = p.maxseg;
-  a.seg = p.seg;
-  a.counters = p.counters;
-  a.partial = partial;
-  a.ymode = io.ymode;
-  a.Y = io.Y;
-  a.ldY = io.ldY;
-  a.yrow = io.yrow;
-  a.ssq_in = io.ssq_in;
-  a.ssq_in_ld = io.ssq_in_ld;
-  a.eps = io.eps;
-  a.ssq_out = io.ssq_out;
-  a.nw = io.nw;
-  a.hout = io.hout;
-  a.timing = timing;
-  a.cta = cta;
-  static int dbg = -1;
-  if (dbg < 0) {
-    const char* e = getenv("SEED_EPI_DEBUG");
-    dbg = e ? atoi(e) : 0;
-  }
-  a.dbg = dbg;
-  if (!io.tmX) return cudaErrorInvalidValue;
+cudaError_t gemm_run(const GemmPlan& p, int M, const GemmIO& io, cudaStream_t st, unsigned long long* timing,
+                     unsigned long long* cta) {
+  const int m_pad = gemm_mpad(M);
+  if (M < 1 || m_pad > 256 || !io.tmX) return cudaErrorInvalidValue;
   if (io.ymode == 1 && (!io.Y || !io.ssq_out || !io.nw || !io.hout)) return cudaErrorInvalidValue;
   if (io.ymode == 2 && (!io.ssq_in || !io.hout || p.N % BLOCK_N)) return cudaErrorInvalidValue;
   if (io.ymode == 0 && !io.Y) return cudaErrorInvalidValue;
-  if (p.split) {
-    // rows leave by 16-byte stores
-    if ((io.ymode == 1 && p.N % 8) || (io.ymode != 2 && io.ldY % 4)) return cudaErrorInvalidValue;
-    SplitArgs b{};
-    b.KB = p.KB;
-    b.c = p.c;
-    b.M = M;
-    b.m_pad = a.m_pad;
-    b.per = (a.m_pad / 4 + p.c - 1) / p.c * 4;
-    b.N = p.N;
-    b.K = p.K;
-    b.ldY = io.ldY;
-    b.ymode = io.ymode;
-    b.ssq_in_ld = io.ssq_in_ld;
-    b.pc = std::min(a.m_pad, 128);
-    b.pitch = (b.pc / 4 + p.c - 1) / p.c * 4 + 4;   // [rank][128][tokens per rank + 4] slots
-    b.dbg = a.dbg;
-    b.eps = io.eps;
-    b.Y = io.Y;
-    b.ssq_in = io.ssq_in;
-    b.yrow = io.yrow;
-    b.ssq_out = io.ssq_out;
-    b.nw = io.nw;
-    b.hout = io.hout;
-    b.timing = timing;
-    b.cta = cta;
-    const int stage_bytes = W_TILE_BYTES + a.m_pad * BLOCK_K * 2;
-    const int extra = (256 + 256 + 2048) * 4 + 64;   // inv_s, rowmap_s, red_s | xch, barriers
-    const char* e = getenv("SEED_SPLIT_SMEM_KB");
-    const int budget = (e ? atoi(e) : p.split_smem_kb) * 1024;
-    int stages = (budget - 1024 - extra - 16 * 16) / stage_bytes;
-    if (stages > MAX_STAGES) stages = MAX_STAGES;
-    // the accumulator dump (c > 1) and the two output staging buffers alias the ring
-    while (stages * stage_bytes < (c_dump_bytes(b) + 1023) / 1024 * 1024 + 2 * 12288) ++stages;
-    if (stages < 2) stages = 2;
-    b.stages = stages;
-    const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 2) * 8 + 16 + extra;
-    static bool sattr = false;
-    if (!sattr) {
-      cudaFuncSetAttribute(gemm_splitk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      if (cudaFuncSetAttribute(gemm_splitk_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
-        cudaGetLastError();
-      sattr = true;
-    }
-    if (smem > 227 * 1024) return cudaErrorInvalidValue;
-    return launch_clustered(gemm_splitk_kernel, dim3(p.c, p.tiles), dim3(192), smem, st, dim3(p.c, 1, 1), p.tmW,
-                            *io.tmX, b);
-  }
-  const int stage_bytes = W_TILE_BYTES + a.m_pad * BLOCK_K * 2;
-  const int extra = (256 + 2048 + 8) * 4;   // inv_s, red_s | xch_s, flags
-  int stages = ((p.smem_kb > 0 ? p.smem_kb * 1024 : smem_budget()) - 1024 - 256 - extra) / stage_bytes;
-  if (stages < 2) stages = 2;
+  // rows leave by 16-byte stores
+  if (p.N % 4 || (io.ymode == 1 && p.N % 8) || (io.ymode != 2 && io.ldY % 4)) return cudaErrorInvalidValue;
+  SplitArgs b{};
+  b.KB = p.KB;
+  b.c = p.c;
+  b.M = M;
+  b.m_pad = m_pad;
+  b.per = (m_pad / 4 + p.c - 1) / p.c * 4;
+  b.N = p.N;
+  b.K = p.K;
+  b.ldY = io.ldY;
+  b.ymode = io.ymode;
+  b.ssq_in_ld = io.ssq_in_ld;
+  b.pc = std::min(m_pad, 128);
+  b.pitch = (b.pc / 4 + p.c - 1) / p.c * 4 + 4;   // [rank][128][tokens per rank + 4] slots
+  b.eps = io.eps;
+  b.Y = io.Y;
+  b.ssq_in = io.ssq_in;
+  b.yrow = io.yrow;
+  b.ssq_out = io.ssq_out;
+  b.nw = io.nw;
+  b.hout = io.hout;
+  b.timing = timing;
+  b.cta = cta;
+  const int stage_bytes = W_TILE_BYTES + m_pad * BLOCK_K * 2;
+  const int extra = (256 + 256 + 2048) * 4 + 64;   // inv_s, rowmap_s, red_s | xch, barriers
+  const char* e = getenv("SEED_SPLIT_SMEM_KB");
+  const int budget = (e ? atoi(e) : p.split_smem_kb) * 1024;
+  int stages = (budget - 1024 - extra - 16 * 16) / stage_bytes;
   if (stages > MAX_STAGES) stages = MAX_STAGES;
-  a.stages = stages;
-  const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 4) * 8 + 16 + extra;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaFuncSetAttribute(gemm_streamk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_done = true;
+  // the accumulator dump (c > 1) and the two output staging buffers alias the ring
+  while (stages * stage_bytes < (c_dump_bytes(b) + 1023) / 1024 * 1024 + 2 * 12288) ++stages;
+  if (stages < 2) stages = 2;
+  b.stages = stages;
+  const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 2) * 8 + 16 + extra;
+  static bool sattr = false;
+  if (!sattr) {
+    cudaFuncSetAttribute(gemm_splitk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (cudaFuncSetAttribute(gemm_splitk_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+      cudaGetLastError();
+    sattr = true;
   }
-  return launch(gemm_streamk_kernel, dim3(p.G), dim3(192), smem, st, p.tmW, *io.tmX, a);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  return launch_clustered(gemm_splitk_kernel, dim3(p.c, p.tiles), dim3(192), smem, st, dim3(p.c, 1, 1), p.tmW,
+                          *io.tmX, b);
 }
 
 }  // namespace seed

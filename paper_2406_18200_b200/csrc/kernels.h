@@ -22,17 +22,12 @@ struct KVLayout {
   }
 };
 
-// ------------------------------------------------------------------ K2: stream-K GEMM
+// ------------------------------------------------------------------ K2: cluster split-K GEMM
 // Y[m][n] = sum_k X[m][k] W[n][k]; W [N][K] bf16, X [Mcap][K] bf16 (rows >= M ignored).
 struct GemmPlan {
-  int N, K, KB, tiles, U, G, S;  // S = max segments per CTA
-  int maxseg;                    // max partial segments per tile
-  int smem_kb;                   // dynamic shared memory per CTA (ring depth); 0: the default budget
-  int c;                         // cluster split-K: CTAs (k-ranges) per tile, a function of (N, K)
-  int split_smem_kb;             // cluster split-K: dynamic shared memory per CTA
-  bool split;                    // launch the cluster split-K form (env SEED_GEMM_SPLIT=0: stream-K)
-  int* seg;                      // device [tiles][maxseg + 1]: count, then segment ids in CTA order
-  int* counters;                 // device [tiles]: split-K tickets (zero between launches)
+  int N, K, KB, tiles;
+  int c;                         // CTAs (k-ranges) per 128-row weight tile, a function of (N, K)
+  int split_smem_kb;             // dynamic shared memory per CTA
   CUtensorMap tmW;
 };
 
@@ -41,7 +36,6 @@ bool encode_tmap_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t 
                     uint32_t box_outer, int swizzle_bytes = 128);
 void gemm_plan(GemmPlan* plan, const void* W, int N, int K, int min_units = 4);
 void gemm_plan_free(GemmPlan* plan);
-size_t gemm_partial_floats(const GemmPlan& plan, int M);
 // Operands and epilogue of one GEMM launch (see gemm.cu):
 // Y = epilogue(X W^T): X is a bf16 [M][K] operand read by TMA (tmX, box 64 x m_pad).
 // ssq_in (optional, [ceil(K/128)][ssq_in_ld]) scales output row m by 1/rms(x_m) = 1/sqrt(sum/K + eps):
@@ -67,7 +61,7 @@ struct GemmIO {
 // timing: optional [4] launch record (kind 1); cta: optional [G][16] per-CTA globaltimer ns:
 // start, producer release, producer done, first stage full, MMA done, first accumulator ready,
 // epilogue done, end, last partial stored, last ticket taken, reduce done, finish done
-cudaError_t gemm_run(const GemmPlan& plan, int M, const GemmIO& io, float* partial, cudaStream_t st,
+cudaError_t gemm_run(const GemmPlan& plan, int M, const GemmIO& io, cudaStream_t st,
                      unsigned long long* timing = nullptr, unsigned long long* cta = nullptr);
 cudaError_t timing_accumulate(unsigned long long* rec, int n, unsigned long long* acc, unsigned long long* last,
                               cudaStream_t st);
@@ -81,8 +75,9 @@ struct RowInfo {         // per row of the ragged batch
 };
 // x = embed[tok] (or x as given when embed == nullptr), ssq[t][m] = sum of x^2 over 128-column
 // tile t, h = bf16(x * nw) (the first RMSNorm's GEMM operand, R24)
-cudaError_t embed_stats(const __nv_bfloat16* embed, const int32_t* tok, int tok_stride, int M, int d, float* x,
-                        float* ssq, const __nv_bfloat16* nw, __nv_bfloat16* h, cudaStream_t st);
+// err (optional): bit 1 is set when a token id is outside [0, V) (the row then reads id 0)
+cudaError_t embed_stats(const __nv_bfloat16* embed, const int32_t* tok, int tok_stride, int M, int d, int V, float* x,
+                        float* ssq, const __nv_bfloat16* nw, __nv_bfloat16* h, int32_t* err, cudaStream_t st);
 cudaError_t rope_table_init(float2* table, int max_pos, int Dh, double theta, cudaStream_t st);
 cudaError_t kv_write_dense(const KVLayout& kv, int layer, int slot, int n, const __nv_bfloat16* k,
                            const __nv_bfloat16* v, cudaStream_t st);
@@ -126,11 +121,12 @@ struct VerifyArgs {
   float* dbg; double* stats;
   int32_t* work;   // device [B][2 (gamma + 1) + 1] scratch (accept flags, candidate tokens, ticket);
                    // the ticket words must be zero before the first launch (the kernel re-zeroes them)
+  int32_t* err;    // optional error word: [0] |= 2 when a race has no finite key, [1] += empty-residual fallbacks
 };
 cudaError_t vocab_verify(const VerifyArgs& a, cudaStream_t st);
 cudaError_t draft_sample(const float* z, long ld, int B, int V, float T, uint32_t k0, uint32_t k1,
                          const uint32_t* sids, const int32_t* rs, int j, int32_t* out, int out_stride, int32_t* out2,
-                         int out2_stride, cudaStream_t st);
+                         int out2_stride, int32_t* err, cudaStream_t st);
 cudaError_t philox_fill(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1, int n,
                         uint32_t* out, cudaStream_t st);
 
@@ -144,8 +140,10 @@ struct StreamState {     // device per-slot state (K5)
   int32_t* hist;         // [slots][max_ctx] validated tokens
   int32_t max_ctx;
 };
+// K5 (one CTA): commit + KV lengths (R6, R7) and this rank's exchange block: records [cap][gamma + 3]
+// (padding pre-filled with -1 by the caller) and, after them, *outside + the batch's undone streams
 cudaError_t rollback_commit(const StreamState& s, const int32_t* batch_slots, int B, int gamma,
-                            const int32_t* out_tok, const int32_t* out_cnt, int max_new, int32_t* records,
-                            const uint32_t* gids, cudaStream_t st);
+                            const int32_t* out_tok, const int32_t* out_cnt, int max_new, int32_t* records, int cap,
+                            const uint32_t* gids, const int32_t* outside, cudaStream_t st);
 
 }  // namespace seed

@@ -289,9 +289,14 @@ vocab_verify_kernel(VerifyArgs A) {
   if (has_d && rank == 0 && threadIdx.x == 0) {
     const Stat sq = glob[1];
     const int x = A.xs[(size_t)b * g + j];
-    const double lp = ((double)scaled_v(__ldg(zt + (size_t)j * V + x), A.T) - st.m) - l1t;
-    const double lq = ((double)scaled_v(__ldg(zd + (size_t)j * V + x), A.T) - sq.m) - log1p(sq.S);
-    const double rho = exp(fmin(0.0, lp - lq));
+    double lp = -INFINITY, lq = 0.0, rho = 0.0;
+    if (x >= 0 && x < V) {
+      lp = ((double)scaled_v(__ldg(zt + (size_t)j * V + x), A.T) - st.m) - l1t;
+      lq = ((double)scaled_v(__ldg(zd + (size_t)j * V + x), A.T) - sq.m) - log1p(sq.S);
+      rho = exp(fmin(0.0, lp - lq));
+    } else if (A.err) {
+      atomicOr(&A.err[0], 1);   // contract violation: a drafted id outside the vocabulary is rejected
+    }
     const Philox4 ph = philox4x32_10(0u, (kTagAccept << 24) | (uint32_t)(j + 1), rr, sid, A.k0, A.k1);
     const double u = philox_uniform(ph.x);
     accept = u < rho ? 1 : 0;
@@ -330,9 +335,11 @@ vocab_verify_kernel(VerifyArgs A) {
       return lq < lp ? lp + log(-expm1(lq - lp)) : -INFINITY;
     };
     y = race_exact(cluster, v0, n, c1, rr, sid, A.k0, A.k1, keys_s, red_f, &cta_f, red_b, &cta_best, res32, res64).v;
-    if (y < 0)  // empty residual (rounding only): bonus rule on the same row, same uniforms
+    if (y < 0) {  // empty residual (rounding only): bonus rule on the same row, same uniforms
       y = race_exact(cluster, v0, n, c1, rr, sid, A.k0, A.k1, keys_s, red_f, &cta_f, red_b, &cta_best, bonus32,
                      bonus64).v;
+      if (A.err && rank == 0 && threadIdx.x == 0) atomicAdd(&A.err[1], 1);
+    }
   } else if (A.bonus) {
     y = race_exact(cluster, v0, n, c1, rr, sid, A.k0, A.k1, keys_s, red_f, &cta_f, red_b, &cta_best, bonus32, bonus64)
             .v;
@@ -355,6 +362,7 @@ vocab_verify_kernel(VerifyArgs A) {
       int a = 0;
       while (a < g && vw[a]) ++a;
       const int ya = vw[g + 1 + a];
+      if (ya < 0 && (a < g || A.bonus) && A.err) atomicOr(&A.err[0], 2);   // no finite key (non-finite logits)
       int32_t* ot = A.out_tok + (size_t)b * (g + 1);
       for (int q = 0; q < a; ++q) ot[q] = A.xs[(size_t)b * g + q];
       int cnt = a;
@@ -371,7 +379,8 @@ vocab_verify_kernel(VerifyArgs A) {
 // K1 sampler: one cluster per row
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(VT)
 draft_sample_kernel(const float* z, long ld, int V, float T, uint32_t k0, uint32_t k1, const uint32_t* sids,
-                    const int32_t* rs, int j, int32_t* out, int out_stride, int32_t* out2, int out2_stride) {
+                    const int32_t* rs, int j, int32_t* out, int out_stride, int32_t* out2, int out2_stride,
+                    int32_t* err) {
   extern __shared__ __align__(128) float rows_s[];  // [slice] row, then [slice] race keys
   __shared__ float red_f[VT / 32];
   __shared__ float cta_f;
@@ -400,6 +409,7 @@ draft_sample_kernel(const float* z, long ld, int V, float T, uint32_t k0, uint32
   if (rank == 0 && threadIdx.x == 0) {
     out[(size_t)b * out_stride] = acc.v;
     if (out2) out2[(size_t)b * out2_stride] = acc.v;
+    if (acc.v < 0 && err) atomicOr(err, 2);   // no finite key (non-finite logits)
   }
 }
 
@@ -411,32 +421,47 @@ __global__ void philox_fill_kernel(uint32_t c0, uint32_t c1, uint32_t c2, uint32
   reinterpret_cast<uint4*>(out)[i] = make_uint4(p.x, p.y, p.z, p.w);
 }
 
-// K5: commit the emitted tokens, truncate to l, roll both KV lengths back (R6, R7).
-__global__ void rollback_commit_kernel(StreamState s, const int32_t* batch_slots, int B, int gamma,
-                                       const int32_t* out_tok, const int32_t* out_cnt, int max_new, int32_t* records,
-                                       const uint32_t* gids) {
+// K5: commit the emitted tokens, truncate to l, roll both KV lengths back (R6, R7), and write this
+// rank's exchange block (a6): one record [gid, c, tokens] per stream, then the number of this rank's
+// streams still undone after the round (*outside = undone streams not in the batch).  One CTA.
+constexpr int K5_THREADS = 256;
+__global__ void __launch_bounds__(K5_THREADS)
+rollback_commit_kernel(StreamState s, const int32_t* batch_slots, int B, int gamma, const int32_t* out_tok,
+                       const int32_t* out_cnt, int max_new, int32_t* records, int cap, const uint32_t* gids,
+                       const int32_t* outside) {
+  __shared__ int red[K5_THREADS / 32];
   pdl_trigger();
   pdl_wait();
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  const int slot = batch_slots[b];
-  const int t_before = s.tlen[slot];
-  const int room = max_new - s.L[slot];
-  const int c = min(out_cnt[b], max(room, 0));
-  int32_t* h = s.hist + (size_t)slot * s.max_ctx;
-  for (int i = 0; i < c; ++i) h[t_before + i] = out_tok[(size_t)b * (gamma + 1) + i];
-  const int t_new = t_before + c;
-  s.tlen[slot] = t_new;
-  s.L[slot] += c;
-  s.r[slot] += 1;
-  s.len_t[slot] = t_new - 1;                              // keep T'[:-1]
-  s.len_d[slot] = min(t_new - 1, t_before + gamma - 1);   // draft wrote up to |T| + gamma - 2
-  s.done[slot] = s.L[slot] >= max_new ? 1 : 0;
-  if (records) {
+  int undone = 0;
+  for (int b = threadIdx.x; b < B; b += K5_THREADS) {
+    const int slot = batch_slots[b];
+    const int t_before = s.tlen[slot];
+    const int room = max_new - s.L[slot];
+    const int c = min(out_cnt[b], max(room, 0));
+    int32_t* h = s.hist + (size_t)slot * s.max_ctx;
+    for (int i = 0; i < c; ++i) h[t_before + i] = out_tok[(size_t)b * (gamma + 1) + i];
+    const int t_new = t_before + c;
+    s.tlen[slot] = t_new;
+    s.L[slot] += c;
+    s.r[slot] += 1;
+    s.len_t[slot] = t_new - 1;                              // keep T'[:-1]
+    s.len_d[slot] = min(t_new - 1, t_before + gamma - 1);   // draft wrote up to |T| + gamma - 2
+    const int done = s.L[slot] >= max_new ? 1 : 0;
+    s.done[slot] = done;
+    undone += 1 - done;
     int32_t* rec = records + (size_t)b * (gamma + 3);
     rec[0] = (int32_t)gids[b];
     rec[1] = c;
     for (int i = 0; i <= gamma; ++i) rec[2 + i] = i < c ? out_tok[(size_t)b * (gamma + 1) + i] : -1;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) undone += __shfl_xor_sync(0xffffffffu, undone, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = undone;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int u = *outside;
+    for (int w = 0; w < K5_THREADS / 32; ++w) u += red[w];
+    records[(size_t)cap * (gamma + 3)] = u;
   }
 }
 }  // namespace
@@ -456,7 +481,7 @@ cudaError_t vocab_verify(const VerifyArgs& a, cudaStream_t st) {
 
 cudaError_t draft_sample(const float* z, long ld, int B, int V, float T, uint32_t k0, uint32_t k1,
                          const uint32_t* sids, const int32_t* rs, int j, int32_t* out, int out_stride, int32_t* out2,
-                         int out2_stride, cudaStream_t st) {
+                         int out2_stride, int32_t* err, cudaStream_t st) {
   const int slice = ((V + CS - 1) / CS + 3) & ~3;
   const size_t smem = (size_t)2 * slice * 4;
   if (smem > 220 * 1024) return cudaErrorInvalidValue;
@@ -466,7 +491,7 @@ cudaError_t draft_sample(const float* z, long ld, int B, int V, float T, uint32_
     attr = smem;
   }
   return launch(draft_sample_kernel, dim3(B * CS), dim3(VT), smem, st, z, ld, V, T, k0, k1, sids, rs, j, out,
-                out_stride, out2, out2_stride);
+                out_stride, out2, out2_stride, err);
 }
 
 cudaError_t philox_fill(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1, int n,
@@ -476,10 +501,10 @@ cudaError_t philox_fill(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint
 }
 
 cudaError_t rollback_commit(const StreamState& s, const int32_t* batch_slots, int B, int gamma,
-                            const int32_t* out_tok, const int32_t* out_cnt, int max_new, int32_t* records,
-                            const uint32_t* gids, cudaStream_t st) {
-  return launch(rollback_commit_kernel, dim3((B + 127) / 128), dim3(128), 0, st, s, batch_slots, B, gamma, out_tok,
-                out_cnt, max_new, records, gids);
+                            const int32_t* out_tok, const int32_t* out_cnt, int max_new, int32_t* records, int cap,
+                            const uint32_t* gids, const int32_t* outside, cudaStream_t st) {
+  return launch(rollback_commit_kernel, dim3(1), dim3(K5_THREADS), 0, st, s, batch_slots, B, gamma, out_tok, out_cnt,
+                max_new, records, cap, gids, outside);
 }
 
 }  // namespace seed

@@ -96,3 +96,63 @@ def test_token_table_merge(lib):
     t.merge(recs)
     t.merge(np.array([[7, 3, 1, 2, 3, -1, -1]], dtype=np.int32))
     assert t.get(7) == [11, 12, 1, 2, 3] and t.get(9) == [5]
+
+
+def test_scheduler_remove_then_readd(lib):
+    """removing an undone stream and adding the same id again must leave one queue entry."""
+    from paper_2406_18200_b200 import Scheduler
+    s = Scheduler([1, 2])
+    assert s.pop(1) == [1]
+    s.complete([1], [False])               # 2, 1 queued
+    assert lib.seed_sched_remove(s.h, 1) == 0
+    s.add(1)                               # 2, 1 (fresh)
+    assert s.pop(4) == [2, 1]
+    s.complete([2, 1], [False, False])
+    assert s.pop(4) == [2, 1]              # no stale duplicate of 1
+
+
+def test_round_book_pack_complete(lib):
+    """The exchange block: records [gid, c, tokens] with c truncated to l (R7), padding gid -1, and the
+    rank's undone count after the round; completion commits, requeues and sums the pending counts."""
+    from paper_2406_18200_b200 import RoundBook, SeedError
+    g, l, cap = 2, 5, 3
+    b = RoundBook(g, l, cap, world=2, rank=1)
+    b.add(10, [3, 4])
+    b.add(12, [3, 4, 5])
+    b.add(14, [9, 9])
+    with pytest.raises(SeedError):
+        b.add(12, [1, 2])                 # duplicate id
+    batch = b.schedule(2)
+    assert batch == [10, 12]
+    tok = np.array([[7, 8, 9], [6, -1, -1]], dtype=np.int32)
+    blk = b.pack(batch, tok, [3, 1])
+    stride = g + 3
+    assert blk.size == cap * stride + 1
+    assert blk[:stride].tolist() == [10, 3, 7, 8, 9]
+    assert blk[stride:2 * stride].tolist() == [12, 1, 6, -1, -1]
+    assert (blk[2 * stride:3 * stride] == -1).all()
+    assert blk[-1] == 3                   # 14 not in the batch + 10, 12 still undone
+    other = np.full(cap * stride + 1, -1, dtype=np.int32)
+    other[:stride] = [11, 2, 1, 2, -1]
+    other[-1] = 1
+    b.complete(np.stack([other, blk]))
+    assert b.global_pending() == 4
+    assert b.tokens(10) == [7, 8, 9] and b.tokens(11) == [1, 2]
+    assert b.info(10)["L"] == 3 and b.info(10)["r"] == 1
+    # truncation to l: 10 has room 2
+    batch = b.schedule(3)
+    assert batch == [14, 10, 12]
+    blk = b.pack(batch, np.array([[1, 1, 1], [5, 5, 5], [2, 2, 2]], dtype=np.int32), [1, 3, 3])
+    assert blk[stride:stride + 2].tolist() == [10, 2]
+    assert blk[-1] == 2                   # 10 done (3 + 2 = l); 14 (1 of 5), 12 (4 of 5) undone
+    other[-1] = 0
+    other[:stride] = -1
+    b.complete(np.stack([other, blk]))
+    assert b.global_pending() == 2 and b.info(10)["done"] == 1
+    assert b.schedule(3) == [14, 12]
+    # remove and re-add an undone id: no stale queue entry, fresh tokens
+    b.remove(14)
+    b.add(14, [8, 8])
+    assert b.tokens(14) == []
+    with pytest.raises(SeedError):
+        b.complete(np.stack([other, other]))   # the own tail cannot be below the own undone count

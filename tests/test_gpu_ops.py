@@ -82,7 +82,7 @@ SETTINGS = [(1.0, 0.3, 1.0), (1.0, 0.1, 1.0), (1.0, 0.02, 1.0), (3.0, 1.0, 0.2),
 
 
 @pytest.mark.parametrize("V,gamma,B", [(32, 4, 3000), (32, 1, 1000), (32, 6, 1000), (32000, 4, 96), (32000, 5, 24),
-                                       (32000, 6, 5)])
+                                       (32000, 6, 5), (32000, 4, 192), (32000, 1, 3)])
 def test_verify_vs_oracle(ops, V, gamma, B):
     """P1: accepted lengths and token ids bit-exact except oracle-flagged near-ties."""
     total = mism = flagged = 0
@@ -177,3 +177,60 @@ def test_gpu_round_chi2(ops):
     exp_ = m * pj[keep] / pj[keep].sum() * (joint[keep].sum() / m)
     chi2 = np.sum((joint[keep] - exp_) ** 2 / exp_)
     assert chi2 < stats.chi2.ppf(0.99, int(keep.sum()) - 1), chi2
+
+
+def test_verify_empty_residual_gpu(ops):
+    """R3 edge case through rounding (see tests/test_oracle_sampling.py::test_empty_residual_fallback):
+    the residual max(0, p - q) is empty in fp64, so K4 falls back to the bonus rule on the same row
+    with the same uniforms -- the same token as the oracle's fallback, for every stream."""
+    V, g, T = 32000, 1, 1.0
+    rng = np.random.default_rng(12)
+    zd = rng.standard_normal((g, V)).astype(np.float32)
+    x = int(np.argmin(zd[0]))
+    zd[0, x] = np.float32(zd[0].max() - 60.0)
+    zt = np.zeros((g + 1, V), dtype=np.float32)
+    zt[:g] = zd
+    zt[0, x] = zd[0, x] - np.float32(5.0)
+    zt[g] = rng.standard_normal(V).astype(np.float32)
+    B = 64
+    ZT = np.broadcast_to(zt, (B, g + 1, V)).copy()
+    ZD = np.broadcast_to(zd, (B, g, V)).copy()
+    xs = np.full((B, g), x, dtype=np.int32)
+    sids = np.arange(B, dtype=np.int64) + 1000
+    rs = np.zeros(B, dtype=np.int32)
+    out = ops.verify(torch.from_numpy(ZT).cuda(), torch.from_numpy(ZD).cuda(), torch.from_numpy(xs).cuda(), T, SEED,
+                     sids, rs)
+    tok, cnt, a = out["out_tok"].cpu().numpy(), out["out_cnt"].cpu().numpy(), out["a"].cpu().numpy()
+    fallbacks = 0
+    for b in range(B):
+        r = sp.verify_stream(ZT[b], ZD[b], [x], T, SEED, int(sids[b]), 0)
+        assert a[b] == r.a and list(tok[b, :cnt[b]]) == r.emitted, b
+        fallbacks += r.fallback
+    assert fallbacks > B // 2
+
+
+def test_gpu_bonus_chi2(ops):
+    """R1 on the GPU: over 1e6 K4 launches' streams with q close to p, the bonus tokens of the
+    all-accepted rounds follow p_{gamma+1} (chi-square at alpha = 0.01, df 31)."""
+    from scipy import stats
+    rng = np.random.default_rng(21)
+    g, V, n, T = 4, 32, 1_000_000, 1.0
+    zt1 = rng.standard_normal((g + 1, V)).astype(np.float32)
+    zd1 = (zt1[:g] + rng.standard_normal((g, V)) * 0.15).astype(np.float32)
+    sids = np.arange(n, dtype=np.int64)
+    rs = np.full(n, 3, dtype=np.int32)
+    zd_dev = torch.from_numpy(np.broadcast_to(zd1, (n, g, V)).copy()).cuda()
+    xs = torch.empty((n, g), dtype=torch.int32, device="cuda")
+    for j in range(g):
+        xs[:, j] = ops.draft_sample(zd_dev[:, j].contiguous(), T, SEED, sids, rs, j + 1)
+    zt_dev = torch.from_numpy(np.broadcast_to(zt1, (n, g + 1, V)).copy()).cuda()
+    out = ops.verify(zt_dev, zd_dev, xs, T, SEED, sids, rs, want_dbg=False)
+    a = out["a"].cpu().numpy()
+    tok = out["out_tok"].cpu().numpy()
+    full = a == g
+    assert full.sum() > 50_000
+    pb = np.exp(sp.logsoftmax_tail(sp.scaled_logits(zt1[g], T)))
+    c = np.bincount(tok[full, g], minlength=V).astype(float)
+    m = c.sum()
+    chi = np.sum((c - m * pb) ** 2 / (m * pb))
+    assert chi < stats.chi2.ppf(0.99, V - 1), chi

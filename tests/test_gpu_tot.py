@@ -106,7 +106,9 @@ def test_tot_bfs_vs_oracle(pkg, depth, n, b):
 
 
 @pytest.mark.parametrize("dname,tname,plen", [("toy_draft", "toy_target", 8), ("toy_draft", "toy_target", 77),
-                                              ("llama_68m", "llama_68m", 150)])
+                                              ("toy_draft", "toy_target", 17), ("toy_draft", "toy_target", 18),
+                                              ("llama_68m", "llama_68m", 150), ("llama_68m", "llama_68m", 145),
+                                              ("llama_68m", "llama_68m", 146)])
 def test_fork_stream_equals_add_stream(pkg, dname, tname, plen):
     """seed_fork_stream (shared full prefix pages + a copied partial page) == seed_add_stream."""
     ds, ts = seedgen.SHAPES[dname], seedgen.SHAPES[tname]

@@ -1,8 +1,11 @@
-"""N > 1 host path on CPU (gloo, world size 2): replicas own the streams g with g mod N = rank,
-run their rounds, exchange fixed-size per-round record blocks with an all-gather (the a6 step,
-NCCL on GPU) and merge them with libseed's token table.  Every rank must end with every
-stream's tokens, identical to a world-size-1 run (world-size invariance): the RNG is
-keyed by global ids and stream-local rounds.  The per-rank rounds are the oracle's (no GPU here).
+"""N > 1 host path on CPU (gloo, world size 2) through libseed's own round book (seed_book_*):
+replicas own the streams g with g mod N = rank; every round each rank schedules (possibly an
+empty batch), runs the round, packs its fixed-size exchange block with seed_book_pack (the host
+twin of the K5 kernel's block), all-gathers the blocks and applies them with seed_book_complete --
+exactly the host logic seed_verify / seed_schedule_round run on the GPU.  The rounds themselves
+are the oracle's (no GPU here).  Every rank must end with every stream's tokens, identical to a
+world-size-1 run (world-size invariance), and ranks whose streams finish early must keep
+joining the collective with empty blocks until the gathered pending count reaches zero.
 """
 import os
 import socket
@@ -17,55 +20,57 @@ import seedgen
 from oracle import llama as ll
 from oracle.seed_round import SeedOracle
 
-GAMMA, MAX_NEW, N_STREAMS, C = 4, 12, 4, 4
+GAMMA, C = 4, 4
 
 
-def _oracle(prompts, ids):
+def _oracle(prompts, ids, max_new):
     cfg = seedgen.CONFIGS["toy"]
     ds, ts = seedgen.SHAPES[cfg["draft"]], seedgen.SHAPES[cfg["target"]]
     o = SeedOracle(ll.LlamaShape(**ts), seedgen.model_weights(ts, seedgen.TARGET_SEED), ll.LlamaShape(**ds),
                    seedgen.model_weights(ds, seedgen.DRAFT_SEED), gamma=GAMMA, temperature=1.0,
-                   seed=seedgen.PHILOX_SEED, max_new=MAX_NEW)
+                   seed=seedgen.PHILOX_SEED, max_new=max_new)
     for g in ids:
         o.add_stream(g, prompts[g])
     return o
 
 
-def _prompts():
-    return seedgen.prompts("toy", n_streams=N_STREAMS - 1) + [[7, 8, 9, 10, 11, 12]]
+def _prompts(n):
+    return (seedgen.prompts("toy", n_streams=3) + [[7, 8, 9, 10, 11, 12], [4, 5, 6], [20, 21, 22, 23]])[:n]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, n_streams, max_new, owner, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from oracle.scheduler import RoundScheduler
-    from paper_2406_18200_b200 import TokenTable
-    prompts = _prompts()
-    mine = [g for g in range(N_STREAMS) if g % world == rank]
-    orc = _oracle(prompts, mine)
-    sched = RoundScheduler(mine)
-    table = TokenTable(GAMMA)
-    stride = GAMMA + 3
+    from paper_2406_18200_b200 import RoundBook
+    prompts = _prompts(n_streams)
+    mine = [g for g in range(n_streams) if owner(g, world) == rank]
+    orc = _oracle(prompts, mine, max_new)
+    book = RoundBook(GAMMA, max_new, C, world=world, rank=rank)
+    for g in mine:
+        book.add(g, prompts[g])
+    rounds, empty_rounds = 0, 0
     while True:
-        busy = torch.tensor([0 if sched.all_done() else 1])
-        dist.all_reduce(busy)
-        if busy.item() == 0:
+        batch = book.schedule(C)
+        out_tok = np.full((len(batch), GAMMA + 1), -1, dtype=np.int32)
+        out_cnt = np.zeros(len(batch), dtype=np.int32)
+        if batch:
+            # the round on this rank (the GPU's role): untruncated emitted tokens per stream
+            for b, rec in enumerate(orc.round(batch)):
+                out_tok[b, :len(rec.emitted)] = rec.emitted
+                out_cnt[b] = len(rec.emitted)
+        else:
+            empty_rounds += 1
+        block = torch.from_numpy(book.pack(batch, out_tok, out_cnt))
+        out = [torch.empty_like(block) for _ in range(world)]
+        dist.all_gather(out, block)
+        book.complete(torch.stack(out).numpy())
+        rounds += 1
+        pending = book.global_pending()
+        if pending == 0:
             break
-        block = np.full((C, stride), -1, dtype=np.int32)      # fixed-size per-rank record block
-        if not sched.all_done():
-            batch = sched.schedule(C)
-            before = {g: len(orc.streams[g].T) for g in batch}
-            orc.round(batch)
-            for b, g in enumerate(batch):
-                st = orc.streams[g]
-                new = st.T[before[g]:]
-                block[b, 0], block[b, 1] = g, len(new)
-                block[b, 2:2 + len(new)] = new
-            sched.complete(batch, [orc.streams[g].done for g in batch])
-        out = [torch.empty((C, stride), dtype=torch.int32) for _ in range(world)]
-        dist.all_gather(out, torch.from_numpy(block))
-        table.merge(torch.stack(out).numpy())
-    q.put((rank, {g: table.get(g) for g in range(N_STREAMS)}))
+        assert rounds < 1000
+    own_ok = all(book.tokens(g) == orc.streams[g].T[orc.streams[g].prompt_len:] for g in mine)
+    q.put((rank, {g: book.tokens(g) for g in range(n_streams)}, rounds, empty_rounds, own_ok))
     dist.destroy_process_group()
 
 
@@ -86,22 +91,52 @@ def lib():
     return _lib.load()
 
 
-def test_world_size_invariance_gloo(lib):
+def _run(world, n_streams, max_new, owner):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n_streams, max_new, owner, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = dict(q.get(timeout=600) for _ in procs)
+    res = {}
+    for _ in procs:
+        rank, toks, rounds, empty, own_ok = q.get(timeout=600)
+        res[rank] = (toks, rounds, empty, own_ok)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    # world size 1 reference
-    prompts = _prompts()
-    orc = _oracle(prompts, range(N_STREAMS))
-    ref, _, _ = orc.run(C)
+    return res
+
+
+def _mod(g, world):
+    return g % world
+
+
+def _all_on_zero(g, world):
+    return 0
+
+
+@pytest.mark.parametrize("n_streams,max_new,owner", [(4, 12, _mod), (5, 17, _mod), (2, 9, _all_on_zero)])
+def test_world_size_invariance_gloo(lib, n_streams, max_new, owner):
+    res = _run(2, n_streams, max_new, owner)
+    prompts = _prompts(n_streams)
+    orc = _oracle(prompts, range(n_streams), max_new)
+    ref, rounds, _ = orc.run(C)
+    # every rank joined the same number of exchanges (no rank left a collective early)
+    assert res[0][1] == res[1][1]
     for rank in (0, 1):
-        for g in range(N_STREAMS):
-            assert res[rank][g] == ref[g], (rank, g)
-            assert len(ref[g]) == MAX_NEW
+        toks, _, _, own_ok = res[rank]
+        assert own_ok
+        for g in range(n_streams):
+            assert toks[g] == ref[g], (rank, g)
+            assert len(ref[g]) == max_new
+    if owner is _all_on_zero:
+        assert res[1][2] == res[1][1]   # rank 1 owns nothing: every one of its rounds was empty
+
+
+def test_uneven_completion_gloo(lib):
+    """Streams of different ranks finish on different rounds (acceptance differs); the rank that
+    finishes first keeps posting empty blocks and nobody hangs."""
+    res = _run(2, 5, 23, _mod)
+    assert res[0][1] == res[1][1]
+    assert res[0][2] + res[1][2] > 0, "expected at least one empty round on one rank"

@@ -265,32 +265,114 @@ def test_race_sampler_chi2():
     assert chi < stats.chi2.ppf(0.99, df), (chi, df)
 
 
+def _rows(rng, n_pos, V, T):
+    """Position-specific target / draft logits rows (context-free, so AR sampling is a product law)."""
+    sc = 1.0 if T == 1.0 else 0.25
+    zt = (rng.standard_normal((n_pos, V)) * sc).astype(np.float32)
+    zd = (zt + rng.standard_normal((n_pos, V)) * 0.5 * sc).astype(np.float32)
+    return zt, zd
+
+
+def _emitted(xs, a, y, gamma):
+    """Emitted token lists per stream from a vectorised round (x_1..x_a, then y when y >= 0)."""
+    return [list(xs[i, :a[i]]) + ([int(y[i])] if y[i] >= 0 else []) for i in range(len(a))]
+
+
 @pytest.mark.parametrize("T", [1.0, 0.2])
 def test_round_chi2_first_tokens(T):
-    """north_star: chi-square at alpha = 0.01 over 1e6 rounds: the first emitted
-    token follows p_1 (df 31) and the first two follow p_1 x p_2 (df 1023)."""
+    """north_star: chi-square at alpha = 0.01 over 1e6 streams: the first emitted token follows
+    p_1 (df 31) and the first two follow p_1 x p_2 (df 1023).  Rows are position-specific and
+    context-free, so target-only sampling is the product law; a stream whose first round emitted one
+    token runs a second round (stream-local round 1, positions 2 ..) for its second token."""
     rng = np.random.default_rng(5)
     gamma, V = 4, 32
-    zt = (rng.standard_normal((gamma + 1, V)) * (1.0 if T == 1.0 else 0.25)).astype(np.float32)
-    zd = (zt[:gamma] + rng.standard_normal((gamma, V)) * 0.5 * (1.0 if T == 1.0 else 0.25)).astype(np.float32)
+    zt, zd = _rows(rng, 2 * gamma + 2, V, T)
     n = 1_000_000
     sids = np.arange(n, dtype=np.uint64)
-    xs, a, y = _round_vec(zt, zd, T, sids, 0)
+    xs, a, y = _round_vec(zt[:gamma + 1], zd[:gamma], T, sids, 0)
     first = np.where(a >= 1, xs[:, 0], y)
+    second = np.where(a >= 2, xs[:, 1], np.where(a == 1, y, -1))
+    one = second < 0                       # the first round emitted one token: round 2 from position 2
+    xs2, a2, y2 = _round_vec(zt[1:gamma + 2], zd[1:gamma + 1], T, sids[one], 1)
+    second[one] = np.where(a2 >= 1, xs2[:, 0], y2)
     p1 = np.exp(sp.logsoftmax_tail(sp.scaled_logits(zt[0], T)))
+    p2 = np.exp(sp.logsoftmax_tail(sp.scaled_logits(zt[1], T)))
     chi, df = _chi2(np.bincount(first, minlength=V).astype(np.float64), p1)
     assert chi < stats.chi2.ppf(0.99, df), (chi, df)
-    # the second emitted token, conditioned on the first: rows are position-specific
-    # (p_2 is the same for every first token here), so the joint law is p_1 x p_2
-    second = np.where(a >= 2, xs[:, 1], np.where(a == 1, y, -1))
-    has2 = second >= 0
+    # joint law of the first two tokens: p_1 x p_2 (df 1023; cells with expectation < 5 pooled)
+    pj = np.outer(p1, p2).reshape(-1)
+    cnt = np.bincount(first * V + second, minlength=V * V).astype(np.float64)
+    keep = n * pj >= 5
+    cj = np.append(cnt[keep], cnt[~keep].sum())
+    pk = np.append(pj[keep], pj[~keep].sum())
+    chi2j, dfj = _chi2(cj, pk)
+    assert dfj >= 500, dfj
+    assert chi2j < stats.chi2.ppf(0.99, dfj), (chi2j, dfj)
+
+
+def test_round_chi2_detects_wrong_bonus():
+    """The joint test must catch a plausible mistake: the bonus token drawn from p_gamma (the row
+    of the last draft position) instead of p_{gamma+1}."""
+    rng = np.random.default_rng(8)
+    gamma, V, T = 1, 32, 1.0
+    zt, zd = _rows(rng, 2 * gamma + 2, V, T)
+    zd[:] = zt                             # q == p: every draft accepted, the bonus is always token 2
+    n = 200_000
+    bad = zt.copy()
+    bad[gamma] = zt[gamma - 1]
+    xs, a, y = _round_vec(bad[:gamma + 1], zd[:gamma], T, np.arange(n, dtype=np.uint64), 0)
     p2 = np.exp(sp.logsoftmax_tail(sp.scaled_logits(zt[1], T)))
-    joint = first[has2] * V + second[has2]
-    # P(second exists | first) depends only on acceptance of position 1, which is
-    # independent of which token was emitted at position 2; test the conditional law
-    chi2, df2 = _chi2(np.bincount(second[has2], minlength=V).astype(np.float64), p2)
-    assert chi2 < stats.chi2.ppf(0.99, df2), (chi2, df2)
-    assert joint.size > 0
+    chi, df = _chi2(np.bincount(y, minlength=V).astype(np.float64), p2)
+    assert chi > stats.chi2.ppf(0.99, df)
+
+
+@pytest.mark.parametrize("T", [1.0, 0.2])
+def test_bonus_token_chi2(T):
+    """R1 (Leviathan et al., cited P:93): on full acceptance the bonus token follows p_{gamma+1}.
+    Over 1e6 rounds on the toy V = 32, the bonus tokens of all-accepted rounds pass chi-square at
+    alpha = 0.01 against p_{gamma+1} (df 31)."""
+    rng = np.random.default_rng(9)
+    gamma, V = 4, 32
+    zt, zd = _rows(rng, gamma + 1, V, T)
+    zd = (zt[:gamma] + (zd[:gamma] - zt[:gamma]) * 0.3).astype(np.float32)   # q close to p: frequent a = gamma
+    n = 1_000_000
+    xs, a, y = _round_vec(zt, zd, T, np.arange(n, dtype=np.uint64), 0)
+    full = a == gamma
+    assert full.sum() > 50_000
+    pb = np.exp(sp.logsoftmax_tail(sp.scaled_logits(zt[gamma], T)))
+    chi, df = _chi2(np.bincount(y[full], minlength=V).astype(np.float64), pb)
+    assert chi < stats.chi2.ppf(0.99, df), (chi, df)
+    # the same rounds against the WRONG row (p_gamma) must fail: the test has power
+    pw = np.exp(sp.logsoftmax_tail(sp.scaled_logits(zt[gamma - 1], T)))
+    chi_w, _ = _chi2(np.bincount(y[full], minlength=V).astype(np.float64), pw)
+    assert chi_w > stats.chi2.ppf(0.99, df)
+
+
+def test_empty_residual_fallback():
+    """R3 edge case (only through rounding): the drafted token x has p(x) < q(x) but every other
+    token's p and q agree to fp64 precision, so max(0, p - q) is empty after rounding.  The oracle
+    then draws from the bonus rule on the same row with the same uniforms and flags the decision."""
+    V, gamma, T = 64, 1, 1.0
+    rng = np.random.default_rng(12)
+    zd = (rng.standard_normal((gamma, V))).astype(np.float32)
+    x = int(np.argmin(zd[0]))
+    zd[0, x] = np.float32(zd[0].max() - 60.0)     # q(x) ~ e^-60: its change is invisible in S'
+    zt = np.zeros((gamma + 1, V), dtype=np.float32)
+    zt[:gamma] = zd
+    zt[0, x] = zd[0, x] - np.float32(5.0)         # p(x) = e^-5 q(x): rho ~ 0.0067
+    zt[gamma] = rng.standard_normal(V).astype(np.float32)
+    lp = sp.logsoftmax_tail(sp.scaled_logits(zt[0], T))
+    lq = sp.logsoftmax_tail(sp.scaled_logits(zd[0], T))
+    assert np.all(sp.residual_logweights(lp, lq) == -np.inf)
+    hits = 0
+    for sid in range(200):
+        r = sp.verify_stream(zt, zd, [x], T, SEED, sid, 0)
+        if r.a == 0:
+            hits += 1
+            assert r.fallback and r.flags >= 1
+            u = ph.race_uniforms(SEED, sid, 0, ph.TAG_RESAMPLE, 1, V)
+            assert r.y == sp.race(sp.scaled_logits(zt[0], T).astype(np.float64), u)[0]
+    assert hits > 150
 
 
 def test_alpha_and_expected_emitted():
