@@ -98,6 +98,14 @@ SEED_DEV void tma_load_2d_u32(uint32_t smem_dst, const void* tmap, uint64_t* bar
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(x), "r"(y)
       : "memory");
 }
+// 3D TMA load (tile mode) to a shared::cta address, default L2 policy
+SEED_DEV void tma_load_3d_u32(uint32_t smem_dst, const void* tmap, uint64_t* bar, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
 SEED_DEV void st_shared_v4(uint32_t addr, uint4 v) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
@@ -183,6 +191,22 @@ SEED_DEV unsigned long long globaltimer_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
+}
+
+// Per-launch device timing record (profiling; kinds: 1 K2 GEMM, 2 K3 attention, 3 K4 vocabulary,
+// 4 K1 draft sampler, 5 embedding + row statistics, 6 K5 rollback): [0] first CTA start, [1] first
+// CTA past the PDL wait, [2] last CTA end, [3] kind.  Thread 0 of every CTA; rec may be null.
+SEED_DEV void rec_start(unsigned long long* rec) {
+  if (rec && threadIdx.x == 0) atomicMin(&rec[0], globaltimer_ns());
+}
+SEED_DEV void rec_release(unsigned long long* rec) {
+  if (rec && threadIdx.x == 0) atomicMin(&rec[1], globaltimer_ns());
+}
+SEED_DEV void rec_end(unsigned long long* rec, int kind) {
+  if (rec && threadIdx.x == 0) {
+    atomicMax(&rec[2], globaltimer_ns());
+    rec[3] = (unsigned long long)kind;
+  }
 }
 
 SEED_DEV bool elect_one() {

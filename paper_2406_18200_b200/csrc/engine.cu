@@ -122,6 +122,7 @@ struct Model {
   // paged KV
   KVLayout kv{};
   CUtensorMap tmkv;                 // 2D tensor map of the KV pool (attention's page-block copies)
+  CUtensorMap tmq;                  // fp32 2D tensor map of the QKV output y (attention's query rows)
   int32_t* page_table_dev = nullptr;
   int32_t* page_table = nullptr;          // pinned host mirror [slots][max_pages]
   std::vector<int32_t> free_pages;
@@ -189,7 +190,7 @@ struct seed_ctx_s {
   int C = 0, G = 0;
   float *tgt_logits = nullptr, *drf_logits = nullptr;
   int32_t *xs = nullptr, *vtok = nullptr, *out_tok = nullptr, *out_cnt = nullptr, *out_acc = nullptr;
-  int32_t* verify_work = nullptr;  // K4 scratch [C][2 (gamma + 1) + 1] (tickets zero between launches)
+  void* verify_work = nullptr;     // K4 scratch (vocab_verify_work_bytes; tickets zero between launches)
   int32_t *records = nullptr, *records_all = nullptr, *records_host = nullptr;   // exchange blocks (a6)
   int block_ints = 0;             // words per rank's block: C records of gamma + 3, then the undone count
   // device error word (SEED_EDEVICE): [0] contract-violation bits, [1] empty-residual fallbacks (K4)
@@ -262,13 +263,17 @@ const CUtensorMap* xmap(seed_ctx ctx, const bf16* buf, int K, int rows_cap, int 
   return &(ctx->xmaps[key] = m);
 }
 
+// the next device timing record of the round being enqueued (profiling), else null; cta: the
+// launch's per-CTA trace words (SEED_CTA_TRACE=1)
+unsigned long long* next_rec(seed_ctx ctx, unsigned long long** cta = nullptr) {
+  if (!(ctx->profile && ctx->in_round && ctx->rec_used < ctx->rec_cap)) return nullptr;
+  if (cta && ctx->cta_rec) *cta = ctx->cta_rec + (size_t)ctx->rec_used * kCtaRec;
+  return ctx->timing_rec + 4 * ctx->rec_used++;
+}
+
 seed_status run_gemm(seed_ctx ctx, const GemmPlan& p, int M, const seed::GemmIO& io, cudaStream_t st) {
-  unsigned long long* rec = nullptr;
   unsigned long long* cta = nullptr;
-  if (ctx->profile && ctx->in_round && ctx->rec_used < ctx->rec_cap) {
-    if (ctx->cta_rec) cta = ctx->cta_rec + (size_t)ctx->rec_used * kCtaRec;
-    rec = ctx->timing_rec + 4 * ctx->rec_used++;
-  }
+  unsigned long long* rec = next_rec(ctx, &cta);
   CK(seed::gemm_run(p, M, io, st, rec, cta));
   if (ctx->in_round) {
     // algorithmic bytes: weights + bf16 X + output (fp32 Y; residual: read + write x, write bf16 h;
@@ -396,7 +401,7 @@ seed_status build_model(seed_ctx ctx, Model& m, const seed_model_shape& sh, cons
   std::memset(m.page_table, 0, (size_t)slots * max_pages * 4);
   CK(cudaMemset(m.page_table_dev, 0, (size_t)slots * max_pages * 4));
   m.kv.page_table = m.page_table_dev;
-  if (!seed::attn_kv_tmap(&m.tmkv, m.kv, pool_pages)) return fail(ctx, SEED_ECUDA, "seed_init", "KV tensor map");
+  if (!seed::attn_kv_tmap(&m.tmkv, m.kv, pool_pages, &m.kv.kv3d)) return fail(ctx, SEED_ECUDA, "seed_init", "KV tensor map");
   m.held.assign(slots, 0);
   for (size_t i = pool_pages; i-- > 0;) m.free_pages.push_back((int32_t)i);
   m.refs.assign(pool_pages, 0);
@@ -417,8 +422,10 @@ seed_status build_model(seed_ctx ctx, Model& m, const seed_model_shape& sh, cons
   CK(cudaMalloc(&m.aws.o_part, (size_t)m.aws.max_splits * mc * dq * 4));
   CK(cudaMalloc(&m.aws.ml_part, (size_t)m.aws.max_splits * mc * m.H * 2 * 4));
   m.aws.max_counters = (int)(mc * m.H);
-  CK(cudaMalloc(&m.aws.counters, (size_t)m.aws.max_counters * 4));
-  CK(cudaMemset(m.aws.counters, 0, (size_t)m.aws.max_counters * 4));
+  CK(cudaMalloc(&m.aws.counters, (size_t)(m.aws.max_counters + 2) * 4));
+  CK(cudaMemset(m.aws.counters, 0, (size_t)(m.aws.max_counters + 2) * 4));
+  if (!seed::encode_tmap_2d_f32(&m.tmq, m.y, (uint64_t)m.nqkv, (uint64_t)mc, (uint64_t)m.nqkv, (uint32_t)m.Dh, 16))
+    return fail(ctx, SEED_ECUDA, "seed_init", "QKV tensor map");
   return SEED_OK;
 }
 
@@ -483,7 +490,8 @@ seed_status forward_chunk(seed_ctx ctx, Model& m, const ChunkDesc& c, cudaStream
   auto next_norm = [&](int l) { return l + 1 < m.L ? m.an[l + 1] : m.final_norm; };
   // embedding (or the given residual), its per-tile sums of squares and h = bf16(x * attn_norm)
   CK(seed::embed_stats(embed ? m.embed : nullptr, c.tok.dev, c.tok.stride, M, m.d, m.V, m.x, m.ssq_b,
-                       first_layer < m.L ? m.an[first_layer] : m.final_norm, m.h, ctx->dev_err, st));
+                       first_layer < m.L ? m.an[first_layer] : m.final_norm, m.h, ctx->dev_err, st,
+                       next_rec(ctx)));
   ctx->kernel_launches++;
   seed::SeqInfo seqs{c.q_start, c.q_len, c.kv_len, c.seq_slot, c.seq_stable};
   const CUtensorMap* tm_h = xmap(ctx, m.h, m.d, m.m_cap, M);
@@ -509,13 +517,10 @@ seed_status forward_chunk(seed_ctx ctx, Model& m, const ChunkDesc& c, cudaStream
     }
     {
       seed::AttnWorkspace aws = m.aws;
-      aws.timing = nullptr;
-      if (ctx->profile && ctx->in_round && ctx->rec_used < ctx->rec_cap) {
-        if (ctx->cta_rec) aws.cta = ctx->cta_rec + (size_t)ctx->rec_used * kCtaRec;
-        aws.timing = ctx->timing_rec + 4 * ctx->rec_used++;
-      }
-      CK(seed::attention(m.y, M, c.n_seq, c.max_q_len, c.max_kv, m.H, m.Hk, m.Dh, seqs, m.rope, m.kv, m.tmkv, l, aws,
-                         m.attn, st));
+      aws.cta = nullptr;
+      aws.timing = next_rec(ctx, &aws.cta);
+      CK(seed::attention(m.y, M, c.n_seq, c.max_q_len, c.max_kv, m.H, m.Hk, m.Dh, seqs, m.rope, m.kv, m.tmkv, m.tmq, l,
+                         aws, m.attn, st));
     }
     // O: x += attn Wo^T; sums of squares -> ssq_a; h = bf16(x * mlp_norm)
     {
@@ -817,7 +822,7 @@ seed_status enqueue_draft(seed_ctx ctx, cudaStream_t st) {
     if ((s = forward_chunk(ctx, ctx->dm, c, st)) != SEED_OK) return s;
     // K1 sampler: x_j -> xs[b][j-1] and the verify input vtok[b][j]
     CK(seed::draft_sample(c.Y, (long)g * V, n, V, ctx->cfg.temperature, k0, k1, ctx->sids_dev, ctx->rs_dev, j,
-                          ctx->xs + (j - 1), g, ctx->vtok + j, g + 1, ctx->dev_err, st));
+                          ctx->xs + (j - 1), g, ctx->vtok + j, g + 1, ctx->dev_err, st, next_rec(ctx)));
     ctx->kernel_launches++;
   }
   return SEED_OK;
@@ -851,6 +856,7 @@ seed_status enqueue_verify(seed_ctx ctx, cudaStream_t st) {
     a.out_acc = ctx->out_acc;
     a.work = ctx->verify_work;
     a.err = ctx->dev_err;
+    a.timing = next_rec(ctx);
     CK(seed::vocab_verify(a, st));
     ctx->kernel_launches++;
   }
@@ -859,7 +865,7 @@ seed_status enqueue_verify(seed_ctx ctx, cudaStream_t st) {
   const size_t blk_bytes = (size_t)ctx->block_ints * 4;
   CK(cudaMemsetAsync(ctx->records, 0xFF, blk_bytes, st));
   CK(seed::rollback_commit(ctx->ds, ctx->slots_dev, n, g, ctx->out_tok, ctx->out_cnt, ctx->cfg.max_new_tokens,
-                           ctx->records, ctx->C, ctx->sids_dev, ctx->arena.dev + P.o_out, st));
+                           ctx->records, ctx->C, ctx->sids_dev, ctx->arena.dev + P.o_out, st, next_rec(ctx)));
   ctx->kernel_launches++;
   if (ctx->profile) {
     // draft records live in [0, half), verify records in [half, ...)
@@ -1065,8 +1071,8 @@ seed_status seed_init(const seed_config* cfg, seed_ctx* out) {
   ok &= cudaMalloc(&ctx->out_tok, (size_t)C * (g + 1) * 4) == cudaSuccess;
   ok &= cudaMalloc(&ctx->out_cnt, (size_t)C * 4) == cudaSuccess;
   ok &= cudaMalloc(&ctx->out_acc, (size_t)C * 4) == cudaSuccess;
-  ok &= cudaMalloc(&ctx->verify_work, (size_t)C * (2 * (g + 1) + 1) * 4) == cudaSuccess;
-  if (ok) ok &= cudaMemset(ctx->verify_work, 0, (size_t)C * (2 * (g + 1) + 1) * 4) == cudaSuccess;
+  ok &= cudaMalloc(&ctx->verify_work, seed::vocab_verify_work_bytes(C, g)) == cudaSuccess;
+  if (ok) ok &= cudaMemset(ctx->verify_work, 0, seed::vocab_verify_work_bytes(C, g)) == cudaSuccess;
   const int world = std::max(cfg->world, 1);
   ctx->block_ints = C * (g + 3) + 1;
   ok &= cudaMalloc(&ctx->records, (size_t)ctx->block_ints * 4) == cudaSuccess;
@@ -1534,7 +1540,7 @@ seed_status seed_op_verify(const float* zt, const float* zd, const int32_t* xs, 
   a.out_acc = out_acc;
   a.dbg = dbg;
   a.stats = stats;
-  const size_t wb = (size_t)B * (2 * (gamma + 1) + 1) * 4;
+  const size_t wb = seed::vocab_verify_work_bytes(B, gamma);
   cudaStream_t st = (cudaStream_t)stream;
   if (cudaMallocAsync(&a.work, wb, st) != cudaSuccess) return SEED_ENOMEM;
   bool ok = cudaMemsetAsync(a.work, 0, wb, st) == cudaSuccess && seed::vocab_verify(a, st) == cudaSuccess;

@@ -30,10 +30,12 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 __global__ void __launch_bounds__(128)
 embed_stats_kernel(const __nv_bfloat16* __restrict__ embed, const int32_t* __restrict__ tok, int tok_stride, int d,
                    int V, float* __restrict__ x, float* __restrict__ ssq, const __nv_bfloat16* __restrict__ nw,
-                   __nv_bfloat16* __restrict__ h, int32_t* err, int M) {
+                   __nv_bfloat16* __restrict__ h, int32_t* err, int M, unsigned long long* rec) {
   __shared__ float red[4];
   pdl_trigger();
+  rec_start(rec);
   pdl_wait();
+  rec_release(rec);
   const int t = blockIdx.x, m = blockIdx.y, n = t * 128 + threadIdx.x;
   float v = 0.f;
   if (n < d) {
@@ -54,6 +56,7 @@ embed_stats_kernel(const __nv_bfloat16* __restrict__ embed, const int32_t* __res
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
   __syncthreads();
   if (threadIdx.x == 0) ssq[(size_t)t * M + m] = ((red[0] + red[1]) + red[2]) + red[3];
+  rec_end(rec, 5);
 }
 
 // cos/sin(pos * theta^(-2i/Dh)) computed in fp64 on the device, stored fp32
@@ -86,9 +89,10 @@ __global__ void kv_write_dense_kernel(KVLayout kv, int layer, int slot, int n, c
 }  // namespace
 
 cudaError_t embed_stats(const __nv_bfloat16* embed, const int32_t* tok, int tok_stride, int M, int d, int V, float* x,
-                        float* ssq, const __nv_bfloat16* nw, __nv_bfloat16* h, int32_t* err, cudaStream_t st) {
+                        float* ssq, const __nv_bfloat16* nw, __nv_bfloat16* h, int32_t* err, cudaStream_t st,
+                        unsigned long long* timing) {
   return launch(embed_stats_kernel, dim3((d + 127) / 128, M), dim3(128), 0, st, embed, tok, tok_stride, d, V, x, ssq,
-                nw, h, err, M);
+                nw, h, err, M, timing);
 }
 
 cudaError_t kv_write_dense(const KVLayout& kv, int layer, int slot, int n, const __nv_bfloat16* k,

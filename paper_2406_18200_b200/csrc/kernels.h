@@ -15,6 +15,7 @@ struct KVLayout {
   const int32_t* page_table;
   int32_t max_pages;  // per slot
   int32_t n_layers, Hk, Dh, P;
+  int32_t kv3d;       // the pool's tensor map is the 3D (64, rows, halves) form (Dh = 128)
   __host__ __device__ size_t page_elems() const { return (size_t)n_layers * 2 * Hk * P * Dh; }
   __host__ __device__ size_t vofs() const { return (size_t)Hk * P * Dh; }  // K -> V of the same layer
   __host__ __device__ size_t offset(int page, int layer, int kv, int h, int slot_in_page) const {
@@ -34,6 +35,11 @@ struct GemmPlan {
 // bf16 2D tensor map, swizzle 128 B (default) or 64 B
 bool encode_tmap_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
                     uint32_t box_outer, int swizzle_bytes = 128);
+// KV pool rows of 128 bf16 as a 3D map (64 elements, rows, 2 halves): one tensor copy per 16-row block
+bool encode_tmap_kv_halves(CUtensorMap* map, const void* ptr, uint64_t rows, uint32_t box_rows);
+// fp32 2D tensor map without swizzle (rows of row_stride_elems elements; inner <= row_stride_elems)
+bool encode_tmap_2d_f32(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_elems,
+                        uint32_t box_inner, uint32_t box_outer);
 void gemm_plan(GemmPlan* plan, const void* W, int N, int K, int min_units = 4);
 void gemm_plan_free(GemmPlan* plan);
 // Operands and epilogue of one GEMM launch (see gemm.cu):
@@ -77,7 +83,8 @@ struct RowInfo {         // per row of the ragged batch
 // tile t, h = bf16(x * nw) (the first RMSNorm's GEMM operand, R24)
 // err (optional): bit 1 is set when a token id is outside [0, V) (the row then reads id 0)
 cudaError_t embed_stats(const __nv_bfloat16* embed, const int32_t* tok, int tok_stride, int M, int d, int V, float* x,
-                        float* ssq, const __nv_bfloat16* nw, __nv_bfloat16* h, int32_t* err, cudaStream_t st);
+                        float* ssq, const __nv_bfloat16* nw, __nv_bfloat16* h, int32_t* err, cudaStream_t st,
+                        unsigned long long* timing = nullptr);
 cudaError_t rope_table_init(float2* table, int max_pos, int Dh, double theta, cudaStream_t st);
 cudaError_t kv_write_dense(const KVLayout& kv, int layer, int slot, int n, const __nv_bfloat16* k,
                            const __nv_bfloat16* v, cudaStream_t st);
@@ -103,10 +110,12 @@ int attn_query_block();
 // fused: QKV epilogue (RoPE, bf16, KV append) + paged attention + split-KV merge; qkv = Y [M][(H+2Hk)Dh]
 // tmkv: 2D tensor map of the KV pool (attn_kv_tmap): rows of Dh elements, boxes of min(Dh, 64) x
 // min(P, 32) with the 128-byte swizzle
-bool attn_kv_tmap(CUtensorMap* map, const KVLayout& kv, size_t n_pages);
+bool attn_kv_tmap(CUtensorMap* map, const KVLayout& kv, size_t n_pages, int* kv3d);
+// tmq: fp32 2D tensor map of the QKV output (rows of (H + 2 Hk) Dh, boxes of Dh x 16); ws.counters holds
+// max_counters split tickets followed by 2 work-list words, all zero between launches
 cudaError_t attention(const float* qkv, int M, int n_seq, int max_q_len, int max_kv, int H, int Hk, int Dh,
-                      const SeqInfo& seqs, const float2* rope, const KVLayout& kv, const CUtensorMap& tmkv, int layer,
-                      const AttnWorkspace& ws, __nv_bfloat16* out, cudaStream_t st);
+                      const SeqInfo& seqs, const float2* rope, const KVLayout& kv, const CUtensorMap& tmkv,
+                      const CUtensorMap& tmq, int layer, const AttnWorkspace& ws, __nv_bfloat16* out, cudaStream_t st);
 
 // ------------------------------------------------------------------ K4 / K1 sampler / K5
 struct VerifyArgs {
@@ -119,14 +128,16 @@ struct VerifyArgs {
   int bonus;
   int32_t* out_tok; int32_t* out_cnt; int32_t* out_acc;
   float* dbg; double* stats;
-  int32_t* work;   // device [B][2 (gamma + 1) + 1] scratch (accept flags, candidate tokens, ticket);
-                   // the ticket words must be zero before the first launch (the kernel re-zeroes them)
+  void* work;      // device scratch of vocab_verify_work_bytes(B, gamma): tickets, accept flags, row statistics;
+                   // zero before the first launch (the kernel re-zeroes the tickets)
   int32_t* err;    // optional error word: [0] |= 2 when a race has no finite key, [1] += empty-residual fallbacks
+  unsigned long long* timing;   // optional launch record (kind 3)
 };
+size_t vocab_verify_work_bytes(int B, int gamma);
 cudaError_t vocab_verify(const VerifyArgs& a, cudaStream_t st);
 cudaError_t draft_sample(const float* z, long ld, int B, int V, float T, uint32_t k0, uint32_t k1,
                          const uint32_t* sids, const int32_t* rs, int j, int32_t* out, int out_stride, int32_t* out2,
-                         int out2_stride, int32_t* err, cudaStream_t st);
+                         int out2_stride, int32_t* err, cudaStream_t st, unsigned long long* timing = nullptr);
 cudaError_t philox_fill(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1, int n,
                         uint32_t* out, cudaStream_t st);
 
@@ -144,6 +155,7 @@ struct StreamState {     // device per-slot state (K5)
 // (padding pre-filled with -1 by the caller) and, after them, *outside + the batch's undone streams
 cudaError_t rollback_commit(const StreamState& s, const int32_t* batch_slots, int B, int gamma,
                             const int32_t* out_tok, const int32_t* out_cnt, int max_new, int32_t* records, int cap,
-                            const uint32_t* gids, const int32_t* outside, cudaStream_t st);
+                            const uint32_t* gids, const int32_t* outside, cudaStream_t st,
+                            unsigned long long* timing = nullptr);
 
 }  // namespace seed

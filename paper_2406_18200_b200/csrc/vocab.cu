@@ -144,6 +144,14 @@ __device__ __forceinline__ Best cluster_best(cg::cluster_group& cluster, Best* c
 // of it (>= 100x the fp32 error bound) and takes the exact argmax, ties to the smallest id.
 constexpr float RACE_MARGIN = 1e-3f;
 
+// -log(E), E = -log1p(-u), for the fp32 screen (pass A): absolute error ~1e-6, far inside
+// RACE_MARGIN (pass B rescoring is exact).  E keeps full relative precision for small u (log1pf),
+// 1 - u is exact in fp32 on the odd 2^-24 grid (R2), and the logarithms run on the SFU.
+__device__ __forceinline__ float neg_log_exp_screen(float u) {
+  const float E = u < 0.25f ? -log1pf(-u) : -__logf(1.0f - u);
+  return -__logf(E);
+}
+
 template <class W32, class W64>
 __device__ Best race_exact(cg::cluster_group& cluster, int v0, int n, uint32_t c1, uint32_t r, uint32_t sid,
                            uint32_t k0, uint32_t k1, float* keys, float* red_f, float* cta_f, Best* red_b,
@@ -162,8 +170,7 @@ __device__ Best race_exact(cg::cluster_group& cluster, int v0, int n, uint32_t c
         const double wd = w64(l + e);
         if (wd != -INFINITY) key = (float)(wd + neg_log_exp(philox_uniform(words[e])));
       } else if (w != -INFINITY) {
-        const float u = (float)philox_uniform(words[e]);
-        key = w - logf(-log1pf(-u));
+        key = w + neg_log_exp_screen((float)philox_uniform(words[e]));
       }
       keys[l + e] = key;
       best32 = fmaxf(best32, key);
@@ -200,12 +207,30 @@ __device__ Best race_exact(cg::cluster_group& cluster, int v0, int n, uint32_t c
   return cluster_best(cluster, cta_best, b);
 }
 
-// K4: one 8-CTA cluster per (stream b, position j = 0..gamma).  Cluster (b, j) computes the
-// statistics of target row j and draft row j, the accept decision for x_{j+1} (j < gamma), and the
-// token that would be emitted if j were the first rejected position: the residual race on row j
-// (slot j + 1), or for j = gamma the bonus race on the last target row.  The last cluster of the
-// stream to finish (ticket) counts the leading accepts a and emits x_1..x_a, y_a -- the same
-// decisions, counters and races as the sequential Alg. 1, evaluated in parallel.
+// Work area of K4 per launch (vocab_verify_work_bytes): tickets int32 [B] (zero between launches, the
+// kernel re-zeroes them), accept flags int32 [B][gamma], then (8-aligned) row statistics fp64
+// [B][2 gamma + 1][2] = (m, log1p(S')) of target rows 0..gamma and draft rows 0..gamma-1.
+struct K4Work {
+  int32_t* ticket;
+  int32_t* acc;
+  double* stats;
+};
+__host__ __device__ inline K4Work k4_work(void* base, int B, int g) {
+  K4Work w;
+  w.ticket = reinterpret_cast<int32_t*>(base);
+  w.acc = w.ticket + B;
+  const size_t off = (((size_t)B * (g + 1) * 4) + 7) & ~(size_t)7;
+  w.stats = reinterpret_cast<double*>(reinterpret_cast<char*>(base) + off);
+  return w;
+}
+
+// K4, two phases in one launch.  Phase 1: one 8-CTA cluster per (stream b, position j = 0..gamma)
+// computes the log-softmax statistics of target row j and draft row j (R13) and the accept decision
+// for x_{j+1} (j < gamma), and publishes them.  Phase 2: the stream's last cluster to
+// finish (ticket) counts the leading accepts a and runs the ONE race Alg. 1 needs: the residual
+// race over norm(max(0, p_{a+1} - q_{a+1})) (a < gamma, slot a + 1; R3) or the bonus race over
+// p_{gamma+1} (a = gamma, R1) -- staging rows a again if they are not its own -- then emits
+// x_1..x_a, y.  The same decisions, counters and races as the sequential Alg. 1.
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(VT)
 vocab_verify_kernel(VerifyArgs A) {
   extern __shared__ __align__(128) float rows_s[];  // [2][slice] target / draft row, [slice] race keys
@@ -218,6 +243,7 @@ vocab_verify_kernel(VerifyArgs A) {
   __shared__ double cta_sum[2];
   __shared__ Stat glob[2];
   __shared__ Best cta_best;
+  __shared__ int last_s;
   __shared__ __align__(8) uint64_t bar;
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
@@ -231,20 +257,22 @@ vocab_verify_kernel(VerifyArgs A) {
   const float* zt = A.zt + (size_t)b * A.zt_stride_b;
   const float* zd = A.zd + (size_t)b * A.zd_stride_b;
   const uint32_t sid = A.sids[b], rr = (uint32_t)A.rs[b];
-  auto rowptr = [&](int row) -> const float* { return row == 0 ? zt + (size_t)j * V : zd + (size_t)j * V; };
+  const K4Work W = k4_work(A.work, A.B, g);
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_barrier_init();
   }
   __syncthreads();
   pdl_trigger();
+  rec_start(A.timing);
   pdl_wait();   // the logits are written by the previous kernels
+  rec_release(A.timing);
   Stager sg{rows_s, &bar, 0u, slice, v0, n, (V % 4 == 0) && (n % 4 == 0)};
   float* keys_s = rows_s + (size_t)2 * slice;
-  sg.stage(0, nrows, rowptr);
+  sg.stage(0, nrows, [&](int row) -> const float* { return row == 0 ? zt + (size_t)j * V : zd + (size_t)j * V; });
 
-  // ---- statistics, two passes per row: (a) fp32 maximum and its first index, merged over the
-  // cluster in rank order; (b) S' = sum over v != argmax of exp(a_v - m), fp32 terms summed in
+  // ---- phase 1: statistics, two passes per row: (a) fp32 maximum and its first index, merged over
+  // the cluster in rank order; (b) S' = sum over v != argmax of exp(a_v - m), fp32 terms summed in
   // fp64 in a fixed thread / warp / rank order (R13, R21) -- no rescaling, no fp64 exponentials
   for (int i = 0; i < nrows; ++i) {
     const float* zs = rows_s + (size_t)i * slice;
@@ -284,103 +312,138 @@ vocab_verify_kernel(VerifyArgs A) {
   const Stat st = glob[0];
   const double l1t = log1p(st.S);
 
-  // ---- accept decision for x_{j+1}: u < min(1, p / q) in log space (R2, R13)
-  int accept = 0;
-  if (has_d && rank == 0 && threadIdx.x == 0) {
-    const Stat sq = glob[1];
-    const int x = A.xs[(size_t)b * g + j];
-    double lp = -INFINITY, lq = 0.0, rho = 0.0;
-    if (x >= 0 && x < V) {
-      lp = ((double)scaled_v(__ldg(zt + (size_t)j * V + x), A.T) - st.m) - l1t;
-      lq = ((double)scaled_v(__ldg(zd + (size_t)j * V + x), A.T) - sq.m) - log1p(sq.S);
-      rho = exp(fmin(0.0, lp - lq));
-    } else if (A.err) {
-      atomicOr(&A.err[0], 1);   // contract violation: a drafted id outside the vocabulary is rejected
+  double* stt = W.stats + (size_t)b * (2 * g + 1) * 2;
+  if (rank == 0 && threadIdx.x == 0) {
+    int accept = 0;
+    stt[2 * j] = st.m;
+    stt[2 * j + 1] = l1t;
+    if (has_d) {
+      // accept decision for x_{j+1}: u < min(1, p / q) in log space (R2, R13)
+      const Stat sq = glob[1];
+      const double l1q = log1p(sq.S);
+      stt[2 * (g + 1 + j)] = sq.m;
+      stt[2 * (g + 1 + j) + 1] = l1q;
+      const int x = A.xs[(size_t)b * g + j];
+      double lp = -INFINITY, lq = 0.0, rho = 0.0;
+      if (x >= 0 && x < V) {
+        lp = ((double)scaled_v(__ldg(zt + (size_t)j * V + x), A.T) - st.m) - l1t;
+        lq = ((double)scaled_v(__ldg(zd + (size_t)j * V + x), A.T) - sq.m) - l1q;
+        rho = exp(fmin(0.0, lp - lq));
+      } else if (A.err) {
+        atomicOr(&A.err[0], 1);   // contract violation: a drafted id outside the vocabulary is rejected
+      }
+      const Philox4 ph = philox4x32_10(0u, (kTagAccept << 24) | (uint32_t)(j + 1), rr, sid, A.k0, A.k1);
+      const double u = philox_uniform(ph.x);
+      accept = u < rho ? 1 : 0;
+      W.acc[(size_t)b * g + j] = accept;
+      if (A.dbg) {
+        float* d = A.dbg + ((size_t)b * g + j) * 4;
+        d[0] = (float)lp;
+        d[1] = (float)lq;
+        d[2] = (float)u;
+        d[3] = (float)rho;
+      }
     }
-    const Philox4 ph = philox4x32_10(0u, (kTagAccept << 24) | (uint32_t)(j + 1), rr, sid, A.k0, A.k1);
-    const double u = philox_uniform(ph.x);
-    accept = u < rho ? 1 : 0;
-    if (A.dbg) {
-      float* d = A.dbg + ((size_t)b * g + j) * 4;
-      d[0] = (float)lp;
-      d[1] = (float)lq;
-      d[2] = (float)u;
-      d[3] = (float)rho;
+    if (A.stats) {
+      A.stats[((size_t)b * (2 * g + 1) + j) * 2] = st.m;
+      A.stats[((size_t)b * (2 * g + 1) + j) * 2 + 1] = l1t;
+      if (has_d) {
+        A.stats[((size_t)b * (2 * g + 1) + g + 1 + j) * 2] = glob[1].m;
+        A.stats[((size_t)b * (2 * g + 1) + g + 1 + j) * 2 + 1] = log1p(glob[1].S);
+      }
     }
+    // publish; the stream's last cluster runs phase 2
+    fence_acq_rel_gpu();
+    const int t = atomicAdd(&W.ticket[b], 1);
+    if (t == g) {
+      fence_acq_rel_gpu();   // acquire every cluster's flags and statistics
+      W.ticket[b] = 0;       // ready for the next launch (graph replay)
+    }
+    last_s = t == g ? 1 : 0;
+  }
+  cluster.sync();
+  const int last = *cluster.map_shared_rank(&last_s, 0);
+  if (!last) {
+    cluster_sync_relaxed();  // keep shared memory alive until every peer has read it
+    rec_end(A.timing, 3);
+    return;
   }
 
-  // ---- the token emitted if position j + 1 is the first rejection (residual race, slot j + 1),
-  // or the bonus token (j = gamma); ties to the smallest id (R14)
-  const uint32_t c1 = (kTagResample << 24) | (uint32_t)(j + 1);
-  const float* zt_s = rows_s;
-  const float* zd_s = rows_s + slice;
-  const float mt = (float)st.m, l1tf = (float)l1t;
-  auto bonus32 = [&](int l) -> float { return scaled_v(zt_s[l], A.T); };
-  auto bonus64 = [&](int l) -> double { return (double)scaled_v(zt_s[l], A.T); };
+  // ---- phase 2 (the stream's last cluster): a, then the one race Alg. 1 needs
+  __shared__ int a_s;
+  if (threadIdx.x == 0) {
+    const volatile int32_t* acc = W.acc + (size_t)b * g;
+    int a = 0;
+    while (a < g && acc[a]) ++a;
+    a_s = a;
+  }
+  __syncthreads();
+  const int a = a_s;
   int y = -1;
-  if (has_d) {
-    const Stat sq = glob[1];
-    const double l1q = log1p(sq.S);
-    const float mq = (float)sq.m, l1qf = (float)l1q;
-    auto res32 = [&](int l) -> float {
-      const float lp = (scaled_v(zt_s[l], A.T) - mt) - l1tf;
-      const float lq = (scaled_v(zd_s[l], A.T) - mq) - l1qf;
-      const float dlt = lq - lp;
-      if (dlt > -0.05f) return dlt >= 0.05f ? -INFINITY : NAN;  // near-equal p, q: fp64
-      return lp + logf(-expm1f(dlt));
-    };
-    auto res64 = [&](int l) -> double {
-      const double lp = ((double)scaled_v(zt_s[l], A.T) - st.m) - l1t;
-      const double lq = ((double)scaled_v(zd_s[l], A.T) - sq.m) - l1q;
-      return lq < lp ? lp + log(-expm1(lq - lp)) : -INFINITY;
-    };
-    y = race_exact(cluster, v0, n, c1, rr, sid, A.k0, A.k1, keys_s, red_f, &cta_f, red_b, &cta_best, res32, res64).v;
-    if (y < 0) {  // empty residual (rounding only): bonus rule on the same row, same uniforms
+  if (a < g || A.bonus) {
+    const int row = a;                          // residual on rows a (slot a + 1), or bonus on target row gamma
+    const bool res = a < g;
+    if (row != j) {
+      // rows `row` were staged by another cluster: stage them here (L2-resident logits); the
+      // generic reads of phase 1 are ordered before the bulk copies overwrite the buffers
+      if (threadIdx.x == 0) fence_proxy_async();
+      sg.stage(0, res ? 2 : 1, [&](int i) -> const float* { return i == 0 ? zt + (size_t)row * V : zd + (size_t)row * V; });
+    } else {
+      __syncthreads();
+    }
+    const volatile double* sv = W.stats + (size_t)b * (2 * g + 1) * 2;
+    const double mt = sv[2 * row], l1t_r = sv[2 * row + 1];
+    const float mtf = (float)mt, l1tf = (float)l1t_r;
+    const float* zt_s = rows_s;
+    const float* zd_s = rows_s + slice;
+    const uint32_t c1 = (kTagResample << 24) | (uint32_t)(row + 1);
+    auto bonus32 = [&](int l) -> float { return scaled_v(zt_s[l], A.T); };
+    auto bonus64 = [&](int l) -> double { return (double)scaled_v(zt_s[l], A.T); };
+    if (res) {
+      const double mq = sv[2 * (g + 1 + row)], l1q = sv[2 * (g + 1 + row) + 1];
+      const float mqf = (float)mq, l1qf = (float)l1q;
+      auto res32 = [&](int l) -> float {
+        const float lp = (scaled_v(zt_s[l], A.T) - mtf) - l1tf;
+        const float lq = (scaled_v(zd_s[l], A.T) - mqf) - l1qf;
+        const float dlt = lq - lp;
+        if (dlt > -0.05f) return dlt >= 0.05f ? -INFINITY : NAN;  // near-equal p, q: fp64
+        return lp + __logf(1.0f - __expf(dlt));                    // screen only (pass B is exact)
+      };
+      auto res64 = [&](int l) -> double {
+        const double lp = ((double)scaled_v(zt_s[l], A.T) - mt) - l1t_r;
+        const double lq = ((double)scaled_v(zd_s[l], A.T) - mq) - l1q;
+        return lq < lp ? lp + log(-expm1(lq - lp)) : -INFINITY;
+      };
+      y = race_exact(cluster, v0, n, c1, rr, sid, A.k0, A.k1, keys_s, red_f, &cta_f, red_b, &cta_best, res32, res64).v;
+      if (y < 0) {  // empty residual (rounding only): bonus rule on the same row, same uniforms
+        y = race_exact(cluster, v0, n, c1, rr, sid, A.k0, A.k1, keys_s, red_f, &cta_f, red_b, &cta_best, bonus32,
+                       bonus64).v;
+        if (A.err && rank == 0 && threadIdx.x == 0) atomicAdd(&A.err[1], 1);
+      }
+    } else {
       y = race_exact(cluster, v0, n, c1, rr, sid, A.k0, A.k1, keys_s, red_f, &cta_f, red_b, &cta_best, bonus32,
                      bonus64).v;
-      if (A.err && rank == 0 && threadIdx.x == 0) atomicAdd(&A.err[1], 1);
     }
-  } else if (A.bonus) {
-    y = race_exact(cluster, v0, n, c1, rr, sid, A.k0, A.k1, keys_s, red_f, &cta_f, red_b, &cta_best, bonus32, bonus64)
-            .v;
   }
-
-  if (A.stats && rank == 0 && threadIdx.x < nrows) {
-    const int row = threadIdx.x == 0 ? j : g + 1 + j;
-    A.stats[((size_t)b * (2 * g + 1) + row) * 2] = glob[threadIdx.x].m;
-    A.stats[((size_t)b * (2 * g + 1) + row) * 2 + 1] = log1p(glob[threadIdx.x].S);
-  }
-  // ---- publish (accept_j, y_j); the stream's last cluster emits x_1..x_a, y_a
   if (rank == 0 && threadIdx.x == 0) {
-    int32_t* w = A.work + (size_t)b * (2 * (g + 1) + 1);
-    w[j] = accept;
-    w[g + 1 + j] = y;
-    fence_acq_rel_gpu();
-    if (atomicAdd(&w[2 * (g + 1)], 1) == g) {
-      fence_acq_rel_gpu();
-      volatile int32_t* vw = w;
-      int a = 0;
-      while (a < g && vw[a]) ++a;
-      const int ya = vw[g + 1 + a];
-      if (ya < 0 && (a < g || A.bonus) && A.err) atomicOr(&A.err[0], 2);   // no finite key (non-finite logits)
-      int32_t* ot = A.out_tok + (size_t)b * (g + 1);
-      for (int q = 0; q < a; ++q) ot[q] = A.xs[(size_t)b * g + q];
-      int cnt = a;
-      if (ya >= 0) ot[cnt++] = ya;
-      for (int q = cnt; q <= g; ++q) ot[q] = -1;
-      if (A.out_cnt) A.out_cnt[b] = cnt;
-      if (A.out_acc) A.out_acc[b] = a;
-      w[2 * (g + 1)] = 0;   // ready for the next launch (graph replay)
-    }
+    if (y < 0 && (a < g || A.bonus) && A.err) atomicOr(&A.err[0], 2);   // no finite key (non-finite logits)
+    int32_t* ot = A.out_tok + (size_t)b * (g + 1);
+    for (int q = 0; q < a; ++q) ot[q] = A.xs[(size_t)b * g + q];
+    int cnt = a;
+    if (y >= 0) ot[cnt++] = y;
+    for (int q = cnt; q <= g; ++q) ot[q] = -1;
+    if (A.out_cnt) A.out_cnt[b] = cnt;
+    if (A.out_acc) A.out_acc[b] = a;
   }
   cluster_sync_relaxed();  // keep shared memory alive until every peer has read it (execution order)
+  rec_end(A.timing, 3);
 }
 
 // K1 sampler: one cluster per row
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(VT)
 draft_sample_kernel(const float* z, long ld, int V, float T, uint32_t k0, uint32_t k1, const uint32_t* sids,
                     const int32_t* rs, int j, int32_t* out, int out_stride, int32_t* out2, int out2_stride,
-                    int32_t* err) {
+                    int32_t* err, unsigned long long* rec) {
   extern __shared__ __align__(128) float rows_s[];  // [slice] row, then [slice] race keys
   __shared__ float red_f[VT / 32];
   __shared__ float cta_f;
@@ -399,7 +462,9 @@ draft_sample_kernel(const float* z, long ld, int V, float T, uint32_t k0, uint32
   }
   __syncthreads();
   pdl_trigger();
+  rec_start(rec);
   pdl_wait();
+  rec_release(rec);
   Stager sg{rows_s, &bar, 0u, slice, v0, n, (V % 4 == 0) && (n % 4 == 0) && (ld % 4 == 0)};
   sg.stage(0, 1, [&](int) { return zr; });
   auto w32 = [&](int l) -> float { return scaled_v(rows_s[l], T); };
@@ -411,6 +476,7 @@ draft_sample_kernel(const float* z, long ld, int V, float T, uint32_t k0, uint32
     if (out2) out2[(size_t)b * out2_stride] = acc.v;
     if (acc.v < 0 && err) atomicOr(err, 2);   // no finite key (non-finite logits)
   }
+  rec_end(rec, 4);
 }
 
 __global__ void philox_fill_kernel(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1, int n,
@@ -428,10 +494,12 @@ constexpr int K5_THREADS = 256;
 __global__ void __launch_bounds__(K5_THREADS)
 rollback_commit_kernel(StreamState s, const int32_t* batch_slots, int B, int gamma, const int32_t* out_tok,
                        const int32_t* out_cnt, int max_new, int32_t* records, int cap, const uint32_t* gids,
-                       const int32_t* outside) {
+                       const int32_t* outside, unsigned long long* rec) {
   __shared__ int red[K5_THREADS / 32];
   pdl_trigger();
+  rec_start(rec);
   pdl_wait();
+  rec_release(rec);
   int undone = 0;
   for (int b = threadIdx.x; b < B; b += K5_THREADS) {
     const int slot = batch_slots[b];
@@ -463,8 +531,13 @@ rollback_commit_kernel(StreamState s, const int32_t* batch_slots, int B, int gam
     for (int w = 0; w < K5_THREADS / 32; ++w) u += red[w];
     records[(size_t)cap * (gamma + 3)] = u;
   }
+  rec_end(rec, 6);
 }
 }  // namespace
+
+size_t vocab_verify_work_bytes(int B, int gamma) {
+  return ((((size_t)B * (gamma + 1) * 4) + 7) & ~(size_t)7) + (size_t)B * (2 * gamma + 1) * 2 * sizeof(double);
+}
 
 cudaError_t vocab_verify(const VerifyArgs& a, cudaStream_t st) {
   if (!a.work || a.gamma < 1) return cudaErrorInvalidValue;
@@ -481,7 +554,7 @@ cudaError_t vocab_verify(const VerifyArgs& a, cudaStream_t st) {
 
 cudaError_t draft_sample(const float* z, long ld, int B, int V, float T, uint32_t k0, uint32_t k1,
                          const uint32_t* sids, const int32_t* rs, int j, int32_t* out, int out_stride, int32_t* out2,
-                         int out2_stride, int32_t* err, cudaStream_t st) {
+                         int out2_stride, int32_t* err, cudaStream_t st, unsigned long long* timing) {
   const int slice = ((V + CS - 1) / CS + 3) & ~3;
   const size_t smem = (size_t)2 * slice * 4;
   if (smem > 220 * 1024) return cudaErrorInvalidValue;
@@ -491,7 +564,7 @@ cudaError_t draft_sample(const float* z, long ld, int B, int V, float T, uint32_
     attr = smem;
   }
   return launch(draft_sample_kernel, dim3(B * CS), dim3(VT), smem, st, z, ld, V, T, k0, k1, sids, rs, j, out,
-                out_stride, out2, out2_stride, err);
+                out_stride, out2, out2_stride, err, timing);
 }
 
 cudaError_t philox_fill(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1, int n,
@@ -502,9 +575,10 @@ cudaError_t philox_fill(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint
 
 cudaError_t rollback_commit(const StreamState& s, const int32_t* batch_slots, int B, int gamma,
                             const int32_t* out_tok, const int32_t* out_cnt, int max_new, int32_t* records, int cap,
-                            const uint32_t* gids, const int32_t* outside, cudaStream_t st) {
+                            const uint32_t* gids, const int32_t* outside, cudaStream_t st,
+                            unsigned long long* timing) {
   return launch(rollback_commit_kernel, dim3(1), dim3(K5_THREADS), 0, st, s, batch_slots, B, gamma, out_tok, out_cnt,
-                max_new, records, cap, gids, outside);
+                max_new, records, cap, gids, outside, timing);
 }
 
 }  // namespace seed
