@@ -36,9 +36,8 @@ constexpr int WARPS = 4;
 constexpr int NT = WARPS * 32;
 constexpr int TK = 16;                   // keys per tile (one page block: P >= 16, P % 16 == 0)
 constexpr int QB = 16;                   // query rows per CTA (one m16 MMA tile)
-constexpr int STAGES = 2;                // per warp
 
-template <int DH>
+template <int DH, int STAGES>
 struct Smem {
   static constexpr int PITCH = DH + 8;                       // bf16 row pitch of Q (conflict-free ldmatrix)
   static constexpr int RB = (DH >= 64 ? 64 : DH) * 2;        // bytes per swizzled row segment (TMA box width)
@@ -50,7 +49,9 @@ struct Smem {
   static constexpr size_t ML = Q + (size_t)QB * PITCH * 2;   // fp32 m, l [WARPS][QB] each, factors [WARPS][QB], row l [QB]
   static constexpr size_t TKT = ML + (size_t)(3 * WARPS + 1) * QB * 4;  // ticket broadcast
   static constexpr size_t BAR = TKT + 16;                    // mbarriers [WARPS][STAGES]
-  static constexpr size_t BYTES = BAR + WARPS * STAGES * 8 + 1024;
+  static constexpr size_t PG = BAR + WARPS * STAGES * 8;     // int [WARPS][32]: page of each of a warp's tiles
+  static constexpr size_t BYTES = PG + WARPS * 32 * 4 + 1024;
+  static constexpr int PER_SM = (int)((227 * 1024) / (BYTES + 1024)) < 1 ? 1 : (int)((227 * 1024) / (BYTES + 1024));
   // merge scratch fp32 [WARPS][QB][OP] aliases the ring after the loop
   static_assert((size_t)WARPS * QB * OP * 4 <= (size_t)WARPS * STAGES * STAGE, "merge scratch must fit the ring");
 };
@@ -60,7 +61,7 @@ struct Smem {
 // bits [4:5] XOR bits [7:8]); a row of Dh > 64 is split into 64-element halves, 16 rows each.
 template <int DH>
 SEED_DEV uint32_t tile_addr(uint32_t tile, int row, int e) {
-  constexpr int RB = Smem<DH>::RB, EH = RB / 2;
+  constexpr int RB = (DH >= 64 ? 64 : DH) * 2, EH = RB / 2;
   constexpr uint32_t MASK = RB == 128 ? 0x70u : 0x30u;
   const uint32_t a = tile + (uint32_t)((e / EH) * TK * RB + row * RB + (e % EH) * 2);
   return a ^ ((a >> 3) & MASK);
@@ -92,13 +93,13 @@ SEED_DEV uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<const uint32_t*>(&v);
 }
 
-template <int DH>
-__global__ void __launch_bounds__(NT, DH >= 128 ? 3 : 4)
+
+template <int DH, int STAGES>
+__global__ void __launch_bounds__(NT, Smem<DH, STAGES>::PER_SM > 4 ? 4 : Smem<DH, STAGES>::PER_SM)
 attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __restrict__ qkv, int H, int Hk,
                    SeqInfo seqs, const float2* __restrict__ rope, KVLayout kv, int layer, int n_qblk, float scale,
-                   AttnWorkspace ws, int M, __nv_bfloat16* __restrict__ out, int SPLIT, int l2pf, int kv3d) {
-  using L = Smem<DH>;
-  auto l2_prefetch_on = [&]() { return l2pf != 0; };
+                   AttnWorkspace ws, int M, __nv_bfloat16* __restrict__ out, int SPLIT, int kv3d) {
+  using L = Smem<DH, STAGES>;
   constexpr int P = L::PITCH;
   constexpr int OP = L::OP;
   constexpr int HALF = DH / 2;
@@ -164,9 +165,16 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __rest
   // ---- this warp's j-th tile: keys [t0, t0 + 16); the cached part by tensor copies (lane 0)
   auto tile_t0 = [&](int j) { return k_lo + (warp + j * WARPS) * TK; };
   auto cached = [&](int j) { return tile_t0(j) < old_end; };
+  // the page of each of this warp's tiles, one lane per tile, before any request: the issue path
+  // below reads shared memory instead of waiting on a global load per tile (page-table rows are
+  // uploaded before the round: safe before the PDL wait)
+  int* pg_s = reinterpret_cast<int*>(smem + L::PG) + warp * 32;
+  for (int j = lane; j < my_tiles; j += 32)
+    if (cached(j)) pg_s[j] = __ldg(kv.page_table + (size_t)slot * kv.max_pages + tile_t0(j) / kv.P);
+  __syncwarp();
   auto issue = [&](int j) {   // lane 0
     const int t0 = tile_t0(j);
-    const int page = __ldg(kv.page_table + (size_t)slot * kv.max_pages + t0 / kv.P);
+    const int page = pg_s[j];
     const int row = (((page * kv.n_layers + layer) * 2) * kv.Hk + kvh) * kv.P + (t0 % kv.P);
     const uint32_t st = ring + (uint32_t)((j % STAGES) * L::STAGE);
     uint64_t* bar = &bar_s[warp * STAGES + j % STAGES];
@@ -182,19 +190,6 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __rest
       }
     }
   };
-  // every tile of this warp whose cached keys were all written before the round: L2 prefetch now
-  // (the page blocks are 4 KB contiguous per head for K and for V), so the ring's tensor copies
-  // below hit L2 -- the ring holds two tiles per warp, L2 holds the rest in flight
-  if (lane == 0 && l2_prefetch_on()) {
-    for (int j = 0; j < my_tiles; ++j) {
-      const int t0 = tile_t0(j);
-      if (!(t0 < old_end && min(t0 + TK, old_end) <= stable)) break;
-      const int page = __ldg(kv.page_table + (size_t)slot * kv.max_pages + t0 / kv.P);
-      const __nv_bfloat16* kp = kv.pool + kv.offset(page, layer, 0, kvh, t0 % kv.P);
-      prefetch_l2(kp, TK * DH * 2);
-      prefetch_l2(kp + kv.vofs(), TK * DH * 2);
-    }
-  }
   // tiles whose cached keys were all written before the round: requested before the PDL wait
   bool pre[STAGES];
 #pragma unroll
@@ -491,507 +486,62 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __rest
   done();
 }
 
-// ============================================================================================
-// Persistent form: one warp per CTA, a work list of units (sequence x 16-row query block, head, split
-// of SPLIT keys), split-major so the big units go first.  Each warp takes its first unit statically
-// (its CTA index) and the rest from an atomic counter, and streams every unit's items -- the query
-// rows (fp32, by tensor copy from the QKV output), then the split's 16-key K/V tiles -- through its
-// own S-stage ring: item k + S is requested as soon as item k is consumed, across unit boundaries,
-// so the next unit's query and first tiles are in flight while the current unit finishes and
-// publishes.  No CTA barrier anywhere.  A unit's arithmetic -- tiles in key order, one online
-// softmax, the split merge in split order by the last split to finish -- depends on the key
-// positions only (R19), whichever warp runs it.
-constexpr int PS = 4;   // ring stages per warp
-
-template <int DH>
-struct PSmem {
-  static constexpr int PITCH = DH + 8;
-  static constexpr size_t STAGE = (size_t)64 * DH;   // = K + V bf16 tile (2 * 16 * DH * 2) = Q fp32 box (16 * DH * 4)
-  static constexpr size_t RING = 0;
-  static constexpr size_t Q = RING + PS * STAGE;     // bf16 [16][PITCH]
-  static constexpr size_t UQ = Q + (size_t)16 * PITCH * 2;   // int [8] unit queue
-  static constexpr size_t BAR = UQ + 32;             // mbarriers [PS]
-  static constexpr size_t BYTES = BAR + PS * 8 + 1024;
-};
-
-struct UnitDesc {      // a decoded work unit
-  int valid, seq, qb, head, split;
-  int q0, ql, nr, new_first, pos0, key_end, k_lo, k_hi, slot, stable, nsplit, n_tiles;
-};
-
-SEED_DEV UnitDesc decode_unit(int u, int n_units, int n_qblk, int n_sb, int H, int SPLIT, const SeqInfo& seqs) {
-  UnitDesc d{};
-  d.valid = 0;
-  if (u >= n_units) return d;
-  const int split = u / (n_sb * H), rem = u % (n_sb * H);
-  const int sb = rem / H;
-  d.head = rem % H;
-  d.split = split;
-  d.seq = sb / n_qblk;
-  d.qb = sb % n_qblk;
-  d.q0 = __ldg(seqs.q_start + d.seq);
-  d.ql = __ldg(seqs.q_len + d.seq);
-  const int kvl = __ldg(seqs.kv_len + d.seq);
-  const int r0 = d.qb * QB;
-  if (r0 >= d.ql) return d;
-  d.nr = min(QB, d.ql - r0);
-  d.new_first = kvl - d.ql;
-  d.pos0 = d.new_first + r0;
-  d.key_end = d.pos0 + d.nr;
-  d.k_lo = split * SPLIT;
-  if (d.k_lo >= d.key_end) return d;
-  d.k_hi = min(d.k_lo + SPLIT, d.key_end);
-  d.slot = __ldg(seqs.slot + d.seq);
-  d.stable = seqs.stable ? min(__ldg(seqs.stable + d.seq), d.new_first) : 0;
-  d.nsplit = (d.key_end + SPLIT - 1) / SPLIT;
-  d.n_tiles = (d.k_hi - d.k_lo + TK - 1) / TK;
-  d.valid = 1;
-  return d;
-}
-
-template <int DH>
-__global__ void __launch_bounds__(32)
-attn_warp_kernel(const __grid_constant__ CUtensorMap tmKV, const __grid_constant__ CUtensorMap tmQ,
-                 const float* __restrict__ qkv, int H, int Hk, SeqInfo seqs, const float2* __restrict__ rope,
-                 KVLayout kv, int layer, int n_qblk, int n_sb, int n_units, float scale, AttnWorkspace ws, int M,
-                 __nv_bfloat16* __restrict__ out, int SPLIT) {
-  using L = PSmem<DH>;
-  constexpr int P = L::PITCH;
-  constexpr int HALF = DH / 2;
-  constexpr int DT = DH / 8;
-  constexpr int RB = (DH >= 64 ? 64 : DH) * 2;
-  constexpr int EH = RB / 2;
-  constexpr uint32_t TX = (uint32_t)L::STAGE;
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  __nv_bfloat16* q_s = reinterpret_cast<__nv_bfloat16*>(smem + L::Q);
-  volatile int* uq = reinterpret_cast<volatile int*>(smem + L::UQ);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::BAR);
-  const uint32_t ring = smem_u32(smem + L::RING);
-  const int lane = threadIdx.x;
-  const int ldq = (H + 2 * Hk) * DH;
-  int* sched = ws.counters + ws.max_counters;   // [0] next dynamic unit, [1] finished warps
-  const int G = gridDim.x;
-
-  if (lane == 0) {
-    prefetch_tmap(&tmKV);
-    prefetch_tmap(&tmQ);
-    for (int i = 0; i < PS; ++i) mbar_init(&bar[i], 1);
-    fence_barrier_init();
-  }
-  __syncwarp();
-  rec_start(ws.timing);
-
-  // ---- issue side (lane 0): the item stream  Q(u0) T(u0, 0..) Q(u1) T(u1, 0..) ...
-  UnitDesc iu{};          // unit being issued
-  int iu_item = 0;        // next item of it (0 = Q, 1 + t = tile t)
-  int iu_idx = 0;         // its position in the unit queue
-  int issue_seq = 0;      // items issued so far
-  bool iu_end = false;
-  bool dyn = false;
-  auto grab = [&](bool first) {   // lane 0: next non-empty unit (or the end) into iu, queued
-    for (;;) {
-      int u;
-      if (first) {
-        u = blockIdx.x;
-        first = false;
-      } else {
-        u = G + atomicAdd(&sched[0], 1);
-      }
-      dyn = true;
-      if (u >= n_units) {
-        iu.valid = 0;
-        iu_end = true;
-        uq[iu_idx & 7] = -1;
-        return;
-      }
-      iu = decode_unit(u, n_units, n_qblk, n_sb, H, SPLIT, seqs);
-      if (iu.valid) {
-        uq[iu_idx & 7] = u;
-        iu_item = 0;
-        return;
-      }
-    }
-  };
-  auto tile_cached = [&](const UnitDesc& d, int t) { return d.k_lo + t * TK < d.new_first; };
-  // issue the next item of the stream into stage issue_seq % PS (post = after the PDL wait)
-  auto issue_next = [&]() {
-    if (iu_end) return;
-    const int s = issue_seq % PS;
-    const uint32_t st = ring + (uint32_t)(s * L::STAGE);
-    if (iu_item == 0) {
-      mbar_arrive_expect_tx(&bar[s], TX);
-      tma_load_2d_u32(st, &tmQ, &bar[s], iu.head * DH, iu.q0 + iu.qb * QB);
-    } else {
-      const int t0 = iu.k_lo + (iu_item - 1) * TK;
-      if (t0 < iu.new_first) {
-        const int page = __ldg(kv.page_table + (size_t)iu.slot * kv.max_pages + t0 / kv.P);
-        const int kvh = iu.head / (H / Hk);
-        const int row = (((page * kv.n_layers + layer) * 2) * kv.Hk + kvh) * kv.P + (t0 % kv.P);
-        mbar_arrive_expect_tx(&bar[s], TX);
-#pragma unroll
-        for (int h = 0; h < DH / EH; ++h) {
-          tma_load_2d_u32(st + (uint32_t)(h * TK * RB), &tmKV, &bar[s], h * EH, row);
-          tma_load_2d_u32(st + (uint32_t)(L::STAGE / 2 + h * TK * RB), &tmKV, &bar[s], h * EH, row + kv.Hk * kv.P);
-        }
-      } else {
-        mbar_arrive(&bar[s]);   // only new keys: formed by the consumer
-      }
-    }
-    ++issue_seq;
-    if (++iu_item > iu.n_tiles) {
-      ++iu_idx;
-      grab(false);
-    }
-  };
-  // before the PDL wait: the first unit's tiles whose cached keys were all written before the round
-  // (items 1 .. PS-1); the query rows and everything else after it
-  uint32_t pre_mask = 0;
-  if (lane == 0) {
-    grab(true);
-    if (iu.valid) {
-      const UnitDesc d = iu;
-      for (int k = 1; k < PS && k <= d.n_tiles; ++k) {
-        const int t0 = d.k_lo + (k - 1) * TK;
-        if (t0 < d.new_first && min(t0 + TK, d.new_first) <= d.stable) {
-          // issue item k of the first unit out of order (its stage is k)
-          const uint32_t st = ring + (uint32_t)(k * L::STAGE);
-          const int page = __ldg(kv.page_table + (size_t)d.slot * kv.max_pages + t0 / kv.P);
-          const int kvh = d.head / (H / Hk);
-          const int row = (((page * kv.n_layers + layer) * 2) * kv.Hk + kvh) * kv.P + (t0 % kv.P);
-          mbar_arrive_expect_tx(&bar[k], TX);
-#pragma unroll
-          for (int h = 0; h < DH / EH; ++h) {
-            tma_load_2d_u32(st + (uint32_t)(h * TK * RB), &tmKV, &bar[k], h * EH, row);
-            tma_load_2d_u32(st + (uint32_t)(L::STAGE / 2 + h * TK * RB), &tmKV, &bar[k], h * EH, row + kv.Hk * kv.P);
-          }
-          pre_mask |= 1u << k;
-        }
-      }
-    }
-  }
-  pdl_wait();
-  rec_release(ws.timing);
-  if (lane == 0) {
-    for (int k = 0; k < PS; ++k) {
-      if (pre_mask >> k & 1) {   // already requested: advance the cursor past it
-        ++issue_seq;
-        if (++iu_item > iu.n_tiles) {
-          ++iu_idx;
-          grab(false);
-        }
-      } else {
-        issue_next();
-      }
-    }
-  }
-  (void)dyn;
-
-  // ---- consume side (whole warp)
-  const int g = lane >> 2, t4 = lane & 3;
-  int cons_seq = 0, cidx = 0;
-  const uint32_t qa = smem_u32(q_s);
-  for (;;) {
-    __syncwarp();
-    const int u = uq[cidx & 7];
-    if (u < 0) break;
-    const UnitDesc d = decode_unit(u, n_units, n_qblk, n_sb, H, SPLIT, seqs);
-    const int kvh = d.head / (H / Hk);
-    // -- item: the query rows (fp32) -> RoPE -> bf16 Q tile (B2); rows past the block are zero
-    {
-      const int s = cons_seq % PS;
-      mbar_wait(&bar[s], (uint32_t)(cons_seq / PS) & 1u);
-      const float* qf = reinterpret_cast<const float*>(smem + L::RING + s * L::STAGE);
-      constexpr int QI = QB * HALF / 4;
-      for (int it = lane; it < QI; it += 32) {
-        const int r = it / (HALF / 4), i = (it % (HALF / 4)) * 4;
-        uint2 lo = make_uint2(0, 0), hi = make_uint2(0, 0);
-        if (r < d.nr) {
-          const float4 x0 = *reinterpret_cast<const float4*>(qf + r * DH + i);
-          const float4 x1 = *reinterpret_cast<const float4*>(qf + r * DH + i + HALF);
-          const float4* cs = reinterpret_cast<const float4*>(rope + (size_t)(d.pos0 + r) * HALF + i);
-          const float4 c0 = __ldg(cs), c1 = __ldg(cs + 1);
-          lo = make_uint2(pack_bf16(x0.x * c0.x - x1.x * c0.y, x0.y * c0.z - x1.y * c0.w),
-                          pack_bf16(x0.z * c1.x - x1.z * c1.y, x0.w * c1.z - x1.w * c1.w));
-          hi = make_uint2(pack_bf16(x1.x * c0.x + x0.x * c0.y, x1.y * c0.z + x0.y * c0.w),
-                          pack_bf16(x1.z * c1.x + x0.z * c1.y, x1.w * c1.z + x0.w * c1.w));
-        }
-        *reinterpret_cast<uint2*>(q_s + r * P + i) = lo;
-        *reinterpret_cast<uint2*>(q_s + r * P + i + HALF) = hi;
-      }
-      __syncwarp();
-      ++cons_seq;
-      if (lane == 0) {
-        fence_proxy_async();
-        issue_next();
-      }
-    }
-    float o_acc[DT][4];
-    float m_row[2] = {-INFINITY, -INFINITY}, l_row[2] = {0.f, 0.f};
-#pragma unroll
-    for (int j = 0; j < DT; ++j) o_acc[j][0] = o_acc[j][1] = o_acc[j][2] = o_acc[j][3] = 0.f;
-    const bool own_head = d.head % (H / Hk) == 0;
-    for (int t = 0; t < d.n_tiles; ++t) {
-      const int t0 = d.k_lo + t * TK, s = cons_seq % PS;
-      const uint32_t kb = ring + (uint32_t)(s * L::STAGE), vb = kb + (uint32_t)(L::STAGE / 2);
-      mbar_wait(&bar[s], (uint32_t)(cons_seq / PS) & 1u);
-      if (lane < TK && t0 + lane >= d.k_hi) {     // rows past the unit's keys: zero
-#pragma unroll
-        for (int e = 0; e < DH; e += 8) {
-          st_shared_v4(tile_addr<DH>(kb, lane, e), make_uint4(0, 0, 0, 0));
-          st_shared_v4(tile_addr<DH>(vb, lane, e), make_uint4(0, 0, 0, 0));
-        }
-      }
-      const int nk0 = max(t0, d.new_first), nk1 = min(t0 + TK, d.k_hi);
-      if (nk0 < nk1) {     // new keys: K (RoPE) and V from the QKV output; one writer appends them
-        const int NI = (nk1 - nk0) * (HALF / 4);
-        for (int it = lane; it < NI; it += 32) {
-          const int key = nk0 + it / (HALF / 4), i = (it % (HALF / 4)) * 4;
-          const int m = d.q0 + (key - d.new_first);
-          const float* yk = qkv + (size_t)m * ldq + (H + kvh) * DH;
-          const float* yv = qkv + (size_t)m * ldq + (H + Hk + kvh) * DH;
-          const float4* cs = reinterpret_cast<const float4*>(rope + (size_t)key * HALF + i);
-          const float4 x0 = *reinterpret_cast<const float4*>(yk + i), x1 = *reinterpret_cast<const float4*>(yk + i + HALF);
-          const float4 va = *reinterpret_cast<const float4*>(yv + i), vv = *reinterpret_cast<const float4*>(yv + i + HALF);
-          const float4 c0 = __ldg(cs), c1 = __ldg(cs + 1);
-          const uint2 klo = make_uint2(pack_bf16(x0.x * c0.x - x1.x * c0.y, x0.y * c0.z - x1.y * c0.w),
-                                       pack_bf16(x0.z * c1.x - x1.z * c1.y, x0.w * c1.z - x1.w * c1.w));
-          const uint2 khi = make_uint2(pack_bf16(x1.x * c0.x + x0.x * c0.y, x1.y * c0.z + x0.y * c0.w),
-                                       pack_bf16(x1.z * c1.x + x0.z * c1.y, x1.w * c1.z + x0.w * c1.w));
-          const uint2 vlo = make_uint2(pack_bf16(va.x, va.y), pack_bf16(va.z, va.w));
-          const uint2 vhi = make_uint2(pack_bf16(vv.x, vv.y), pack_bf16(vv.z, vv.w));
-          const int kk = key - t0;
-          st_shared_v2(tile_addr<DH>(kb, kk, i), klo);
-          st_shared_v2(tile_addr<DH>(kb, kk, i + HALF), khi);
-          st_shared_v2(tile_addr<DH>(vb, kk, i), vlo);
-          st_shared_v2(tile_addr<DH>(vb, kk, i + HALF), vhi);
-          if (own_head && d.qb == (key - d.new_first) / QB) {
-            const int page = __ldg(kv.page_table + (size_t)d.slot * kv.max_pages + key / kv.P);
-            __nv_bfloat16* kdst = kv.pool + kv.offset(page, layer, 0, kvh, key % kv.P);
-            *reinterpret_cast<uint2*>(kdst + i) = klo;
-            *reinterpret_cast<uint2*>(kdst + i + HALF) = khi;
-            *reinterpret_cast<uint2*>(kdst + kv.vofs() + i) = vlo;
-            *reinterpret_cast<uint2*>(kdst + kv.vofs() + i + HALF) = vhi;
-          }
-        }
-      }
-      __syncwarp();
-      // S = Q K^T (two accumulator chains), scaled and masked; online base-2 softmax
-      float sc[2][4], s2[2][4];
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
-        sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = s2[nt][0] = s2[nt][1] = s2[nt][2] = s2[nt][3] = 0.f;
-#pragma unroll
-      for (int ks = 0; ks < DH / 16; ++ks) {
-        uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
-        ldsm_x4(qa + ((lane & 15) * P + ks * 16 + (lane >> 4) * 8) * 2, a0, a1, a2, a3);
-        ldsm_x4(tile_addr<DH>(kb, (lane >> 4) * 8 + (lane & 7), ks * 16 + ((lane >> 3) & 1) * 8), b0, b1, b2, b3);
-        float (*acc)[4] = (ks & 1) ? s2 : sc;
-        mma_bf16(acc[0], a0, a1, a2, a3, b0, b1);
-        mma_bf16(acc[1], a0, a1, a2, a3, b2, b3);
-      }
-      float f_row[2];
-#pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        const int r = g + 8 * h2;
-        float mx = -INFINITY;
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const int key = t0 + nt * 8 + 2 * t4 + c;
-            const bool ok = r < d.nr && key < d.k_hi && key <= d.pos0 + r;
-            float& v = sc[nt][2 * h2 + c];
-            v = ok ? (v + s2[nt][2 * h2 + c]) * scale : -INFINITY;
-            mx = fmaxf(mx, v);
-          }
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        const float mn = fmaxf(m_row[h2], mx);
-        f_row[h2] = (m_row[h2] == -INFINITY) ? 0.f : exp2_approx(m_row[h2] - mn);
-        float sum = 0.f;
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            float& v = sc[nt][2 * h2 + c];
-            v = (mn == -INFINITY) ? 0.f : exp2_approx(v - mn);
-            sum += v;
-          }
-        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-        m_row[h2] = mn;
-        l_row[h2] = l_row[h2] * f_row[h2] + sum;
-      }
-      const uint32_t pa0 = pack_bf16(sc[0][0], sc[0][1]), pa1 = pack_bf16(sc[0][2], sc[0][3]);
-      const uint32_t pa2 = pack_bf16(sc[1][0], sc[1][1]), pa3 = pack_bf16(sc[1][2], sc[1][3]);
-#pragma unroll
-      for (int dt = 0; dt < DT; dt += 2) {
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(tile_addr<DH>(vb, (lane & 7) + ((lane >> 3) & 1) * 8, dt * 8 + (lane >> 4) * 8), b0, b1, b2, b3);
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          o_acc[dt + q][0] *= f_row[0];
-          o_acc[dt + q][1] *= f_row[0];
-          o_acc[dt + q][2] *= f_row[1];
-          o_acc[dt + q][3] *= f_row[1];
-        }
-        mma_bf16(o_acc[dt], pa0, pa1, pa2, pa3, b0, b1);
-        mma_bf16(o_acc[dt + 1], pa0, pa1, pa2, pa3, b2, b3);
-      }
-      __syncwarp();
-      ++cons_seq;
-      if (lane == 0) {
-        fence_proxy_async();   // the generic reads / writes of the stage before the tensor copy
-        issue_next();
-      }
-    }
-    ++cidx;
-    if (lane == 0 && iu_end) pdl_trigger();   // nothing left to request: the successor may launch
-    // -- the unit's result: output (one split) or partial + split merge (several)
-    const size_t row0 = (size_t)(d.q0 + d.qb * QB);
-    if (d.nsplit == 1) {
-#pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        const int r = g + 8 * h2;
-        if (r >= d.nr) continue;
-        const float inv = 1.0f / l_row[h2];
-        __nv_bfloat16* o = out + ((row0 + r) * H + d.head) * DH + 2 * t4;
-#pragma unroll
-        for (int dt = 0; dt < DT; ++dt)
-          *reinterpret_cast<uint32_t*>(o + dt * 8) = pack_bf16(o_acc[dt][2 * h2] * inv, o_acc[dt][2 * h2 + 1] * inv);
-      }
-      continue;
-    }
-#pragma unroll
-    for (int h2 = 0; h2 < 2; ++h2) {
-      const int r = g + 8 * h2;
-      if (r >= d.nr) continue;
-      float* op = ws.o_part + (((size_t)d.split * M + row0 + r) * H + d.head) * DH + 2 * t4;
-#pragma unroll
-      for (int dt = 0; dt < DT; ++dt) *reinterpret_cast<float2*>(op + dt * 8) = make_float2(o_acc[dt][2 * h2], o_acc[dt][2 * h2 + 1]);
-      if (t4 == 0) {
-        float* ml = ws.ml_part + (((size_t)d.split * M + row0 + r) * H + d.head) * 2;
-        ml[0] = m_row[h2];
-        ml[1] = l_row[h2];
-      }
-    }
-    __syncwarp();
-    int tk = 0;
-    int* ctr = ws.counters + ((size_t)(d.seq * n_qblk + d.qb) * H + d.head);
-    if (lane == 0) {
-      fence_acq_rel_gpu();   // release this split's partial
-      tk = atomicAdd(ctr, 1);
-      if (tk == d.nsplit - 1) {
-        fence_acq_rel_gpu(); // acquire the other splits'
-        *ctr = 0;            // ready for the next launch (graph replay)
-      }
-    }
-    tk = __shfl_sync(0xffffffffu, tk, 0);
-    if (tk != d.nsplit - 1) continue;
-    for (int e = lane; e < d.nr * (DH / 4); e += 32) {
-      const int r = e / (DH / 4), dd = (e % (DH / 4)) * 4;
-      const size_t row = row0 + r;
-      float mx = -INFINITY;
-      for (int sp = 0; sp < d.nsplit; ++sp)
-        mx = fmaxf(mx, __ldcg(ws.ml_part + (((size_t)sp * M + row) * H + d.head) * 2));
-      float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-      float l = 0.f;
-      for (int sp = 0; sp < d.nsplit; ++sp) {
-        const float2 ml = __ldcg(reinterpret_cast<const float2*>(ws.ml_part + (((size_t)sp * M + row) * H + d.head) * 2));
-        if (ml.x == -INFINITY) continue;
-        const float4 v = __ldcg(reinterpret_cast<const float4*>(ws.o_part + (((size_t)sp * M + row) * H + d.head) * DH + dd));
-        const float f = exp2_approx(ml.x - mx);
-        o.x += v.x * f;
-        o.y += v.y * f;
-        o.z += v.z * f;
-        o.w += v.w * f;
-        l += ml.y * f;
-      }
-      *reinterpret_cast<uint2*>(out + (row * H + d.head) * DH + dd) =
-          make_uint2(pack_bf16(o.x / l, o.y / l), pack_bf16(o.z / l, o.w / l));
-    }
-  }
-  // the last warp out resets the work counter for the next launch (graph replay)
-  if (lane == 0) {
-    pdl_trigger();
-    if (atomicAdd(&sched[1], 1) == G - 1) {
-      sched[0] = 0;
-      sched[1] = 0;
-    }
-  }
-  rec_end(ws.timing, 2);
-}
-
-template <int DH>
-cudaError_t launch_warp(int M, int n_seq, int max_q_len, int max_kv, int H, int Hk, const CUtensorMap& tmkv,
-                        const CUtensorMap& tmq, const float* qkv, const SeqInfo& seqs, const float2* rope,
-                        const KVLayout& kv, int layer, const AttnWorkspace& ws, __nv_bfloat16* out, cudaStream_t st) {
-  if (kv.P < TK || kv.P % TK) return cudaErrorInvalidValue;
-  const int n_qblk = (max_q_len + QB - 1) / QB;
-  const int SPLIT = attn_chunk_tokens();
-  const int splits = (max_kv + SPLIT - 1) / SPLIT;
-  const int n_sb = n_seq * n_qblk;
-  const int n_units = splits * n_sb * H;
-  const size_t smem = PSmem<DH>::BYTES;
-  static int per_sm = 0;
-  if (!per_sm) {
-    if (cudaFuncSetAttribute(attn_warp_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return cudaErrorInvalidValue;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_warp_kernel<DH>, 32, smem);
-    if (per_sm < 1) per_sm = 1;
-  }
-  const int grid = std::min(n_units, kNumSMs * per_sm);
-  const float scale = 1.0f / sqrtf((float)DH) * 1.4426950408889634f;
-  return launch(attn_warp_kernel<DH>, dim3(grid), dim3(32), smem, st, tmkv, tmq, qkv, H, Hk, seqs, rope, kv, layer,
-                n_qblk, n_sb, n_units, scale, ws, M, out, SPLIT);
-}
-
-// env SEED_ATTN_L2PF=1 enables the L2 prefetch of a warp's tiles (experiments; measured slower at N = 24)
-int attn_l2_prefetch() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("SEED_ATTN_L2PF");
-    on = (e && e[0] == '1') ? 1 : 0;
-  }
-  return on;
-}
-
-template <int DH>
-cudaError_t launch_dh(int M, int n_seq, int max_q_len, int max_kv, int H, int Hk, const CUtensorMap& tmkv,
+template <int DH, int ST>
+cudaError_t launch_st(int M, int n_seq, int max_q_len, int max_kv, int H, int Hk, const CUtensorMap& tmkv,
                       const float* qkv, const SeqInfo& seqs, const float2* rope, const KVLayout& kv, int layer,
                       const AttnWorkspace& ws, __nv_bfloat16* out, cudaStream_t st) {
-  // page blocks of 16 keys land by one tensor copy each: 16 | P
-  if (kv.P < TK || kv.P % TK) return cudaErrorInvalidValue;
   const int n_qblk = (max_q_len + QB - 1) / QB;
-  const int SPLIT = attn_chunk_tokens();
+  const int SPLIT = attn_chunk_tokens(DH);
   const int splits = (max_kv + SPLIT - 1) / SPLIT;
-  const size_t smem = Smem<DH>::BYTES;
+  if (SPLIT / (TK * WARPS) > 32) return cudaErrorInvalidValue;   // tiles per warp held in pg_s
+  const size_t smem = Smem<DH, ST>::BYTES;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(attn_stream_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+    if (cudaFuncSetAttribute(attn_stream_kernel<DH, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return cudaErrorInvalidValue;
     attr = true;
   }
   // scores are kept in the base-2 domain: s = q.k / sqrt(Dh) * log2(e), p = 2^(s - max)
   const float scale = 1.0f / sqrtf((float)DH) * 1.4426950408889634f;
-  return launch(attn_stream_kernel<DH>, dim3(n_seq * n_qblk, H, splits), dim3(NT), smem, st, tmkv, qkv, H, Hk, seqs,
-                rope, kv, layer, n_qblk, scale, ws, M, out, SPLIT, attn_l2_prefetch(), kv.kv3d);
+  return launch(attn_stream_kernel<DH, ST>, dim3(n_seq * n_qblk, H, splits), dim3(NT), smem, st, tmkv, qkv, H, Hk,
+                seqs, rope, kv, layer, n_qblk, scale, ws, M, out, SPLIT, kv.kv3d);
+}
+
+// env SEED_ATTN_STAGES: ring stages per warp (2 default; 3, 4 for experiments)
+template <int DH>
+cudaError_t launch_dh(int M, int n_seq, int max_q_len, int max_kv, int H, int Hk, const CUtensorMap& tmkv,
+                      const float* qkv, const SeqInfo& seqs, const float2* rope, const KVLayout& kv, int layer,
+                      const AttnWorkspace& ws, __nv_bfloat16* out, cudaStream_t st) {
+  // page blocks of 16 keys land by one tensor copy each: 16 | P
+  if (kv.P < TK || kv.P % TK) return cudaErrorInvalidValue;
+  static int stages = -1;
+  if (stages < 0) {
+    const char* e = getenv("SEED_ATTN_STAGES");
+    stages = e ? atoi(e) : 2;
+  }
+  if (stages == 3)
+    return launch_st<DH, 3>(M, n_seq, max_q_len, max_kv, H, Hk, tmkv, qkv, seqs, rope, kv, layer, ws, out, st);
+  if (stages == 4)
+    return launch_st<DH, 4>(M, n_seq, max_q_len, max_kv, H, Hk, tmkv, qkv, seqs, rope, kv, layer, ws, out, st);
+  return launch_st<DH, 2>(M, n_seq, max_q_len, max_kv, H, Hk, tmkv, qkv, seqs, rope, kv, layer, ws, out, st);
 }
 }  // namespace
 
-// keys per CTA: a fixed split grid (R19); env SEED_ATTN_SPLIT (a multiple of 16) for experiments
-int attn_chunk_tokens() {
-  static int split = -1;
-  if (split < 0) {
+// keys per CTA: a fixed split grid, a function of the head size only (R19): 512 keys at Dh = 128
+// (the 7B / 13B targets: fewer, longer CTAs keep more bytes in flight at N = 24), 128 at Dh <= 64 (the
+// draft models: 12 heads leave few CTAs otherwise).  Env SEED_ATTN_SPLIT / SEED_ATTN_SPLIT_SMALL
+// (multiples of 16) for experiments.
+int attn_chunk_tokens(int Dh) {
+  static int big = -1, small = -1;
+  if (big < 0) {
     const char* e = getenv("SEED_ATTN_SPLIT");
-    split = e ? std::max(16, atoi(e) / 16 * 16) : 512;
+    big = e ? std::max(16, atoi(e) / 16 * 16) : 512;
+    const char* f = getenv("SEED_ATTN_SPLIT_SMALL");
+    small = f ? std::max(16, atoi(f) / 16 * 16) : 128;
   }
-  return split;
+  return Dh >= 128 ? big : small;
 }
-int attn_query_block() { return QB; }
 
 bool attn_kv_tmap(CUtensorMap* map, const KVLayout& kv, size_t n_pages, int* kv3d) {
   const uint64_t rows = (uint64_t)n_pages * kv.n_layers * 2 * kv.Hk * kv.P;
@@ -1008,22 +558,11 @@ bool attn_kv_tmap(CUtensorMap* map, const KVLayout& kv, size_t n_pages, int* kv3
 }
 
 cudaError_t attention(const float* qkv, int M, int n_seq, int max_q_len, int max_kv, int H, int Hk, int Dh,
-                      const SeqInfo& seqs, const float2* rope, const KVLayout& kv, const CUtensorMap& tmkv,
-                      const CUtensorMap& tmq, int layer, const AttnWorkspace& ws, __nv_bfloat16* out, cudaStream_t st) {
-  const int splits = (max_kv + attn_chunk_tokens() - 1) / attn_chunk_tokens();
+                      const SeqInfo& seqs, const float2* rope, const KVLayout& kv, const CUtensorMap& tmkv, int layer,
+                      const AttnWorkspace& ws, __nv_bfloat16* out, cudaStream_t st) {
+  const int splits = (max_kv + attn_chunk_tokens(Dh) - 1) / attn_chunk_tokens(Dh);
   if (splits > ws.max_splits) return cudaErrorInvalidValue;
   if ((size_t)n_seq * ((max_q_len + QB - 1) / QB) * H > (size_t)ws.max_counters) return cudaErrorInvalidValue;
-  static int form = -1;
-  if (form < 0) {
-    const char* e = getenv("SEED_ATTN_FORM");
-    form = e ? atoi(e) : 0;
-  }
-  if (form == 1 && !kv.kv3d) {
-    if (Dh == 128) return launch_warp<128>(M, n_seq, max_q_len, max_kv, H, Hk, tmkv, tmq, qkv, seqs, rope, kv, layer, ws, out, st);
-    if (Dh == 64) return launch_warp<64>(M, n_seq, max_q_len, max_kv, H, Hk, tmkv, tmq, qkv, seqs, rope, kv, layer, ws, out, st);
-    if (Dh == 32) return launch_warp<32>(M, n_seq, max_q_len, max_kv, H, Hk, tmkv, tmq, qkv, seqs, rope, kv, layer, ws, out, st);
-    return cudaErrorInvalidValue;
-  }
   if (Dh == 128) return launch_dh<128>(M, n_seq, max_q_len, max_kv, H, Hk, tmkv, qkv, seqs, rope, kv, layer, ws, out, st);
   if (Dh == 64) return launch_dh<64>(M, n_seq, max_q_len, max_kv, H, Hk, tmkv, qkv, seqs, rope, kv, layer, ws, out, st);
   if (Dh == 32) return launch_dh<32>(M, n_seq, max_q_len, max_kv, H, Hk, tmkv, qkv, seqs, rope, kv, layer, ws, out, st);

@@ -122,7 +122,6 @@ struct Model {
   // paged KV
   KVLayout kv{};
   CUtensorMap tmkv;                 // 2D tensor map of the KV pool (attention's page-block copies)
-  CUtensorMap tmq;                  // fp32 2D tensor map of the QKV output y (attention's query rows)
   int32_t* page_table_dev = nullptr;
   int32_t* page_table = nullptr;          // pinned host mirror [slots][max_pages]
   std::vector<int32_t> free_pages;
@@ -166,7 +165,7 @@ struct RoundPlan {  // descriptors of one round at batch-size-determined arena o
   std::vector<int> verify_b0;
 };
 
-constexpr int kMaxChunkRows = 256;
+constexpr int kMaxChunkRows = 1024;   // rows per forward chunk (the GEMM runs token tiles of 256)
 constexpr size_t kCtaRec = 8192;  // per-launch per-CTA trace words (GEMM: 148 x 16, attention: grid x 8)
 
 }  // namespace
@@ -179,6 +178,7 @@ struct seed_ctx_s {
   Model dm, tm;                   // draft, target
   int P = 16, max_pages = 0, n_slots = 0;
   std::map<std::tuple<const void*, int, int>, CUtensorMap> xmaps;
+  std::map<std::tuple<const void*, int, int, int>, CUtensorMap> ymaps;
   Arena arena;
   // stream registry
   std::vector<SlotState> slots;
@@ -287,6 +287,19 @@ seed_status run_gemm(seed_ctx ctx, const GemmPlan& p, int M, const seed::GemmIO&
 }
 
 // X operand from a bf16 activation buffer by TMA
+// the output's store map (whole-tile tensor stores, gemm.cu): exactly M rows starting at `ptr`
+const CUtensorMap* ymap(seed_ctx ctx, const void* ptr, bool fp32, int cols, int ld, int M) {
+  const int m_pad = seed::gemm_mpad(M);
+  if (m_pad > 256) return nullptr;
+  auto key = std::make_tuple(ptr, (int)fp32 * (1 << 30) + cols, ld, M);
+  auto it = ctx->ymaps.find(key);
+  if (it != ctx->ymaps.end()) return &it->second;
+  CUtensorMap m;
+  if (!seed::encode_tmap_store(&m, ptr, fp32, (uint64_t)cols, (uint64_t)M, (uint64_t)ld, fp32 ? 128 : 64, (uint32_t)m_pad))
+    return nullptr;
+  return &(ctx->ymaps[key] = m);
+}
+
 seed::GemmIO io_tma(seed_ctx ctx, const bf16* X, int K, int rows_cap, int M, float* Y, int ldY) {
   seed::GemmIO io;
   io.tmX = xmap(ctx, X, K, rows_cap, M);
@@ -413,19 +426,17 @@ seed_status build_model(seed_ctx ctx, Model& m, const seed_model_shape& sh, cons
   CK(cudaMalloc(&m.x, mc * d * 4));
   CK(cudaMalloc(&m.ssq_a, ((d + 127) / 128) * mc * 4));
   CK(cudaMalloc(&m.ssq_b, ((d + 127) / 128) * mc * 4));
-  CK(cudaMalloc(&m.y, mc * std::max<size_t>((size_t)m.nqkv, d) * 4));
+  CK(cudaMalloc(&m.y, mc * (size_t)m.nqkv * 4));   // QKV output
   m.attn = alloc(mc * dq);
   m.h = alloc(mc * d);
   m.act = alloc(mc * ff);
   if (!m.attn || !m.h || !m.act) return fail(ctx, SEED_ENOMEM, "seed_init", "activations");
-  m.aws.max_splits = (max_pos + seed::attn_chunk_tokens() - 1) / seed::attn_chunk_tokens();
+  m.aws.max_splits = (max_pos + seed::attn_chunk_tokens(m.Dh) - 1) / seed::attn_chunk_tokens(m.Dh);
   CK(cudaMalloc(&m.aws.o_part, (size_t)m.aws.max_splits * mc * dq * 4));
   CK(cudaMalloc(&m.aws.ml_part, (size_t)m.aws.max_splits * mc * m.H * 2 * 4));
   m.aws.max_counters = (int)(mc * m.H);
-  CK(cudaMalloc(&m.aws.counters, (size_t)(m.aws.max_counters + 2) * 4));
-  CK(cudaMemset(m.aws.counters, 0, (size_t)(m.aws.max_counters + 2) * 4));
-  if (!seed::encode_tmap_2d_f32(&m.tmq, m.y, (uint64_t)m.nqkv, (uint64_t)mc, (uint64_t)m.nqkv, (uint32_t)m.Dh, 16))
-    return fail(ctx, SEED_ECUDA, "seed_init", "QKV tensor map");
+  CK(cudaMalloc(&m.aws.counters, (size_t)m.aws.max_counters * 4));
+  CK(cudaMemset(m.aws.counters, 0, (size_t)m.aws.max_counters * 4));
   return SEED_OK;
 }
 
@@ -513,14 +524,15 @@ seed_status forward_chunk(seed_ctx ctx, Model& m, const ChunkDesc& c, cudaStream
       seed::GemmIO io = norm_io(m.ssq_b);
       io.Y = m.y;
       io.ldY = m.nqkv;
+      io.tmY = ymap(ctx, m.y, true, m.nqkv, m.nqkv, M);
       if ((s = run_gemm(ctx, m.pq[l], M, io, st)) != SEED_OK) return s;
     }
     {
       seed::AttnWorkspace aws = m.aws;
       aws.cta = nullptr;
       aws.timing = next_rec(ctx, &aws.cta);
-      CK(seed::attention(m.y, M, c.n_seq, c.max_q_len, c.max_kv, m.H, m.Hk, m.Dh, seqs, m.rope, m.kv, m.tmkv, m.tmq, l,
-                         aws, m.attn, st));
+      CK(seed::attention(m.y, M, c.n_seq, c.max_q_len, c.max_kv, m.H, m.Hk, m.Dh, seqs, m.rope, m.kv, m.tmkv, l, aws,
+                         m.attn, st));
     }
     // O: x += attn Wo^T; sums of squares -> ssq_a; h = bf16(x * mlp_norm)
     {
@@ -562,6 +574,7 @@ seed_status forward_chunk(seed_ctx ctx, Model& m, const ChunkDesc& c, cudaStream
     io.Y = c.Y;
     io.ldY = c.ldY;
     io.yrow = c.n_logits == M ? nullptr : c.compact;
+    if (!io.yrow) io.tmY = ymap(ctx, c.Y, true, m.V, c.ldY, M);
     if ((s = run_gemm(ctx, m.plm, M, io, st)) != SEED_OK) return s;
   }
   return SEED_OK;
@@ -623,7 +636,7 @@ seed_status prefill(seed_ctx ctx, Model& m, int slot, const int32_t* toks, int n
                     cudaStream_t st) {
   int done = 0;
   while (done < n) {
-    const int q = std::min(kMaxChunkRows, n - done);
+    const int q = std::min(std::min(kMaxChunkRows, m.m_cap), n - done);
     ctx->arena.begin();
     const size_t to = ctx->arena.alloc(q);
     if (to == (size_t)-1) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
@@ -759,7 +772,7 @@ seed_status build_round_plan(seed_ctx ctx, const std::vector<int32_t>& ids, cons
     segs[b] = Segment{slots[b], T - 2, 2, (int)to, T - 2};
   }
   size_t tok_off;
-  if (2 * n > kMaxChunkRows || !pack_chunk(ctx, segs, 2, &P.draft[0], &tok_off))
+  if (2 * n > ctx->tm.m_cap || 2 * n > ctx->dm.m_cap || !pack_chunk(ctx, segs, 2, &P.draft[0], &tok_off))
     return fail(ctx, SEED_ECAPACITY, "seed_draft_round", "batch too large");
   for (int j = 2; j <= g; ++j) {
     for (int b = 0; b < n; ++b) {
@@ -770,7 +783,7 @@ seed_status build_round_plan(seed_ctx ctx, const std::vector<int32_t>& ids, cons
     P.draft[j - 1].tok = TokSrc{ctx->xs + (j - 2), g};  // x_{j-1} of every stream ([B][g] layout)
   }
   // verify chunks of whole streams
-  const int per_chunk = std::max(1, kMaxChunkRows / (g + 1));
+  const int per_chunk = std::max(1, ctx->tm.m_cap / (g + 1));
   for (int b0 = 0; b0 < n; b0 += per_chunk) {
     const int nb = std::min(per_chunk, n - b0);
     std::vector<Segment> vs(nb);
@@ -789,16 +802,16 @@ seed_status build_round_plan(seed_ctx ctx, const std::vector<int32_t>& ids, cons
   // attention grids sized by the round's longest context, rounded up to whole splits; the
   // graphs are keyed by (batch size, split counts), so a graph is re-captured only when a
   // context crosses a split boundary (R23)
-  const int ch = seed::attn_chunk_tokens();
+  const int chd = seed::attn_chunk_tokens(ctx->dm.Dh), cht = seed::attn_chunk_tokens(ctx->tm.Dh);
   int dk = 0, vk = 0;
   for (auto& c : P.draft) dk = std::max(dk, c.max_kv);
   for (auto& c : P.verify) vk = std::max(vk, c.max_kv);
-  dk = std::min(max_pos, (dk + ch - 1) / ch * ch);
-  vk = std::min(max_pos, (vk + ch - 1) / ch * ch);
+  dk = std::min(max_pos, (dk + chd - 1) / chd * chd);
+  vk = std::min(max_pos, (vk + cht - 1) / cht * cht);
   for (auto& c : P.draft) c.max_kv = dk;
   for (auto& c : P.verify) c.max_kv = vk;
-  P.key_draft = ((int64_t)n << 32) | (dk / ch);
-  P.key_verify = ((int64_t)n << 32) | (vk / ch);
+  P.key_draft = ((int64_t)n << 32) | (dk / chd);
+  P.key_verify = ((int64_t)n << 32) | (vk / cht);
   return SEED_OK;
 }
 
@@ -1481,34 +1494,19 @@ seed_status seed_op_gemm(const void* W, int32_t N, int32_t K, const void* X, int
   cudaStream_t st = (cudaStream_t)stream;
   GemmPlan p;
   seed::gemm_plan(&p, W, N, K);
-  int done = 0;
-  bf16* xpad = nullptr;
-  if (cudaMallocAsync(&xpad, (size_t)256 * K * 2, st) != cudaSuccess) return SEED_ENOMEM;
-  cudaMemsetAsync(xpad, 0, (size_t)256 * K * 2, st);
+  // X read in place: boxes of 64 x m_pad rows per 256-row token tile (rows past M read as zero and
+  // only feed accumulator columns that are never stored)
+  CUtensorMap tm;
   seed_status s = SEED_OK;
-  while (done < M && s == SEED_OK) {
-    const int m = std::min(256, M - done);
-    const bf16* Xc = reinterpret_cast<const bf16*>(X) + (size_t)done * K;
-    // copy into a buffer of >= m_pad rows so the TMA box never leaves the tensor; the pad
-    // rows only feed accumulator columns that are never stored
-    if (cudaMemcpyAsync(xpad, Xc, (size_t)m * K * 2, cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
-      s = SEED_ECUDA;
-      break;
-    }
-    CUtensorMap tm;
-    if (!seed::encode_tmap_2d(&tm, xpad, (uint64_t)K, 256, 64, (uint32_t)seed::gemm_mpad(m))) {
-      s = SEED_ECUDA;
-      break;
-    }
+  if (!seed::encode_tmap_2d(&tm, X, (uint64_t)K, (uint64_t)M, 64, (uint32_t)seed::gemm_mpad(M))) s = SEED_ECUDA;
+  if (s == SEED_OK) {
     seed::GemmIO io;
     io.tmX = &tm;
-    io.Y = Y + (size_t)done * N;
+    io.Y = Y;
     io.ldY = N;
-    if (seed::gemm_run(p, m, io, st) != cudaSuccess) s = SEED_ECUDA;
-    done += m;
+    if (seed::gemm_run(p, M, io, st) != cudaSuccess) s = SEED_ECUDA;
   }
-  cudaFreeAsync(xpad, st);
-  cudaStreamSynchronize(st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) s = SEED_ECUDA;
   seed::gemm_plan_free(&p);
   return s;
 }

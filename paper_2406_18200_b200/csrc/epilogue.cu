@@ -26,36 +26,48 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 
 // x[m] = embed[tok[m]] (fp32, exact) -- or x given -- and the per-128-column-tile sums of
 // squares ssq[t][m] and h = bf16(x * nw) the next GEMM consumes (RMSNorm scale 1/rms applied
-// in its epilogue, R24).  grid (ceil(d/128), M), block 128.
+// in its epilogue, R24).  grid (ceil(d / 1024), M), 128 threads: a CTA covers eight 128-column
+// tiles of one row, every load issued before the first use, one barrier.
+constexpr int EMB_TILES = 8;
 __global__ void __launch_bounds__(128)
 embed_stats_kernel(const __nv_bfloat16* __restrict__ embed, const int32_t* __restrict__ tok, int tok_stride, int d,
                    int V, float* __restrict__ x, float* __restrict__ ssq, const __nv_bfloat16* __restrict__ nw,
                    __nv_bfloat16* __restrict__ h, int32_t* err, int M, unsigned long long* rec) {
-  __shared__ float red[4];
+  __shared__ float red[EMB_TILES][4];
   pdl_trigger();
   rec_start(rec);
   pdl_wait();
   rec_release(rec);
-  const int t = blockIdx.x, m = blockIdx.y, n = t * 128 + threadIdx.x;
-  float v = 0.f;
-  if (n < d) {
-    if (embed) {
-      int id = tok[(size_t)m * tok_stride];
-      if (id < 0 || id >= V) {   // contract violation (SEED_EDEVICE): never read outside the table
-        if (err && threadIdx.x == 0 && t == 0) atomicOr(err, 1);
-        id = 0;
-      }
-      v = bf2f(embed[(size_t)id * d + n]);
-      x[(size_t)m * d + n] = v;
-    } else {
-      v = x[(size_t)m * d + n];
+  const int m = blockIdx.y, t0 = blockIdx.x * EMB_TILES, tid = threadIdx.x;
+  int id = 0;
+  if (embed) {
+    id = tok[(size_t)m * tok_stride];
+    if (id < 0 || id >= V) {   // contract violation (SEED_EDEVICE): never read outside the table
+      if (err && tid == 0 && blockIdx.x == 0) atomicOr(err, 1);
+      id = 0;
     }
-    if (h) h[(size_t)m * d + n] = f2bf(v * bf2f(nw[n]));
   }
-  float sq = warp_sum(v * v);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+  float v[EMB_TILES];
+#pragma unroll
+  for (int k = 0; k < EMB_TILES; ++k) {
+    const int n = (t0 + k) * 128 + tid;
+    v[k] = 0.f;
+    if (n < d) v[k] = embed ? bf2f(embed[(size_t)id * d + n]) : x[(size_t)m * d + n];
+  }
+#pragma unroll
+  for (int k = 0; k < EMB_TILES; ++k) {
+    const int n = (t0 + k) * 128 + tid;
+    if (n < d) {
+      if (embed) x[(size_t)m * d + n] = v[k];
+      if (h) h[(size_t)m * d + n] = f2bf(v[k] * bf2f(nw[n]));
+    }
+    const float sq = warp_sum(v[k] * v[k]);
+    if ((tid & 31) == 0) red[k][tid >> 5] = sq;
+  }
   __syncthreads();
-  if (threadIdx.x == 0) ssq[(size_t)t * M + m] = ((red[0] + red[1]) + red[2]) + red[3];
+  const int nt = (d + 127) / 128;
+  if (tid < EMB_TILES && t0 + tid < nt)
+    ssq[(size_t)(t0 + tid) * M + m] = ((red[tid][0] + red[tid][1]) + red[tid][2]) + red[tid][3];
   rec_end(rec, 5);
 }
 
@@ -91,8 +103,9 @@ __global__ void kv_write_dense_kernel(KVLayout kv, int layer, int slot, int n, c
 cudaError_t embed_stats(const __nv_bfloat16* embed, const int32_t* tok, int tok_stride, int M, int d, int V, float* x,
                         float* ssq, const __nv_bfloat16* nw, __nv_bfloat16* h, int32_t* err, cudaStream_t st,
                         unsigned long long* timing) {
-  return launch(embed_stats_kernel, dim3((d + 127) / 128, M), dim3(128), 0, st, embed, tok, tok_stride, d, V, x, ssq,
-                nw, h, err, M, timing);
+  const int nt = (d + 127) / 128;
+  return launch(embed_stats_kernel, dim3((nt + EMB_TILES - 1) / EMB_TILES, M), dim3(128), 0, st, embed, tok, tok_stride,
+                d, V, x, ssq, nw, h, err, M, timing);
 }
 
 cudaError_t kv_write_dense(const KVLayout& kv, int layer, int slot, int n, const __nv_bfloat16* k,

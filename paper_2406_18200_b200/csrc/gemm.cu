@@ -29,6 +29,7 @@ constexpr int BLOCK_N = 128;   // weight rows per tile (UMMA M)
 constexpr int BLOCK_K = 64;    // one 128-byte swizzle row of bf16
 constexpr int W_TILE_BYTES = BLOCK_N * BLOCK_K * 2;
 constexpr int MAX_STAGES = 16;
+constexpr int TOKEN_TILE = 256;   // rows per CTA (UMMA N <= 256); more rows -> several token tiles
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -56,6 +57,7 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
 // c-way parallel reduction and epilogue that never leaves the cluster.
 struct SplitArgs {
   int KB, c, per, M, m_pad, stages, N, K, ldY, ymode, ssq_in_ld, pc, pitch;
+  int Mtot;                    // rows of the whole launch; a CTA's token tile holds rows [row0, row0 + M)
   float eps;
   float* Y;
   const float* ssq_in;
@@ -65,6 +67,8 @@ struct SplitArgs {
   __nv_bfloat16* hout;
   unsigned long long* timing;
   unsigned long long* cta;
+  int tstore;                  // c = 1, ymode 0 without a row map or ymode 2: the whole tile is staged in the
+                               // idle ring and leaves by one tensor store (tmY)
 };
 
 // rows m0 .. m0 + 15 below mlim of tile column nl (weight row n = 128 t + nl), v = the reduced
@@ -167,7 +171,8 @@ __device__ __forceinline__ void split_finish16(const SplitArgs& a, int t, int nl
 }
 
 __global__ void __launch_bounds__(192, 2)
-gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, SplitArgs a) {
+gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                   const __grid_constant__ CUtensorMap tmY, SplitArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned by pointer arithmetic on the shared array (the compiler keeps the shared
   // state space: ld/st.shared instead of generic accesses)
@@ -188,12 +193,23 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
   uint8_t* stg0 = smem + (c_dump_bytes(a) + 1023) / 1024 * 1024;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x, t = blockIdx.y, c = a.c;
+  const int c = a.c, r = blockIdx.x % c, t = blockIdx.y;
+  // token tile: rows [row0, row0 + M) of the launch (blockIdx.x / c); every row's reduction order is
+  // the same whatever tile it falls in (R19).  The pointers below are rebased to the tile.
+  const int row0 = (blockIdx.x / c) * TOKEN_TILE;
+  a.M = min(TOKEN_TILE, a.Mtot - row0);
+  if (row0 > 0) {
+    if (a.ymode == 0 && a.yrow) a.yrow += row0;
+    else if (a.Y) a.Y += (size_t)row0 * a.ldY;
+    if (a.hout) a.hout += (size_t)row0 * (a.ymode == 2 ? a.N / 2 : a.N);
+    if (a.ssq_in) a.ssq_in += row0;
+    if (a.ssq_out) a.ssq_out += row0;
+  }
   const int kb0 = (int)((long)r * a.KB / c), kb1 = (int)((long)(r + 1) * a.KB / c);
   const int nk = kb1 - kb0;
   pdl_trigger();
   if (a.timing && threadIdx.x == 0) atomicMin(&a.timing[0], globaltimer());
-  unsigned long long* ct = a.cta ? a.cta + (size_t)(t * c + r) * 16 : nullptr;
+  unsigned long long* ct = a.cta && blockIdx.x < c ? a.cta + (size_t)(t * c + r) * 16 : nullptr;
   if (ct && threadIdx.x == 0) ct[0] = globaltimer();
 
   uint32_t cols = 32;
@@ -232,14 +248,14 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
       if (a.timing) atomicMin(&a.timing[1], globaltimer());
       if (ct) ct[1] = globaltimer();
       for (int i = 0; i < n_pre; ++i)
-        tma_load_2d(sX + i * x_bytes, &tmX, &full[i], (kb0 + i) * BLOCK_K, 0, pol_x);
+        tma_load_2d(sX + i * x_bytes, &tmX, &full[i], (kb0 + i) * BLOCK_K, row0, pol_x);
       int stage = n_pre % S;
       uint32_t phase = n_pre == S ? 1u : 0u;
       for (int k = n_pre; k < nk; ++k) {
         mbar_wait(&empty[stage], phase ^ 1);
         mbar_arrive_expect_tx(&full[stage], tx);
         tma_load_2d(sW + stage * W_TILE_BYTES, &tmW, &full[stage], (kb0 + k) * BLOCK_K, t * BLOCK_N, pol_w);
-        tma_load_2d(sX + stage * x_bytes, &tmX, &full[stage], (kb0 + k) * BLOCK_K, 0, pol_x);
+        tma_load_2d(sX + stage * x_bytes, &tmX, &full[stage], (kb0 + k) * BLOCK_K, row0, pol_x);
         if (++stage == S) {
           stage = 0;
           phase ^= 1;
@@ -314,7 +330,52 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
     if (ct && et == 0) ct[5] = globaltimer();
     const uint32_t row_addr = tmem_base + ((uint32_t)(lane_grp * 32) << 16);
     int chunk = 0;
-    if (c == 1) {
+    if (a.tstore) {
+      // whole tile: every accumulator column straight into a staging tile in the idle ring (32 columns
+      // per TMEM load), one barrier, one tensor store -- no per-chunk barrier or store round trip
+      float* sf = reinterpret_cast<float*>(smem);   // ymode 0: fp32 [m_pad][128]; ymode 2: fp32 [m_pad][128] gate | up
+      for (int m0 = 0; m0 < mcols; m0 += 32) {
+        float v[32];
+        if (m0 + 16 < mcols) {
+          tmem_ld32(row_addr + m0, v);
+        } else {
+          tmem_ld16(row_addr + m0, v);
+#pragma unroll
+          for (int i = 16; i < 32; ++i) v[i] = 0.f;
+        }
+        const int nv = min(32, mcols - m0);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          if (i >= nv) break;
+          const int m = m0 + i;
+          const float sc = a.ssq_in ? inv_s[min(m, 255)] : 1.0f;
+          sf[m * 128 + nl] = (m < a.M && a.ssq_in) ? v[i] * sc : v[i];
+        }
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (a.ymode == 2) {
+        // SwiGLU: output j (0..63) of row m from gate column j and up column 64 + j (B4)
+        __nv_bfloat16* sh = reinterpret_cast<__nv_bfloat16*>(smem + (size_t)a.m_pad * 128 * 4);   // bf16 [m_pad][64]
+        const int j = et & 63;
+        for (int m = et >> 6; m < mcols; m += 2) {
+          const float g = sf[m * 128 + j], u = sf[m * 128 + 64 + j];
+          sh[m * 64 + j] = f2bf(g * rcp_approx(1.0f + __expf(-g)) * u);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (et == 0) {
+          fence_proxy_async();
+          tma_store_2d(&tmY, sh, t * 64, row0);
+          bulk_commit();
+          bulk_wait_read0();
+        }
+      } else if (et == 0) {
+        fence_proxy_async();
+        tma_store_2d(&tmY, sf, t * BLOCK_N, row0);
+        bulk_commit();
+        bulk_wait_read0();
+      }
+      if (ct && et == 0) ct[11] = globaltimer();
+    } else if (c == 1) {
       for (int m0 = 0; m0 < a.M; m0 += 16) {
         float v[16];
         tmem_ld16(row_addr + m0, v);
@@ -398,7 +459,7 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
           // per-tile sums of squares of this rank's rows, warps in a fixed order
           asm volatile("bar.sync 1, 128;" ::: "memory");
           for (int m = lo + et; m < hi; m += 128)
-            a.ssq_out[(size_t)t * a.M + m] = ((red_s[m] + red_s[256 + m]) + red_s[512 + m]) + red_s[768 + m];
+            a.ssq_out[(size_t)t * a.Mtot + m] = ((red_s[m] + red_s[256 + m]) + red_s[512 + m]) + red_s[768 + m];
         }
         if (pass + 1 < npass) cluster_sync();   // slots are rewritten by the next pass
       }
@@ -407,7 +468,7 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
       // per-tile sums of squares of the updated residual rows, warps in a fixed order
       asm volatile("bar.sync 1, 128;" ::: "memory");
       for (int m = m_lo + et; m < m_hi; m += 128)
-        a.ssq_out[(size_t)t * a.M + m] = ((red_s[m] + red_s[256 + m]) + red_s[512 + m]) + red_s[768 + m];
+        a.ssq_out[(size_t)t * a.Mtot + m] = ((red_s[m] + red_s[256 + m]) + red_s[512 + m]) + red_s[768 + m];
     }
     if (ct && et == 0) ct[6] = globaltimer();
   }
@@ -466,7 +527,7 @@ void load_encode() {
 }
 }  // namespace
 
-int gemm_mpad(int M) { return ((M + 15) / 16) * 16; }
+int gemm_mpad(int M) { return std::min(((M + 15) / 16) * 16, TOKEN_TILE); }
 
 bool encode_tmap_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
                     uint32_t box_outer, int swizzle_bytes) {
@@ -498,17 +559,18 @@ bool encode_tmap_kv_halves(CUtensorMap* map, const void* ptr, uint64_t rows, uin
   return r == CUDA_SUCCESS;
 }
 
-bool encode_tmap_2d_f32(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_elems,
-                        uint32_t box_inner, uint32_t box_outer) {
+bool encode_tmap_store(CUtensorMap* map, const void* ptr, bool fp32, uint64_t inner, uint64_t outer,
+                       uint64_t row_stride_elems, uint32_t box_inner, uint32_t box_outer) {
   std::call_once(g_encode_once, load_encode);
   if (!g_encode) return false;
+  const int es = fp32 ? 4 : 2;
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {row_stride_elems * 4};
+  cuuint64_t strides[1] = {row_stride_elems * es};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = g_encode(map, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                        const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -599,8 +661,9 @@ cudaError_t timing_accumulate(unsigned long long* rec, int n, unsigned long long
 
 cudaError_t gemm_run(const GemmPlan& p, int M, const GemmIO& io, cudaStream_t st, unsigned long long* timing,
                      unsigned long long* cta) {
-  const int m_pad = gemm_mpad(M);
-  if (M < 1 || m_pad > 256 || !io.tmX) return cudaErrorInvalidValue;
+  const int m_pad = std::min(gemm_mpad(M), TOKEN_TILE);
+  const int ttiles = (M + TOKEN_TILE - 1) / TOKEN_TILE;
+  if (M < 1 || !io.tmX) return cudaErrorInvalidValue;
   if (io.ymode == 1 && (!io.Y || !io.ssq_out || !io.nw || !io.hout)) return cudaErrorInvalidValue;
   if (io.ymode == 2 && (!io.ssq_in || !io.hout || p.N % BLOCK_N)) return cudaErrorInvalidValue;
   if (io.ymode == 0 && !io.Y) return cudaErrorInvalidValue;
@@ -609,7 +672,8 @@ cudaError_t gemm_run(const GemmPlan& p, int M, const GemmIO& io, cudaStream_t st
   SplitArgs b{};
   b.KB = p.KB;
   b.c = p.c;
-  b.M = M;
+  b.M = std::min(M, TOKEN_TILE);
+  b.Mtot = M;
   b.m_pad = m_pad;
   b.per = (m_pad / 4 + p.c - 1) / p.c * 4;
   b.N = p.N;
@@ -628,6 +692,7 @@ cudaError_t gemm_run(const GemmPlan& p, int M, const GemmIO& io, cudaStream_t st
   b.hout = io.hout;
   b.timing = timing;
   b.cta = cta;
+  b.tstore = 0;
   const int stage_bytes = W_TILE_BYTES + m_pad * BLOCK_K * 2;
   const int extra = (256 + 256 + 2048) * 4 + 64;   // inv_s, rowmap_s, red_s | xch, barriers
   const char* e = getenv("SEED_SPLIT_SMEM_KB");
@@ -638,6 +703,10 @@ cudaError_t gemm_run(const GemmPlan& p, int M, const GemmIO& io, cudaStream_t st
   while (stages * stage_bytes < (c_dump_bytes(b) + 1023) / 1024 * 1024 + 2 * 12288) ++stages;
   if (stages < 2) stages = 2;
   b.stages = stages;
+  // whole-tile staging + one tensor store (c = 1): the staging tile must fit the idle ring
+  if (p.c == 1 && io.tmY && io.ymode == 0 && !io.yrow &&
+      (size_t)m_pad * (512 + (io.ymode == 2 ? 128 : 0)) <= (size_t)stages * stage_bytes && !getenv("SEED_GEMM_NO_TSTORE"))
+    b.tstore = 1;
   const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 2) * 8 + 16 + extra;
   static bool sattr = false;
   if (!sattr) {
@@ -647,8 +716,8 @@ cudaError_t gemm_run(const GemmPlan& p, int M, const GemmIO& io, cudaStream_t st
     sattr = true;
   }
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  return launch_clustered(gemm_splitk_kernel, dim3(p.c, p.tiles), dim3(192), smem, st, dim3(p.c, 1, 1), p.tmW,
-                          *io.tmX, b);
+  return launch_clustered(gemm_splitk_kernel, dim3(p.c * ttiles, p.tiles), dim3(192), smem, st, dim3(p.c, 1, 1), p.tmW,
+                          *io.tmX, b.tstore ? *io.tmY : p.tmW, b);
 }
 
 }  // namespace seed

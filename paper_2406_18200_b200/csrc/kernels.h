@@ -37,9 +37,10 @@ bool encode_tmap_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t 
                     uint32_t box_outer, int swizzle_bytes = 128);
 // KV pool rows of 128 bf16 as a 3D map (64 elements, rows, 2 halves): one tensor copy per 16-row block
 bool encode_tmap_kv_halves(CUtensorMap* map, const void* ptr, uint64_t rows, uint32_t box_rows);
-// fp32 2D tensor map without swizzle (rows of row_stride_elems elements; inner <= row_stride_elems)
-bool encode_tmap_2d_f32(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_elems,
-                        uint32_t box_inner, uint32_t box_outer);
+// 2D store map (fp32 or bf16) without swizzle, rows of row_stride_elems elements
+bool encode_tmap_store(CUtensorMap* map, const void* ptr, bool fp32, uint64_t inner, uint64_t outer,
+                       uint64_t row_stride_elems, uint32_t box_inner, uint32_t box_outer);
+
 void gemm_plan(GemmPlan* plan, const void* W, int N, int K, int min_units = 4);
 void gemm_plan_free(GemmPlan* plan);
 // Operands and epilogue of one GEMM launch (see gemm.cu):
@@ -63,6 +64,9 @@ struct GemmIO {
   float* ssq_out = nullptr;
   const __nv_bfloat16* nw = nullptr;
   __nv_bfloat16* hout = nullptr;
+  // optional tensor map of the output for whole-tile stores (c = 1): ymode 0 -> Y (fp32, exactly M rows,
+  // boxes of 128 x m_pad), ymode 2 -> hout (bf16, exactly M rows, boxes of 64 x m_pad); no swizzle
+  const CUtensorMap* tmY = nullptr;
 };
 // timing: optional [4] launch record (kind 1); cta: optional [G][16] per-CTA globaltimer ns:
 // start, producer release, producer done, first stage full, MMA done, first accumulator ready,
@@ -105,17 +109,16 @@ struct AttnWorkspace {
   unsigned long long* timing;  // optional profile record [4] (start, release, end)
   unsigned long long* cta = nullptr;  // optional per-block phase words [grid][8] (diagnostics)
 };
-int attn_chunk_tokens();
+int attn_chunk_tokens(int Dh);   // keys per attention CTA (split grid) for head size Dh
 int attn_query_block();
 // fused: QKV epilogue (RoPE, bf16, KV append) + paged attention + split-KV merge; qkv = Y [M][(H+2Hk)Dh]
 // tmkv: 2D tensor map of the KV pool (attn_kv_tmap): rows of Dh elements, boxes of min(Dh, 64) x
 // min(P, 32) with the 128-byte swizzle
 bool attn_kv_tmap(CUtensorMap* map, const KVLayout& kv, size_t n_pages, int* kv3d);
-// tmq: fp32 2D tensor map of the QKV output (rows of (H + 2 Hk) Dh, boxes of Dh x 16); ws.counters holds
-// max_counters split tickets followed by 2 work-list words, all zero between launches
+// qkv: the QKV projection's fp32 output; ws.counters holds max_counters split tickets, zero between launches
 cudaError_t attention(const float* qkv, int M, int n_seq, int max_q_len, int max_kv, int H, int Hk, int Dh,
-                      const SeqInfo& seqs, const float2* rope, const KVLayout& kv, const CUtensorMap& tmkv,
-                      const CUtensorMap& tmq, int layer, const AttnWorkspace& ws, __nv_bfloat16* out, cudaStream_t st);
+                      const SeqInfo& seqs, const float2* rope, const KVLayout& kv, const CUtensorMap& tmkv, int layer,
+                      const AttnWorkspace& ws, __nv_bfloat16* out, cudaStream_t st);
 
 // ------------------------------------------------------------------ K4 / K1 sampler / K5
 struct VerifyArgs {

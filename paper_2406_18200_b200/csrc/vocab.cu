@@ -10,27 +10,17 @@
 //       acceptance (bonus, R1); ties to the smallest id (R14)                 (R3)
 // Every decision is taken in fp64 after the exact fp32 front end, exactly as the oracle takes
 // it (DESIGN "decision precision"), so accepted lengths and token ids match bit for bit.
-#include <cooperative_groups.h>
-
 #include <algorithm>
 
 #include "common.cuh"
 #include "kernels.h"
 #include "philox.cuh"
 
-namespace cg = cooperative_groups;
-
 namespace seed {
 
 namespace {
-constexpr int CS = 8;         // CTAs per cluster (portable maximum)
-constexpr int VT = 512;       // threads per CTA
-
-struct Stat {  // log-softmax running statistic over a set of indices
-  double m;    // max of a (as fp64)
-  double S;    // sum over the set minus the argmax of exp(a - m)
-  int i;       // first argmax (-1: empty)
-};
+constexpr int CS = 8;         // CTAs per cluster (portable maximum): CTA r holds vocabulary slice r
+constexpr int VT = 256;       // threads per CTA
 
 struct MaxI {   // fp32 maximum and its first index (-1: empty)
   float m;
@@ -51,9 +41,13 @@ __device__ __forceinline__ Best best_merge(Best A, Best B) {
   if (A.v < 0) return B;
   return (B.k > A.k || (B.k == A.k && B.v < A.v)) ? B : A;
 }
-__device__ __forceinline__ Best best_shfl(const Best& b, int o) {
-  return Best{__shfl_xor_sync(0xffffffffu, b.k, o), __shfl_xor_sync(0xffffffffu, b.v, o)};
-}
+
+// a CTA's partial log-softmax statistic of one row slice, exchanged through distributed shared memory
+struct SliceStat {
+  double S;    // sum over the slice minus its own argmax of exp(a_v - m) (fp32 terms, fp64 sum)
+  float m;     // slice maximum of a
+  int i;       // its first index (-1: empty slice)
+};
 
 // block-wide deterministic reductions (warp butterflies, then warps in order)
 __device__ MaxI block_maxi(MaxI s, MaxI* red) {
@@ -65,6 +59,7 @@ __device__ MaxI block_maxi(MaxI s, MaxI* red) {
   if ((threadIdx.x & 31) == 0) red[w] = s;
   __syncthreads();
   MaxI r = red[0];
+#pragma unroll
   for (int i = 1; i < VT / 32; ++i) r = maxi_merge(r, red[i]);
   return r;
 }
@@ -76,17 +71,31 @@ __device__ double block_sum(double s, double* red) {
   if ((threadIdx.x & 31) == 0) red[w] = s;
   __syncthreads();
   double r = red[0];
+#pragma unroll
   for (int i = 1; i < VT / 32; ++i) r += red[i];
+  return r;
+}
+__device__ float block_maxf(float v, float* red) {
+  v = warp_max(v);
+  const int w = threadIdx.x >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  float r = red[0];
+#pragma unroll
+  for (int i = 1; i < VT / 32; ++i) r = fmaxf(r, red[i]);
   return r;
 }
 __device__ Best block_best(Best b, Best* red) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) b = best_merge(b, best_shfl(b, o));
+  for (int o = 16; o > 0; o >>= 1)
+    b = best_merge(b, Best{__shfl_xor_sync(0xffffffffu, b.k, o), __shfl_xor_sync(0xffffffffu, b.v, o)});
   const int w = threadIdx.x >> 5;
   __syncthreads();
   if ((threadIdx.x & 31) == 0) red[w] = b;
   __syncthreads();
   Best r = red[0];
+#pragma unroll
   for (int i = 1; i < VT / 32; ++i) r = best_merge(r, red[i]);
   return r;
 }
@@ -96,6 +105,14 @@ __device__ __forceinline__ float scaled_v(float z, float T) { return T == 1.0f ?
 
 // -log(E), E = -log1p(-u): the exponential-race offset, fp64
 __device__ __forceinline__ double neg_log_exp(double u) { return -log(-log1p(-u)); }
+
+// -log(E) for the fp32 screen: absolute error ~1e-6, far inside RACE_MARGIN (the rescoring is
+// exact).  E keeps full relative precision for small u (log1pf), 1 - u is exact in fp32 on the odd
+// 2^-24 grid (R2), and the logarithms run on the SFU.
+__device__ __forceinline__ float neg_log_exp_screen(float u) {
+  const float E = u < 0.25f ? -log1pf(-u) : -__logf(1.0f - u);
+  return -__logf(E);
+}
 
 // Stage rows of this CTA's vocabulary slice into shared memory: one bulk TMA copy per row
 // when the slice is 16-byte aligned, coalesced loads otherwise.  All threads call it.
@@ -107,7 +124,10 @@ struct Stager {
   bool bulk;
   template <class RowPtr>
   __device__ void stage(int first, int k, RowPtr rowptr) {
-    if (n <= 0) return;
+    if (n <= 0) {
+      __syncthreads();
+      return;
+    }
     if (bulk) {
       if (threadIdx.x == 0) {
         mbar_arrive_expect_tx(bar, (uint32_t)(k * n * 4));
@@ -125,37 +145,58 @@ struct Stager {
   }
 };
 
-
-__device__ __forceinline__ Best cluster_best(cg::cluster_group& cluster, Best* cta_best, Best mine) {
-  if (threadIdx.x == 0) *cta_best = mine;
-  cluster.sync();
-  Best acc = *cluster.map_shared_rank(cta_best, 0);
-  for (int c = 1; c < CS; ++c) acc = best_merge(acc, *cluster.map_shared_rank(cta_best, c));
-  // every peer has read cta_best (the values are consumed above) before it may change:
-  // execution order only, no GPU-scope fence
-  cluster_sync_relaxed();
-  return acc;
+// This CTA's slice statistic of the staged row zs: fp32 maximum and first argmax, then
+// S'_c = sum over the slice minus the argmax of exp(a_v - m_c), fp32 terms summed in fp64 in a
+// fixed thread / warp order (R13, R21).
+__device__ SliceStat slice_stat(const float* zs, int v0, int n, float T, MaxI* red_m, double* red_d) {
+  MaxI mi{-INFINITY, -1};
+  for (int l = threadIdx.x; l < n; l += VT) {
+    const float xf = scaled_v(zs[l], T);
+    if (mi.i < 0 || xf > mi.m) mi = MaxI{xf, v0 + l};
+  }
+  mi = block_maxi(mi, red_m);
+  double S = 0.0;
+  if (mi.i >= 0)
+    for (int l = threadIdx.x; l < n; l += VT)
+      if (v0 + l != mi.i) S += (double)expf(scaled_v(zs[l], T) - mi.m);
+  S = block_sum(S, red_d);
+  return SliceStat{S, mi.m, mi.i};
 }
 
+// The row's statistic from the CS slice statistics (rank order): m = max, i* = its first index,
+// S' = sum_c S'_c e^{m_c - m} + sum_{c != c*} e^{m_c - m}  -- every slice's own maximum re-enters
+// except the global argmax (the tail-excluded log-sum-exp of R13, merged in fp64).
+struct RowStat {
+  double m, l1p;   // m and log1p(S')
+};
+__device__ RowStat merge_stats(const SliceStat* st) {
+  int cs = -1;
+  for (int c = 0; c < CS; ++c) {
+    if (st[c].i < 0) continue;
+    if (cs < 0 || st[c].m > st[cs].m || (st[c].m == st[cs].m && st[c].i < st[cs].i)) cs = c;
+  }
+  const double m = st[cs].m;
+  double S = 0.0;
+  for (int c = 0; c < CS; ++c) {
+    if (st[c].i < 0) continue;
+    const double f = c == cs ? 1.0 : exp((double)st[c].m - m);
+    S += st[c].S * f;
+    if (c != cs) S += f;
+  }
+  return RowStat{m, log1p(S)};
+}
 
-// Exponential race over this CTA's slice, decided exactly as in fp64 (R21): pass A scores every
-// id in fp32 (w32 returns NAN where fp32 is not accurate enough; those ids are scored in fp64),
-// the cluster agrees on the best fp32 key; pass B rescoring in fp64 every id within RACE_MARGIN
-// of it (>= 100x the fp32 error bound) and takes the exact argmax, ties to the smallest id.
+// Exponential race over this CTA's slice, decided exactly as in fp64 (R21).  Pass A scores every id
+// in fp32 (w32 returns NAN where fp32 is not accurate enough: those are scored in fp64); pass B
+// rescores in fp64 every id within RACE_MARGIN of the SLICE's best fp32 key and keeps the exact
+// slice argmax.  The global exact argmax is within the margin of its own slice's best (the slice
+// best is at most the global best), so the maximum of the CS slice results is the exact argmax --
+// one exchange, ties to the smallest id (R14).
 constexpr float RACE_MARGIN = 1e-3f;
 
-// -log(E), E = -log1p(-u), for the fp32 screen (pass A): absolute error ~1e-6, far inside
-// RACE_MARGIN (pass B rescoring is exact).  E keeps full relative precision for small u (log1pf),
-// 1 - u is exact in fp32 on the odd 2^-24 grid (R2), and the logarithms run on the SFU.
-__device__ __forceinline__ float neg_log_exp_screen(float u) {
-  const float E = u < 0.25f ? -log1pf(-u) : -__logf(1.0f - u);
-  return -__logf(E);
-}
-
 template <class W32, class W64>
-__device__ Best race_exact(cg::cluster_group& cluster, int v0, int n, uint32_t c1, uint32_t r, uint32_t sid,
-                           uint32_t k0, uint32_t k1, float* keys, float* red_f, float* cta_f, Best* red_b,
-                           Best* cta_best, W32 w32, W64 w64) {
+__device__ Best race_slice(int v0, int n, uint32_t c1, uint32_t r, uint32_t sid, uint32_t k0, uint32_t k1, float* keys,
+                           float* red_f, Best* red_b, W32 w32, W64 w64) {
   float best32 = -INFINITY;
   for (int l = 4 * (int)threadIdx.x; l < n; l += 4 * VT) {
     const int g = v0 + l;
@@ -176,22 +217,10 @@ __device__ Best race_exact(cg::cluster_group& cluster, int v0, int n, uint32_t c
       best32 = fmaxf(best32, key);
     }
   }
-  // cluster-wide max of the fp32 keys
-  best32 = warp_max(best32);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red_f[threadIdx.x >> 5] = best32;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float m = red_f[0];
-    for (int i = 1; i < VT / 32; ++i) m = fmaxf(m, red_f[i]);
-    *cta_f = m;
-  }
-  cluster.sync();
-  float gmax = -INFINITY;
-  for (int c = 0; c < CS; ++c) gmax = fmaxf(gmax, *cluster.map_shared_rank(cta_f, c));
+  const float lmax = block_maxf(best32, red_f);
   Best b{-INFINITY, -1};
-  if (gmax != -INFINITY) {
-    const float thr = gmax - RACE_MARGIN;
+  if (lmax != -INFINITY) {
+    const float thr = lmax - RACE_MARGIN;
     for (int l = threadIdx.x; l < n; l += VT) {
       if (keys[l] < thr) continue;
       const int g = v0 + l;
@@ -203,8 +232,7 @@ __device__ Best race_exact(cg::cluster_group& cluster, int v0, int n, uint32_t c
       if (b.v < 0 || key > b.k || (key == b.k && g < b.v)) b = Best{key, g};
     }
   }
-  b = block_best(b, red_b);
-  return cluster_best(cluster, cta_best, b);
+  return block_best(b, red_b);
 }
 
 // Work area of K4 per launch (vocab_verify_work_bytes): tickets int32 [B] (zero between launches, the
@@ -225,28 +253,25 @@ __host__ __device__ inline K4Work k4_work(void* base, int B, int g) {
 }
 
 // K4, two phases in one launch.  Phase 1: one 8-CTA cluster per (stream b, position j = 0..gamma)
-// computes the log-softmax statistics of target row j and draft row j (R13) and the accept decision
-// for x_{j+1} (j < gamma), and publishes them.  Phase 2: the stream's last cluster to
-// finish (ticket) counts the leading accepts a and runs the ONE race Alg. 1 needs: the residual
-// race over norm(max(0, p_{a+1} - q_{a+1})) (a < gamma, slot a + 1; R3) or the bonus race over
-// p_{gamma+1} (a = gamma, R1) -- staging rows a again if they are not its own -- then emits
-// x_1..x_a, y.  The same decisions, counters and races as the sequential Alg. 1.
+// computes the log-softmax statistics of target row j and draft row j (R13) -- every CTA pushes its
+// slice statistics into every peer's shared memory, one cluster barrier, every CTA merges them --
+// and the accept decision for x_{j+1} (j < gamma), and publishes them.  Phase 2: the
+// stream's last cluster to finish (ticket) counts the leading accepts a and runs the ONE race Alg. 1
+// needs: the residual race over norm(max(0, p_{a+1} - q_{a+1})) (a < gamma, slot a + 1; R3) or the
+// bonus race over p_{gamma+1} (a = gamma, R1) -- staging rows a again if they are not its own -- then
+// emits x_1..x_a, y.  The same decisions, counters and races as the sequential Alg. 1.
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(VT)
 vocab_verify_kernel(VerifyArgs A) {
   extern __shared__ __align__(128) float rows_s[];  // [2][slice] target / draft row, [slice] race keys
   __shared__ float red_f[VT / 32];
-  __shared__ float cta_f;
   __shared__ MaxI red_m[VT / 32];
   __shared__ double red_d[VT / 32];
   __shared__ Best red_b[VT / 32];
-  __shared__ MaxI cta_max[2];
-  __shared__ double cta_sum[2];
-  __shared__ Stat glob[2];
-  __shared__ Best cta_best;
-  __shared__ int last_s;
+  __shared__ SliceStat xst[2][CS];   // the cluster's slice statistics (pushed by every rank)
+  __shared__ Best xbest[CS];         // the race's slice winners (pushed to rank 0)
+  __shared__ int last_s, a_s;
   __shared__ __align__(8) uint64_t bar;
-  cg::cluster_group cluster = cg::this_cluster();
-  const int rank = (int)cluster.block_rank();
+  const int rank = (int)cluster_ctarank();
   const int g = A.gamma, V = A.V;
   const int cid = blockIdx.x / CS;
   const int b = cid / (g + 1), j = cid % (g + 1);
@@ -271,71 +296,41 @@ vocab_verify_kernel(VerifyArgs A) {
   float* keys_s = rows_s + (size_t)2 * slice;
   sg.stage(0, nrows, [&](int row) -> const float* { return row == 0 ? zt + (size_t)j * V : zd + (size_t)j * V; });
 
-  // ---- phase 1: statistics, two passes per row: (a) fp32 maximum and its first index, merged over
-  // the cluster in rank order; (b) S' = sum over v != argmax of exp(a_v - m), fp32 terms summed in
-  // fp64 in a fixed thread / warp / rank order (R13, R21) -- no rescaling, no fp64 exponentials
-  for (int i = 0; i < nrows; ++i) {
-    const float* zs = rows_s + (size_t)i * slice;
-    MaxI mi{-INFINITY, -1};
-    for (int l = threadIdx.x; l < n; l += VT) {
-      const float xf = scaled_v(zs[l], A.T);
-      if (mi.i < 0 || xf > mi.m) mi = MaxI{xf, v0 + l};
-    }
-    mi = block_maxi(mi, red_m);
-    if (threadIdx.x == 0) cta_max[i] = mi;
+  // ---- phase 1: slice statistics of both rows, pushed to every rank, one cluster barrier
+  SliceStat my[2];
+  for (int i = 0; i < nrows; ++i) my[i] = slice_stat(rows_s + (size_t)i * slice, v0, n, A.T, red_m, red_d);
+  if (threadIdx.x < nrows * CS) {
+    const int i = threadIdx.x / CS, c = threadIdx.x % CS;
+    const SliceStat v = my[i];
+    const uint32_t dst = dsmem_addr(&xst[i][rank], (uint32_t)c);
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(dst), "d"(v.S) : "memory");
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(dst + 8), "f"(v.m) : "memory");
+    asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(dst + 12), "r"(v.i) : "memory");
   }
-  cluster.sync();
-  if (threadIdx.x < nrows) {
-    MaxI acc = *cluster.map_shared_rank(&cta_max[threadIdx.x], 0);
-    for (int c = 1; c < CS; ++c) acc = maxi_merge(acc, *cluster.map_shared_rank(&cta_max[threadIdx.x], c));
-    glob[threadIdx.x] = Stat{(double)acc.m, 0.0, acc.i};
-  }
-  __syncthreads();
-  for (int i = 0; i < nrows; ++i) {
-    const float* zs = rows_s + (size_t)i * slice;
-    const float m = (float)glob[i].m;
-    const int im = glob[i].i;
-    double S = 0.0;
-    if (im >= 0)
-      for (int l = threadIdx.x; l < n; l += VT)
-        if (v0 + l != im) S += (double)expf(scaled_v(zs[l], A.T) - m);
-    S = block_sum(S, red_d);
-    if (threadIdx.x == 0) cta_sum[i] = S;
-  }
-  cluster.sync();
-  if (threadIdx.x < nrows) {
-    double acc = *cluster.map_shared_rank(&cta_sum[threadIdx.x], 0);
-    for (int c = 1; c < CS; ++c) acc += *cluster.map_shared_rank(&cta_sum[threadIdx.x], c);
-    glob[threadIdx.x].S = acc;
-  }
-  cluster.sync();   // peers have read cta_max / cta_sum; glob visible to the CTA
-  const Stat st = glob[0];
-  const double l1t = log1p(st.S);
+  cluster_sync();
+  const RowStat st = merge_stats(xst[0]);
 
   double* stt = W.stats + (size_t)b * (2 * g + 1) * 2;
   if (rank == 0 && threadIdx.x == 0) {
-    int accept = 0;
     stt[2 * j] = st.m;
-    stt[2 * j + 1] = l1t;
+    stt[2 * j + 1] = st.l1p;
     if (has_d) {
       // accept decision for x_{j+1}: u < min(1, p / q) in log space (R2, R13)
-      const Stat sq = glob[1];
-      const double l1q = log1p(sq.S);
+      const RowStat sq = merge_stats(xst[1]);
       stt[2 * (g + 1 + j)] = sq.m;
-      stt[2 * (g + 1 + j) + 1] = l1q;
+      stt[2 * (g + 1 + j) + 1] = sq.l1p;
       const int x = A.xs[(size_t)b * g + j];
       double lp = -INFINITY, lq = 0.0, rho = 0.0;
       if (x >= 0 && x < V) {
-        lp = ((double)scaled_v(__ldg(zt + (size_t)j * V + x), A.T) - st.m) - l1t;
-        lq = ((double)scaled_v(__ldg(zd + (size_t)j * V + x), A.T) - sq.m) - l1q;
+        lp = ((double)scaled_v(__ldg(zt + (size_t)j * V + x), A.T) - st.m) - st.l1p;
+        lq = ((double)scaled_v(__ldg(zd + (size_t)j * V + x), A.T) - sq.m) - sq.l1p;
         rho = exp(fmin(0.0, lp - lq));
       } else if (A.err) {
         atomicOr(&A.err[0], 1);   // contract violation: a drafted id outside the vocabulary is rejected
       }
       const Philox4 ph = philox4x32_10(0u, (kTagAccept << 24) | (uint32_t)(j + 1), rr, sid, A.k0, A.k1);
       const double u = philox_uniform(ph.x);
-      accept = u < rho ? 1 : 0;
-      W.acc[(size_t)b * g + j] = accept;
+      W.acc[(size_t)b * g + j] = u < rho ? 1 : 0;
       if (A.dbg) {
         float* d = A.dbg + ((size_t)b * g + j) * 4;
         d[0] = (float)lp;
@@ -343,34 +338,33 @@ vocab_verify_kernel(VerifyArgs A) {
         d[2] = (float)u;
         d[3] = (float)rho;
       }
+      if (A.stats) {
+        A.stats[((size_t)b * (2 * g + 1) + g + 1 + j) * 2] = sq.m;
+        A.stats[((size_t)b * (2 * g + 1) + g + 1 + j) * 2 + 1] = sq.l1p;
+      }
     }
     if (A.stats) {
       A.stats[((size_t)b * (2 * g + 1) + j) * 2] = st.m;
-      A.stats[((size_t)b * (2 * g + 1) + j) * 2 + 1] = l1t;
-      if (has_d) {
-        A.stats[((size_t)b * (2 * g + 1) + g + 1 + j) * 2] = glob[1].m;
-        A.stats[((size_t)b * (2 * g + 1) + g + 1 + j) * 2 + 1] = log1p(glob[1].S);
-      }
+      A.stats[((size_t)b * (2 * g + 1) + j) * 2 + 1] = st.l1p;
     }
-    // publish; the stream's last cluster runs phase 2
+    // publish; the stream's last cluster runs phase 2 (the flag goes to every rank's shared memory)
     fence_acq_rel_gpu();
     const int t = atomicAdd(&W.ticket[b], 1);
     if (t == g) {
       fence_acq_rel_gpu();   // acquire every cluster's flags and statistics
       W.ticket[b] = 0;       // ready for the next launch (graph replay)
     }
-    last_s = t == g ? 1 : 0;
+    for (int c = 0; c < CS; ++c)
+      asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(dsmem_addr(&last_s, (uint32_t)c)), "r"(t == g ? 1 : 0)
+                   : "memory");
   }
-  cluster.sync();
-  const int last = *cluster.map_shared_rank(&last_s, 0);
-  if (!last) {
-    cluster_sync_relaxed();  // keep shared memory alive until every peer has read it
+  cluster_sync();   // the flag has landed; every peer is done reading xst
+  if (!last_s) {
     rec_end(A.timing, 3);
     return;
   }
 
   // ---- phase 2 (the stream's last cluster): a, then the one race Alg. 1 needs
-  __shared__ int a_s;
   if (threadIdx.x == 0) {
     const volatile int32_t* acc = W.acc + (size_t)b * g;
     int a = 0;
@@ -388,17 +382,26 @@ vocab_verify_kernel(VerifyArgs A) {
       // generic reads of phase 1 are ordered before the bulk copies overwrite the buffers
       if (threadIdx.x == 0) fence_proxy_async();
       sg.stage(0, res ? 2 : 1, [&](int i) -> const float* { return i == 0 ? zt + (size_t)row * V : zd + (size_t)row * V; });
-    } else {
-      __syncthreads();
     }
     const volatile double* sv = W.stats + (size_t)b * (2 * g + 1) * 2;
-    const double mt = sv[2 * row], l1t_r = sv[2 * row + 1];
-    const float mtf = (float)mt, l1tf = (float)l1t_r;
+    const double mt = sv[2 * row], l1t = sv[2 * row + 1];
+    const float mtf = (float)mt, l1tf = (float)l1t;
     const float* zt_s = rows_s;
     const float* zd_s = rows_s + slice;
     const uint32_t c1 = (kTagResample << 24) | (uint32_t)(row + 1);
     auto bonus32 = [&](int l) -> float { return scaled_v(zt_s[l], A.T); };
     auto bonus64 = [&](int l) -> double { return (double)scaled_v(zt_s[l], A.T); };
+    auto exchange = [&](Best mine) -> Best {   // slice winners to every rank, one barrier, merged by each
+      if (threadIdx.x < CS) {
+        const uint32_t dst = dsmem_addr(&xbest[rank], (uint32_t)threadIdx.x);
+        asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(dst), "d"(mine.k) : "memory");
+        asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(dst + 8), "r"(mine.v) : "memory");
+      }
+      cluster_sync();
+      Best r{-INFINITY, -1};
+      for (int c = 0; c < CS; ++c) r = best_merge(r, xbest[c]);
+      return r;
+    };
     if (res) {
       const double mq = sv[2 * (g + 1 + row)], l1q = sv[2 * (g + 1 + row) + 1];
       const float mqf = (float)mq, l1qf = (float)l1q;
@@ -410,19 +413,21 @@ vocab_verify_kernel(VerifyArgs A) {
         return lp + __logf(1.0f - __expf(dlt));                    // screen only (pass B is exact)
       };
       auto res64 = [&](int l) -> double {
-        const double lp = ((double)scaled_v(zt_s[l], A.T) - mt) - l1t_r;
+        const double lp = ((double)scaled_v(zt_s[l], A.T) - mt) - l1t;
         const double lq = ((double)scaled_v(zd_s[l], A.T) - mq) - l1q;
         return lq < lp ? lp + log(-expm1(lq - lp)) : -INFINITY;
       };
-      y = race_exact(cluster, v0, n, c1, rr, sid, A.k0, A.k1, keys_s, red_f, &cta_f, red_b, &cta_best, res32, res64).v;
-      if (y < 0) {  // empty residual (rounding only): bonus rule on the same row, same uniforms
-        y = race_exact(cluster, v0, n, c1, rr, sid, A.k0, A.k1, keys_s, red_f, &cta_f, red_b, &cta_best, bonus32,
-                       bonus64).v;
+      y = exchange(race_slice(v0, n, c1, rr, sid, A.k0, A.k1, keys_s, red_f, red_b, res32, res64)).v;
+      // empty residual (rounding only): bonus rule on the same row, same uniforms (every rank merged
+      // the same winners, so the decision is uniform); the slice winners are rewritten only after
+      // every rank has read them
+      if (y < 0) {
+        cluster_sync_relaxed();
+        y = exchange(race_slice(v0, n, c1, rr, sid, A.k0, A.k1, keys_s, red_f, red_b, bonus32, bonus64)).v;
         if (A.err && rank == 0 && threadIdx.x == 0) atomicAdd(&A.err[1], 1);
       }
     } else {
-      y = race_exact(cluster, v0, n, c1, rr, sid, A.k0, A.k1, keys_s, red_f, &cta_f, red_b, &cta_best, bonus32,
-                     bonus64).v;
+      y = exchange(race_slice(v0, n, c1, rr, sid, A.k0, A.k1, keys_s, red_f, red_b, bonus32, bonus64)).v;
     }
   }
   if (rank == 0 && threadIdx.x == 0) {
@@ -435,23 +440,20 @@ vocab_verify_kernel(VerifyArgs A) {
     if (A.out_cnt) A.out_cnt[b] = cnt;
     if (A.out_acc) A.out_acc[b] = a;
   }
-  cluster_sync_relaxed();  // keep shared memory alive until every peer has read it (execution order)
   rec_end(A.timing, 3);
 }
 
-// K1 sampler: one cluster per row
+// K1 sampler: one cluster per row; slice winners pushed to rank 0, one barrier
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(VT)
 draft_sample_kernel(const float* z, long ld, int V, float T, uint32_t k0, uint32_t k1, const uint32_t* sids,
                     const int32_t* rs, int j, int32_t* out, int out_stride, int32_t* out2, int out2_stride,
                     int32_t* err, unsigned long long* rec) {
   extern __shared__ __align__(128) float rows_s[];  // [slice] row, then [slice] race keys
   __shared__ float red_f[VT / 32];
-  __shared__ float cta_f;
   __shared__ Best red_b[VT / 32];
-  __shared__ Best cta_best;
+  __shared__ Best xbest[CS];
   __shared__ __align__(8) uint64_t bar;
-  cg::cluster_group cluster = cg::this_cluster();
-  const int rank = (int)cluster.block_rank();
+  const int rank = (int)cluster_ctarank();
   const int b = blockIdx.x / CS;
   const int slice = ((V + CS - 1) / CS + 3) & ~3;
   const int v0 = min(V, rank * slice), n = min(V, v0 + slice) - v0;
@@ -469,9 +471,17 @@ draft_sample_kernel(const float* z, long ld, int V, float T, uint32_t k0, uint32
   sg.stage(0, 1, [&](int) { return zr; });
   auto w32 = [&](int l) -> float { return scaled_v(rows_s[l], T); };
   auto w64 = [&](int l) -> double { return (double)scaled_v(rows_s[l], T); };
-  const Best acc = race_exact(cluster, v0, n, (kTagDraft << 24) | (uint32_t)j, (uint32_t)rs[b], sids[b], k0, k1,
-                              rows_s + slice, red_f, &cta_f, red_b, &cta_best, w32, w64);
+  const Best mine = race_slice(v0, n, (kTagDraft << 24) | (uint32_t)j, (uint32_t)rs[b], sids[b], k0, k1, rows_s + slice,
+                               red_f, red_b, w32, w64);
+  if (threadIdx.x == 0) {
+    const uint32_t dst = dsmem_addr(&xbest[rank], 0u);
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(dst), "d"(mine.k) : "memory");
+    asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(dst + 8), "r"(mine.v) : "memory");
+  }
+  cluster_sync();
   if (rank == 0 && threadIdx.x == 0) {
+    Best acc{-INFINITY, -1};
+    for (int c = 0; c < CS; ++c) acc = best_merge(acc, xbest[c]);
     out[(size_t)b * out_stride] = acc.v;
     if (out2) out2[(size_t)b * out2_stride] = acc.v;
     if (acc.v < 0 && err) atomicOr(err, 2);   // no finite key (non-finite logits)

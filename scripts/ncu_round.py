@@ -1,4 +1,4 @@
-"""One GSM8K-shape round bracketed by cudaProfilerStart/Stop, for `ncu --profile-from-start off`."""
+"""One round (CFG, default the sweep shape) bracketed by cudaProfilerStart/Stop, for `ncu --profile-from-start off`."""
 import os
 import sys
 
@@ -8,10 +8,10 @@ import torch
 import seedgen
 import paper_2406_18200_b200 as pkg
 
-CFG = os.environ.get("CFG", "gsm8k")
+CFG = os.environ.get("CFG", "sweep")
 cfg = seedgen.CONFIGS[CFG]
 ds, ts = seedgen.SHAPES[cfg["draft"]], seedgen.SHAPES[cfg["target"]]
-n, g = cfg["n_streams"], cfg["gamma"]
+n, g = int(os.environ.get("STREAMS", cfg["n_streams"])), cfg["gamma"]
 prompts = seedgen.prompts(CFG, n_streams=n)
 dW = seedgen.model_weights(ds, seedgen.DRAFT_SEED, device="cuda")
 tW = seedgen.model_weights(ts, seedgen.TARGET_SEED, device="cuda")

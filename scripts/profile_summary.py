@@ -1,7 +1,7 @@
 """Summarise the ncu evidence of scripts/profile_round.sh into profiles/<round>/ and
-profiles/ncu_traffic.json (read by bench.py for roofline.traffic).
+profiles/ncu_traffic.json (read by bench.py for roofline.traffic, keyed by config).
 
-    python scripts/profile_summary.py gpurun_out/prof profiles/r01
+    CFG=sweep python scripts/profile_summary.py gpurun_out/prof profiles/r02
 """
 import collections
 import csv
@@ -53,7 +53,7 @@ for n, v in tail:
     x[1] += v
 tot = sum(v for _, v in tail)
 unit = 1e3 if max(v for _, v in tail) > 1e3 else 1.0   # ns -> us when ncu printed ns
-lines.append("## Launch list (`--metrics gpu__time_duration.sum --clock-control none`, bench.py --steps 2 --warmup 3)\n")
+lines.append("## Launch list (`--metrics gpu__time_duration.sum --clock-control none`, bench.py --steps 2 --warmup 3 --no-cpu-baseline)\n")
 lines.append("Cold-cache, serialised per-launch times (no PDL overlap), last two rounds, per round:\n")
 lines.append("| kernel | launches | us / round | avg us | share |\n|---|---|---|---|---|")
 for k, (c, v) in sorted(agg.items(), key=lambda x: -x[1][1]):
@@ -88,14 +88,18 @@ if bench:
     alg = bench["roofline"]["bytes_per_launch"]
     lines.append(f"\nK2 (gemm_splitk) over the round's {len(gem)} launches: DRAM {avg_tr/1e6:.2f} MB per launch vs "
                  f"{alg/1e6:.2f} MB algorithmic (ratio {avg_tr/alg:.3f}).\n")
-json.dump({"k2_gemm": avg_tr, "source": f"{dst}/summary.md: ncu dram__bytes_read.sum + dram__bytes_write.sum, "
-           f"mean over the {len(gem)} GEMM launches of one GSM8K round"},
-          open(os.path.join(os.path.dirname(dst.rstrip('/')), "ncu_traffic.json"), "w"), indent=1)
+tpath = os.path.join(os.path.dirname(dst.rstrip('/')), "ncu_traffic.json")
+traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
+traffic = {k: v for k, v in traffic.items() if isinstance(v, dict)}
+cfgname = os.environ.get("CFG", "sweep")
+traffic[cfgname] = {"k2_gemm": avg_tr, "source": f"{dst}/summary.md: ncu dram__bytes_read.sum + dram__bytes_write.sum, "
+                    f"mean over the {len(gem)} GEMM launches of one {cfgname} round"}
+json.dump(traffic, open(tpath, "w"), indent=1)
 
 # ---- full captures
-for rep, what in (("gemm_gu_l1", "verify gate/up GEMM, layer 1"), ("attn_l1", "verify attention, layer 1"),
-                  ("gemm_o_l1_sweep", "verify O GEMM, layer 1, N = 24 streams (M = 120)"),
-                  ("attn_l1_sweep", "verify attention, layer 1, N = 24 streams")):
+for rep, what in (("gemm_gu_l1", "verify gate/up GEMM, layer 1"), ("gemm_qkv_l1", "verify QKV GEMM, layer 1"),
+                  ("gemm_o_l1", "verify O GEMM, layer 1"), ("attn_l1", "verify attention, layer 1"),
+                  ("k4", "K4 vocab_verify_kernel"), ("k1", "K1 draft_sample_kernel (draft step 2)")):
     p = os.path.join(src, rep + ".ncu-rep")
     if not os.path.exists(p):
         continue
@@ -107,7 +111,8 @@ for rep, what in (("gemm_gu_l1", "verify gate/up GEMM, layer 1"), ("attn_l1", "v
             "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
             "launch__shared_mem_per_block_dynamic", "smsp__inst_executed.sum", "lts__t_sector_hit_rate.pct",
             "launch__cluster_size", "launch__occupancy_limit_shared_mem", "launch__occupancy_limit_registers",
-            "sm__warps_active.avg.pct_of_peak_sustained_active"]
+            "sm__warps_active.avg.pct_of_peak_sustained_active", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+            "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"]
     lines.append(f"## Full capture: {what} (`--set full --clock-control none`)\n")
     lines.append("| metric | value |\n|---|---|")
     for w in want:

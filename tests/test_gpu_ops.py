@@ -44,7 +44,8 @@ def test_philox_kat_and_oracle(ops):
 
 @pytest.mark.parametrize("N,K,M", [(128, 64, 1), (192, 128, 15), (32, 128, 3), (300, 256, 37), (4096, 4096, 15),
                                    (12288, 4096, 120), (4096, 11008, 5), (2304, 768, 48), (1000, 512, 256),
-                                   (640, 1024, 300), (32000, 768, 3), (5120, 5120, 72), (5120, 13824, 15)])
+                                   (640, 1024, 300), (32000, 768, 3), (5120, 5120, 72), (5120, 13824, 15),
+                                   (4096, 4096, 600), (12288, 4096, 960), (22016, 4096, 513)])
 def test_gemm_vs_fp64(ops, N, K, M):
     W = seedgen.bf16_matrix(N, K, seed=N * 7 + K).cuda()
     X = seedgen.bf16_matrix(M, K, seed=M * 13 + K + 1).cuda()
@@ -67,6 +68,12 @@ def test_gemm_batch_invariance(ops, N, K):
     for m in (15, 16, 64):
         assert torch.equal(Y120[:m], ops.gemm(W, X[:m].contiguous())), m
     assert torch.equal(Y120[7:8], ops.gemm(W, X[7:8].contiguous()))
+    # several 256-row token tiles: every row reduced in the same order as alone
+    X960 = seedgen.bf16_matrix(960, K, seed=3).cuda()
+    X960[:120] = X
+    Y960 = ops.gemm(W, X960)
+    assert torch.equal(Y960[:120], Y120)
+    assert torch.equal(Y960[700:701], ops.gemm(W, X960[700:701].contiguous()))
 
 
 def _oracle_xs(zd, T, sids, rs):

@@ -201,3 +201,15 @@ def test_round_api_state_rules(pkg):
     eng.add_stream(0, [3, 4, 5, 6])      # a removed id may be added again, from scratch
     assert eng.tokens(0) == []
     eng.close()
+
+
+@pytest.mark.parametrize("n", [48, 192])
+def test_teacher_forced_rounds_large_n(pkg, n):
+    """Scaling-sweep shape beyond one 256-row token tile (BASELINE configs[4], N up to 192 on one GPU):
+    the verify forward runs M = 5n rows in token tiles of 256 (weights streamed once per token tile,
+    L2-shared), draft step 1 runs 2n rows; decisions re-derived from the GPU's logits as above."""
+    eng, cfg, _ = _engine(pkg, "sweep", n=n, max_new=40)
+    decisions, flagged, compared = _teacher_forced_rounds(eng, cfg["gamma"], 1.0, 3)
+    eng.close()
+    assert compared > 0.9 * 3 * n
+    assert flagged <= max(1, 1e-5 * decisions)
