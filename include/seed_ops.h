@@ -45,6 +45,28 @@ SEED_API seed_status seed_op_draft_sample(const float* z, int32_t ld, int32_t B,
                                  uint64_t seed, const uint32_t* sids, const int32_t* rs, int32_t j,
                                  int32_t* out, void* stream);
 
+/* k_config trees (§3.2, App. B; SPEC.md S:90-134;
+ * DESIGN.md R36).  A tree of K = n_counts levels is laid out breadth-first: node 0 is the root (the
+ * context), each depth-(d-1) node has counts[d-1] children, children are contiguous.
+ *
+ * K1T: the children of node `node` for every row: the `m` largest keys of the exponential race
+ * over z [B][V] (row stride ld floats) with tag DRAFT, slot node + 1 -- m distinct ids drawn without
+ * replacement from softmax(fl32(z / T)), in draw order.  out: device int32, row b written at
+ * out[b * out_stride + first .. + m).  1 <= m <= 8. */
+SEED_API seed_status seed_op_draft_topk(const float* z, int32_t ld, int32_t B, int32_t V, float temperature,
+                                        uint64_t seed, const uint32_t* sids, const int32_t* rs, int32_t node,
+                                        int32_t m, int32_t* out, int32_t out_stride, int32_t first, void* stream);
+
+/* K4T: verification of a drafted tree by recursive rejection (DESIGN R36): zt, zd [B][n+1][V] fp32 --
+ * row i = the target / draft logits after node i's path (zd rows of leaves unused); tok [B][n+1]
+ * node tokens (tok[.][0] unused); counts_host [n_counts] the k_config (each 1..8, n_counts <= 15).
+ * out_tok [B][K+1]: the accepted path's tokens, then the correction or bonus token, -1 padding;
+ * out_cnt [B]; out_node [B][K] (optional): accepted node indices, -1 padding. */
+SEED_API seed_status seed_op_verify_tree(const float* zt, const float* zd, const int32_t* tok, int32_t B,
+                                         const int32_t* counts_host, int32_t n_counts, int32_t V, float temperature,
+                                         uint64_t seed, const uint32_t* sids, const int32_t* rs, int32_t bonus,
+                                         int32_t* out_tok, int32_t* out_cnt, int32_t* out_node, void* stream);
+
 /* One decoder layer of `shape` on hidden states (per-layer parity).
  * w: host array of the 9 device pointers of seed_model_weights.layers for one layer.
  * x_in/x_out: fp32 [M][d]; the M rows are q_len consecutive positions

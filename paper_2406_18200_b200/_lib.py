@@ -96,6 +96,10 @@ _SIGS = {
                        _P, _P, _P, _P, _P, _P],
     "seed_op_draft_sample": [_P, C.c_int32, C.c_int32, C.c_int32, C.c_float, C.c_uint64, _P, _P, C.c_int32, _P,
                              _P],
+    "seed_op_draft_topk": [_P, C.c_int32, C.c_int32, C.c_int32, C.c_float, C.c_uint64, _P, _P, C.c_int32, C.c_int32,
+                           _P, C.c_int32, C.c_int32, _P],
+    "seed_op_verify_tree": [_P, _P, _P, C.c_int32, _I32P, C.c_int32, C.c_int32, C.c_float, C.c_uint64, _P, _P,
+                            C.c_int32, _P, _P, _P, _P],
     "seed_op_decoder_layer": [C.POINTER(ModelShape), C.POINTER(C.c_void_p), _P, C.c_int32, C.c_int32, _P, _P, _P,
                               _P, _P, _P],
 }

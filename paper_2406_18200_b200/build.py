@@ -18,7 +18,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
           "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
 CU_FLAGS = ARCH + COMMON + ["-lineinfo", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
-SOURCES = ["gemm.cu", "epilogue.cu", "attention.cu", "vocab.cu", "engine.cu", "host_sched.cpp"]
+SOURCES = ["gemm.cu", "epilogue.cu", "attention.cu", "vocab.cu", "tree.cu", "engine.cu", "host_sched.cpp"]
 
 
 def _compile(src):

@@ -1555,6 +1555,55 @@ seed_status seed_op_draft_sample(const float* z, int32_t ld, int32_t B, int32_t 
              : SEED_ECUDA;
 }
 
+seed_status seed_op_draft_topk(const float* z, int32_t ld, int32_t B, int32_t V, float temperature, uint64_t seed,
+                               const uint32_t* sids, const int32_t* rs, int32_t node, int32_t m, int32_t* out,
+                               int32_t out_stride, int32_t first, void* stream) {
+  if (!z || B < 1 || V < 1 || !sids || !rs || !out || !(temperature > 0.f) || m < 1 || m > 8 || node < 0 || m > V)
+    return SEED_EINVAL;
+  return seed::draft_topk(z, ld, B, V, temperature, (uint32_t)(seed & 0xFFFFFFFFu), (uint32_t)(seed >> 32), sids, rs,
+                          node, m, out, out_stride, first, nullptr, 0, nullptr, (cudaStream_t)stream) == cudaSuccess
+             ? SEED_OK
+             : SEED_ECUDA;
+}
+
+seed_status seed_op_verify_tree(const float* zt, const float* zd, const int32_t* tok, int32_t B, const int32_t* counts,
+                                int32_t n_counts, int32_t V, float temperature, uint64_t seed, const uint32_t* sids,
+                                const int32_t* rs, int32_t bonus, int32_t* out_tok, int32_t* out_cnt, int32_t* out_node,
+                                void* stream) {
+  if (!zt || !zd || !tok || B < 1 || !counts || n_counts < 1 || n_counts > 15 || V < 1 || !(temperature > 0.f) ||
+      !sids || !rs || !out_tok || !out_cnt)
+    return SEED_EINVAL;
+  // breadth-first shape: children of every node contiguous
+  std::vector<int32_t> first(1, 0), cnt(1, 0);
+  std::vector<int> level{0};
+  for (int d = 0; d < n_counts; ++d) {
+    if (counts[d] < 1 || counts[d] > 8 || counts[d] > V) return SEED_EINVAL;
+    std::vector<int> nxt;
+    for (int p : level) {
+      first[p] = (int32_t)first.size();
+      cnt[p] = counts[d];
+      for (int i = 0; i < counts[d]; ++i) {
+        first.push_back(0);
+        cnt.push_back(0);
+        nxt.push_back((int)first.size() - 1);
+      }
+    }
+    level = nxt;
+  }
+  const int nn = (int)first.size();   // nodes incl. the root
+  cudaStream_t st = (cudaStream_t)stream;
+  int32_t* dev = nullptr;
+  if (cudaMallocAsync(&dev, (size_t)2 * nn * 4, st) != cudaSuccess) return SEED_ENOMEM;
+  bool ok = cudaMemcpyAsync(dev, first.data(), (size_t)nn * 4, cudaMemcpyHostToDevice, st) == cudaSuccess &&
+            cudaMemcpyAsync(dev + nn, cnt.data(), (size_t)nn * 4, cudaMemcpyHostToDevice, st) == cudaSuccess &&
+            seed::verify_tree(zt, (long)nn * V, zd, (long)nn * V, tok, nn, dev, dev + nn, B, n_counts, V, temperature,
+                              (uint32_t)(seed & 0xFFFFFFFFu), (uint32_t)(seed >> 32), sids, rs, bonus, out_tok, out_cnt,
+                              out_node, nullptr, st) == cudaSuccess;
+  ok &= cudaStreamSynchronize(st) == cudaSuccess;
+  cudaFree(dev);
+  return ok ? SEED_OK : SEED_ECUDA;
+}
+
 seed_status seed_op_decoder_layer(const seed_model_shape* shape, const void* const* w, const float* x_in, int32_t M,
                                   int32_t ctx_len, const void* k_prev, const void* v_prev, float* x_out, void* k_new,
                                   void* v_new, void* stream) {

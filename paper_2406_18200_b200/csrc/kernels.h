@@ -141,6 +141,15 @@ cudaError_t vocab_verify(const VerifyArgs& a, cudaStream_t st);
 cudaError_t draft_sample(const float* z, long ld, int B, int V, float T, uint32_t k0, uint32_t k1,
                          const uint32_t* sids, const int32_t* rs, int j, int32_t* out, int out_stride, int32_t* out2,
                          int out2_stride, int32_t* err, cudaStream_t st, unsigned long long* timing = nullptr);
+// K1T / K4T (tree.cu): k_config tree drafting and verification (DESIGN R36)
+cudaError_t draft_topk(const float* z, long ld, int B, int V, float T, uint32_t k0, uint32_t k1, const uint32_t* sids,
+                       const int32_t* rs, int node, int m, int32_t* out, int out_stride, int first, int32_t* out2,
+                       int out2_stride, int32_t* err, cudaStream_t st, unsigned long long* timing = nullptr);
+cudaError_t verify_tree(const float* zt, long zt_stride_b, const float* zd, long zd_stride_b, const int32_t* tok,
+                        int tok_stride, const int32_t* ch_first, const int32_t* ch_cnt, int B, int K, int V, float T,
+                        uint32_t k0, uint32_t k1, const uint32_t* sids, const int32_t* rs, int bonus, int32_t* out_tok,
+                        int32_t* out_cnt, int32_t* out_node, int32_t* err, cudaStream_t st,
+                        unsigned long long* timing = nullptr);
 cudaError_t philox_fill(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1, int n,
                         uint32_t* out, cudaStream_t st);
 

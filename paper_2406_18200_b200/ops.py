@@ -80,3 +80,34 @@ def decoder_layer(shape, L, x_in, ctx_len, k_prev=None, v_prev=None):
                                             _p(k_prev), _p(v_prev), _p(x_out), _p(k_new), _p(v_new), _s()), None,
           "seed_op_decoder_layer")
     return x_out, k_new, v_new
+
+
+def draft_topk(z, temperature, seed, sids, rs, node, m):
+    """K1T: the m children of `node` for each row of z [B][V] fp32 CUDA -> int32 [B][m] (draw order)."""
+    B, V = z.shape
+    dev = z.device
+    sids_t = torch.as_tensor(np.asarray(sids, dtype=np.int64).astype(np.uint32).view(np.int32), device=dev)
+    rs_t = torch.as_tensor(np.asarray(rs, dtype=np.int32), device=dev)
+    out = torch.empty((B, m), dtype=torch.int32, device=dev)
+    check(_lib.load().seed_op_draft_topk(_p(z.contiguous()), V, B, V, float(temperature), int(seed), _p(sids_t),
+                                         _p(rs_t), int(node), int(m), _p(out), int(m), 0, _s()), None,
+          "seed_op_draft_topk")
+    return out
+
+
+def verify_tree(zt, zd, tok, counts, temperature, seed, sids, rs, bonus=True):
+    """K4T: zt, zd [B][n+1][V] fp32 CUDA, tok [B][n+1] int32 CUDA, counts = k_config."""
+    B, nn, V = zt.shape
+    K = len(counts)
+    dev = zt.device
+    sids_t = torch.as_tensor(np.asarray(sids, dtype=np.int64).astype(np.uint32).view(np.int32), device=dev)
+    rs_t = torch.as_tensor(np.asarray(rs, dtype=np.int32), device=dev)
+    c = np.ascontiguousarray(counts, dtype=np.int32)
+    out_tok = torch.empty((B, K + 1), dtype=torch.int32, device=dev)
+    out_cnt = torch.empty(B, dtype=torch.int32, device=dev)
+    out_node = torch.empty((B, K), dtype=torch.int32, device=dev)
+    check(_lib.load().seed_op_verify_tree(_p(zt.contiguous()), _p(zd.contiguous()), _p(tok.contiguous()), B,
+                                          c.ctypes.data_as(_lib._I32P), K, V, float(temperature), int(seed),
+                                          _p(sids_t), _p(rs_t), int(bool(bonus)), _p(out_tok), _p(out_cnt),
+                                          _p(out_node), _s()), None, "seed_op_verify_tree")
+    return {"out_tok": out_tok, "out_cnt": out_cnt, "out_node": out_node}
