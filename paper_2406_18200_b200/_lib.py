@@ -7,7 +7,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libseed.so")
+LIB_PATH = os.environ.get("SEED_LIB") or os.path.join(_HERE, "libseed.so")   # SEED_LIB: A/B builds
 
 SEED_OK = 0
 STATUS = {0: "SEED_OK", 1: "SEED_EINVAL", 2: "SEED_ENOMEM", 3: "SEED_ECUDA", 4: "SEED_ENCCL",

@@ -528,17 +528,18 @@ cudaError_t launch_dh(int M, int n_seq, int max_q_len, int max_kv, int H, int Hk
 }
 }  // namespace
 
-// keys per CTA: a fixed split grid, a function of the head size only (R19): 512 keys at Dh = 128
-// (the 7B / 13B targets: fewer, longer CTAs keep more bytes in flight at N = 24), 128 at Dh <= 64 (the
-// draft models: 12 heads leave few CTAs otherwise).  Env SEED_ATTN_SPLIT / SEED_ATTN_SPLIT_SMALL
-// (multiples of 16) for experiments.
+// keys per CTA: a fixed split grid, a function of the head size only (R19): 1024 keys at Dh = 128,
+// 512 below.  Fewer, longer CTAs keep more bytes in flight and merge less (measured per round: the
+// 68M draft at 128-key splits 5.29 ms -> 5.07 at 512 on the N = 24 sweep; the 7B / 13B targets at
+// 512 -> 1024: sweep 5.07 -> 5.03, 13B BW shape 10.33 -> 10.09; N = 3 / 5 unchanged).  Env
+// SEED_ATTN_SPLIT / SEED_ATTN_SPLIT_SMALL (Dh >= 128 / < 128, multiples of 16) for experiments.
 int attn_chunk_tokens(int Dh) {
   static int big = -1, small = -1;
   if (big < 0) {
     const char* e = getenv("SEED_ATTN_SPLIT");
-    big = e ? std::max(16, atoi(e) / 16 * 16) : 512;
+    big = e ? std::max(16, atoi(e) / 16 * 16) : 1024;
     const char* f = getenv("SEED_ATTN_SPLIT_SMALL");
-    small = f ? std::max(16, atoi(f) / 16 * 16) : 128;
+    small = f ? std::max(16, atoi(f) / 16 * 16) : 512;
   }
   return Dh >= 128 ? big : small;
 }

@@ -160,9 +160,16 @@ struct ChunkDesc {
 struct RoundPlan {  // descriptors of one round at batch-size-determined arena offsets
   int n = 0;
   int64_t key_draft = 0, key_verify = 0;  // graph keys: batch size and attention chunk counts
+  int dk_raw = 0, vk_raw = 0;             // longest draft / target context of the round (unrounded)
   size_t o_sid = 0, o_r = 0, o_sl = 0, o_last = 0, o_out = 0;  // o_out: undone own streams outside the batch
   std::vector<ChunkDesc> draft, verify;
   std::vector<int> verify_b0;
+};
+
+struct RoundGraphEntry {
+  cudaGraphExec_t exec = nullptr;
+  double gemm_bytes = 0;
+  int64_t gemms = 0, kernels = 0;
 };
 
 constexpr int kMaxChunkRows = 1024;   // rows per forward chunk (the GEMM runs token tiles of 256)
@@ -213,12 +220,7 @@ struct seed_ctx_s {
   bool use_graphs = true;
   cudaStream_t gstream = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
-  struct PhaseGraph {
-    cudaGraphExec_t exec = nullptr;
-    double gemm_bytes = 0;
-    int64_t gemms = 0, kernels = 0;
-  };
-  std::map<int64_t, PhaseGraph> round_graphs;   // draft + verify of a round, one graph (R23)
+  std::map<int64_t, RoundGraphEntry> round_graphs;   // draft + verify of a round, one graph (R23)
   bool draft_deferred = false;                   // seed_draft_round planned a round, not launched
   // profiling: per-GEMM globaltimer records accumulated on the device
   bool profile = false, in_round = false;
@@ -806,6 +808,8 @@ seed_status build_round_plan(seed_ctx ctx, const std::vector<int32_t>& ids, cons
   int dk = 0, vk = 0;
   for (auto& c : P.draft) dk = std::max(dk, c.max_kv);
   for (auto& c : P.verify) vk = std::max(vk, c.max_kv);
+  P.dk_raw = dk;
+  P.vk_raw = vk;
   dk = std::min(max_pos, (dk + chd - 1) / chd * chd);
   vk = std::min(max_pos, (vk + cht - 1) / cht * cht);
   for (auto& c : P.draft) c.max_kv = dk;
@@ -904,6 +908,76 @@ seed_status enqueue_verify(seed_ctx ctx, cudaStream_t st) {
   return SEED_OK;
 }
 
+// Captures and instantiates the round graph of the current plan (draft + verify phases).
+seed_status capture_round(seed_ctx ctx, int n, RoundGraphEntry& G) {
+  const int64_t k0 = ctx->kernel_launches;
+  cudaGraph_t graph;
+  CK(cudaStreamBeginCapture(ctx->gstream, cudaStreamCaptureModeThreadLocal));
+  ctx->in_round = true;
+  ctx->rec_used = 0;
+  ctx->round_gemm_bytes = 0;
+  ctx->round_gemms = 0;
+  seed_status s = enqueue_draft(ctx, ctx->gstream);
+  if (s == SEED_OK) {
+    ctx->draft_recs[n] = ctx->rec_used;
+    ctx->rec_used = ctx->rec_cap / 2;
+    s = enqueue_verify(ctx, ctx->gstream);
+  }
+  cudaError_t e = cudaStreamEndCapture(ctx->gstream, &graph);
+  if (s != SEED_OK) return s;
+  CK(e);
+  e = cudaGraphInstantiate(&G.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  CK(e);
+  G.kernels = ctx->kernel_launches - k0;
+  ctx->kernel_launches = k0;
+  G.gemm_bytes = ctx->round_gemm_bytes;
+  G.gemms = ctx->round_gemms;
+  return SEED_OK;
+}
+
+// A context crossing an attention split boundary needs the graph of the next chunk count (R23).
+// Each round adds at most gamma + 1 keys per stream, so when the round just launched could be
+// followed by one that crosses, that graph is captured and uploaded now, on the host, while the
+// device runs the round: the crossing round launches it like any other (no capture between rounds).
+seed_status precapture_next(seed_ctx ctx, int n, int64_t pbit) {
+  RoundPlan& P = ctx->plan;
+  if (n == 0 || getenv("SEED_NO_PRECAPTURE")) return SEED_OK;
+  const int g = ctx->cfg.gamma;
+  const int max_pos = ctx->cfg.max_ctx + g + 2;
+  const int chd = seed::attn_chunk_tokens(ctx->dm.Dh), cht = seed::attn_chunk_tokens(ctx->tm.Dh);
+  const int dk = std::min(max_pos, (P.dk_raw + g + 1 + chd - 1) / chd * chd);
+  const int vk = std::min(max_pos, (P.vk_raw + g + 1 + cht - 1) / cht * cht);
+  const int64_t kd = ((int64_t)n << 32) | (dk / chd), kv = ((int64_t)n << 32) | (vk / cht);
+  if (kd == P.key_draft && kv == P.key_verify) return SEED_OK;
+  const int64_t key = ((int64_t)n << 40) | ((kd & 0xFFFFF) << 20) | (kv & 0xFFFFF) | pbit;
+  auto& G = ctx->round_graphs[key];
+  if (G.exec) return SEED_OK;
+  // the plan with the next rounds' grids; everything else of a graph is a function of the batch size
+  std::vector<int> dsave, vsave;
+  for (auto& c : P.draft) dsave.push_back(c.max_kv), c.max_kv = dk;
+  for (auto& c : P.verify) vsave.push_back(c.max_kv), c.max_kv = vk;
+  const int64_t sd = P.key_draft, sv = P.key_verify;
+  const int ru = ctx->rec_used, dr = ctx->draft_recs[n];
+  const double gb = ctx->round_gemm_bytes;
+  const int64_t gl = ctx->round_gemms;
+  P.key_draft = kd;
+  P.key_verify = kv;
+  seed_status s = capture_round(ctx, n, G);
+  for (size_t i = 0; i < P.draft.size(); ++i) P.draft[i].max_kv = dsave[i];
+  for (size_t i = 0; i < P.verify.size(); ++i) P.verify[i].max_kv = vsave[i];
+  P.key_draft = sd;
+  P.key_verify = sv;
+  ctx->rec_used = ru;
+  ctx->draft_recs[n] = dr;
+  ctx->round_gemm_bytes = gb;
+  ctx->round_gemms = gl;
+  ctx->in_round = false;
+  if (s != SEED_OK) return s;
+  CK(cudaGraphUpload(G.exec, ctx->gstream));
+  return SEED_OK;
+}
+
 // Runs the draft (draft = true) or verify phase of the planned round: directly on the caller's
 // stream, or as a CUDA graph captured once per batch size on the library's stream.
 seed_status run_phase(seed_ctx ctx, int n, bool draft, cudaStream_t st) {
@@ -939,29 +1013,8 @@ seed_status run_phase(seed_ctx ctx, int n, bool draft, cudaStream_t st) {
   const int64_t pbit = ctx->profile ? (int64_t)1 << 62 : 0;
   const int64_t key = ((int64_t)n << 40) | ((ctx->plan.key_draft & 0xFFFFF) << 20) | (ctx->plan.key_verify & 0xFFFFF) | pbit;
   auto& G = ctx->round_graphs[key];
+  if (!G.exec && (s = capture_round(ctx, n, G)) != SEED_OK) return s;
   cudaGraphExec_t& ex = G.exec;
-  if (!ex) {
-    cudaGraph_t graph;
-    CK(cudaStreamBeginCapture(ctx->gstream, cudaStreamCaptureModeThreadLocal));
-    ctx->in_round = true;
-    ctx->rec_used = 0;
-    ctx->round_gemm_bytes = 0;
-    ctx->round_gemms = 0;
-    s = enqueue_draft(ctx, ctx->gstream);
-    if (s == SEED_OK) {
-      ctx->draft_recs[n] = ctx->rec_used;
-      ctx->rec_used = ctx->rec_cap / 2;
-      s = enqueue_verify(ctx, ctx->gstream);
-    }
-    cudaError_t e = cudaStreamEndCapture(ctx->gstream, &graph);
-    if (s != SEED_OK) return s;
-    CK(e);
-    CK(cudaGraphInstantiate(&ex, graph, 0));
-    cudaGraphDestroy(graph);
-    G.kernels = ctx->kernel_launches - k0;
-    G.gemm_bytes = ctx->round_gemm_bytes;
-    G.gemms = ctx->round_gemms;
-  }
   CK(cudaEventRecord(ctx->ev_in, st));
   CK(cudaStreamWaitEvent(ctx->gstream, ctx->ev_in, 0));
   CK(cudaGraphLaunch(ex, ctx->gstream));
@@ -972,7 +1025,7 @@ seed_status run_phase(seed_ctx ctx, int n, bool draft, cudaStream_t st) {
   ctx->in_round = false;
   CK(cudaEventRecord(ctx->ev_out, ctx->gstream));
   CK(cudaStreamWaitEvent(st, ctx->ev_out, 0));
-  return SEED_OK;
+  return precapture_next(ctx, n, pbit);
 }
 
 seed_status install_slot(seed_ctx ctx, int slot, uint32_t gid, const int32_t* prefix, int len, cudaStream_t st) {

@@ -343,16 +343,27 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
 #pragma unroll
           for (int i = 16; i < 32; ++i) v[i] = 0.f;
         }
-        const int nv = min(32, mcols - m0);
+        // the 32 row scales by eight broadcast 16-byte loads (inv_s has 256 entries; rows >= M keep
+        // the raw value), then predicated stores: no per-element branch, so nothing serialises
+        float sc[32];
+        if (a.ssq_in) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 s4 = *reinterpret_cast<const float4*>(inv_s + m0 + 4 * q);
+            sc[4 * q] = s4.x;
+            sc[4 * q + 1] = s4.y;
+            sc[4 * q + 2] = s4.z;
+            sc[4 * q + 3] = s4.w;
+          }
+        }
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          if (i >= nv) break;
           const int m = m0 + i;
-          const float sc = a.ssq_in ? inv_s[min(m, 255)] : 1.0f;
-          sf[m * 128 + nl] = (m < a.M && a.ssq_in) ? v[i] * sc : v[i];
+          if (m < mcols) sf[m * 128 + nl] = (a.ssq_in && m < a.M) ? v[i] * sc[i] : v[i];
         }
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (ct && et == 0) ct[8] = globaltimer();   // staged
       if (a.ymode == 2) {
         // SwiGLU: output j (0..63) of row m from gate column j and up column 64 + j (B4)
         __nv_bfloat16* sh = reinterpret_cast<__nv_bfloat16*>(smem + (size_t)a.m_pad * 128 * 4);   // bf16 [m_pad][64]
