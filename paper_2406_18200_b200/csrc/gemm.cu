@@ -85,19 +85,20 @@ SEED_DEV float rcp_approx(float x) {
   return y;
 }
 
+template <int YM>
 __device__ __forceinline__ void split_finish16(const SplitArgs& a, int t, int nl, int et, int lane, int m0, int mlim,
                                                const float* v, const float* inv_s, const int* rowmap_s, float* red_s,
                                                const float* xo, float w, uint8_t* stg) {
   const int n = t * BLOCK_N + nl;
   float* sf = reinterpret_cast<float*>(stg);                       // [16][128] fp32 rows
   __nv_bfloat16* sh = reinterpret_cast<__nv_bfloat16*>(stg + 8192); // [16][128] | [16][64] bf16 rows
-  if (a.ymode == 0) {
+  if constexpr (YM == 0) {
     float sc[16];   // every load before the first store (no load-after-store chains)
 #pragma unroll
     for (int i = 0; i < 16; ++i) sc[i] = a.ssq_in ? inv_s[min(m0 + i, 255)] : 1.0f;
 #pragma unroll
     for (int i = 0; i < 16; ++i) sf[i * 128 + nl] = a.ssq_in ? v[i] * sc[i] : v[i];
-  } else if (a.ymode == 1) {
+  } else if constexpr (YM == 1) {
     float sq[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -139,20 +140,20 @@ __device__ __forceinline__ void split_finish16(const SplitArgs& a, int t, int nl
   asm volatile("bar.sync 1, 128;" ::: "memory");
   {
     const int ncols = min(BLOCK_N, a.N - t * BLOCK_N);
-    if (a.ymode != 2) {
+    if (YM != 2) {
       // fp32 rows: 16 x 32 float4, a warp per row
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int q = et + 128 * k, i = q >> 5, c4 = (q & 31) * 4, m = m0 + i;
         if (m < mlim && c4 < ncols) {
-          const int row = a.ymode == 0 && a.yrow ? rowmap_s[m] : m;
+          const int row = YM == 0 && a.yrow ? rowmap_s[m] : m;
           if (row >= 0)
             *reinterpret_cast<float4*>(a.Y + (size_t)row * a.ldY + t * BLOCK_N + c4) =
                 *reinterpret_cast<const float4*>(sf + i * 128 + c4);
         }
       }
     }
-    if (a.ymode == 1) {
+    if (YM == 1) {
       // bf16 rows: 16 x 16 uint4
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
@@ -161,7 +162,7 @@ __device__ __forceinline__ void split_finish16(const SplitArgs& a, int t, int nl
           *reinterpret_cast<uint4*>(a.hout + (size_t)m * a.N + t * BLOCK_N + c8) =
               *reinterpret_cast<const uint4*>(sh + i * 128 + c8);
       }
-    } else if (a.ymode == 2) {
+    } else if (YM == 2) {
       const int i = et >> 3, c8 = (et & 7) * 8, m = m0 + i;
       if (m < mlim)
         *reinterpret_cast<uint4*>(a.hout + (size_t)m * (a.N / 2) + t * 64 + c8) =
@@ -170,6 +171,11 @@ __device__ __forceinline__ void split_finish16(const SplitArgs& a, int t, int nl
   }
 }
 
+// One instantiation per epilogue form (YM = ymode, SPLIT = c > 1, TST = whole-tile tensor store):
+// each holds only its own epilogue, so the code a CTA runs after its mainloop stays within the SM's
+// instruction cache (the all-forms kernel was ~100 KB of SASS; its epilogue fetched instructions
+// from L2 behind the weight stream, ~3 us per CTA at M = 120).
+template <int YM, int SPLIT, int TST>
 __global__ void __launch_bounds__(192, 2)
 gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                    const __grid_constant__ CUtensorMap tmY, SplitArgs a) {
@@ -193,15 +199,15 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
   uint8_t* stg0 = smem + (c_dump_bytes(a) + 1023) / 1024 * 1024;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = a.c, r = blockIdx.x % c, t = blockIdx.y;
+  const int c = SPLIT ? a.c : 1, r = blockIdx.x % c, t = blockIdx.y;
   // token tile: rows [row0, row0 + M) of the launch (blockIdx.x / c); every row's reduction order is
   // the same whatever tile it falls in (R19).  The pointers below are rebased to the tile.
   const int row0 = (blockIdx.x / c) * TOKEN_TILE;
   a.M = min(TOKEN_TILE, a.Mtot - row0);
   if (row0 > 0) {
-    if (a.ymode == 0 && a.yrow) a.yrow += row0;
+    if (YM == 0 && a.yrow) a.yrow += row0;
     else if (a.Y) a.Y += (size_t)row0 * a.ldY;
-    if (a.hout) a.hout += (size_t)row0 * (a.ymode == 2 ? a.N / 2 : a.N);
+    if (a.hout) a.hout += (size_t)row0 * (YM == 2 ? a.N / 2 : a.N);
     if (a.ssq_in) a.ssq_in += row0;
     if (a.ssq_out) a.ssq_out += row0;
   }
@@ -313,7 +319,7 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
     }
     if (a.yrow)
       for (int m = et; m < a.M; m += 128) rowmap_s[m] = __ldg(a.yrow + m);
-    const bool res = a.ymode == 1;
+    constexpr bool res = YM == 1;
     const float w = (res && n < a.N) ? bf2f(a.nw[n]) : 0.f;
     float xo[16], xn[16];
     auto load_res = [&](int m0, float* dst) {
@@ -330,7 +336,7 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
     if (ct && et == 0) ct[5] = globaltimer();
     const uint32_t row_addr = tmem_base + ((uint32_t)(lane_grp * 32) << 16);
     int chunk = 0;
-    if (a.tstore) {
+    if constexpr (TST != 0) {
       // whole tile: every accumulator column straight into a staging tile in the idle ring (32 columns
       // per TMEM load), one barrier, one tensor store -- no per-chunk barrier or store round trip
       float* sf = reinterpret_cast<float*>(smem);   // ymode 0: fp32 [m_pad][128]; ymode 2: fp32 [m_pad][128] gate | up
@@ -364,7 +370,7 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (ct && et == 0) ct[8] = globaltimer();   // staged
-      if (a.ymode == 2) {
+      if constexpr (YM == 2) {
         // SwiGLU: output j (0..63) of row m from gate column j and up column 64 + j (B4)
         __nv_bfloat16* sh = reinterpret_cast<__nv_bfloat16*>(smem + (size_t)a.m_pad * 128 * 4);   // bf16 [m_pad][64]
         const int j = et & 63;
@@ -386,12 +392,12 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
         bulk_wait_read0();
       }
       if (ct && et == 0) ct[11] = globaltimer();
-    } else if (c == 1) {
+    } else if constexpr (!SPLIT) {
       for (int m0 = 0; m0 < a.M; m0 += 16) {
         float v[16];
         tmem_ld16(row_addr + m0, v);
         if (res && m0 + 16 < a.M) load_res(m0 + 16, xn);
-        split_finish16(a, t, nl, et, lane, m0, min(m0 + 16, a.M), v, inv_s, rowmap_s, red_s, xo, w,
+        split_finish16<YM>(a, t, nl, et, lane, m0, min(m0 + 16, a.M), v, inv_s, rowmap_s, red_s, xo, w,
                        stg0 + (chunk++ & 1) * 12288);
         if (ct && et == 0 && m0 == 0) ct[11] = globaltimer();
         if (res) {
@@ -458,7 +464,7 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
           }
           if (ct && et == 0) ct[10] = globaltimer() + (v[0] == 1.2345e-30f ? 1 : 0);
             // (the next chunk's residual rows are already in flight)
-          split_finish16(a, t, nl, et, lane, m0, min(m0 + 16, hi), v, inv_s, rowmap_s, red_s, xo, w,
+          split_finish16<YM>(a, t, nl, et, lane, m0, min(m0 + 16, hi), v, inv_s, rowmap_s, red_s, xo, w,
                          stg0 + (chunk++ & 1) * 12288);
           if (res) {
 #pragma unroll
@@ -496,6 +502,23 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
     atomicMax(&a.timing[2], globaltimer());
     a.timing[3] = 1;
   }
+}
+
+using GemmKernel = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, SplitArgs);
+constexpr GemmKernel kGemmKernels[7] = {gemm_splitk_kernel<0, 0, 0>, gemm_splitk_kernel<1, 0, 0>, gemm_splitk_kernel<2, 0, 0>,
+                                        gemm_splitk_kernel<0, 1, 0>, gemm_splitk_kernel<1, 1, 0>, gemm_splitk_kernel<2, 1, 0>,
+                                        gemm_splitk_kernel<0, 0, 1>};
+GemmKernel gemm_kernel_for(int ymode, bool split, bool tstore) {
+  return tstore ? kGemmKernels[6] : kGemmKernels[(split ? 3 : 0) + ymode];
+}
+void gemm_kernel_attrs() {
+  static bool done = false;
+  if (done) return;
+  for (GemmKernel k : kGemmKernels) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) cudaGetLastError();
+  }
+  done = true;
 }
 
 // GEMM records (kind 1): acc[0] += end - release (ns on the critical path), acc[1] += 1,
@@ -587,11 +610,7 @@ bool encode_tmap_store(CUtensorMap* map, const void* ptr, bool fp32, uint64_t in
 
 // clusters of c gemm_splitk_kernel CTAs (smem_kb each) the device can hold at once
 int split_cluster_capacity(int c, int smem_kb) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gemm_splitk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  gemm_kernel_attrs();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(c, 1024);
   cfg.blockDim = dim3(192);
@@ -604,7 +623,7 @@ int split_cluster_capacity(int c, int smem_kb) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, gemm_splitk_kernel, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, gemm_kernel_for(0, true, false), &cfg) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
@@ -719,15 +738,9 @@ cudaError_t gemm_run(const GemmPlan& p, int M, const GemmIO& io, cudaStream_t st
       (size_t)m_pad * (512 + (io.ymode == 2 ? 128 : 0)) <= (size_t)stages * stage_bytes && !getenv("SEED_GEMM_NO_TSTORE"))
     b.tstore = 1;
   const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 2) * 8 + 16 + extra;
-  static bool sattr = false;
-  if (!sattr) {
-    cudaFuncSetAttribute(gemm_splitk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (cudaFuncSetAttribute(gemm_splitk_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
-      cudaGetLastError();
-    sattr = true;
-  }
+  gemm_kernel_attrs();
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  return launch_clustered(gemm_splitk_kernel, dim3(p.c * ttiles, p.tiles), dim3(192), smem, st, dim3(p.c, 1, 1), p.tmW,
+  return launch_clustered(gemm_kernel_for(io.ymode, p.c > 1, b.tstore != 0), dim3(p.c * ttiles, p.tiles), dim3(192), smem, st, dim3(p.c, 1, 1), p.tmW,
                           *io.tmX, b.tstore ? *io.tmY : p.tmW, b);
 }
 
