@@ -228,6 +228,7 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
       mbar_init(&empty[i], 1);
     }
     mbar_init(&tfull[0], 1);
+    mbar_init(&tfull[1], 1);   // split-K exchange: the slices this rank reduces have landed
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, cols);
@@ -324,7 +325,7 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
     float xo[16], xn[16];
     auto load_res = [&](int m0, float* dst) {
 #pragma unroll
-      for (int i = 0; i < 16; ++i)
+      for (int i = 0; i < 16; ++i)   // (clamped unconditional loads measured slower: 4.92 vs 5.08 ms at N = 24)
         dst[i] = (m0 + i < a.M && n < a.N) ? a.Y[(size_t)(m0 + i) * a.ldY + n] : 0.f;
     };
     // the first two chunks' residual rows (c > 1: the rest stays one chunk ahead in the loop)
@@ -340,33 +341,25 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
       // whole tile: every accumulator column straight into a staging tile in the idle ring (32 columns
       // per TMEM load), one barrier, one tensor store -- no per-chunk barrier or store round trip
       float* sf = reinterpret_cast<float*>(smem);   // ymode 0: fp32 [m_pad][128]; ymode 2: fp32 [m_pad][128] gate | up
+      // Branch-free: 32 columns per TMEM load (the allocation holds max(32, m_pad) rounded to a power
+      // of two), every row of the 32-row group stored (rows past m_pad land in the idle ring and are
+      // never stored out), rows >= M scaled by 1 (a per-element branch here cost ~3x the stores)
+      const bool scaled = a.ssq_in != nullptr;
       for (int m0 = 0; m0 < mcols; m0 += 32) {
         float v[32];
-        if (m0 + 16 < mcols) {
-          tmem_ld32(row_addr + m0, v);
-        } else {
-          tmem_ld16(row_addr + m0, v);
-#pragma unroll
-          for (int i = 16; i < 32; ++i) v[i] = 0.f;
-        }
-        // the 32 row scales by eight broadcast 16-byte loads (inv_s has 256 entries; rows >= M keep
-        // the raw value), then predicated stores: no per-element branch, so nothing serialises
+        tmem_ld32(row_addr + m0, v);
         float sc[32];
-        if (a.ssq_in) {
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float4 s4 = *reinterpret_cast<const float4*>(inv_s + m0 + 4 * q);
-            sc[4 * q] = s4.x;
-            sc[4 * q + 1] = s4.y;
-            sc[4 * q + 2] = s4.z;
-            sc[4 * q + 3] = s4.w;
-          }
+        for (int q = 0; q < 8; ++q) {
+          float4 s4 = make_float4(1.f, 1.f, 1.f, 1.f);
+          if (scaled) s4 = *reinterpret_cast<const float4*>(inv_s + m0 + 4 * q);
+          sc[4 * q] = m0 + 4 * q < a.M ? s4.x : 1.f;
+          sc[4 * q + 1] = m0 + 4 * q + 1 < a.M ? s4.y : 1.f;
+          sc[4 * q + 2] = m0 + 4 * q + 2 < a.M ? s4.z : 1.f;
+          sc[4 * q + 3] = m0 + 4 * q + 3 < a.M ? s4.w : 1.f;
         }
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int m = m0 + i;
-          if (m < mcols) sf[m * 128 + nl] = (a.ssq_in && m < a.M) ? v[i] * sc[i] : v[i];
-        }
+        for (int i = 0; i < 32; ++i) sf[(m0 + i) * 128 + nl] = v[i] * sc[i];
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (ct && et == 0) ct[8] = globaltimer();   // staged
@@ -412,22 +405,27 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
         // the slots alias the peers' rings: every rank's MMAs have finished reading its ring
         if (pass == 0) cluster_sync_relaxed();
         // push: every 4-token group of this CTA's partial goes straight into the shared memory of
-        // the rank that reduces it (posted DSMEM stores, no round trips), slot [my rank][group][nl]
-        // of float4: a warp's store covers 512 contiguous bytes, and the owner's 16-byte reads of
-        // consecutive lanes are conflict-free
+        // the rank that reduces it, slot [my rank][group][nl] of float4 (a warp's store covers 512
+        // contiguous bytes, the owner's 16-byte reads of consecutive lanes are conflict-free), by
+        // asynchronous remote stores that complete on the owner's mbarrier: the owner waits for
+        // exactly its bytes -- no cluster barrier, so no GPU-scope fence behind the epilogue's
+        // global stores
         const int ng = perp / 4;   // token groups per rank
+        const int mine = max(0, min((pe - pb) / 4, (r + 1) * ng) - r * ng);
+        if (et == 0) mbar_arrive_expect_tx(&tfull[1], (uint32_t)(c * mine * 128 * 16));
         for (int col = pb; col < pe; col += 16) {
           float v[16];
           tmem_ld16(row_addr + col, v);
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const int cc = col + 4 * j - pb, owner = cc / perp, grp = (cc - owner * perp) / 4;
-            st_dsmem_f4(dsmem_addr(part_s + (((size_t)r * ng + grp) * 128 + nl) * 4, (uint32_t)owner),
-                        make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+            st_async_f4(dsmem_addr(part_s + (((size_t)r * ng + grp) * 128 + nl) * 4, (uint32_t)owner),
+                        make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]),
+                        dsmem_addr(&tfull[1], (uint32_t)owner));
           }
         }
         if (ct && et == 0) ct[8] = globaltimer();
-        cluster_sync();   // every rank's slices have landed
+        mbar_wait(&tfull[1], (uint32_t)(pass & 1));   // every rank's slices have landed
         if (ct && et == 0) ct[9] = globaltimer();
         const int lo = min(a.M, pb + r * perp), hi = min(a.M, min(pe, pb + (r + 1) * perp));
         if (res && pass > 0 && lo < hi) {
@@ -447,9 +445,10 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
             for (int ss = 0; ss < 4; ++ss)
 #pragma unroll
               for (int j = 0; j < 4; ++j)
-                q[ss][j] = (s0 + ss < c && j < nq)
-                               ? *reinterpret_cast<const float4*>(src + ((size_t)(s0 + ss) * ng + j) * 128 * 4)
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
+              {   // every slot inside the (idle) ring: load unconditionally, keep the valid ones
+                const float4 t4 = *reinterpret_cast<const float4*>(src + ((size_t)(s0 + ss) * ng + j) * 128 * 4);
+                q[ss][j] = (s0 + ss < c && j < nq) ? t4 : make_float4(0.f, 0.f, 0.f, 0.f);
+              }
 #pragma unroll
             for (int ss = 0; ss < 4; ++ss) {
               if (s0 + ss >= c) break;
@@ -491,7 +490,7 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
   }
   if (warp < 2 && npass > 0) {
     cluster_sync_relaxed();
-    for (int p = 0; p < 2 * npass - 1; ++p) cluster_sync();
+    for (int p = 0; p < npass - 1; ++p) cluster_sync();
   }
   tc_fence_before();
   __syncthreads();
@@ -516,6 +515,7 @@ void gemm_kernel_attrs() {
   if (done) return;
   for (GemmKernel k : kGemmKernels) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) cudaGetLastError();
   }
   done = true;
@@ -649,7 +649,9 @@ void gemm_plan(GemmPlan* p, const void* W, int N, int K, int min_units) {
   // SM); shrink c until the device reports room for all tiles
   for (; c > 1; --c) {
     const int smem_kb = p->tiles * c <= kNumSMs ? 180 : 112;
-    if (split_cluster_capacity(c, smem_kb) >= p->tiles) break;
+    const int cap = split_cluster_capacity(c, smem_kb);
+    if (getenv("SEED_GEMM_VERBOSE")) fprintf(stderr, "[seed] gemm N=%d K=%d try c=%d smem=%dKB capacity=%d\n", N, K, c, smem_kb, cap);
+    if (cap >= p->tiles) break;
   }
   p->c = c;
   // one CTA per SM with the deep ring while the grid fits the SMs, else two per SM (gate/up and
@@ -662,6 +664,7 @@ void gemm_plan(GemmPlan* p, const void* W, int N, int K, int min_units) {
 }
 
 void gemm_plan_free(GemmPlan*) {}
+
 
 void carveout_once(const void* kern) {
   static std::vector<const void*> done;
@@ -735,7 +738,7 @@ cudaError_t gemm_run(const GemmPlan& p, int M, const GemmIO& io, cudaStream_t st
   b.stages = stages;
   // whole-tile staging + one tensor store (c = 1): the staging tile must fit the idle ring
   if (p.c == 1 && io.tmY && io.ymode == 0 && !io.yrow &&
-      (size_t)m_pad * (512 + (io.ymode == 2 ? 128 : 0)) <= (size_t)stages * stage_bytes && !getenv("SEED_GEMM_NO_TSTORE"))
+      (size_t)((m_pad + 31) / 32 * 32) * 512 <= (size_t)stages * stage_bytes && !getenv("SEED_GEMM_NO_TSTORE"))
     b.tstore = 1;
   const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 2) * 8 + 16 + extra;
   gemm_kernel_attrs();

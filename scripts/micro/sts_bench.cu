@@ -1,29 +1,67 @@
-// Shared-memory store throughput of the GEMM epilogue's staging pattern (4 warps, thread nl writes
-// column nl of rows 0..M-1 of an fp32 [M][128] tile): cycles per CTA, one CTA per SM.
+// Epilogue staging pattern of the GEMM's whole-tile store (4 warps, thread nl writes column nl of
+// rows 0..M-1 of an fp32 [M][128] tile) in isolation: cycles per pass, one CTA per SM.
+//   mode 0: stores only; 1: + row scales from shared memory; 2: + tcgen05.ld of 32 TMEM columns
+#include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
-__global__ void __launch_bounds__(192, 1) sts_kernel(int M, int reps, long long* out, float* sink) {
-  extern __shared__ float sf[];
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__global__ void __launch_bounds__(192, 1) sts_kernel(int M, int reps, int mode, long long* out, float* sink) {
+  extern __shared__ __align__(1024) float sf[];
+  __shared__ uint32_t tslot;
+  __shared__ __align__(16) float inv_s[256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp < 2) return;
-  const int nl = (warp & 3) * 32 + lane;
-  float v[32];
-  for (int i = 0; i < 32; ++i) v[i] = nl * 0.5f + i;
-  asm volatile("bar.sync 1, 128;" ::: "memory");
-  long long t0 = clock64();
-  for (int r = 0; r < reps; ++r) {
-    for (int m0 = 0; m0 < M; m0 += 32) {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int m = m0 + i;
-        if (m < M) sf[m * 128 + nl] = v[i] + r;
-      }
-    }
+  if (warp == 1) asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&tslot)));
+  for (int i = threadIdx.x; i < 256; i += 192) inv_s[i] = 1.0f + i * 1e-3f;
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tbase = tslot;
+  long long t0 = 0, t1 = 0;
+  if (warp >= 2) {
+    const int nl = (warp & 3) * 32 + lane;
+    const uint32_t row_addr = tbase + ((uint32_t)((warp & 3) * 32) << 16);
+    float v[32];
+    for (int i = 0; i < 32; ++i) v[i] = nl * 0.5f + i;
     asm volatile("bar.sync 1, 128;" ::: "memory");
+    t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      for (int m0 = 0; m0 < M; m0 += 32) {
+        if (mode >= 2) {
+          uint32_t q[32];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+              "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+              : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7]), "=r"(q[8]),
+                "=r"(q[9]), "=r"(q[10]), "=r"(q[11]), "=r"(q[12]), "=r"(q[13]), "=r"(q[14]), "=r"(q[15]), "=r"(q[16]),
+                "=r"(q[17]), "=r"(q[18]), "=r"(q[19]), "=r"(q[20]), "=r"(q[21]), "=r"(q[22]), "=r"(q[23]), "=r"(q[24]),
+                "=r"(q[25]), "=r"(q[26]), "=r"(q[27]), "=r"(q[28]), "=r"(q[29]), "=r"(q[30]), "=r"(q[31])
+              : "r"(row_addr + (uint32_t)(m0 & 127)));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(q[i]) + v[i];
+        }
+        float sc[32];
+        if (mode >= 1) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 s4 = *reinterpret_cast<const float4*>(inv_s + m0 + 4 * q);
+            sc[4 * q] = s4.x; sc[4 * q + 1] = s4.y; sc[4 * q + 2] = s4.z; sc[4 * q + 3] = s4.w;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int m = m0 + i;
+          if (m < M) sf[m * 128 + nl] = mode >= 1 ? v[i] * sc[i] : v[i] + r;
+        }
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
+    t1 = clock64();
   }
-  long long t1 = clock64();
   if (threadIdx.x == 64 && blockIdx.x == 0) out[0] = (t1 - t0) / reps;
   if (sf[(threadIdx.x * 7) % (M * 128)] == 12345.f) sink[0] = 1;
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tbase));
 }
 int main() {
   long long* d;
@@ -31,14 +69,13 @@ int main() {
   cudaMalloc(&d, 8);
   cudaMalloc(&s, 4);
   cudaFuncSetAttribute(sts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 180 * 1024);
-  for (int M : {16, 64, 120, 128}) {
-    for (int grid : {1, 148}) {
-      sts_kernel<<<grid, 192, 180 * 1024>>>(M, 100, d, s);
+  for (int mode = 0; mode < 3; ++mode)
+    for (int M : {16, 120}) {
+      sts_kernel<<<148, 192, 180 * 1024>>>(M, 100, mode, d, s);
       long long c;
-      cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
-      printf("M=%d grid=%d: %lld cycles per staging pass (%.2f us at 1.965 GHz), %.1f B/cycle\n", M, grid, c,
-             c / 1965.0, M * 128 * 4.0 / c);
+      cudaError_t e = cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
+      printf("mode=%d M=%d: %lld cycles per pass (%.2f us at 1.965 GHz)\n", mode, M, c, c / 1965.0);
     }
-  }
   return 0;
 }
