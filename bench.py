@@ -328,6 +328,9 @@ def run_ours(args):
     ms = e0.elapsed_time(e1)
     emitted = sum(eng.stream_info(gid)["L"] - t_before[gid] for gid in my_ids)
     per_stream_round = emitted / (steps * len(my_ids))
+    # mean target context over the timed rounds (prompt + tokens before + half of those emitted during)
+    ctx_mean = statistics.mean(len(prompts[gid]) + t_before[gid] + 0.5 * (eng.stream_info(gid)["L"] - t_before[gid])
+                               for gid in my_ids)
 
     # e2e: the same rounds through the public host-buffer call seed_round_host (batch ids in,
     # emitted tokens + counts out, every round), wall clock around the K rounds
@@ -410,6 +413,15 @@ def run_ours(args):
                 "timing": "wall clock (perf_counter) around the K seed_round_host rounds, host-synchronised"},
         "clocks": clk,
     }
+    # the north-star number: T_roof / T per round (sum over phases of max(bytes / HBM,
+    # flops / sustained bf16), at this run's mean context; scripts/troof.py)
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "scripts"))
+    from troof import troof
+    tr = troof(args.config, n_local, ctx_mean)
+    line["round_roofline"] = {"t_roof_ms": tr["t_roof_ms"], "t_round_ms": step_ms, "frac": tr["t_roof_ms"] / step_ms,
+                              "ctx_mean": ctx_mean, "phases_ms": tr["phases_ms"],
+                              "definition": "SURVEY 8(d): T_roof = sum_phase max(B/BW_hbm, F/F_bf16_sustained), "
+                                            "phases GEMM / attention / draft / vocab; north_star bar 0.60"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import torch as _t
         smp = OracleSampler(args.config, args.temperature, n_local)
