@@ -188,13 +188,15 @@ vocab_verify_kernel(VerifyArgs A) {
     };
     if (res) {
       const double mq = sv[2 * (g + 1 + row)], l1q = sv[2 * (g + 1 + row) + 1];
-      const float mqf = (float)mq, l1qf = (float)l1q;
+      const double cq = (mq + l1q) - (mt + l1t);   // lq - lp = (a_q - a_t) - cq
       auto res32 = [&](int l) -> float {
-        const float lp = (scaled_v(zt_s[l], A.T) - mtf) - l1tf;
-        const float lq = (scaled_v(zd_s[l], A.T) - mqf) - l1qf;
-        const float dlt = lq - lp;
-        if (dlt > -0.05f) return dlt >= 0.05f ? -INFINITY : NAN;  // near-equal p, q: fp64
-        return lp + __logf(1.0f - __expf(dlt));                    // screen only (pass B is exact)
+        // lq - lp from the two fp32 logits in fp64 (their difference is exact there), so the fp32
+        // screen below holds to ~1e-6 for any sign-definite difference; only |lq - lp| < 1e-12 is
+        // left to fp64 (pass B).  Screen only: pass B is exact.
+        const float at = scaled_v(zt_s[l], A.T);
+        const double d = ((double)scaled_v(zd_s[l], A.T) - (double)at) - cq;
+        if (d > -1e-12) return d >= 1e-12 ? -INFINITY : NAN;
+        return ((at - mtf) - l1tf) + __logf(-expm1f((float)d));
       };
       auto res64 = [&](int l) -> double {
         const double lp = ((double)scaled_v(zt_s[l], A.T) - mt) - l1t;

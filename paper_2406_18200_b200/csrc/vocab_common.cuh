@@ -98,11 +98,13 @@ __device__ __forceinline__ float scaled_v(float z, float T) { return T == 1.0f ?
 // -log(E), E = -log1p(-u): the exponential-race offset, fp64
 __device__ __forceinline__ double neg_log_exp(double u) { return -log(-log1p(-u)); }
 
-// -log(E) for the fp32 screen: absolute error ~1e-6, far inside RACE_MARGIN (the rescoring is
-// exact).  E keeps full relative precision for small u (log1pf), 1 - u is exact in fp32 on the odd
-// 2^-24 grid (R2), and the logarithms run on the SFU.
+// -log(E) for the fp32 screen: absolute error < 1e-4, far inside RACE_MARGIN / 2 (the rescoring is
+// exact): the candidate set of pass B holds every id whose exact key can be the maximum.  The
+// logarithms run on the SFU.
 __device__ __forceinline__ float neg_log_exp_screen(float u) {
-  const float E = u < 0.25f ? -log1pf(-u) : -__logf(1.0f - u);
+  // u < 2^-7: E = u (1 + u/2 + u^2/3 + u^3/4), truncation < 1e-9 relative; else 1 - u is exact
+  // (the uniform grid, R2) and __logf's absolute error (< 4e-7 on [0.5, 1)) is < 5e-5 of E >= 2^-7
+  const float E = u < 0.0078125f ? u * (1.0f + u * (0.5f + u * (0.33333334f + u * 0.25f))) : -__logf(1.0f - u);
   return -__logf(E);
 }
 
@@ -186,44 +188,81 @@ __device__ RowStat merge_stats(const SliceStat* st) {
 // one exchange, ties to the smallest id (R14).
 constexpr float RACE_MARGIN = 1e-3f;
 
+constexpr int RACE_NB = 4;   // register-resident screen keys: 4 blocks of 4 ids per thread (n <= 4096)
+
 template <class W32, class W64>
 __device__ Best race_slice(int v0, int n, uint32_t c1, uint32_t r, uint32_t sid, uint32_t k0, uint32_t k1, float* keys,
                            float* red_f, Best* red_b, W32 w32, W64 w64) {
-  float best32 = -INFINITY;
-  for (int l = 4 * (int)threadIdx.x; l < n; l += 4 * VT) {
+  Best b{-INFINITY, -1};
+  auto rescore = [&](int l) {   // pass B: the exact fp64 key of id v0 + l
     const int g = v0 + l;
     const Philox4 ph = philox4x32_10((uint32_t)(g >> 2), c1, r, sid, k0, k1);
+    const uint32_t words[4] = {ph.x, ph.y, ph.z, ph.w};
+    const double wd = w64(l);
+    if (!(wd > -INFINITY)) return;   // -inf, or NaN (non-finite logits: no finite key, R35)
+    const double key = wd + neg_log_exp(philox_uniform(words[g & 3]));
+    if (b.v < 0 || key > b.k || (key == b.k && g < b.v)) b = Best{key, g};
+  };
+  // pass A: fp32 screen keys; an id whose weight fp32 cannot screen (w32 = NaN) is a candidate by
+  // construction (+inf) and is scored in pass B only.  The threshold is taken over screened keys:
+  // the exact argmax is screened within RACE_MARGIN / 2 of its key, or is an fp64 candidate.
+  auto screen = [&](int l, uint32_t word) -> float {
+    const float w = w32(l);
+    if (w != w) return INFINITY;
+    return w != -INFINITY ? w + neg_log_exp_screen((float)philox_uniform(word)) : -INFINITY;
+  };
+  float best32 = -INFINITY;
+  if (n <= 4 * VT * RACE_NB) {
+    // the 16 screen keys of a thread stay in registers; pass B walks a candidate bit mask (one
+    // out-of-loop copy of the fp64 rescoring code)
+    float kr[RACE_NB][4];
+#pragma unroll
+    for (int i = 0; i < RACE_NB; ++i) {
+      const int l = 4 * (int)threadIdx.x + i * 4 * VT;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) kr[i][e] = -INFINITY;
+      if (l < n) {
+        const Philox4 ph = philox4x32_10((uint32_t)((v0 + l) >> 2), c1, r, sid, k0, k1);
+        const uint32_t words[4] = {ph.x, ph.y, ph.z, ph.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (l + e < n) kr[i][e] = screen(l + e, words[e]);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (kr[i][e] != INFINITY) best32 = fmaxf(best32, kr[i][e]);
+    }
+    const float lmax = block_maxf(best32, red_f);
+    const float thr = lmax - RACE_MARGIN;
+    uint32_t mask = 0;
+#pragma unroll
+    for (int i = 0; i < RACE_NB; ++i)
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (kr[i][e] == INFINITY || (kr[i][e] != -INFINITY && kr[i][e] >= thr)) mask |= 1u << (4 * i + e);
+    while (mask) {
+      const int bit = __ffs(mask) - 1;
+      mask &= mask - 1;
+      rescore(4 * (int)threadIdx.x + (bit >> 2) * 4 * VT + (bit & 3));
+    }
+    return block_best(b, red_b);
+  }
+  // large slices: screen keys through shared memory
+  for (int l = 4 * (int)threadIdx.x; l < n; l += 4 * VT) {
+    const Philox4 ph = philox4x32_10((uint32_t)((v0 + l) >> 2), c1, r, sid, k0, k1);
     const uint32_t words[4] = {ph.x, ph.y, ph.z, ph.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       if (l + e >= n) break;
-      const float w = w32(l + e);
-      float key = -INFINITY;
-      if (w != w) {  // NaN: fp64 needed
-        const double wd = w64(l + e);
-        if (wd != -INFINITY) key = (float)(wd + neg_log_exp(philox_uniform(words[e])));
-      } else if (w != -INFINITY) {
-        key = w + neg_log_exp_screen((float)philox_uniform(words[e]));
-      }
+      const float key = screen(l + e, words[e]);
       keys[l + e] = key;
-      best32 = fmaxf(best32, key);
+      if (key != INFINITY) best32 = fmaxf(best32, key);
     }
   }
   const float lmax = block_maxf(best32, red_f);
-  Best b{-INFINITY, -1};
-  if (lmax != -INFINITY) {
-    const float thr = lmax - RACE_MARGIN;
-    for (int l = threadIdx.x; l < n; l += VT) {
-      if (keys[l] < thr) continue;
-      const int g = v0 + l;
-      const Philox4 ph = philox4x32_10((uint32_t)(g >> 2), c1, r, sid, k0, k1);
-      const uint32_t words[4] = {ph.x, ph.y, ph.z, ph.w};
-      const double wd = w64(l);
-      if (wd == -INFINITY) continue;
-      const double key = wd + neg_log_exp(philox_uniform(words[g & 3]));
-      if (b.v < 0 || key > b.k || (key == b.k && g < b.v)) b = Best{key, g};
-    }
-  }
+  const float thr = lmax - RACE_MARGIN;
+  for (int l = threadIdx.x; l < n; l += VT)
+    if (keys[l] == INFINITY || (keys[l] != -INFINITY && keys[l] >= thr)) rescore(l);
   return block_best(b, red_b);
 }
 
