@@ -77,6 +77,18 @@ SEED_API seed_status seed_op_decoder_layer(const seed_model_shape* shape, const 
                                   int32_t M, int32_t ctx, const void* k_prev, const void* v_prev,
                                   float* x_out, void* k_new, void* v_new, void* stream);
 
+/* The same layer over a TREE of M <= 64 rows (k_config verification, §3.2 P:107-113 and
+ * Figure 7 of App. B; R36): parent (host int32 [M]): parent[0] = -1 (the root,
+ * the sequence's next token at position ctx), 0 <= parent[i] < i otherwise.  Row i is rotated at
+ * position ctx + depth(i) and attends to the ctx cached keys and to its ancestors and itself only,
+ * so every row equals the last row of the causal layer over its root-to-row path.  k_new/v_new: the
+ * rows' K/V as appended (row i at cache slot ctx + i, rotated at its tree position; the accepted
+ * path compacts into consecutive slots without re-rotation).  Errors: SEED_EINVAL on a malformed
+ * parent array or M > 64. */
+SEED_API seed_status seed_op_decoder_layer_tree(const seed_model_shape* shape, const void* const* w, const float* x_in,
+                                       int32_t M, int32_t ctx, const int32_t* parent, const void* k_prev,
+                                       const void* v_prev, float* x_out, void* k_new, void* v_new, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

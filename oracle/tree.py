@@ -30,6 +30,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from . import llama as _ll
 from . import philox as _ph
 from . import sampling as _sp
 
@@ -196,3 +197,23 @@ def verify_tree(zt_of, zd_of, tree, T, seed, sid, r, bonus=True, flag_eps=1e-6):
             res.y = y
     res.emitted = list(res.path) + ([int(res.y)] if res.y is not None else [])
     return res
+
+
+def tree_layer_forward(shape, L, x, parent, ctx, k_cache, v_cache, mode="bf16"):
+    """One decoder layer over a tree of rows (Figure 7): row 0 is the root at
+    position ctx, row i (parent[i] < i) sits at position ctx + depth(i) and sees the cached keys and
+    the rows on its root-to-row path.  By definition each row's output is the last row of the causal
+    layer (`llama.layer_forward`) over its path; returns (x_out, k_new, v_new) like layer_forward."""
+    x = np.asarray(x, dtype=np.float64)
+    M = len(parent)
+    outs, ks, vs = [None] * M, [None] * M, [None] * M
+    for i in range(M):
+        path = []
+        n = i
+        while n >= 0:
+            path.append(n)
+            n = parent[n]
+        path = path[::-1]
+        xo, kn, vn = _ll.layer_forward(shape, L, x[path], np.arange(ctx, ctx + len(path)), k_cache, v_cache, mode=mode)
+        outs[i], ks[i], vs[i] = xo[-1], kn[-1], vn[-1]
+    return np.stack(outs), np.stack(ks), np.stack(vs)

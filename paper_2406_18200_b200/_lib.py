@@ -102,6 +102,8 @@ _SIGS = {
                             C.c_int32, _P, _P, _P, _P],
     "seed_op_decoder_layer": [C.POINTER(ModelShape), C.POINTER(C.c_void_p), _P, C.c_int32, C.c_int32, _P, _P, _P,
                               _P, _P, _P],
+    "seed_op_decoder_layer_tree": [C.POINTER(ModelShape), C.POINTER(C.c_void_p), _P, C.c_int32, C.c_int32, _I32P, _P,
+                                   _P, _P, _P, _P, _P],
 }
 _RESTYPE = {"seed_last_error": C.c_char_p, "seed_destroy": None, "seed_sched_destroy": None,
             "seed_table_destroy": None, "seed_sched_all_done": C.c_int32, "seed_book_destroy": None,

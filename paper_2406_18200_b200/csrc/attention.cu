@@ -215,7 +215,8 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __rest
       x0[k] = x1[k] = c0[k] = c1[k] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (it < QI && r < nr) {
         const float* yr = qkv + (size_t)(q0 + r0 + r) * ldq + head * DH;
-        const float4* cs = reinterpret_cast<const float4*>(rope + (size_t)(pos0 + r) * HALF + i);
+        const int rp = seqs.row_pos ? seqs.row_pos[q0 + r0 + r] : pos0 + r;   // tree rows: depth positions
+        const float4* cs = reinterpret_cast<const float4*>(rope + (size_t)rp * HALF + i);
         x0[k] = *reinterpret_cast<const float4*>(yr + i);
         x1[k] = *reinterpret_cast<const float4*>(yr + i + HALF);
         c0[k] = __ldg(cs);
@@ -240,6 +241,13 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __rest
 
   // ---- the warp's tiles, online softmax over them (rows g, g + 8 of the MMA fragments)
   const int g = lane >> 2, t4 = lane & 3;
+  // tree rows: the new rows each row attends to (rows g, g + 8 of the fragments; 0 = causal row)
+  uint64_t anc_rows[2] = {0ull, 0ull};
+  if (seqs.anc) {
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2)
+      if (g + 8 * h2 < nr) anc_rows[h2] = seqs.anc[q0 + r0 + g + 8 * h2];
+  }
   float o_acc[DT][4];
   float m_row[2] = {-INFINITY, -INFINITY}, l_row[2] = {0.f, 0.f};
 #pragma unroll
@@ -272,7 +280,8 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __rest
         const int m = q0 + (key - new_first);
         const float* yk = qkv + (size_t)m * ldq + (H + kvh) * DH;
         const float* yv = qkv + (size_t)m * ldq + (H + Hk + kvh) * DH;
-        const float4* cs = reinterpret_cast<const float4*>(rope + (size_t)key * HALF + i);
+        const int kp = seqs.row_pos ? seqs.row_pos[m] : key;
+        const float4* cs = reinterpret_cast<const float4*>(rope + (size_t)kp * HALF + i);
         const float4 x0 = *reinterpret_cast<const float4*>(yk + i), x1 = *reinterpret_cast<const float4*>(yk + i + HALF);
         const float4 va = *reinterpret_cast<const float4*>(yv + i), vv = *reinterpret_cast<const float4*>(yv + i + HALF);
         const float4 c0 = __ldg(cs), c1 = __ldg(cs + 1);
@@ -315,13 +324,15 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __rest
 #pragma unroll
     for (int h2 = 0; h2 < 2; ++h2) {
       const int r = g + 8 * h2;
+      const uint64_t anc_r = anc_rows[h2];
       float mx = -INFINITY;
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           const int key = t0 + nt * 8 + 2 * t4 + c;
-          const bool ok = r < nr && key < k_hi && key <= pos0 + r;
+          const bool ok = r < nr && key < k_hi &&
+                          (anc_r ? (key < new_first || ((anc_r >> (key - new_first)) & 1ull)) : key <= pos0 + r);
           float& v = sc[nt][2 * h2 + c];
           v = ok ? (v + s2[nt][2 * h2 + c]) * scale : -INFINITY;
           mx = fmaxf(mx, v);

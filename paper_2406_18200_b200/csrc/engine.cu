@@ -150,6 +150,8 @@ struct SlotState {  // one stream slot; the validated tokens live in the round b
 struct ChunkDesc {
   int M, n_seq, max_q_len, max_kv;
   const int32_t *pos, *slot, *q_start, *q_len, *kv_len, *seq_slot, *seq_stable, *compact;  // device (slot: per row)
+  const int32_t* row_pos = nullptr;   // tree rows (R36): per-row RoPE positions and attended new rows
+  const uint64_t* anc = nullptr;
   TokSrc tok;
   int n_logits;
   const int32_t* logit_rows;  // device [n_logits]: chunk row of each logits row
@@ -506,7 +508,7 @@ seed_status forward_chunk(seed_ctx ctx, Model& m, const ChunkDesc& c, cudaStream
                        first_layer < m.L ? m.an[first_layer] : m.final_norm, m.h, ctx->dev_err, st,
                        next_rec(ctx)));
   ctx->kernel_launches++;
-  seed::SeqInfo seqs{c.q_start, c.q_len, c.kv_len, c.seq_slot, c.seq_stable};
+  seed::SeqInfo seqs{c.q_start, c.q_len, c.kv_len, c.seq_slot, c.seq_stable, c.row_pos, c.anc};
   const CUtensorMap* tm_h = xmap(ctx, m.h, m.d, m.m_cap, M);
   const CUtensorMap* tm_attn = xmap(ctx, m.attn, m.H * m.Dh, m.m_cap, M);
   const CUtensorMap* tm_act = xmap(ctx, m.act, m.ff, m.m_cap, M);
@@ -1063,6 +1065,12 @@ int free_slot(seed_ctx ctx) {
 }  // namespace
 
 // ====================================================================== C ABI
+namespace {
+seed_status decoder_layer_impl(const seed_model_shape* shape, const void* const* w, const float* x_in, int32_t M,
+                               int32_t ctx_len, const int32_t* parent, const void* k_prev, const void* v_prev,
+                               float* x_out, void* k_new, void* v_new, void* stream);
+}  // namespace
+
 extern "C" {
 
 const char* seed_last_error(seed_ctx ctx) { return ctx ? ctx->err.c_str() : "null context"; }
@@ -1657,10 +1665,40 @@ seed_status seed_op_verify_tree(const float* zt, const float* zd, const int32_t*
   return ok ? SEED_OK : SEED_ECUDA;
 }
 
+seed_status seed_op_decoder_layer_tree(const seed_model_shape* shape, const void* const* w, const float* x_in,
+                                       int32_t M, int32_t ctx_len, const int32_t* parent, const void* k_prev,
+                                       const void* v_prev, float* x_out, void* k_new, void* v_new, void* stream) {
+  return decoder_layer_impl(shape, w, x_in, M, ctx_len, parent, k_prev, v_prev, x_out, k_new, v_new, stream);
+}
+
 seed_status seed_op_decoder_layer(const seed_model_shape* shape, const void* const* w, const float* x_in, int32_t M,
                                   int32_t ctx_len, const void* k_prev, const void* v_prev, float* x_out, void* k_new,
                                   void* v_new, void* stream) {
+  return decoder_layer_impl(shape, w, x_in, M, ctx_len, nullptr, k_prev, v_prev, x_out, k_new, v_new, stream);
+}
+
+}  // extern "C"
+
+namespace {
+// one decoder layer on M rows of one sequence after ctx_len cached keys; parent (host, optional):
+// the rows form a tree (row 0 the root, parent[i] < i) -- RoPE position ctx_len + depth, attention
+// to the cached keys and the row's ancestors and itself (Figure 7, R36)
+seed_status decoder_layer_impl(const seed_model_shape* shape, const void* const* w, const float* x_in, int32_t M,
+                               int32_t ctx_len, const int32_t* parent, const void* k_prev, const void* v_prev,
+                               float* x_out, void* k_new, void* v_new, void* stream) {
   if (!shape || !w || !x_in || !x_out || M < 1 || M > kMaxChunkRows || ctx_len < 0) return SEED_EINVAL;
+  if (parent && M > 64) return SEED_EINVAL;
+  std::vector<int32_t> tpos;
+  std::vector<uint64_t> tanc;
+  if (parent) {
+    tpos.resize(M);
+    tanc.resize(M);
+    for (int i = 0; i < M; ++i) {
+      if ((i == 0) != (parent[i] < 0) || parent[i] >= i) return SEED_EINVAL;
+      tpos[i] = i == 0 ? ctx_len : tpos[parent[i]] + 1;
+      tanc[i] = (i == 0 ? 0ull : tanc[parent[i]]) | (1ull << i);
+    }
+  }
   if (ctx_len > 0 && (!k_prev || !v_prev)) return SEED_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   // a throw-away context holding a one-layer model (weights packed exactly as seed_init does)
@@ -1694,7 +1732,18 @@ seed_status seed_op_decoder_layer(const seed_model_shape* shape, const void* con
     ChunkDesc c;
     size_t tok_off;
     pack_chunk(ctx, segs, 0, &c, &tok_off);
-    if (ctx->arena.upload(st) != cudaSuccess) s = SEED_ECUDA;
+    if (parent) {   // per-row tree positions and ancestor masks in the descriptor arena
+      const size_t o_p = ctx->arena.alloc(M), o_a = ctx->arena.alloc(2 * M + 2);
+      if (o_a == (size_t)-1) s = SEED_ENOMEM;
+      if (s == SEED_OK) {
+        const size_t o_a8 = (o_a + 1) & ~(size_t)1;   // 8-byte aligned
+        std::memcpy(ctx->arena.host + o_p, tpos.data(), (size_t)M * 4);
+        std::memcpy(ctx->arena.host + o_a8, tanc.data(), (size_t)M * 8);
+        c.row_pos = ctx->arena.dev + o_p;
+        c.anc = reinterpret_cast<const uint64_t*>(ctx->arena.dev + o_a8);
+      }
+    }
+    if (s == SEED_OK && ctx->arena.upload(st) != cudaSuccess) s = SEED_ECUDA;
     const float eps = sh.rms_eps > 0 ? sh.rms_eps : 1e-5f;
     if (s == SEED_OK && cudaMemcpyAsync(m.x, x_in, (size_t)M * m.d * 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
       s = SEED_ECUDA;
@@ -1730,5 +1779,4 @@ seed_status seed_op_decoder_layer(const seed_model_shape* shape, const void* con
   delete ctx;
   return s;
 }
-
-}  // extern "C"
+}  // namespace

@@ -100,6 +100,11 @@ struct SeqInfo {          // per sequence of the ragged batch (device arrays)
   const int32_t* kv_len;  // keys after append = pos(last row) + 1
   const int32_t* slot;
   const int32_t* stable;  // keys written before the round (safe to prefetch early); may be null
+  // tree rows (k_config verification, R36; both null for causal rows): per chunk row, the RoPE
+  // position and the bit mask of the sequence's new rows it attends to (bit j = new row j; the
+  // cached keys are always visible).  A sequence then has at most 64 new rows.
+  const int32_t* row_pos = nullptr;
+  const uint64_t* anc = nullptr;
 };
 struct AttnWorkspace {
   float* o_part;   // [splits][M][H][Dh]

@@ -82,6 +82,25 @@ def decoder_layer(shape, L, x_in, ctx_len, k_prev=None, v_prev=None):
     return x_out, k_new, v_new
 
 
+def decoder_layer_tree(shape, L, x_in, ctx_len, parent, k_prev=None, v_prev=None):
+    """One decoder layer over a tree of rows (parent[0] = -1, parent[i] < i): row i at position
+    ctx_len + depth(i), attending to the cache and its ancestors; returns (x_out, k_new, v_new)."""
+    from . import LAYER_KEYS, model_shape
+    M, d = x_in.shape
+    hk = shape.get("n_kv_heads", 0) or shape["n_heads"]
+    dh = d // shape["n_heads"]
+    ptrs = (C.c_void_p * 9)(*[L[k].data_ptr() for k in LAYER_KEYS])
+    sh = model_shape(shape)
+    par = np.ascontiguousarray(np.asarray(parent, dtype=np.int32))
+    x_out = torch.empty_like(x_in)
+    k_new = torch.empty((M, hk, dh), dtype=torch.bfloat16, device=x_in.device)
+    v_new = torch.empty_like(k_new)
+    check(_lib.load().seed_op_decoder_layer_tree(C.byref(sh), ptrs, _p(x_in.contiguous()), M, int(ctx_len),
+                                                 par.ctypes.data_as(_lib._I32P), _p(k_prev), _p(v_prev), _p(x_out),
+                                                 _p(k_new), _p(v_new), _s()), None, "seed_op_decoder_layer_tree")
+    return x_out, k_new, v_new
+
+
 def draft_topk(z, temperature, seed, sids, rs, node, m):
     """K1T: the m children of `node` for each row of z [B][V] fp32 CUDA -> int32 [B][m] (draw order)."""
     B, V = z.shape

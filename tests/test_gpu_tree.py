@@ -97,3 +97,38 @@ def test_all_ones_tree_equals_chain_kernel(ops):
                        torch.from_numpy(tok[:, 1:].copy()).cuda(), T, SEED, sids, rs, want_dbg=False)
     assert torch.equal(tree["out_cnt"], chain["out_cnt"])
     assert torch.equal(tree["out_tok"], chain["out_tok"])
+
+
+def _rel_rows(a, b):
+    return (np.abs(a - b).max(axis=-1) / np.maximum(np.abs(b).max(axis=-1), 1e-30))
+
+
+@pytest.mark.parametrize("name,counts,ctx", [("toy_target", (2, 2, 1), 37), ("llama_68m", (3, 1), 300),
+                                             ("llama2_7b", (2, 2, 1), 290), ("llama2_7b", (4, 2, 1), 129),
+                                             ("llama2_7b", (1, 1, 1, 1), 200)])
+def test_tree_layer_vs_oracle(ops, name, counts, ctx):
+    """Tree attention (Figure 7): the GPU layer over a k_config tree (root + BFS nodes, RoPE at
+    ctx + depth, ancestor mask) against the oracle's per-path causal layers; 2e-2 relative per row
+    (bf16 GEMMs, like the decoder-layer test)."""
+    from oracle import llama as ll
+    parent, _ = tr.tree_shape(counts)
+    M = len(parent)
+    shape = seedgen.SHAPES[name]
+    sh = ll.LlamaShape(**shape)
+    L = seedgen.layer_weights(shape, 77, 0)
+    x = seedgen.hidden_states(M, sh.d_model, seed=M + ctx)
+    hk, dh = sh.kv_heads, sh.head_dim
+    kp = seedgen.bf16_matrix(ctx, hk * dh, seed=ctx + 1, std=1.0).reshape(ctx, hk, dh)
+    vp = seedgen.bf16_matrix(ctx, hk * dh, seed=ctx + 2, std=1.0).reshape(ctx, hk, dh)
+    x_out, k_new, v_new = ops.decoder_layer_tree(shape, {k: v.cuda() for k, v in L.items()},
+                                                 torch.from_numpy(x).cuda(), ctx, parent, kp.cuda().contiguous(),
+                                                 vp.cuda().contiguous())
+    ref_x, ref_k, ref_v = tr.tree_layer_forward(sh, L, x, parent, ctx, kp.double().numpy(), vp.double().numpy(),
+                                                mode="bf16")
+    assert _rel_rows(x_out.double().cpu().numpy() - x, ref_x - x).max() < 2e-2
+    assert _rel_rows(k_new.double().cpu().numpy().reshape(M, -1), ref_k.reshape(M, -1)).max() < 2e-2
+    assert _rel_rows(v_new.double().cpu().numpy().reshape(M, -1), ref_v.reshape(M, -1)).max() < 2e-2
+    if all(c == 1 for c in counts):   # the chain tree is the causal layer bit for bit
+        xo, kn, vn = ops.decoder_layer(shape, {k: v.cuda() for k, v in L.items()}, torch.from_numpy(x).cuda(), ctx,
+                                       kp.cuda().contiguous(), vp.cuda().contiguous())
+        assert torch.equal(xo, x_out) and torch.equal(kn, k_new) and torch.equal(vn, v_new)

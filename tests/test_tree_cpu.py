@@ -226,3 +226,29 @@ def test_more_candidates_accept_more():
     m2, s2 = mean_acc((2, 1, 1))
     assert m2 >= m1 - 3 * math.hypot(s1, s2), (m1, m2)
     assert m2 > m1
+
+
+def test_tree_layer_chain_is_causal_layer():
+    """A chain-shaped tree (parent[i] = i - 1) is the causal layer over the same rows, and a row's
+    output does not depend on rows outside its path (siblings swapped -> same outputs)."""
+    import seedgen
+    from oracle import llama as ll
+    shape = seedgen.SHAPES["toy_target"]
+    sh = ll.LlamaShape(**shape)
+    L = seedgen.layer_weights(shape, 77, 0)
+    M, ctx = 5, 7
+    x = seedgen.hidden_states(M, sh.d_model, seed=3)
+    kc = np.random.default_rng(1).standard_normal((ctx, sh.kv_heads, sh.head_dim))
+    vc = np.random.default_rng(2).standard_normal((ctx, sh.kv_heads, sh.head_dim))
+    got = tr.tree_layer_forward(sh, L, x, [-1, 0, 1, 2, 3], ctx, kc, vc, mode="fp64")
+    ref = ll.layer_forward(sh, L, x, np.arange(ctx, ctx + M), kc, vc, mode="fp64")
+    for a, b in zip(got, ref):
+        assert np.allclose(a, b, rtol=0, atol=1e-12)
+    # star tree: rows 1..4 children of the root; reordering the children permutes their outputs only
+    star = tr.tree_layer_forward(sh, L, x, [-1, 0, 0, 0, 0], ctx, kc, vc, mode="fp64")[0]
+    perm = [0, 3, 1, 4, 2]
+    star_p = tr.tree_layer_forward(sh, L, x[perm], [-1, 0, 0, 0, 0], ctx, kc, vc, mode="fp64")[0]
+    assert np.allclose(star_p, star[perm], rtol=0, atol=1e-12)
+    # and a child of the root equals the two-row causal layer [root, child]
+    two = ll.layer_forward(sh, L, x[[0, 2]], np.arange(ctx, ctx + 2), kc, vc, mode="fp64")[0]
+    assert np.allclose(star[2], two[1], rtol=0, atol=1e-12)
