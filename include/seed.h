@@ -99,6 +99,13 @@ typedef struct {
   int32_t rank, world;                   /* data-parallel replica index / count (replicas, R20) */
   const void* nccl_id;                   /* 128-byte ncclUniqueId (same on all ranks) or NULL if world == 1 */
   uint32_t flags;                        /* SEED_FLAG_* */
+  /* k_config tree rounds (§3.2, App. B; R36): n_tree = 0 runs
+   * the chain; n_tree = K > 0 drafts a tree with tree_counts[d] candidates per node at depth d
+   * (1..8 each), verified by one target pass with tree attention and recursive rejection.  gamma
+   * must equal K; the tree holds at most 64 rows (root + nodes).  Tokens are emitted like the chain's
+   * (at most K + 1 per round) and the accepted path's KV is compacted in place. */
+  int32_t n_tree;
+  int32_t tree_counts[8];
 } seed_config;
 
 /* Validates shapes, packs weights (R18), allocates the KV pool and scratch, builds TMA

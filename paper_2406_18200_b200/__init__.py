@@ -60,8 +60,11 @@ class SeedEngine:
 
     def __init__(self, draft_shape, draft_w, target_shape, target_w, gamma, temperature, seed, bonus=True,
                  max_new=64, max_streams=8, max_batch=8, max_ctx=2048, page_tokens=16, kv_pool_bytes=0,
-                 rank=0, world=1, nccl_id=None, profile=False):
+                 rank=0, world=1, nccl_id=None, profile=False, tree=None):
         self.lib = _lib.load()
+        if tree:   # k_config tree rounds (R36): gamma is the tree depth
+            gamma = len(tree)
+        self.tree = tuple(int(c) for c in tree) if tree else None
         self.gamma, self.vocab = int(gamma), int(target_shape["vocab"])
         keep = []
         cfg = _lib.Config()
@@ -74,6 +77,10 @@ class SeedEngine:
         self._nccl_id = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
         cfg.nccl_id = C.cast(self._nccl_id, C.c_void_p) if self._nccl_id is not None else None
         cfg.flags = FLAG_PROFILE if profile else 0
+        if self.tree:
+            cfg.n_tree = len(self.tree)
+            for i, c in enumerate(self.tree):
+                cfg.tree_counts[i] = c
         torch.cuda.synchronize()
         ctx = C.c_void_p()
         st = self.lib.seed_init(C.byref(cfg), C.byref(ctx))
@@ -160,10 +167,18 @@ class SeedEngine:
         return out
 
     def last_round(self, n):
-        """(target logits [n][g+1][V], draft logits [n][g][V], draft tokens [n][g]) copies (device)."""
+        """(target logits [n][g+1][V], draft logits [n][g][V], draft tokens [n][g]) copies (device);
+        tree rounds: (target [n][rows][V], draft [n][rows][V], root + node tokens [n][rows])."""
         t, d, x = C.c_void_p(), C.c_void_p(), C.c_void_p()
         self._check(self.lib.seed_last_round_buffers(self.ctx, C.byref(t), C.byref(d), C.byref(x)), "buffers")
         g, V = self.gamma, self.vocab
+        if self.tree:
+            rows, lvl = 1, 1
+            for c in self.tree:
+                lvl *= c
+                rows += lvl
+            return (_wrap(t.value, (n, rows, V), torch.float32), _wrap(d.value, (n, rows, V), torch.float32),
+                    _wrap(x.value, (n, rows), torch.int32))
         return (_wrap(t.value, (n, g + 1, V), torch.float32), _wrap(d.value, (n, g, V), torch.float32),
                 _wrap(x.value, (n, g), torch.int32))
 

@@ -36,7 +36,8 @@ class Config(C.Structure):
                 ("gamma", C.c_int32), ("temperature", C.c_float), ("seed", C.c_uint64), ("bonus", C.c_int32),
                 ("max_new_tokens", C.c_int32), ("max_streams", C.c_int32), ("max_batch", C.c_int32),
                 ("max_ctx", C.c_int32), ("page_tokens", C.c_int32), ("kv_pool_bytes", C.c_int64),
-                ("rank", C.c_int32), ("world", C.c_int32), ("nccl_id", C.c_void_p), ("flags", C.c_uint32)]
+                ("rank", C.c_int32), ("world", C.c_int32), ("nccl_id", C.c_void_p), ("flags", C.c_uint32),
+                ("n_tree", C.c_int32), ("tree_counts", C.c_int32 * 8)]
 
 
 _P = C.c_void_p

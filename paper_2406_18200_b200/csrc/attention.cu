@@ -241,7 +241,9 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __rest
 
   // ---- the warp's tiles, online softmax over them (rows g, g + 8 of the MMA fragments)
   const int g = lane >> 2, t4 = lane & 3;
-  // tree rows: the new rows each row attends to (rows g, g + 8 of the fragments; 0 = causal row)
+  // tree rows: the tree rows each row attends to (rows g, g + 8 of the fragments; 0 = causal row);
+  // bit j = cache slot tbase + j
+  const int tbase = seqs.tree_base ? seqs.tree_base[seq] : new_first;
   uint64_t anc_rows[2] = {0ull, 0ull};
   if (seqs.anc) {
 #pragma unroll
@@ -332,7 +334,7 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __rest
         for (int c = 0; c < 2; ++c) {
           const int key = t0 + nt * 8 + 2 * t4 + c;
           const bool ok = r < nr && key < k_hi &&
-                          (anc_r ? (key < new_first || ((anc_r >> (key - new_first)) & 1ull)) : key <= pos0 + r);
+                          (anc_r ? (key < tbase || ((anc_r >> (key - tbase)) & 1ull)) : key <= pos0 + r);
           float& v = sc[nt][2 * h2 + c];
           v = ok ? (v + s2[nt][2 * h2 + c]) * scale : -INFINITY;
           mx = fmaxf(mx, v);

@@ -150,8 +150,10 @@ struct SlotState {  // one stream slot; the validated tokens live in the round b
 struct ChunkDesc {
   int M, n_seq, max_q_len, max_kv;
   const int32_t *pos, *slot, *q_start, *q_len, *kv_len, *seq_slot, *seq_stable, *compact;  // device (slot: per row)
-  const int32_t* row_pos = nullptr;   // tree rows (R36): per-row RoPE positions and attended new rows
+  const int32_t* row_pos = nullptr;   // tree rows (R36): per-row RoPE positions and attended tree rows
   const uint64_t* anc = nullptr;
+  const int32_t* tree_base = nullptr; // per sequence: cache slot of the tree's root (bit 0 of anc)
+  bool rowmap = false;                // logits rows through `compact` even when every row has logits
   TokSrc tok;
   int n_logits;
   const int32_t* logit_rows;  // device [n_logits]: chunk row of each logits row
@@ -216,6 +218,17 @@ struct seed_ctx_s {
   bool draft_called = false;        // seed_draft_round called for `drafted` (n may be 0 when world > 1)
   RoundPlan plan;
   bool round_pending = false;
+  // k_config tree rounds (R36; tree.n == 0: chain rounds)
+  struct Tree {
+    int n = 0, nn = 1;                       // levels K, rows per stream (root + nodes)
+    std::vector<int> counts, parent, depth, first, cnt, lvl_start, lvl_len;
+    std::vector<uint64_t> anc;
+    int32_t* ch_dev = nullptr;               // device [2][nn]: first child, child count (K4T)
+    int32_t* tok_lvl = nullptr;              // device: draft input tokens of levels 2..K, level-major [B][len]
+    std::vector<size_t> lvl_off;             // offset of level d's block in tok_lvl
+    int32_t* tree_tok = nullptr;             // device [C][nn]: root + node tokens (verify input)
+    int32_t* out_node = nullptr;             // device [C][K]: accepted nodes (-1 pad)
+  } tree;
   // NCCL
   void* comm = nullptr;
   // CUDA graphs of the round, one pair per batch size (R23)
@@ -465,6 +478,9 @@ void free_model(Model& m) {
 }
 
 // make sure `slot` holds pages for positions [0, n_tokens)
+// cache positions a round may write past |T| - 1: gamma + 1 (chain) or every tree row
+int round_rows(seed_ctx ctx) { return ctx->tree.n > 0 ? std::max(ctx->tree.nn, ctx->cfg.gamma + 1) : ctx->cfg.gamma + 1; }
+
 seed_status ensure_pages(seed_ctx ctx, Model& m, int slot, int n_tokens, cudaStream_t st) {
   const int need = (n_tokens + ctx->P - 1) / ctx->P;
   if (need > ctx->max_pages) return fail(ctx, SEED_ECAPACITY, "KV", "context longer than max_ctx");
@@ -508,7 +524,7 @@ seed_status forward_chunk(seed_ctx ctx, Model& m, const ChunkDesc& c, cudaStream
                        first_layer < m.L ? m.an[first_layer] : m.final_norm, m.h, ctx->dev_err, st,
                        next_rec(ctx)));
   ctx->kernel_launches++;
-  seed::SeqInfo seqs{c.q_start, c.q_len, c.kv_len, c.seq_slot, c.seq_stable, c.row_pos, c.anc};
+  seed::SeqInfo seqs{c.q_start, c.q_len, c.kv_len, c.seq_slot, c.seq_stable, c.row_pos, c.anc, c.tree_base};
   const CUtensorMap* tm_h = xmap(ctx, m.h, m.d, m.m_cap, M);
   const CUtensorMap* tm_attn = xmap(ctx, m.attn, m.H * m.Dh, m.m_cap, M);
   const CUtensorMap* tm_act = xmap(ctx, m.act, m.ff, m.m_cap, M);
@@ -577,7 +593,7 @@ seed_status forward_chunk(seed_ctx ctx, Model& m, const ChunkDesc& c, cudaStream
     seed::GemmIO io = norm_io(m.ssq_b);
     io.Y = c.Y;
     io.ldY = c.ldY;
-    io.yrow = c.n_logits == M ? nullptr : c.compact;
+    io.yrow = c.n_logits == M && !c.rowmap ? nullptr : c.compact;
     if (!io.yrow) io.tmY = ymap(ctx, c.Y, true, m.V, c.ldY, M);
     if ((s = run_gemm(ctx, m.plm, M, io, st)) != SEED_OK) return s;
   }
@@ -736,6 +752,123 @@ seed_status map_batch(seed_ctx ctx, const int32_t* ids, int n, std::vector<int>&
 // All descriptors of a round (draft steps and verify chunks) are packed into the arena at
 // offsets that depend on the batch size only, so the captured graph of a batch size can be
 // replayed with fresh descriptor contents (R23).
+// Tree round descriptors (R36): level 1 = the chain's draft step 1 (T[-2], T[-1]: the root's draft
+// row); level d = 2..K = the depth d - 1 nodes of every stream as tree rows (RoPE at the root's
+// position + depth, attention to the context and the row's ancestors; the node's K/V at cache
+// position root + node); the verify chunk = root + every node as tree rows.  Node logits rows go to
+// [stream][node][V] through the row map.
+seed_status build_tree_plan(seed_ctx ctx, const std::vector<const seed::BookStream*>& bs, const std::vector<int>& slots,
+                            RoundPlan& P, int max_pos) {
+  auto& TR = ctx->tree;
+  Arena& A = ctx->arena;
+  const int n = P.n, K = TR.n, nn = TR.nn, V = ctx->cfg.target.vocab;
+  size_t tok_off;
+  // tree-row descriptors of a chunk whose segment b holds the tree rows [row0, row0 + len) of stream b
+  auto tree_rows = [&](ChunkDesc& c, int row0, int len, bool map_logits) -> bool {
+    const int M = n * len;
+    const size_t o_p = A.alloc(M), o_b = A.alloc(n), o_a = A.alloc(2 * M + 2);
+    if (o_a == (size_t)-1) return false;
+    const size_t o_a8 = (o_a + 1) & ~(size_t)1;
+    for (int b = 0; b < n; ++b) {
+      const int root = (int)bs[b]->T.size() - 1;
+      A.host[o_b + b] = root;
+      for (int k = 0; k < len; ++k) {
+        const int node = row0 + k, r = b * len + k;
+        A.host[o_p + r] = root + TR.depth[node];
+        std::memcpy(A.host + o_a8 + 2 * r, &TR.anc[node], 8);
+      }
+    }
+    c.row_pos = A.dev + o_p;
+    c.tree_base = A.dev + o_b;
+    c.anc = reinterpret_cast<const uint64_t*>(A.dev + o_a8);
+    if (map_logits) {   // chunk row (b, k) -> logits row b * nn + row0 + k
+      const size_t o_c = A.alloc(M);
+      if (o_c == (size_t)-1) return false;
+      for (int b = 0; b < n; ++b)
+        for (int k = 0; k < len; ++k) A.host[o_c + b * len + k] = b * nn + row0 + k;
+      c.compact = A.dev + o_c;
+      c.rowmap = true;
+    }
+    return true;
+  };
+  P.draft.assign(K, ChunkDesc{});
+  std::vector<Segment> segs(n);
+  for (int b = 0; b < n; ++b) {
+    const int T = (int)bs[b]->T.size();
+    const size_t to = A.alloc(2);
+    if (to == (size_t)-1) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
+    A.host[to] = bs[b]->T[T - 2];
+    A.host[to + 1] = bs[b]->T[T - 1];
+    segs[b] = Segment{slots[b], T - 2, 2, (int)to, T - 2};
+  }
+  if (2 * n > ctx->tm.m_cap || 2 * n > ctx->dm.m_cap || !pack_chunk(ctx, segs, 2, &P.draft[0], &tok_off))
+    return fail(ctx, SEED_ECAPACITY, "seed_draft_round", "batch too large");
+  P.draft[0].Y = ctx->drf_logits;               // the root's draft row: [b][node 0]
+  P.draft[0].ldY = nn * V;
+  for (int d = 2; d <= K; ++d) {
+    const int row0 = TR.lvl_start[d - 1], len = TR.lvl_len[d - 1];
+    if (n * len > ctx->dm.m_cap) return fail(ctx, SEED_ECAPACITY, "seed_draft_round", "tree level too wide");
+    for (int b = 0; b < n; ++b) {
+      const int T = (int)bs[b]->T.size();
+      segs[b] = Segment{slots[b], T - 1 + row0, len, -1, T - 2};
+    }
+    ChunkDesc& c = P.draft[d - 1];
+    if (!pack_chunk(ctx, segs, 1, &c, &tok_off) || !tree_rows(c, row0, len, true))
+      return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
+    c.tok = TokSrc{TR.tok_lvl + TR.lvl_off[d], 1};
+    c.Y = ctx->drf_logits;
+    c.ldY = V;
+  }
+  // verify chunks of whole streams: root + nodes
+  const int per_chunk = std::max(1, ctx->tm.m_cap / nn);
+  for (int b0 = 0; b0 < n; b0 += per_chunk) {
+    const int nb = std::min(per_chunk, n - b0);
+    std::vector<Segment> vs(nb);
+    for (int b = 0; b < nb; ++b) {
+      const int T = (int)bs[b0 + b]->T.size();
+      vs[b] = Segment{slots[b0 + b], T - 1, nn, -1, T - 1};
+    }
+    ChunkDesc c;
+    std::vector<const seed::BookStream*> sub(bs.begin() + b0, bs.begin() + b0 + nb);
+    if (!pack_chunk(ctx, vs, 1, &c, &tok_off)) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
+    {
+      const int M = nb * nn;
+      const size_t o_p = A.alloc(M), o_b = A.alloc(nb), o_a = A.alloc(2 * M + 2);
+      if (o_a == (size_t)-1) return fail(ctx, SEED_ENOMEM, "arena", "descriptors");
+      const size_t o_a8 = (o_a + 1) & ~(size_t)1;
+      for (int b = 0; b < nb; ++b) {
+        const int root = (int)sub[b]->T.size() - 1;
+        A.host[o_b + b] = root;
+        for (int k = 0; k < nn; ++k) {
+          A.host[o_p + b * nn + k] = root + TR.depth[k];
+          std::memcpy(A.host + o_a8 + 2 * (b * nn + k), &TR.anc[k], 8);
+        }
+      }
+      c.row_pos = A.dev + o_p;
+      c.tree_base = A.dev + o_b;
+      c.anc = reinterpret_cast<const uint64_t*>(A.dev + o_a8);
+    }
+    c.tok = TokSrc{TR.tree_tok + (size_t)b0 * nn, 1};
+    c.Y = ctx->tgt_logits + (size_t)b0 * nn * V;
+    c.ldY = V;
+    P.verify.push_back(c);
+    P.verify_b0.push_back(b0);
+  }
+  const int chd = seed::attn_chunk_tokens(ctx->dm.Dh), cht = seed::attn_chunk_tokens(ctx->tm.Dh);
+  int dk = 0, vk = 0;
+  for (auto& c : P.draft) dk = std::max(dk, c.max_kv);
+  for (auto& c : P.verify) vk = std::max(vk, c.max_kv);
+  P.dk_raw = dk;
+  P.vk_raw = vk;
+  dk = std::min(max_pos, (dk + chd - 1) / chd * chd);
+  vk = std::min(max_pos, (vk + cht - 1) / cht * cht);
+  for (auto& c : P.draft) c.max_kv = dk;
+  for (auto& c : P.verify) c.max_kv = vk;
+  P.key_draft = ((int64_t)n << 32) | (dk / chd);
+  P.key_verify = ((int64_t)n << 32) | (vk / cht);
+  return SEED_OK;
+}
+
 seed_status build_round_plan(seed_ctx ctx, const std::vector<int32_t>& ids, const std::vector<int>& slots,
                              RoundPlan& P) {
   const int g = ctx->cfg.gamma, n = (int)ids.size();
@@ -762,7 +895,8 @@ seed_status build_round_plan(seed_ctx ctx, const std::vector<int32_t>& ids, cons
   P.verify_b0.clear();
   P.key_draft = P.key_verify = 0;
   if (n == 0) return SEED_OK;   // a rank with nothing to run still joins the exchange (world > 1)
-  const int max_pos = ctx->cfg.max_ctx + g + 2;
+  const int max_pos = ctx->cfg.max_ctx + std::max(g, ctx->tree.n > 0 ? ctx->tree.nn : g + 1) + 2;
+  if (ctx->tree.n > 0) return build_tree_plan(ctx, bs, slots, P, max_pos);
   // draft step 1 feeds (T[-2], T[-1]); when one token is pending the first row rewrites an
   // existing entry with identical values (R22), so M = 2n every round
   P.draft.assign(g, ChunkDesc{});
@@ -831,9 +965,36 @@ seed_status enqueue_draft(seed_ctx ctx, cudaStream_t st) {
   CK(cudaMemcpyAsync(ctx->sids_dev, A.dev + P.o_sid, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(ctx->rs_dev, A.dev + P.o_r, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(ctx->slots_dev, A.dev + P.o_sl, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+  const uint32_t k0 = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu), k1 = (uint32_t)(ctx->cfg.seed >> 32);
+  if (ctx->tree.n > 0) {
+    // tree drafting (R36): level by level, every node's children are the top-m of its draft row's
+    // race (K1T, slot node + 1), written as the next level's input and into the verify rows
+    auto& TR = ctx->tree;
+    const int nn = TR.nn, K = TR.n;
+    CK(cudaMemcpy2DAsync(TR.tree_tok, (size_t)nn * 4, A.dev + P.o_last, 4, 4, n, cudaMemcpyDeviceToDevice, st));
+    for (int d = 1; d <= K; ++d) {
+      if ((s = forward_chunk(ctx, ctx->dm, P.draft[d - 1], st)) != SEED_OK) return s;
+      const int row0 = TR.lvl_start[d - 1], len = TR.lvl_len[d - 1], m = TR.counts[d - 1];
+      for (int k = 0; k < len; ++k) {
+        const int node = row0 + k;
+        int32_t* nxt = d < K ? TR.tok_lvl + TR.lvl_off[d + 1] : nullptr;   // level d + 1 rows: [b][len * m]
+        int32_t* vrow = TR.tree_tok + TR.first[node];                      // verify rows: children of `node`
+        if (nxt) {
+          CK(seed::draft_topk(ctx->drf_logits + (size_t)node * V, (long)nn * V, n, V, ctx->cfg.temperature, k0, k1,
+                              ctx->sids_dev, ctx->rs_dev, node, m, nxt, len * m, k * m, vrow - k * m, nn,
+                              ctx->dev_err, st, next_rec(ctx)));
+        } else {
+          CK(seed::draft_topk(ctx->drf_logits + (size_t)node * V, (long)nn * V, n, V, ctx->cfg.temperature, k0, k1,
+                              ctx->sids_dev, ctx->rs_dev, node, m, vrow, nn, 0, nullptr, 0, ctx->dev_err, st,
+                              next_rec(ctx)));
+        }
+        ctx->kernel_launches++;
+      }
+    }
+    return SEED_OK;
+  }
   // verify input column 0 = T[-1]
   CK(cudaMemcpy2DAsync(ctx->vtok, (size_t)(g + 1) * 4, A.dev + P.o_last, 4, 4, n, cudaMemcpyDeviceToDevice, st));
-  const uint32_t k0 = (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu), k1 = (uint32_t)(ctx->cfg.seed >> 32);
   for (int j = 1; j <= g; ++j) {
     ChunkDesc& c = P.draft[j - 1];
     c.Y = ctx->drf_logits + (size_t)(j - 1) * V;
@@ -853,7 +1014,20 @@ seed_status enqueue_verify(seed_ctx ctx, cudaStream_t st) {
   seed_status s;
   for (auto& c : P.verify)
     if ((s = forward_chunk(ctx, ctx->tm, c, st)) != SEED_OK) return s;
-  if (n > 0) {
+  if (n > 0 && ctx->tree.n > 0) {
+    // a4 on a tree: K4T (recursive rejection over each node's candidates), then the accepted path's
+    // K/V compacted into consecutive positions of both caches (the draft holds nodes to depth K - 1)
+    auto& TR = ctx->tree;
+    CK(seed::verify_tree(ctx->tgt_logits, (long)TR.nn * V, ctx->drf_logits, (long)TR.nn * V, TR.tree_tok, TR.nn,
+                         TR.ch_dev, TR.ch_dev + TR.nn, n, TR.n, V, ctx->cfg.temperature,
+                         (uint32_t)(ctx->cfg.seed & 0xFFFFFFFFu), (uint32_t)(ctx->cfg.seed >> 32), ctx->sids_dev,
+                         ctx->rs_dev, ctx->cfg.bonus, ctx->out_tok, ctx->out_cnt, TR.out_node, ctx->dev_err, st,
+                         next_rec(ctx)));
+    CK(seed::kv_compact(ctx->tm.kv, ctx->slots_dev, ctx->ds.tlen, TR.out_node, TR.n, TR.n, n, st, next_rec(ctx)));
+    if (TR.n > 1)
+      CK(seed::kv_compact(ctx->dm.kv, ctx->slots_dev, ctx->ds.tlen, TR.out_node, TR.n, TR.n - 1, n, st, next_rec(ctx)));
+    ctx->kernel_launches += TR.n > 1 ? 3 : 2;
+  } else if (n > 0) {
     // a4: K4 fused vocabulary kernel
     seed::VerifyArgs a{};
     a.zt = ctx->tgt_logits;
@@ -1109,10 +1283,58 @@ seed_status seed_init(const seed_config* cfg, seed_ctx* out) {
   ctx->C = std::min(cfg->max_batch, cfg->max_streams);
   ctx->profile = (cfg->flags & SEED_FLAG_PROFILE) != 0;
   const int g = cfg->gamma;
-  const int max_pos = cfg->max_ctx + g + 2;
+  // k_config tree (R36): breadth-first shape, ancestor masks, level spans
+  auto& TR = ctx->tree;
+  if (cfg->n_tree < 0 || cfg->n_tree > 8 || (cfg->n_tree > 0 && cfg->n_tree != g)) {
+    delete ctx;
+    return SEED_EINVAL;
+  }
+  if (cfg->n_tree > 0) {
+    TR.n = cfg->n_tree;
+    TR.parent = {-1};
+    TR.depth = {0};
+    TR.lvl_start = {0};
+    TR.lvl_len = {1};
+    std::vector<int> level{0};
+    for (int d = 0; d < TR.n; ++d) {
+      const int m = cfg->tree_counts[d];
+      if (m < 1 || m > 8) {
+        delete ctx;
+        return SEED_EINVAL;
+      }
+      TR.counts.push_back(m);
+      std::vector<int> nxt;
+      TR.lvl_start.push_back((int)TR.parent.size());
+      for (int p : level)
+        for (int i = 0; i < m; ++i) {
+          TR.parent.push_back(p);
+          TR.depth.push_back(d + 1);
+          nxt.push_back((int)TR.parent.size() - 1);
+        }
+      TR.lvl_len.push_back((int)nxt.size());
+      level = nxt;
+      if (TR.parent.size() > 64) {
+        delete ctx;
+        return SEED_EINVAL;
+      }
+    }
+    TR.nn = (int)TR.parent.size();
+    TR.first.assign(TR.nn, 0);
+    TR.cnt.assign(TR.nn, 0);
+    TR.anc.assign(TR.nn, 0);
+    for (int i = 0; i < TR.nn; ++i) {
+      TR.anc[i] = (i == 0 ? 0ull : TR.anc[TR.parent[i]]) | (1ull << i);
+      if (i > 0) {
+        const int p = TR.parent[i];
+        if (TR.cnt[p]++ == 0) TR.first[p] = i;
+      }
+    }
+  }
+  const int rows = TR.n > 0 ? TR.nn : g + 1;   // verify rows per stream
+  const int max_pos = cfg->max_ctx + std::max(g, rows) + 2;
   ctx->max_pages = (max_pos + ctx->P - 1) / ctx->P;
   ctx->n_slots = cfg->max_streams + 1;  // + one scratch slot for seed_forward_logits / ops
-  const int m_cap = std::min(kMaxChunkRows, std::max(ctx->C * (g + 1), 2 * ctx->C));
+  const int m_cap = std::min(kMaxChunkRows, std::max(ctx->C * rows, 2 * ctx->C));
   auto pool_pages_for = [&](const seed_model_shape& sh) -> size_t {
     const size_t full = (size_t)ctx->n_slots * ctx->max_pages;
     if (cfg->kv_pool_bytes <= 0) return full;
@@ -1138,8 +1360,24 @@ seed_status seed_init(const seed_config* cfg, seed_ctx* out) {
   const int V = cfg->target.vocab, C = ctx->C, S = ctx->n_slots;
   ctx->slots.resize(S);
   bool ok = true;
-  ok &= cudaMalloc(&ctx->tgt_logits, (size_t)C * (g + 1) * V * 4) == cudaSuccess;
-  ok &= cudaMalloc(&ctx->drf_logits, (size_t)C * g * V * 4) == cudaSuccess;
+  ok &= cudaMalloc(&ctx->tgt_logits, (size_t)C * rows * V * 4) == cudaSuccess;
+  ok &= cudaMalloc(&ctx->drf_logits, (size_t)C * (TR.n > 0 ? TR.nn : g) * V * 4) == cudaSuccess;
+  if (TR.n > 0) {
+    size_t lvl = 0;
+    TR.lvl_off.assign(TR.n + 2, 0);
+    for (int d = 2; d <= TR.n; ++d) {   // level d's draft rows: the depth d - 1 nodes
+      TR.lvl_off[d] = lvl;
+      lvl += (size_t)C * TR.lvl_len[d - 1];
+    }
+    ok &= cudaMalloc(&TR.tok_lvl, std::max<size_t>(lvl, 1) * 4) == cudaSuccess;
+    ok &= cudaMalloc(&TR.tree_tok, (size_t)C * TR.nn * 4) == cudaSuccess;
+    ok &= cudaMalloc(&TR.out_node, (size_t)C * TR.n * 4) == cudaSuccess;
+    ok &= cudaMalloc(&TR.ch_dev, (size_t)2 * TR.nn * 4) == cudaSuccess;
+    if (ok) {
+      ok &= cudaMemcpy(TR.ch_dev, TR.first.data(), (size_t)TR.nn * 4, cudaMemcpyHostToDevice) == cudaSuccess;
+      ok &= cudaMemcpy(TR.ch_dev + TR.nn, TR.cnt.data(), (size_t)TR.nn * 4, cudaMemcpyHostToDevice) == cudaSuccess;
+    }
+  }
   ok &= cudaMalloc(&ctx->xs, (size_t)C * g * 4) == cudaSuccess;
   ok &= cudaMalloc(&ctx->vtok, (size_t)C * (g + 1) * 4) == cudaSuccess;
   ok &= cudaMalloc(&ctx->out_tok, (size_t)C * (g + 1) * 4) == cudaSuccess;
@@ -1216,7 +1454,8 @@ void seed_destroy(seed_ctx ctx) {
   void* bufs[] = {ctx->dev_err, ctx->tgt_logits, ctx->drf_logits, ctx->xs, ctx->vtok, ctx->out_tok,
                   ctx->out_cnt, ctx->out_acc, ctx->verify_work, ctx->records, ctx->records_all, ctx->sids_dev, ctx->rs_dev,
                   ctx->slots_dev, ctx->ds.tlen, ctx->ds.len_t, ctx->ds.len_d, ctx->ds.L, ctx->ds.r,
-                  ctx->ds.done, ctx->ds.hist};
+                  ctx->ds.done, ctx->ds.hist, ctx->tree.tok_lvl, ctx->tree.tree_tok, ctx->tree.out_node,
+                  ctx->tree.ch_dev};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (ctx->records_host) cudaFreeHost(ctx->records_host);
@@ -1255,8 +1494,8 @@ seed_status seed_add_stream(seed_ctx ctx, uint32_t gid, const int32_t* prefix, i
   const int slot = free_slot(ctx);
   if (slot < 0) return fail(ctx, SEED_ECAPACITY, "seed_add_stream", "max_streams reached");
   const int g = ctx->cfg.gamma;
-  if ((s = ensure_pages(ctx, ctx->tm, slot, len + g + 1, st)) != SEED_OK) return s;
-  if ((s = ensure_pages(ctx, ctx->dm, slot, len + g + 1, st)) != SEED_OK) return s;
+  if ((s = ensure_pages(ctx, ctx->tm, slot, len + round_rows(ctx), st)) != SEED_OK) return s;
+  if ((s = ensure_pages(ctx, ctx->dm, slot, len + round_rows(ctx), st)) != SEED_OK) return s;
   // Alg. 1 Initialize: prefill both models with the prefix (all but the last token, R6)
   if ((s = prefill(ctx, ctx->tm, slot, prefix, len - 1, 0, nullptr, st)) != SEED_OK) return s;
   if ((s = prefill(ctx, ctx->dm, slot, prefix, len - 1, 0, nullptr, st)) != SEED_OK) return s;
@@ -1298,7 +1537,7 @@ seed_status seed_fork_stream(seed_ctx ctx, uint32_t src_gid, uint32_t gid, void*
     if (shared > 0)
       CK(cudaMemcpyAsync(m->page_table_dev + (size_t)slot * ctx->max_pages, pt_new, (size_t)shared * 4,
                          cudaMemcpyHostToDevice, st));
-    if ((s = ensure_pages(ctx, *m, slot, len + g + 1, st)) != SEED_OK) {
+    if ((s = ensure_pages(ctx, *m, slot, len + round_rows(ctx), st)) != SEED_OK) {
       release_pages(ctx->tm, slot, ctx->max_pages);  // the slot was never installed: drop its references
       release_pages(ctx->dm, slot, ctx->max_pages);
       return s;
@@ -1348,8 +1587,8 @@ seed_status seed_draft_round(seed_ctx ctx, const int32_t* ids, int32_t n, void* 
   std::vector<int32_t> batch(ids, ids + n);
   for (int b = 0; b < n; ++b) {
     const int T = (int)stream_of(ctx, (uint32_t)ids[b]).T.size();
-    if ((s = ensure_pages(ctx, ctx->tm, slots[b], T + g + 1, st)) != SEED_OK) return s;
-    if ((s = ensure_pages(ctx, ctx->dm, slots[b], T + g + 1, st)) != SEED_OK) return s;
+    if ((s = ensure_pages(ctx, ctx->tm, slots[b], T + round_rows(ctx), st)) != SEED_OK) return s;
+    if ((s = ensure_pages(ctx, ctx->dm, slots[b], T + round_rows(ctx), st)) != SEED_OK) return s;
   }
   RoundPlan& P = ctx->plan;
   if ((s = build_round_plan(ctx, batch, slots, P)) != SEED_OK) return s;
@@ -1470,7 +1709,7 @@ seed_status seed_last_round_buffers(seed_ctx ctx, const float** t, const float**
   if (!ctx) return SEED_EINVAL;
   if (t) *t = ctx->tgt_logits;
   if (d) *d = ctx->drf_logits;
-  if (x) *x = ctx->xs;
+  if (x) *x = ctx->tree.n > 0 ? ctx->tree.tree_tok : ctx->xs;   // trees: [n][nodes + 1] root + node tokens
   return SEED_OK;
 }
 

@@ -98,7 +98,41 @@ __global__ void kv_write_dense_kernel(KVLayout kv, int layer, int slot, int n, c
   kv.pool[kv.offset(page, layer, 1, h, pos % kv.P) + d] = v[idx];
 }
 
+// one block per (stream, layer x K|V x kv head); threads over the head dim
+__global__ void kv_compact_kernel(KVLayout kv, const int32_t* __restrict__ slots, const int32_t* __restrict__ tlen,
+                                  const int32_t* __restrict__ node, int node_stride, int max_depth,
+                                  unsigned long long* rec) {
+  pdl_trigger();
+  rec_start(rec);
+  pdl_wait();
+  rec_release(rec);
+  const int b = blockIdx.x;
+  const int lkh = blockIdx.y;                       // (layer * 2 + kv) * Hk + h
+  const int h = lkh % kv.Hk, lk = lkh / kv.Hk, layer = lk / 2, which = lk % 2;
+  const int slot = slots[b];
+  const int root = tlen[slot] - 1;
+  const int32_t* pt = kv.page_table + (size_t)slot * kv.max_pages;
+  for (int d = 1; d <= max_depth; ++d) {
+    const int nd = node[(size_t)b * node_stride + d - 1];
+    if (nd < 0) break;
+    if (nd == d) continue;
+    const int src = root + nd, dst = root + d;
+    const __nv_bfloat16* s = kv.pool + kv.offset(pt[src / kv.P], layer, which, h, src % kv.P);
+    __nv_bfloat16* t = kv.pool + kv.offset(pt[dst / kv.P], layer, which, h, dst % kv.P);
+    for (int e = threadIdx.x; e < kv.Dh / 2; e += blockDim.x)
+      reinterpret_cast<uint32_t*>(t)[e] = reinterpret_cast<const uint32_t*>(s)[e];
+  }
+  rec_end(rec, 7);
+}
+
 }  // namespace
+
+cudaError_t kv_compact(const KVLayout& kv, const int32_t* slots, const int32_t* tlen, const int32_t* node,
+                       int node_stride, int max_depth, int B, cudaStream_t st, unsigned long long* timing) {
+  if (B <= 0 || max_depth <= 0) return cudaSuccess;
+  return launch(kv_compact_kernel, dim3(B, kv.n_layers * 2 * kv.Hk), dim3(64), 0, st, kv, slots, tlen, node,
+                node_stride, max_depth, timing);
+}
 
 cudaError_t embed_stats(const __nv_bfloat16* embed, const int32_t* tok, int tok_stride, int M, int d, int V, float* x,
                         float* ssq, const __nv_bfloat16* nw, __nv_bfloat16* h, int32_t* err, cudaStream_t st,

@@ -90,6 +90,12 @@ cudaError_t embed_stats(const __nv_bfloat16* embed, const int32_t* tok, int tok_
                         float* ssq, const __nv_bfloat16* nw, __nv_bfloat16* h, int32_t* err, cudaStream_t st,
                         unsigned long long* timing = nullptr);
 cudaError_t rope_table_init(float2* table, int max_pos, int Dh, double theta, cudaStream_t st);
+// tree rounds: the accepted path's K/V rows of every layer move to consecutive slots -- for
+// stream b (stream slot slots[b], root at cache position tlen[slots[b]] - 1 before the commit) and
+// depth d = 1 .. max_depth while node[b][d - 1] >= 0: position root + node -> root + d (a node's
+// index is at least its depth, so in-order copies never overwrite a later source)
+cudaError_t kv_compact(const KVLayout& kv, const int32_t* slots, const int32_t* tlen, const int32_t* node,
+                       int node_stride, int max_depth, int B, cudaStream_t st, unsigned long long* timing = nullptr);
 cudaError_t kv_write_dense(const KVLayout& kv, int layer, int slot, int n, const __nv_bfloat16* k,
                            const __nv_bfloat16* v, cudaStream_t st);
 
@@ -105,6 +111,7 @@ struct SeqInfo {          // per sequence of the ragged batch (device arrays)
   // cached keys are always visible).  A sequence then has at most 64 new rows.
   const int32_t* row_pos = nullptr;
   const uint64_t* anc = nullptr;
+  const int32_t* tree_base = nullptr;  // per sequence: cache slot of bit 0 of anc (default: its first new row)
 };
 struct AttnWorkspace {
   float* o_part;   // [splits][M][H][Dh]
