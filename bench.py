@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--temperature", type=float, default=1.0)
     ap.add_argument("--streams", type=int, default=0, help="streams per GPU (default: the config's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tree", default="", help="k_config tree rounds, e.g. 2,2,1 (default: the chain)")
     return ap.parse_args()
 
 
@@ -204,7 +205,10 @@ class OracleSampler:
 
 def config_of(args, cfg, n_local, world):
     """The workload description shared by both arms' JSON lines."""
-    return {"workload": args.config, "streams_per_gpu": n_local, "gamma": cfg["gamma"], "draft": cfg["draft"],
+    tree = [int(c) for c in args.tree.split(",")] if getattr(args, "tree", "") else None
+    extra = {"k_config": tree} if tree else {}
+    return {"workload": args.config, "streams_per_gpu": n_local, "gamma": len(tree) if tree else cfg["gamma"],
+            **extra, "draft": cfg["draft"],
             "target": cfg["target"], "prompt_len": list(cfg["prompt_len"]), "temperature": args.temperature,
             "parallelism": f"replicas x{world}",
             "l2": "inputs larger than L2: all target weights (13.2 GB at 7B) streamed every round"}
@@ -267,7 +271,9 @@ def run_ours(args):
     import paper_2406_18200_b200 as pkg
 
     cfg = seedgen.CONFIGS[args.config]
-    g = cfg["gamma"]
+    tree = [int(c) for c in args.tree.split(",")] if args.tree else None
+    g = len(tree) if tree else cfg["gamma"]
+    rows = 1 + sum(int(np.prod(tree[:d + 1])) for d in range(len(tree))) if tree else g + 1
     n_local = args.streams or cfg["n_streams"]
     ds, ts = seedgen.SHAPES[cfg["draft"]], seedgen.SHAPES[cfg["target"]]
     steps, warm = args.steps, args.warmup
@@ -276,7 +282,7 @@ def run_ours(args):
     # e2e pass adds another warm + steps rounds; a stream must not finish inside any timed region
     prof_rounds = max(3, min(steps, 10))   # profiled rounds for the roofline, after the timed ones
     max_new = (2 * (steps + warm) + prof_rounds + 6) * (g + 1)
-    max_ctx = max_prompt + max_new + g + 8
+    max_ctx = max_prompt + max_new + max(g, rows) + 8
 
     # random-init weights drawn on the device (same recipe as seedgen on CPU)
     dW = seedgen.model_weights(ds, seedgen.DRAFT_SEED, device="cuda")
@@ -288,7 +294,7 @@ def run_ours(args):
         nccl_id = obj[0]
     eng = pkg.SeedEngine(ds, dW, ts, tW, gamma=g, temperature=args.temperature, seed=seedgen.PHILOX_SEED,
                          max_new=max_new, max_streams=n_local, max_batch=n_local, max_ctx=max_ctx, rank=rank,
-                         world=world, nccl_id=nccl_id, profile=True)
+                         world=world, nccl_id=nccl_id, profile=True, tree=tree)
     del dW, tW
     torch.cuda.empty_cache()
     eng.set_profile(False)   # the timed rounds run without the device timing records
@@ -394,7 +400,7 @@ def run_ours(args):
         "dtype": "bf16", "data": "synthetic (random-init weights, seedgen prompts)",
         "config": config_of(args, cfg, n_local, world),
         "emitted_per_stream_round": per_stream_round,
-        "verified_positions_per_s": world * n_local * (g + 1) / (step_ms * 1e-3),
+        "verified_positions_per_s": world * n_local * rows / (step_ms * 1e-3),
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "kernel": "gemm_splitk_kernel (K2)", "achieved": achieved, "peak": hbm,
                      "unit": "GB/s", "frac": achieved / hbm, "peak_source": peak_src,
@@ -417,7 +423,7 @@ def run_ours(args):
     # flops / sustained bf16), at this run's mean context; scripts/troof.py)
     sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "scripts"))
     from troof import troof
-    tr = troof(args.config, n_local, ctx_mean)
+    tr = troof(args.config, n_local, ctx_mean, rows=rows, draft_steps=g)
     line["round_roofline"] = {"t_roof_ms": tr["t_roof_ms"], "t_round_ms": step_ms, "frac": tr["t_roof_ms"] / step_ms,
                               "ctx_mean": ctx_mean, "phases_ms": tr["phases_ms"],
                               "definition": "SURVEY 8(d): T_roof = sum_phase max(B/BW_hbm, F/F_bf16_sustained), "

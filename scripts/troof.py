@@ -22,7 +22,7 @@ def params(sh):
     return L * layer + V * d, L * layer      # streamed weights (layers + LM head), layer weights
 
 
-def troof(cfg_name, n=None, ctx=None, peaks=None):
+def troof(cfg_name, n=None, ctx=None, peaks=None, rows=None, draft_steps=None):
     cfg = seedgen.CONFIGS[cfg_name]
     t, dm = seedgen.SHAPES[cfg["target"]], seedgen.SHAPES[cfg["draft"]]
     g = cfg["gamma"]
@@ -34,7 +34,9 @@ def troof(cfg_name, n=None, ctx=None, peaks=None):
                                                  "MEASURED_PEAKS.json")))
     bw = peaks["hbm_gbs"] * 1e9
     fp = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) * 1e12
-    M = n * (g + 1)
+    rows = rows or g + 1            # verified positions per stream (a k_config tree: root + nodes)
+    g = draft_steps or g
+    M = n * rows
     Pt, _ = params(t)
     Pd, _ = params(dm)
     kv_t = 2 * t["n_layers"] * t["d_model"] * 2          # K and V, bf16, every layer, per position
@@ -42,7 +44,7 @@ def troof(cfg_name, n=None, ctx=None, peaks=None):
     V = t["vocab"]
     gemm = max(2 * Pt / bw, 2 * Pt * M / fp)
     attn_b = n * ctx * kv_t + M * kv_t
-    attn_f = 4 * t["n_layers"] * t["d_model"] * n * (g + 1) * (ctx + g / 2 + 1)
+    attn_f = 4 * t["n_layers"] * t["d_model"] * M * (ctx + g / 2 + 1)
     attn = max(attn_b / bw, attn_f / fp)
     draft_b = g * 2 * Pd + sum(n * (ctx + j) * kv_d for j in range(g))
     draft = max(draft_b / bw, 2 * Pd * n * g / fp)
