@@ -241,3 +241,24 @@ def test_gpu_bonus_chi2(ops):
     m = c.sum()
     chi = np.sum((c - m * pb) ** 2 / (m * pb))
     assert chi < stats.chi2.ppf(0.99, V - 1), chi
+
+
+def test_near_tie_rate_gpu(ops):
+    """north_star: decisions the kernel and the oracle may legitimately take differently (|u - rho| <
+    1e-6, R16) must stay below 1e-5 of all decisions -- counted here on 1M accept decisions at
+    V = 32000 from the kernel's own (u, rho) (the oracle agrees with every other decision, P1)."""
+    B, g, V = 2048, 4, 32000
+    total = near = 0
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    for it in range(128):
+        sigma, noise, T = ((1.0, 0.3, 1.0), (3.0, 1.0, 0.2))[it % 2]
+        zt = torch.randn((B, g + 1, V), device="cuda", generator=gen) * sigma
+        zd = (zt[:, :g] + torch.randn((B, g, V), device="cuda", generator=gen) * noise).contiguous()
+        xs = torch.randint(0, V, (B, g), device="cuda", dtype=torch.int32, generator=gen)
+        sids = np.arange(B, dtype=np.int64) * 104729 + it
+        rs = (np.arange(B) % 7).astype(np.int32)
+        dbg = ops.verify(zt, zd, xs, T, SEED, sids, rs)["dbg"]
+        near += int((dbg[..., 2] - dbg[..., 3]).abs().lt(1e-6).sum().item())
+        total += B * g
+    assert total >= 1_000_000
+    assert near <= 1e-5 * total, (near, total)
