@@ -251,14 +251,20 @@ draft_sample_kernel(const float* z, long ld, int V, float T, uint32_t k0, uint32
   __syncthreads();
   pdl_trigger();
   rec_start(rec);
+  // the race's screen offsets before the wait (they need only the counters: sids / rs are uploaded
+  // before the round's first kernel)
+  const uint32_t c1 = (kTagDraft << 24) | (uint32_t)j, rr = (uint32_t)rs[b], sid = sids[b];
+  ScreenPre pre;
+  const bool use_pre = n <= 4 * VT * RACE_NB;
+  if (use_pre) screen_precompute(v0, n, c1, rr, sid, k0, k1, pre);
   pdl_wait();
   rec_release(rec);
   Stager sg{rows_s, &bar, 0u, slice, v0, n, (V % 4 == 0) && (n % 4 == 0) && (ld % 4 == 0)};
   sg.stage(0, 1, [&](int) { return zr; });
   auto w32 = [&](int l) -> float { return scaled_v(rows_s[l], T); };
   auto w64 = [&](int l) -> double { return (double)scaled_v(rows_s[l], T); };
-  const Best mine = race_slice(v0, n, (kTagDraft << 24) | (uint32_t)j, (uint32_t)rs[b], sids[b], k0, k1, rows_s + slice,
-                               red_f, red_b, w32, w64);
+  const Best mine = race_slice(v0, n, c1, rr, sid, k0, k1, rows_s + slice, red_f, red_b, w32, w64,
+                               use_pre ? &pre : nullptr);
   if (threadIdx.x == 0) {
     const uint32_t dst = dsmem_addr(&xbest[rank], 0u);
     asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(dst), "d"(mine.k) : "memory");

@@ -194,9 +194,31 @@ constexpr float RACE_MARGIN = 1e-3f;
 
 constexpr int RACE_NB = 4;   // register-resident screen keys: 4 blocks of 4 ids per thread (n <= 4096)
 
+// the fp32 screen offsets -log(E) of a thread's ids on the register-resident path: they depend on
+// the Philox counters only, so a sampler computes them before its PDL wait, while its predecessor
+// (the LM head) still runs
+struct ScreenPre {
+  float s[RACE_NB][4];
+};
+__device__ __forceinline__ void screen_precompute(int v0, int n, uint32_t c1, uint32_t r, uint32_t sid, uint32_t k0,
+                                                  uint32_t k1, ScreenPre& p) {
+#pragma unroll
+  for (int i = 0; i < RACE_NB; ++i) {
+    const int l = 4 * (int)threadIdx.x + i * 4 * VT;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) p.s[i][e] = 0.f;
+    if (l < n) {
+      const Philox4 ph = philox4x32_10((uint32_t)((v0 + l) >> 2), c1, r, sid, k0, k1);
+      const uint32_t words[4] = {ph.x, ph.y, ph.z, ph.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) p.s[i][e] = neg_log_exp_screen((float)philox_uniform(words[e]));
+    }
+  }
+}
+
 template <class W32, class W64>
 __device__ Best race_slice(int v0, int n, uint32_t c1, uint32_t r, uint32_t sid, uint32_t k0, uint32_t k1, float* keys,
-                           float* red_f, Best* red_b, W32 w32, W64 w64) {
+                           float* red_f, Best* red_b, W32 w32, W64 w64, const ScreenPre* pre = nullptr) {
   Best b{-INFINITY, -1};
   auto rescore = [&](int l) {   // pass B: the exact fp64 key of id v0 + l
     const int g = v0 + l;
@@ -226,11 +248,20 @@ __device__ Best race_slice(int v0, int n, uint32_t c1, uint32_t r, uint32_t sid,
 #pragma unroll
       for (int e = 0; e < 4; ++e) kr[i][e] = -INFINITY;
       if (l < n) {
-        const Philox4 ph = philox4x32_10((uint32_t)((v0 + l) >> 2), c1, r, sid, k0, k1);
-        const uint32_t words[4] = {ph.x, ph.y, ph.z, ph.w};
+        if (pre) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (l + e < n) kr[i][e] = screen(l + e, words[e]);
+          for (int e = 0; e < 4; ++e)
+            if (l + e < n) {
+              const float w = w32(l + e);
+              kr[i][e] = w != w ? INFINITY : (w != -INFINITY ? w + pre->s[i][e] : -INFINITY);
+            }
+        } else {
+          const Philox4 ph = philox4x32_10((uint32_t)((v0 + l) >> 2), c1, r, sid, k0, k1);
+          const uint32_t words[4] = {ph.x, ph.y, ph.z, ph.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (l + e < n) kr[i][e] = screen(l + e, words[e]);
+        }
       }
 #pragma unroll
       for (int e = 0; e < 4; ++e)
