@@ -1056,7 +1056,6 @@ seed_status enqueue_verify(seed_ctx ctx, cudaStream_t st) {
   // a5: K5 commit + rollback and this rank's exchange block (records, then the undone count)
   const int world = std::max(ctx->cfg.world, 1);
   const size_t blk_bytes = (size_t)ctx->block_ints * 4;
-  CK(cudaMemsetAsync(ctx->records, 0xFF, blk_bytes, st));
   CK(seed::rollback_commit(ctx->ds, ctx->slots_dev, n, g, ctx->out_tok, ctx->out_cnt, ctx->cfg.max_new_tokens,
                            ctx->records, ctx->C, ctx->sids_dev, ctx->arena.dev + P.o_out, st, next_rec(ctx)));
   ctx->kernel_launches++;

@@ -324,6 +324,9 @@ rollback_commit_kernel(StreamState s, const int32_t* batch_slots, int B, int gam
     rec[1] = c;
     for (int i = 0; i <= gamma; ++i) rec[2 + i] = i < c ? out_tok[(size_t)b * (gamma + 1) + i] : -1;
   }
+  // the block's unused records read as empty (-1): written here rather than by a memset before the
+  // kernel, which would break the PDL chain from K4 (a graph memset node waits for K4 to finish)
+  for (int i = B * (gamma + 3) + threadIdx.x; i < cap * (gamma + 3); i += K5_THREADS) records[i] = -1;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) undone += __shfl_xor_sync(0xffffffffu, undone, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = undone;
