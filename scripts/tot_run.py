@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--b", type=int, default=1)
     ap.add_argument("--l", type=int, default=64)
     ap.add_argument("--no-share", action="store_true", help="prefill every sibling (no seed_fork_stream)")
+    ap.add_argument("--tree", default="", help="k_config tree rounds, e.g. 2,2,1 (default: the chain)")
     a = ap.parse_args()
     cfg = seedgen.CONFIGS[a.config]
     depth = a.depth or DEPTH[a.config]
@@ -42,9 +43,10 @@ def main():
     tW = seedgen.model_weights(ts, seedgen.TARGET_SEED, device="cuda")
     prompt = seedgen.prompts(a.config)[0]
     width = a.n * a.b
-    max_ctx = len(prompt) + 8 + (depth + 1) * a.l + 64
+    max_ctx = len(prompt) + 8 + (depth + 1) * a.l + 128
+    tree = [int(c) for c in a.tree.split(",")] if a.tree else None
     eng = pkg.SeedEngine(ds, dW, ts, tW, gamma=cfg["gamma"], temperature=1.0, seed=seedgen.PHILOX_SEED,
-                         max_new=a.l, max_streams=width, max_batch=width, max_ctx=max_ctx)
+                         max_new=a.l, max_streams=width, max_batch=width, max_ctx=max_ctx, tree=tree)
     V = ts["vocab"]
     tcfg = tot.ToTConfig(depth=depth, n=a.n, b=a.b, eval_prefix=(1, 29871), eval_suffix=(29901,),
                          digit_base=29896 if V > 29906 else 3)
@@ -55,7 +57,7 @@ def main():
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     streams = sum(c[1] for c in res.calls)
-    print(json.dumps({"workload": a.config, "depth": depth, "n": a.n, "b": a.b, "l": a.l,
+    print(json.dumps({"workload": a.config, "k_config": tree, "depth": depth, "n": a.n, "b": a.b, "l": a.l,
                       "scheduler_calls": len(res.calls), "streams": streams, "rounds": gen.rounds,
                       "prefills": gen.prefills, "t_admit_s": gen.t_add, "t_rounds_s": gen.t_rounds, "share_prefix": gen.share_prefix,
                       "tokens": streams * a.l, "wall_s": dt, "tokens_per_s_wall": streams * a.l / dt,
