@@ -530,7 +530,7 @@ cudaError_t launch_dh(int M, int n_seq, int max_q_len, int max_kv, int H, int Hk
   if (kv.P < TK || kv.P % TK) return cudaErrorInvalidValue;
   static int stages = -1;
   if (stages < 0) {
-    const char* e = getenv("SEED_ATTN_STAGES");
+    const char* e = getenv(DH >= 128 ? "SEED_ATTN_STAGES" : "SEED_ATTN_STAGES_SMALL");
     stages = e ? atoi(e) : 2;
   }
   if (stages == 3)
