@@ -418,6 +418,12 @@ seed_status build_model(seed_ctx ctx, Model& m, const seed_model_shape& sh, cons
     m.pd.push_back(pd);
   }
   seed::gemm_plan(&m.plm, m.lm_head, m.V, m.d, min_units);
+  {   // a small model (the draft) runs every draft step: its weights stay L2-resident between steps
+    const double layer_bytes = (double)m.L * ((double)m.nqkv * m.d + (double)m.d * dq + 3.0 * m.ff * m.d) * 2;
+    if (layer_bytes <= 64e6)
+      for (auto* v : {&m.pq, &m.po, &m.pgu, &m.pd})
+        for (auto& p : *v) p.keep_w = 1;
+  }
   // KV pool
   m.kv.n_layers = m.L;
   m.kv.Hk = m.Hk;

@@ -67,6 +67,7 @@ struct SplitArgs {
   __nv_bfloat16* hout;
   unsigned long long* timing;
   unsigned long long* cta;
+  int keep_w;                  // weights evict-last (small models re-read every draft step stay in L2)
   int tstore;                  // c = 1, ymode 0 without a row map or ymode 2: the whole tile is staged in the
                                // idle ring and leaves by one tensor store (tmY)
 };
@@ -243,7 +244,7 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constan
     // ---------------- producer (one lane): weight + X k-blocks by TMA; the weights of the first
     // ring fill are requested before the PDL wait (they do not depend on the predecessor)
     if (lane == 0) {
-      const uint64_t pol_w = l2_policy_evict_first();
+      const uint64_t pol_w = a.keep_w ? l2_policy_evict_last() : l2_policy_evict_first();
       const uint64_t pol_x = l2_policy_evict_last();
       const uint32_t tx = W_TILE_BYTES + x_bytes;
       const int n_pre = min(S, nk);
@@ -726,6 +727,7 @@ cudaError_t gemm_run(const GemmPlan& p, int M, const GemmIO& io, cudaStream_t st
   b.timing = timing;
   b.cta = cta;
   b.tstore = 0;
+  b.keep_w = p.keep_w;
   const int stage_bytes = W_TILE_BYTES + m_pad * BLOCK_K * 2;
   const int extra = (256 + 256 + 2048) * 4 + 64;   // inv_s, rowmap_s, red_s | xch, barriers
   const char* e = getenv("SEED_SPLIT_SMEM_KB");

@@ -29,6 +29,7 @@ struct GemmPlan {
   int N, K, KB, tiles;
   int c;                         // CTAs (k-ranges) per 128-row weight tile, a function of (N, K)
   int split_smem_kb;             // dynamic shared memory per CTA
+  int keep_w = 0;                // weights streamed with the L2 evict-last policy (a draft model re-read every step)
   CUtensorMap tmW;
 };
 
