@@ -179,14 +179,15 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __rest
     const uint32_t st = ring + (uint32_t)((j % STAGES) * L::STAGE);
     uint64_t* bar = &bar_s[warp * STAGES + j % STAGES];
     mbar_arrive_expect_tx(bar, TX);
+    const uint64_t pol = kv.kv_once ? l2_policy_evict_first() : l2_policy_evict_normal();
     if (kv3d) {
-      tma_load_3d_u32(st, &tmKV, bar, 0, row, 0);
-      tma_load_3d_u32(st + (uint32_t)L::TILE, &tmKV, bar, 0, row + kv.Hk * kv.P, 0);
+      tma_load_3d_u32_hint(st, &tmKV, bar, 0, row, 0, pol);
+      tma_load_3d_u32_hint(st + (uint32_t)L::TILE, &tmKV, bar, 0, row + kv.Hk * kv.P, 0, pol);
     } else {
 #pragma unroll
       for (int h = 0; h < DH / EH; ++h) {
-        tma_load_2d_u32(st + (uint32_t)(h * TK * L::RB), &tmKV, bar, h * EH, row);
-        tma_load_2d_u32(st + (uint32_t)(L::TILE + h * TK * L::RB), &tmKV, bar, h * EH, row + kv.Hk * kv.P);
+        tma_load_2d_u32_hint(st + (uint32_t)(h * TK * L::RB), &tmKV, bar, h * EH, row, pol);
+        tma_load_2d_u32_hint(st + (uint32_t)(L::TILE + h * TK * L::RB), &tmKV, bar, h * EH, row + kv.Hk * kv.P, pol);
       }
     }
   };

@@ -76,6 +76,11 @@ SEED_DEV uint64_t l2_policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+SEED_DEV uint64_t l2_policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 SEED_DEV uint64_t l2_policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -98,12 +103,21 @@ SEED_DEV void tma_load_2d_u32(uint32_t smem_dst, const void* tmap, uint64_t* bar
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(x), "r"(y)
       : "memory");
 }
-// 3D TMA load (tile mode) to a shared::cta address, default L2 policy
-SEED_DEV void tma_load_3d_u32(uint32_t smem_dst, const void* tmap, uint64_t* bar, int x, int y, int z) {
+// 2D TMA load to a shared::cta address with an L2 cache policy
+SEED_DEV void tma_load_2d_u32_hint(uint32_t smem_dst, const void* tmap, uint64_t* bar, int x, int y, uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_dst),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(policy)
+      : "memory");
+}
+// 3D TMA load with an L2 cache policy
+SEED_DEV void tma_load_3d_u32_hint(uint32_t smem_dst, const void* tmap, uint64_t* bar, int x, int y, int z,
+                                   uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "l"(policy)
       : "memory");
 }
 SEED_DEV void st_shared_v4(uint32_t addr, uint4 v) {

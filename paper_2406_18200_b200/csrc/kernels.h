@@ -16,6 +16,7 @@ struct KVLayout {
   int32_t max_pages;  // per slot
   int32_t n_layers, Hk, Dh, P;
   int32_t kv3d;       // the pool's tensor map is the 3D (64, rows, halves) form (Dh = 128)
+  int32_t kv_once;    // the cache is read once per round (the target): K/V tiles loaded evict-first
   __host__ __device__ size_t page_elems() const { return (size_t)n_layers * 2 * Hk * P * Dh; }
   __host__ __device__ size_t vofs() const { return (size_t)Hk * P * Dh; }  // K -> V of the same layer
   __host__ __device__ size_t offset(int page, int layer, int kv, int h, int slot_in_page) const {
