@@ -2,12 +2,12 @@
 // split-KV merge, fused in one kernel.
 //
 // For each sequence of the ragged batch, rows q_start .. q_start + q_len - 1 sit at positions
-// kv_len - q_len .. kv_len - 1 and attend to keys 0 .. pos (R15: causal MHA).  One CTA of 4
-// warps owns (sequence x 16-row query block, head, split of SPLIT = 256 keys) and streams the
-// split's keys as 16-key tiles:
+// kv_len - q_len .. kv_len - 1 and attend to keys 0 .. pos (R15: causal MHA).  One CTA of W
+// warps (4 at Dh = 128, 8 below: attn_warps) owns (sequence x 16-row query block, head, split of
+// SPLIT keys, R33) and streams the split's keys as 16-key tiles:
 //   * it reads the QKV GEMM's fp32 output for its query rows, applies RoPE and rounds Q to bf16
 //     (B2) -- no separate epilogue kernel;
-//   * warp w owns tiles w, w + 4, w + 8, ... of the split, each through its own two-stage ring in
+//   * warp w owns tiles w, w + W, w + 2W, ... of the split, each through its own two-stage ring in
 //     shared memory: cached K/V page blocks (16 keys of one head) land by 2-D tensor copies (TMA)
 //     in the 128-byte swizzle ldmatrix reads conflict-free; the warp requests its tile j + 2 as
 //     soon as tile j is consumed, so every warp keeps two tiles in flight with no CTA barrier;
@@ -17,7 +17,7 @@
 //     tiles by the warp that owns them, and appended to the cache pages by one writer per key;
 //   * S = Q K^T and O = P V run as bf16 mma.sync.m16n8k16 (Q padded to 16 rows; P re-packed from
 //     the S accumulators as the A operand, B5) with an online base-2 softmax per warp;
-//   * the 4 warps merge (m, l, O) in warp order; with several splits every split publishes its
+//   * the W warps merge (m, l, O) in warp order; with several splits every split publishes its
 //     partial and the last to finish (atomic ticket) merges them in split order; the output is
 //     rounded to bf16 (B3).
 // Tile-to-warp assignment, split boundaries and every merge order are functions of the key
@@ -32,12 +32,11 @@
 namespace seed {
 
 namespace {
-constexpr int WARPS = 4;
-constexpr int NT = WARPS * 32;
+constexpr int STAGES = 2;               // tiles in flight per warp (3 and 4 measured: no gain, §7)
 constexpr int TK = 16;                   // keys per tile (one page block: P >= 16, P % 16 == 0)
 constexpr int QB = 16;                   // query rows per CTA (one m16 MMA tile)
 
-template <int DH, int STAGES>
+template <int DH, int WARPS>
 struct Smem {
   static constexpr int PITCH = DH + 8;                       // bf16 row pitch of Q (conflict-free ldmatrix)
   static constexpr int RB = (DH >= 64 ? 64 : DH) * 2;        // bytes per swizzled row segment (TMA box width)
@@ -94,12 +93,13 @@ SEED_DEV uint32_t pack_bf16(float lo, float hi) {
 }
 
 
-template <int DH, int STAGES>
-__global__ void __launch_bounds__(NT, Smem<DH, STAGES>::PER_SM > 4 ? 4 : Smem<DH, STAGES>::PER_SM)
+template <int DH, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, Smem<DH, WARPS>::PER_SM > 4 ? 4 : Smem<DH, WARPS>::PER_SM)
 attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __restrict__ qkv, int H, int Hk,
                    SeqInfo seqs, const float2* __restrict__ rope, KVLayout kv, int layer, int n_qblk, float scale,
                    AttnWorkspace ws, int M, __nv_bfloat16* __restrict__ out, int SPLIT, int kv3d) {
-  using L = Smem<DH, STAGES>;
+  using L = Smem<DH, WARPS>;
+  constexpr int NT = WARPS * 32;
   constexpr int P = L::PITCH;
   constexpr int OP = L::OP;
   constexpr int HALF = DH / 2;
@@ -239,6 +239,9 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __rest
     }
   }
   __syncthreads();
+#if ATTN_STAMPS
+  stamp(6);
+#endif
 
   // ---- the warp's tiles, online softmax over them (rows g, g + 8 of the MMA fragments)
   const int g = lane >> 2, t4 = lane & 3;
@@ -377,6 +380,9 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __rest
     }
     // stage s is free: request this warp's tile j + 2 into it
     __syncwarp();
+#if ATTN_STAMPS
+    if (j == 1) stamp(7);
+#endif
     if (j + STAGES < my_tiles && cached(j + STAGES) && lane == 0) {
       fence_proxy_async();   // the generic reads / writes of the stage before the tensor copy
       issue(j + STAGES);
@@ -388,7 +394,7 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __rest
   // waves need while they wait for this grid to finish.
   pdl_trigger();
 
-  // ---- merge the 4 warps (fixed order) into this split's result
+  // ---- merge the W warps (fixed order) into this split's result
   __syncthreads();   // o_s aliases the ring
   if (t4 == 0) {
     m_s[warp * QB + g] = m_row[0];
@@ -500,46 +506,61 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __rest
   done();
 }
 
-template <int DH, int ST>
-cudaError_t launch_st(int M, int n_seq, int max_q_len, int max_kv, int H, int Hk, const CUtensorMap& tmkv,
-                      const float* qkv, const SeqInfo& seqs, const float2* rope, const KVLayout& kv, int layer,
-                      const AttnWorkspace& ws, __nv_bfloat16* out, cudaStream_t st) {
+// warps per CTA (each with its own tile ring), a function of the head size only (R19)
+// (measured per round, §7: the 68M draft at 8 warps 13.8 -> 11.7 us per layer at N = 24, 9.7 -> 7.9
+// at N = 3; the 7B at 6 / 8 / 12 warps wins at N = 3..12 but loses at N = 24, where 4-warp CTAs
+// three per SM keep the most warps resident)
+int attn_warps(int Dh) { return Dh >= 128 ? 4 : 8; }
+
+template <int DH, int W>
+cudaError_t launch_w(int M, int n_seq, int max_q_len, int max_kv, int H, int Hk, const CUtensorMap& tmkv,
+                     const float* qkv, const SeqInfo& seqs, const float2* rope, const KVLayout& kv, int layer,
+                     const AttnWorkspace& ws, __nv_bfloat16* out, cudaStream_t st) {
   const int n_qblk = (max_q_len + QB - 1) / QB;
   const int SPLIT = attn_chunk_tokens(DH);
   const int splits = (max_kv + SPLIT - 1) / SPLIT;
-  if (SPLIT / (TK * WARPS) > 32) return cudaErrorInvalidValue;   // tiles per warp held in pg_s
-  const size_t smem = Smem<DH, ST>::BYTES;
+  if (SPLIT / (TK * W) > 32) return cudaErrorInvalidValue;   // tiles per warp held in pg_s
+  const size_t smem = Smem<DH, W>::BYTES;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(attn_stream_kernel<DH, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+    if (cudaFuncSetAttribute(attn_stream_kernel<DH, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return cudaErrorInvalidValue;
     attr = true;
   }
   // scores are kept in the base-2 domain: s = q.k / sqrt(Dh) * log2(e), p = 2^(s - max)
   const float scale = 1.0f / sqrtf((float)DH) * 1.4426950408889634f;
-  return launch(attn_stream_kernel<DH, ST>, dim3(n_seq * n_qblk, H, splits), dim3(NT), smem, st, tmkv, qkv, H, Hk,
+  return launch(attn_stream_kernel<DH, W>, dim3(n_seq * n_qblk, H, splits), dim3(W * 32), smem, st, tmkv, qkv, H, Hk,
                 seqs, rope, kv, layer, n_qblk, scale, ws, M, out, SPLIT, kv.kv3d);
 }
 
-// env SEED_ATTN_STAGES: ring stages per warp (2 default; 3, 4 for experiments)
+// warps per CTA: a function of the head size only (R19); env SEED_ATTN_WARPS (Dh = 128) /
+// SEED_ATTN_WARPS_SMALL (below) override it for experiments (4, 8; 16 below Dh = 128)
 template <int DH>
 cudaError_t launch_dh(int M, int n_seq, int max_q_len, int max_kv, int H, int Hk, const CUtensorMap& tmkv,
                       const float* qkv, const SeqInfo& seqs, const float2* rope, const KVLayout& kv, int layer,
                       const AttnWorkspace& ws, __nv_bfloat16* out, cudaStream_t st) {
   // page blocks of 16 keys land by one tensor copy each: 16 | P
   if (kv.P < TK || kv.P % TK) return cudaErrorInvalidValue;
-  static int stages = -1;
-  if (stages < 0) {
-    const char* e = getenv(DH >= 128 ? "SEED_ATTN_STAGES" : "SEED_ATTN_STAGES_SMALL");
-    stages = e ? atoi(e) : 2;
+  static int w = -1;
+  if (w < 0) {
+    const char* e = getenv(DH >= 128 ? "SEED_ATTN_WARPS" : "SEED_ATTN_WARPS_SMALL");
+    w = e ? atoi(e) : attn_warps(DH);
   }
-  if (stages == 3)
-    return launch_st<DH, 3>(M, n_seq, max_q_len, max_kv, H, Hk, tmkv, qkv, seqs, rope, kv, layer, ws, out, st);
-  if (stages == 4)
-    return launch_st<DH, 4>(M, n_seq, max_q_len, max_kv, H, Hk, tmkv, qkv, seqs, rope, kv, layer, ws, out, st);
-  return launch_st<DH, 2>(M, n_seq, max_q_len, max_kv, H, Hk, tmkv, qkv, seqs, rope, kv, layer, ws, out, st);
+  if (w == 8)
+    return launch_w<DH, 8>(M, n_seq, max_q_len, max_kv, H, Hk, tmkv, qkv, seqs, rope, kv, layer, ws, out, st);
+  if constexpr (DH < 128) {
+    if (w == 16)
+      return launch_w<DH, 16>(M, n_seq, max_q_len, max_kv, H, Hk, tmkv, qkv, seqs, rope, kv, layer, ws, out, st);
+  } else {
+    if (w == 6)
+      return launch_w<DH, 6>(M, n_seq, max_q_len, max_kv, H, Hk, tmkv, qkv, seqs, rope, kv, layer, ws, out, st);
+    if (w == 12)
+      return launch_w<DH, 12>(M, n_seq, max_q_len, max_kv, H, Hk, tmkv, qkv, seqs, rope, kv, layer, ws, out, st);
+  }
+  return launch_w<DH, 4>(M, n_seq, max_q_len, max_kv, H, Hk, tmkv, qkv, seqs, rope, kv, layer, ws, out, st);
 }
+
 }  // namespace
 
 // keys per CTA: a fixed split grid, a function of the head size only (R19): 1024 keys at Dh = 128,

@@ -420,9 +420,11 @@ seed_status build_model(seed_ctx ctx, Model& m, const seed_model_shape& sh, cons
   seed::gemm_plan(&m.plm, m.lm_head, m.V, m.d, min_units);
   {   // a small model (the draft) runs every draft step: its weights stay L2-resident between steps
     const double layer_bytes = (double)m.L * ((double)m.nqkv * m.d + (double)m.d * dq + 3.0 * m.ff * m.d) * 2;
-    if (layer_bytes <= 64e6)
+    if (layer_bytes <= 64e6) {   // (and its LM head, re-read every step: GSM8K -9 us per round)
       for (auto* v : {&m.pq, &m.po, &m.pgu, &m.pd})
         for (auto& p : *v) p.keep_w = 1;
+      m.plm.keep_w = 1;
+    }
     // a large model's cache is streamed once per round and would only displace what is re-read:
     // its K/V tiles are loaded evict-first (7B at N = 24: attention 38.3 -> 35.7 us per layer)
     m.kv.kv_once = layer_bytes > 64e6 ? 1 : 0;

@@ -124,15 +124,16 @@ if os.environ.get("SEED_CTA_TRACE") == "1":
             print(f"    {name:11s} {v.min():8.2f} {np.median(v):8.2f} {v.max():8.2f}")
         last = np.argmax(ct[:, 7])
         print("    last CTA:", " ".join(f"{(ct[last, k + 1] - rel)/1e3:.2f}" for k in range(len(ph))))
-    i = names.index("t.L1.attn")
-    raw = eng.gemm_cta_trace(i).reshape(-1, 8)
-    rel = tr[i, 1]
-    used = raw[:, 5] >= tr[i, 0]
-    ct = raw[used]
-    print(f"t.L1.attn: {used.sum()} CTAs; release->end {(tr[i,2]-rel)/1e3:.2f} us; phase - release (us): min / med / max")
-    for k, name in enumerate(["start", "release", "tiles", "stored", "merge", "end"]):
-        v = (ct[:, k] - rel) / 1e3
-        v = v[ct[:, k] >= tr[i, 0]]
-        if len(v):
-            print(f"    {name:11s} {v.min():8.2f} {np.median(v):8.2f} {v.max():8.2f}")
+    for want in ["t.L1.attn", "d1.L0.attn", "d1.L1.attn"]:
+        i = names.index(want)
+        raw = eng.gemm_cta_trace(i).reshape(-1, 8)
+        rel = tr[i, 1]
+        used = raw[:, 5] >= tr[i, 0]
+        ct = raw[used]
+        print(f"{want}: {used.sum()} CTAs; release->end {(tr[i,2]-rel)/1e3:.2f} us; phase - release (us): min / med / max")
+        for k, name in enumerate(["start", "release", "tiles", "stored", "merge", "end", "q_ready", "tile1_done"]):
+            v = (ct[:, k] - rel) / 1e3
+            v = v[ct[:, k] >= tr[i, 0]]
+            if len(v):
+                print(f"    {name:11s} {v.min():8.2f} {np.median(v):8.2f} {v.max():8.2f}")
 eng.close()
