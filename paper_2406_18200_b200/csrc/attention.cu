@@ -326,23 +326,37 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __rest
       mma_bf16(acc[0], a0, a1, a2, a3, b0, b1);
       mma_bf16(acc[1], a0, a1, a2, a3, b2, b3);
     }
+    // a tile of cached keys below every row's position (and below the tree) needs no mask; padding
+    // rows then score finite values that only their own, discarded, outputs see
+    const bool interior = t0 + TK <= min(k_hi, new_first) && (!seqs.anc || t0 + TK <= tbase);
     float f_row[2];
 #pragma unroll
     for (int h2 = 0; h2 < 2; ++h2) {
       const int r = g + 8 * h2;
       const uint64_t anc_r = anc_rows[h2];
       float mx = -INFINITY;
+      if (interior) {
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
+        for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int key = t0 + nt * 8 + 2 * t4 + c;
-          const bool ok = r < nr && key < k_hi &&
-                          (anc_r ? (key < tbase || ((anc_r >> (key - tbase)) & 1ull)) : key <= pos0 + r);
-          float& v = sc[nt][2 * h2 + c];
-          v = ok ? (v + s2[nt][2 * h2 + c]) * scale : -INFINITY;
-          mx = fmaxf(mx, v);
-        }
+          for (int c = 0; c < 2; ++c) {
+            float& v = sc[nt][2 * h2 + c];
+            v = (v + s2[nt][2 * h2 + c]) * scale;
+            mx = fmaxf(mx, v);
+          }
+      } else {
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const int key = t0 + nt * 8 + 2 * t4 + c;
+            const bool ok = r < nr && key < k_hi &&
+                            (anc_r ? (key < tbase || ((anc_r >> (key - tbase)) & 1ull)) : key <= pos0 + r);
+            float& v = sc[nt][2 * h2 + c];
+            v = ok ? (v + s2[nt][2 * h2 + c]) * scale : -INFINITY;
+            mx = fmaxf(mx, v);
+          }
+      }
       mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
       mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
       const float mn = fmaxf(m_row[h2], mx);
@@ -361,20 +375,23 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __rest
       m_row[h2] = mn;
       l_row[h2] = l_row[h2] * f_row[h2] + sum;
     }
-    // O = O * f + P V (P rounded to bf16 as the A operand, B5); V via ldmatrix.trans
+    // O = O * f + P V (P rounded to bf16 as the A operand, B5); V via ldmatrix.trans.  Once the
+    // running maxima settle f = 1 exactly (ex2(0)) and the warp skips the rescaling (bit-identical)
     const uint32_t pa0 = pack_bf16(sc[0][0], sc[0][1]), pa1 = pack_bf16(sc[0][2], sc[0][3]);
     const uint32_t pa2 = pack_bf16(sc[1][0], sc[1][1]), pa3 = pack_bf16(sc[1][2], sc[1][3]);
+    if (__any_sync(0xffffffffu, f_row[0] != 1.f || f_row[1] != 1.f)) {
+#pragma unroll
+      for (int dt = 0; dt < DT; ++dt) {
+        o_acc[dt][0] *= f_row[0];
+        o_acc[dt][1] *= f_row[0];
+        o_acc[dt][2] *= f_row[1];
+        o_acc[dt][3] *= f_row[1];
+      }
+    }
 #pragma unroll
     for (int dt = 0; dt < DT; dt += 2) {
       uint32_t b0, b1, b2, b3;
       ldsm_x4_t(tile_addr<DH>(vb, (lane & 7) + ((lane >> 3) & 1) * 8, dt * 8 + (lane >> 4) * 8), b0, b1, b2, b3);
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        o_acc[dt + u][0] *= f_row[0];
-        o_acc[dt + u][1] *= f_row[0];
-        o_acc[dt + u][2] *= f_row[1];
-        o_acc[dt + u][3] *= f_row[1];
-      }
       mma_bf16(o_acc[dt], pa0, pa1, pa2, pa3, b0, b1);
       mma_bf16(o_acc[dt + 1], pa0, pa1, pa2, pa3, b2, b3);
     }
