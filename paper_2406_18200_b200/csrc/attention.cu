@@ -66,6 +66,19 @@ SEED_DEV uint32_t tile_addr(uint32_t tile, int row, int e) {
   return a ^ ((a >> 3) & MASK);
 }
 
+// tile_addr(tile, row, e) for e = e0 + E, E a multiple of 16 (compile-time after unrolling) and e0 < 16
+// the lane's part, given x = tile_addr(0, row, e0): with 128-byte rows the swizzle XORs bits [4:6]
+// with the row's bits [0:2], E's in-row part only touches bits [5:6] and the tile base is 1024-aligned,
+// so the address is ((tile + x) ^ ((E % 64) * 2)) + (E / 64) * 16 rows * 128 B -- one XOR per ldmatrix
+template <int DH>
+SEED_DEV uint32_t tile_at(uint32_t tile, uint32_t x, int row, int e, int E) {
+  if constexpr (DH >= 64) {
+    return ((tile + x) ^ (uint32_t)((E % 64) * 2)) + (uint32_t)((E / 64) * TK * 128);
+  } else {
+    return tile_addr<DH>(tile, row, e);
+  }
+}
+
 SEED_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
@@ -258,6 +271,10 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __rest
   float m_row[2] = {-INFINITY, -INFINITY}, l_row[2] = {0.f, 0.f};
 #pragma unroll
   for (int j = 0; j < DT; ++j) o_acc[j][0] = o_acc[j][1] = o_acc[j][2] = o_acc[j][3] = 0.f;
+  // this lane's swizzled ldmatrix offsets in a tile (K: key row, column 8 x bit 3 of the lane; V: the
+  // transposed read), element 0 of the tile's first 64-column half (tile_at)
+  const uint32_t kx = tile_addr<DH>(0u, (lane >> 4) * 8 + (lane & 7), ((lane >> 3) & 1) * 8);
+  const uint32_t vx = tile_addr<DH>(0u, (lane & 7) + ((lane >> 3) & 1) * 8, (lane >> 4) * 8);
   uint32_t phase = 0;   // bit s: parity of stage s's next completion
   const uint32_t qa = smem_u32(q_s);
   const bool own_head = head % (H / Hk) == 0;
@@ -321,7 +338,8 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __rest
     for (int ks = 0; ks < DH / 16; ++ks) {
       uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
       ldsm_x4(qa + ((lane & 15) * P + ks * 16 + (lane >> 4) * 8) * 2, a0, a1, a2, a3);
-      ldsm_x4(tile_addr<DH>(kb, (lane >> 4) * 8 + (lane & 7), ks * 16 + ((lane >> 3) & 1) * 8), b0, b1, b2, b3);
+      ldsm_x4(tile_at<DH>(kb, kx, (lane >> 4) * 8 + (lane & 7), ks * 16 + ((lane >> 3) & 1) * 8, ks * 16), b0, b1, b2,
+              b3);
       float (*acc)[4] = (ks & 1) ? s2 : sc;
       mma_bf16(acc[0], a0, a1, a2, a3, b0, b1);
       mma_bf16(acc[1], a0, a1, a2, a3, b2, b3);
@@ -391,7 +409,8 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __rest
 #pragma unroll
     for (int dt = 0; dt < DT; dt += 2) {
       uint32_t b0, b1, b2, b3;
-      ldsm_x4_t(tile_addr<DH>(vb, (lane & 7) + ((lane >> 3) & 1) * 8, dt * 8 + (lane >> 4) * 8), b0, b1, b2, b3);
+      ldsm_x4_t(tile_at<DH>(vb, vx, (lane & 7) + ((lane >> 3) & 1) * 8, dt * 8 + (lane >> 4) * 8, dt * 8), b0, b1, b2,
+                b3);
       mma_bf16(o_acc[dt], pa0, pa1, pa2, pa3, b0, b1);
       mma_bf16(o_acc[dt + 1], pa0, pa1, pa2, pa3, b2, b3);
     }
