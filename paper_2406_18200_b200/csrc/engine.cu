@@ -154,6 +154,7 @@ struct ChunkDesc {
   const uint64_t* anc = nullptr;
   const int32_t* tree_base = nullptr; // per sequence: cache slot of the tree's root (bit 0 of anc)
   bool rowmap = false;                // logits rows through `compact` even when every row has logits
+  bool pre_embedded = false;          // x, ssq and h of the rows were written by the previous step's K1
   TokSrc tok;
   int n_logits;
   const int32_t* logit_rows;  // device [n_logits]: chunk row of each logits row
@@ -531,10 +532,12 @@ seed_status forward_chunk(seed_ctx ctx, Model& m, const ChunkDesc& c, cudaStream
   // the RMSNorm weight applied to the residual after layer l (B1, R24)
   auto next_norm = [&](int l) { return l + 1 < m.L ? m.an[l + 1] : m.final_norm; };
   // embedding (or the given residual), its per-tile sums of squares and h = bf16(x * attn_norm)
-  CK(seed::embed_stats(embed ? m.embed : nullptr, c.tok.dev, c.tok.stride, M, m.d, m.V, m.x, m.ssq_b,
-                       first_layer < m.L ? m.an[first_layer] : m.final_norm, m.h, ctx->dev_err, st,
-                       next_rec(ctx)));
-  ctx->kernel_launches++;
+  if (!(embed && c.pre_embedded)) {   // (the previous draft step's K1 already wrote them: EmbedNext)
+    CK(seed::embed_stats(embed ? m.embed : nullptr, c.tok.dev, c.tok.stride, M, m.d, m.V, m.x, m.ssq_b,
+                         first_layer < m.L ? m.an[first_layer] : m.final_norm, m.h, ctx->dev_err, st,
+                         next_rec(ctx)));
+    ctx->kernel_launches++;
+  }
   seed::SeqInfo seqs{c.q_start, c.q_len, c.kv_len, c.seq_slot, c.seq_stable, c.row_pos, c.anc, c.tree_base};
   const CUtensorMap* tm_h = xmap(ctx, m.h, m.d, m.m_cap, M);
   const CUtensorMap* tm_attn = xmap(ctx, m.attn, m.H * m.Dh, m.m_cap, M);
@@ -1011,9 +1014,23 @@ seed_status enqueue_draft(seed_ctx ctx, cudaStream_t st) {
     c.Y = ctx->drf_logits + (size_t)(j - 1) * V;
     c.ldY = g * V;
     if ((s = forward_chunk(ctx, ctx->dm, c, st)) != SEED_OK) return s;
-    // K1 sampler: x_j -> xs[b][j-1] and the verify input vtok[b][j]
+    // K1 sampler: x_j -> xs[b][j-1] and the verify input vtok[b][j]; below the last step it also
+    // embeds x_j as the next step's rows (that step's chunk: one row per stream, in batch order)
+    seed::EmbedNext en;
+    if (j < g) {
+      Model& dm = ctx->dm;
+      en.emb = dm.embed;
+      en.d = dm.d;
+      en.x = dm.x;
+      en.ssq = dm.ssq_b;
+      en.ssq_ld = P.draft[j].M;
+      en.nw = dm.an[0];
+      en.h = dm.h;
+      P.draft[j].pre_embedded = P.draft[j].M == n;
+      if (!P.draft[j].pre_embedded) en.emb = nullptr;
+    }
     CK(seed::draft_sample(c.Y, (long)g * V, n, V, ctx->cfg.temperature, k0, k1, ctx->sids_dev, ctx->rs_dev, j,
-                          ctx->xs + (j - 1), g, ctx->vtok + j, g + 1, ctx->dev_err, st, next_rec(ctx)));
+                          ctx->xs + (j - 1), g, ctx->vtok + j, g + 1, ctx->dev_err, st, next_rec(ctx), en));
     ctx->kernel_launches++;
   }
   return SEED_OK;

@@ -152,9 +152,22 @@ struct VerifyArgs {
 };
 size_t vocab_verify_work_bytes(int B, int gamma);
 cudaError_t vocab_verify(const VerifyArgs& a, cudaStream_t st);
+// K1's fused successor work: the next draft step's embedding of the sampled token (what
+// embed_stats computes for that step's rows, bit for bit): x[b] = E[y_b] (fp32), ssq[tile][b]
+// (ld = rows of the next step), h[b] = bf16(x * nw); emb == nullptr: none
+struct EmbedNext {
+  const __nv_bfloat16* emb = nullptr;
+  int d = 0;
+  float* x = nullptr;
+  float* ssq = nullptr;
+  int ssq_ld = 0;
+  const __nv_bfloat16* nw = nullptr;
+  __nv_bfloat16* h = nullptr;
+};
 cudaError_t draft_sample(const float* z, long ld, int B, int V, float T, uint32_t k0, uint32_t k1,
                          const uint32_t* sids, const int32_t* rs, int j, int32_t* out, int out_stride, int32_t* out2,
-                         int out2_stride, int32_t* err, cudaStream_t st, unsigned long long* timing = nullptr);
+                         int out2_stride, int32_t* err, cudaStream_t st, unsigned long long* timing = nullptr,
+                         const EmbedNext& en = EmbedNext{});
 // K1T / K4T (tree.cu): k_config tree drafting and verification (DESIGN R36)
 cudaError_t draft_topk(const float* z, long ld, int B, int V, float T, uint32_t k0, uint32_t k1, const uint32_t* sids,
                        const int32_t* rs, int node, int m, int32_t* out, int out_stride, int first, int32_t* out2,

@@ -233,9 +233,10 @@ vocab_verify_kernel(VerifyArgs A) {
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(VT)
 draft_sample_kernel(const float* z, long ld, int V, float T, uint32_t k0, uint32_t k1, const uint32_t* sids,
                     const int32_t* rs, int j, int32_t* out, int out_stride, int32_t* out2, int out2_stride,
-                    int32_t* err, unsigned long long* rec) {
+                    int32_t* err, unsigned long long* rec, EmbedNext en) {
   extern __shared__ __align__(128) float rows_s[];  // [slice] row, then [slice] race keys
   __shared__ float red_f[VT / 32];
+  __shared__ float red_e[VT / 32];
   __shared__ Best red_b[VT / 32];
   __shared__ Best xbest[CS];
   __shared__ __align__(8) uint64_t bar;
@@ -265,8 +266,10 @@ draft_sample_kernel(const float* z, long ld, int V, float T, uint32_t k0, uint32
   auto w64 = [&](int l) -> double { return (double)scaled_v(rows_s[l], T); };
   const Best mine = race_slice(v0, n, c1, rr, sid, k0, k1, rows_s + slice, red_f, red_b, w32, w64,
                                use_pre ? &pre : nullptr);
-  if (threadIdx.x == 0) {
-    const uint32_t dst = dsmem_addr(&xbest[rank], 0u);
+  // slice winners to rank 0 (to every rank when the next step's embedding is fused: each merges)
+  const int npush = en.emb ? CS : 1;
+  if (threadIdx.x < npush) {
+    const uint32_t dst = dsmem_addr(&xbest[rank], (uint32_t)threadIdx.x);
     asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(dst), "d"(mine.k) : "memory");
     asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(dst + 8), "r"(mine.v) : "memory");
   }
@@ -277,6 +280,31 @@ draft_sample_kernel(const float* z, long ld, int V, float T, uint32_t k0, uint32
     out[(size_t)b * out_stride] = acc.v;
     if (out2) out2[(size_t)b * out2_stride] = acc.v;
     if (acc.v < 0 && err) atomicOr(err, 2);   // no finite key (non-finite logits)
+  }
+  if (en.emb) {
+    // the next draft step's embedding of row b, 128-column tiles rank, rank + CS, ...: the same
+    // values, warp sums and warp order as embed_stats (a token outside the table reads row 0)
+    Best acc{-INFINITY, -1};
+    for (int c = 0; c < CS; ++c) acc = best_merge(acc, xbest[c]);
+    const int id = acc.v >= 0 && acc.v < V ? acc.v : 0;
+    const int nt = (en.d + 127) / 128, w = threadIdx.x >> 5;
+    for (int t0 = rank * 2; t0 < nt; t0 += 2 * CS) {   // two tiles per pass: warps 0-3 and 4-7
+      const int tile = t0 + (w >> 2), n = tile * 128 + (threadIdx.x & 127);
+      float v = 0.f;
+      if (tile < nt && n < en.d) {
+        v = bf2f(en.emb[(size_t)id * en.d + n]);
+        en.x[(size_t)b * en.d + n] = v;
+        en.h[(size_t)b * en.d + n] = f2bf(v * bf2f(en.nw[n]));
+      }
+      const float sq = warp_sum(v * v);
+      if ((threadIdx.x & 31) == 0) red_e[w] = sq;
+      __syncthreads();
+      if ((threadIdx.x & 127) == 0 && tile < nt) {
+        const int q = w & ~3;
+        en.ssq[(size_t)tile * en.ssq_ld + b] = ((red_e[q] + red_e[q + 1]) + red_e[q + 2]) + red_e[q + 3];
+      }
+      __syncthreads();
+    }
   }
   rec_end(rec, 4);
 }
@@ -359,7 +387,8 @@ cudaError_t vocab_verify(const VerifyArgs& a, cudaStream_t st) {
 
 cudaError_t draft_sample(const float* z, long ld, int B, int V, float T, uint32_t k0, uint32_t k1,
                          const uint32_t* sids, const int32_t* rs, int j, int32_t* out, int out_stride, int32_t* out2,
-                         int out2_stride, int32_t* err, cudaStream_t st, unsigned long long* timing) {
+                         int out2_stride, int32_t* err, cudaStream_t st, unsigned long long* timing,
+                         const EmbedNext& en) {
   const int slice = ((V + CS - 1) / CS + 3) & ~3;
   const size_t smem = (size_t)2 * slice * 4;
   if (smem > 220 * 1024) return cudaErrorInvalidValue;
@@ -369,7 +398,7 @@ cudaError_t draft_sample(const float* z, long ld, int B, int V, float T, uint32_
     attr = smem;
   }
   return launch(draft_sample_kernel, dim3(B * CS), dim3(VT), smem, st, z, ld, V, T, k0, k1, sids, rs, j, out,
-                out_stride, out2, out2_stride, err, timing);
+                out_stride, out2, out2_stride, err, timing, en);
 }
 
 cudaError_t philox_fill(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1, int n,

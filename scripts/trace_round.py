@@ -54,7 +54,8 @@ KIND = {1: "gemm", 2: "attn", 3: "K4", 4: "K1", 5: "embed", 6: "K5"}
 L_d, L_t = ds["n_layers"], ts["n_layers"]
 names = []
 for j in range(g):
-    names.append(f"d{j}.embed")
+    if j == 0:   # later steps' embeddings are written by the previous step's K1 (EmbedNext)
+        names.append(f"d{j}.embed")
     for l in range(L_d):
         names += [f"d{j}.L{l}.qkv", f"d{j}.L{l}.attn", f"d{j}.L{l}.o", f"d{j}.L{l}.gu", f"d{j}.L{l}.down"]
     names += [f"d{j}.lm", f"d{j}.K1"]
@@ -82,7 +83,7 @@ kinds = traces[0][:, 3]
 for k in sorted(set(kinds.tolist())):
     sel = kinds == k
     print(f"  {KIND.get(int(k), k):6s} n={sel.sum():4d} exposed/round {np.median(ex[:, sel, 0].sum(1)):8.1f} us")
-nd = g * (1 + 5 * L_d + 2)
+nd = 1 + g * (5 * L_d + 2)
 print(f"draft phase exposed {np.median(ex[:, :nd, 0].sum(1)):.1f} us; verify phase {np.median(ex[:, nd:, 0].sum(1)):.1f} us")
 
 
