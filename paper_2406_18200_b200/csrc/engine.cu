@@ -204,6 +204,7 @@ struct seed_ctx_s {
   int32_t *xs = nullptr, *vtok = nullptr, *out_tok = nullptr, *out_cnt = nullptr, *out_acc = nullptr;
   void* verify_work = nullptr;     // K4 scratch (vocab_verify_work_bytes; tickets zero between launches)
   int32_t *records = nullptr, *records_all = nullptr, *records_host = nullptr;   // exchange blocks (a6)
+  int32_t* out_host = nullptr;   // pinned staging of seed_round_host's results: [C][gamma + 1] tokens, [C] counts
   int block_ints = 0;             // words per rank's block: C records of gamma + 3, then the undone count
   // device error word (SEED_EDEVICE): [0] contract-violation bits, [1] empty-residual fallbacks (K4)
   int32_t* dev_err = nullptr;
@@ -1417,6 +1418,7 @@ seed_status seed_init(const seed_config* cfg, seed_ctx* out) {
   ok &= cudaMalloc(&ctx->records, (size_t)ctx->block_ints * 4) == cudaSuccess;
   ok &= cudaMalloc(&ctx->records_all, (size_t)world * ctx->block_ints * 4) == cudaSuccess;
   ok &= cudaMallocHost(&ctx->records_host, (size_t)world * ctx->block_ints * 4) == cudaSuccess;
+  ok &= cudaMallocHost(&ctx->out_host, (size_t)C * (g + 2) * 4) == cudaSuccess;
   ok &= cudaMalloc(&ctx->dev_err, 2 * sizeof(int32_t)) == cudaSuccess;
   if (ok) ok &= cudaMemset(ctx->dev_err, 0, 2 * sizeof(int32_t)) == cudaSuccess;
   ok &= cudaMallocHost(&ctx->err_host, 2 * sizeof(int32_t)) == cudaSuccess;
@@ -1486,6 +1488,7 @@ void seed_destroy(seed_ctx ctx) {
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (ctx->records_host) cudaFreeHost(ctx->records_host);
+  if (ctx->out_host) cudaFreeHost(ctx->out_host);
   if (ctx->err_host) cudaFreeHost(ctx->err_host);
   ctx->arena.destroy();
   if (ctx->round_done) cudaEventDestroy(ctx->round_done);
@@ -1651,10 +1654,16 @@ seed_status seed_round_host(seed_ctx ctx, const int32_t* ids, int32_t n, int32_t
   if ((s = seed_verify(ctx, ids, n, nullptr, nullptr, stream)) != SEED_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
   const int g = ctx->cfg.gamma;
+  // through pinned staging: both copies queue behind the round, one synchronisation (a copy into
+  // pageable memory would block the host per copy)
+  int32_t* stage_tok = ctx->out_host;
+  int32_t* stage_cnt = ctx->out_host + (size_t)ctx->C * (g + 1);
   if (out_tok_host && n > 0)
-    CK(cudaMemcpyAsync(out_tok_host, ctx->out_tok, (size_t)n * (g + 1) * 4, cudaMemcpyDeviceToHost, st));
-  if (out_cnt_host && n > 0) CK(cudaMemcpyAsync(out_cnt_host, ctx->out_cnt, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(stage_tok, ctx->out_tok, (size_t)n * (g + 1) * 4, cudaMemcpyDeviceToHost, st));
+  if (out_cnt_host && n > 0) CK(cudaMemcpyAsync(stage_cnt, ctx->out_cnt, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (out_tok_host && n > 0) std::memcpy(out_tok_host, stage_tok, (size_t)n * (g + 1) * 4);
+  if (out_cnt_host && n > 0) std::memcpy(out_cnt_host, stage_cnt, (size_t)n * 4);
   return SEED_OK;
 }
 
