@@ -106,8 +106,10 @@ SEED_DEV uint32_t pack_bf16(float lo, float hi) {
 }
 
 
-template <int DH, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, Smem<DH, WARPS>::PER_SM > 4 ? 4 : Smem<DH, WARPS>::PER_SM)
+// MINB: resident CTAs per SM the registers are budgeted for (launch_w picks it per launch; register
+// allocation does not change the arithmetic)
+template <int DH, int WARPS, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB)
 attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __restrict__ qkv, int H, int Hk,
                    SeqInfo seqs, const float2* __restrict__ rope, KVLayout kv, int layer, int n_qblk, float scale,
                    AttnWorkspace ws, int M, __nv_bfloat16* __restrict__ out, int SPLIT, int kv3d) {
@@ -548,6 +550,24 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __rest
 // three per SM keep the most warps resident)
 int attn_warps(int Dh) { return Dh >= 128 ? 4 : 8; }
 
+template <int DH, int W, int MINB>
+cudaError_t launch_wm(dim3 grid, int M, int H, int Hk, const CUtensorMap& tmkv, const float* qkv, const SeqInfo& seqs,
+                      const float2* rope, const KVLayout& kv, int layer, int n_qblk, int SPLIT, const AttnWorkspace& ws,
+                      __nv_bfloat16* out, cudaStream_t st) {
+  const size_t smem = Smem<DH, W>::BYTES;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(attn_stream_kernel<DH, W, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return cudaErrorInvalidValue;
+    attr = true;
+  }
+  // scores are kept in the base-2 domain: s = q.k / sqrt(Dh) * log2(e), p = 2^(s - max)
+  const float scale = 1.0f / sqrtf((float)DH) * 1.4426950408889634f;
+  return launch(attn_stream_kernel<DH, W, MINB>, grid, dim3(W * 32), smem, st, tmkv, qkv, H, Hk, seqs, rope, kv, layer,
+                n_qblk, scale, ws, M, out, SPLIT, kv.kv3d);
+}
+
 template <int DH, int W>
 cudaError_t launch_w(int M, int n_seq, int max_q_len, int max_kv, int H, int Hk, const CUtensorMap& tmkv,
                      const float* qkv, const SeqInfo& seqs, const float2* rope, const KVLayout& kv, int layer,
@@ -556,18 +576,16 @@ cudaError_t launch_w(int M, int n_seq, int max_q_len, int max_kv, int H, int Hk,
   const int SPLIT = attn_chunk_tokens(DH);
   const int splits = (max_kv + SPLIT - 1) / SPLIT;
   if (SPLIT / (TK * W) > 32) return cudaErrorInvalidValue;   // tiles per warp held in pg_s
-  const size_t smem = Smem<DH, W>::BYTES;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(attn_stream_kernel<DH, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return cudaErrorInvalidValue;
-    attr = true;
+  const dim3 grid(n_seq * n_qblk, H, splits);
+  constexpr int per_sm = Smem<DH, W>::PER_SM > 4 ? 4 : Smem<DH, W>::PER_SM;
+  // 8 warps: when the grid fits two CTAs per SM, the variant with twice the registers (the 68M
+  // draft at N = 24: 128 registers, no spill, 9.5 vs 10.3 us per layer); larger grids (the 160M
+  // draft's longer contexts) keep the resident count shared memory allows
+  if constexpr (W == 8 && per_sm > 2) {
+    if ((long)grid.x * grid.y * grid.z <= 2L * kNumSMs)
+      return launch_wm<DH, W, 2>(grid, M, H, Hk, tmkv, qkv, seqs, rope, kv, layer, n_qblk, SPLIT, ws, out, st);
   }
-  // scores are kept in the base-2 domain: s = q.k / sqrt(Dh) * log2(e), p = 2^(s - max)
-  const float scale = 1.0f / sqrtf((float)DH) * 1.4426950408889634f;
-  return launch(attn_stream_kernel<DH, W>, dim3(n_seq * n_qblk, H, splits), dim3(W * 32), smem, st, tmkv, qkv, H, Hk,
-                seqs, rope, kv, layer, n_qblk, scale, ws, M, out, SPLIT, kv.kv3d);
+  return launch_wm<DH, W, per_sm>(grid, M, H, Hk, tmkv, qkv, seqs, rope, kv, layer, n_qblk, SPLIT, ws, out, st);
 }
 
 // warps per CTA: a function of the head size only (R19); env SEED_ATTN_WARPS (Dh = 128) /
