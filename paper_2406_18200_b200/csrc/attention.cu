@@ -280,9 +280,9 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmKV, const float* __rest
   uint32_t phase = 0;   // bit s: parity of stage s's next completion
   const uint32_t qa = smem_u32(q_s);
   const bool own_head = head % (H / Hk) == 0;
-  // one resident CTA per SM (MINB = 1): registers to spare, so Q's MMA fragments are loaded once
-  // instead of once per tile (the same values: bit-identical)
-  constexpr bool QREG = MINB == 1;
+  // at most 256 threads per SM (MINB x warps): registers to spare, so Q's MMA fragments are loaded
+  // once instead of once per tile (the same values: bit-identical)
+  constexpr bool QREG = WARPS * 32 * MINB <= 256;
   uint32_t qf[QREG ? DH / 16 : 1][4];
   if constexpr (QREG) {
 #pragma unroll
@@ -601,11 +601,15 @@ cudaError_t launch_w(int M, int n_seq, int max_q_len, int max_kv, int H, int Hk,
     if ((long)grid.x * grid.y * grid.z <= 2L * kNumSMs)
       return launch_wm<DH, W, 2>(grid, M, H, Hk, tmkv, qkv, seqs, rope, kv, layer, n_qblk, SPLIT, ws, out, st);
   }
-  // 4 warps: a grid within one CTA per SM takes the variant with Q held in registers (the 7B at
-  // GSM8K's N = 3: 12.5 -> 11.6 us per layer, rounds -0.8 %)
+  // 4 warps: a grid within one or two CTAs per SM takes a variant with Q held in registers (the 7B
+  // at N = 3 / 5 / 6 / 8: 96-256 CTAs; GSM8K 12.5 -> 11.6 us per layer, rounds -0.8 %, CW -1.3 %,
+  // N = 6 -2 %); the N = 24 grid (768 CTAs) keeps three per SM
   if constexpr (W == 4 && per_sm > 1) {
     if ((long)grid.x * grid.y * grid.z <= (long)kNumSMs)
       return launch_wm<DH, W, 1>(grid, M, H, Hk, tmkv, qkv, seqs, rope, kv, layer, n_qblk, SPLIT, ws, out, st);
+    if constexpr (per_sm > 2)
+      if ((long)grid.x * grid.y * grid.z <= 2L * kNumSMs)
+        return launch_wm<DH, W, 2>(grid, M, H, Hk, tmkv, qkv, seqs, rope, kv, layer, n_qblk, SPLIT, ws, out, st);
   }
   return launch_wm<DH, W, per_sm>(grid, M, H, Hk, tmkv, qkv, seqs, rope, kv, layer, n_qblk, SPLIT, ws, out, st);
 }
